@@ -1,0 +1,330 @@
+#!/usr/bin/env python
+"""bench.py — randomized ID (arXiv 1205.3830) on B200: one JSON line per run.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: one process per GPU, NCCL)
+
+A "step" is one rid_decompose of the whole configured matrix (all ranks together): Philox
+regeneration of R, the DMMA sketch Y = R A, the all-gather of Y (N > 1), the pivoted Householder QR
+of Y, and T = R11^-1 R12 with the P = [I T] assembly — the hot path of SURVEY.md §8(a) rows a2–a5,
+with A (a1's output) resident in HBM before the timed region. a1 (generation) and a6 (the error
+estimate) are timed in the same run and reported under "phases" (they are not inside the step).
+
+metric (BASELINE.json): "ID sketch FP64-complex TFLOP/s & end-to-end ID s at 1/2/4/8 B200 vs
+roofline". value = 8 l m n (the complex sketch's real flops, whole matrix) / end-to-end step time;
+"id_seconds" is that step time, "sketch_tflops" the sketch kernel alone; "roofline" describes the
+dominant kernel (the sketch) against the measured FP64 tensor-pipe (DMMA) peak.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from paper_1205_3830_b200.configs import CONFIGS, HEADLINE_SEED  # noqa: E402
+
+METRIC = "ID sketch FP64-complex TFLOP/s & end-to-end ID s at 1/2/4/8 B200 vs roofline"
+UNIT = "TFLOP/s"
+# FP64 tensor-pipe (DMMA.8x8x4) peak measured on this pool's B200 with tools/microbench_fp64.cu:
+# 37.11 TFLOP/s sustained (400 launches, ~2 s) and 37.10 burst; clocks stayed at 1965 MHz
+# (profiles/r01_box_facts_fp64_microbench.txt). MEASURED_PEAKS.json has no FP64 entry.
+FP64_DMMA_PEAK_TFLOPS = 37.11
+FP64_PEAK_SOURCE = "measured DMMA m8n8k4 microbenchmark, profiles/r01_box_facts_fp64_microbench.txt"
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+# ------------------------------------------------------------------------------ clocks -----------
+class ClockSampler:
+    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ oracle arm -------
+def oracle_sample(cfg, seed: int, target_s: float = 15.0):
+    """The CPU oracle (as it stands) on a bounded sample of the workload: the sketch of n_s
+    columns of A (R regenerated inside, as the GPU step does). Returns (TFLOP/s, seconds, n_s,
+    threads)."""
+    import oracle
+
+    threads = oracle.set_threads(os.cpu_count() or 1)
+    n_s = 8
+    A = oracle.generate(seed, cfg.m, cfg.n, cfg.k, cfg.noise, 0, n_s)
+    t0 = time.perf_counter()
+    oracle.sketch(A, seed, cfg.l)
+    dt = time.perf_counter() - t0
+    n_s = max(threads, min(cfg.n, int(n_s * target_s / max(dt, 1e-3))))
+    n_s = max(threads, (n_s // threads) * threads)
+    A = oracle.generate(seed, cfg.m, cfg.n, cfg.k, cfg.noise, 0, n_s)
+    t0 = time.perf_counter()
+    oracle.sketch(A, seed, cfg.l)
+    dt = time.perf_counter() - t0
+    return 8.0 * cfg.l * cfg.m * n_s / dt / 1e12, dt, n_s, threads
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    steps = []
+    info = None
+    for i in range(args.warmup + args.steps):
+        tf, dt, n_s, threads = oracle_sample(cfg, args.seed, target_s=args.ref_seconds)
+        if i >= args.warmup:
+            steps.append((tf, dt))
+        info = (n_s, threads)
+    tf = statistics.median(s[0] for s in steps)
+    ms = statistics.median(s[1] for s in steps) * 1e3
+    sample = (f"oracle/rid_oracle.c sketch (naive ascending fused loops, R regenerated) of "
+              f"{info[0]} of {cfg.n} columns of {cfg.name}; TFLOP/s at 8*l*m*n_sample")
+    line = {"impl": "reference", "metric": METRIC, "value": tf, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n,
+                                            "k": cfg.k, "l": cfg.l, "noise": cfg.noise,
+                                            "seed": args.seed},
+            "cpu_baseline": {"value": tf, "unit": UNIT, "cores": info[1], "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": tf, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------ our arm ----------
+def run_ours(args, cfg):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1205_3830_b200 as rid
+    from paper_1205_3830_b200 import build as rid_build
+    from paper_1205_3830_b200.dist import init_comm
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    rid_build.build()
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    stream = torch.cuda.Stream()
+    ctx = rid.Context(local, stream)
+    if world > 1:
+        init_comm(ctx)
+    col0, n_loc = rid.shard_range(cfg.n, rank, world)
+    m, n, k, l, seed = cfg.m, cfg.n, cfg.k, cfg.l, args.seed
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    with torch.cuda.stream(stream):
+        # ---- a1: generation (timed separately, outside the step) ----------------------------
+        A = rid.colmajor_empty(m, n_loc, device="cuda")
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        rid.generate(seed, m, n, k, cfg.noise, col0, n_loc, out=A, ctx=ctx)
+        g1.record(stream)
+        J = torch.empty(k, dtype=torch.int64, device="cuda")
+        P = rid.colmajor_empty(k, n_loc, device="cuda")
+        for _ in range(args.warmup):
+            rid.decompose(A, k, l, seed, n=n, col0=col0, J=J, P=P, ctx=ctx)
+        barrier()
+        gen_s = g0.elapsed_time(g1) * 1e-3
+
+        # ---- timed region: K steps of rid_decompose on resident A -------------------------
+        clocks = ClockSampler(local)
+        clocks.start()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        diags = []
+        e0.record(stream)
+        for _ in range(args.steps):
+            r = rid.decompose(A, k, l, seed, n=n, col0=col0, J=J, P=P, ctx=ctx)
+            diags.append(r.diag)
+        e1.record(stream)
+        barrier()
+        clk = clocks.stop()
+        step_s = max_over_ranks(e0.elapsed_time(e1) * 1e-3 / args.steps)
+        launches = sum(d["launches"] for d in diags)
+
+        # ---- e2e: the same call with HOST buffers (H2D of A_loc, D2H of P_loc inside) ------
+        e2e = None
+        if not args.no_e2e:
+            A_h = rid.colmajor_empty(m, n_loc, device="cpu", pin_memory=True)
+            A_h.copy_(A)
+            P_h = rid.colmajor_empty(k, n_loc, device="cpu", pin_memory=True)
+            J_h = torch.empty(k, dtype=torch.int64).numpy()
+            rid.decompose(A_h, k, l, seed, n=n, col0=col0, J=J_h, P=P_h, ctx=ctx)  # warm staging
+            barrier()
+            e_steps = max(1, min(args.steps, 3))
+            t0 = time.perf_counter()
+            for _ in range(e_steps):
+                rid.decompose(A_h, k, l, seed, n=n, col0=col0, J=J_h, P=P_h, ctx=ctx)
+            barrier()
+            e2e_s = max_over_ranks((time.perf_counter() - t0) / e_steps)
+            e2e = {"value": 8.0 * l * m * n / e2e_s / 1e12, "unit": UNIT,
+                   "seconds_per_step": e2e_s,
+                   "h2d_bytes_per_step": 16 * m * n_loc,
+                   "d2h_bytes_per_step": 16 * k * n_loc + 8 * k}
+            assert torch.equal(torch.from_numpy(J_h), J.cpu()), "host path J differs"
+            del A_h, P_h
+
+        # ---- a6: the error estimate (timed separately) ------------------------------------
+        est = None
+        est_s = None
+        if args.q > 0:
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            est = rid.error_estimate(A, J, P, args.q, seed, n=n, col0=col0, ctx=ctx)
+            est_s = max_over_ranks(time.perf_counter() - t0)
+
+    sketch_s = max_over_ranks(statistics.mean(d["t_sketch"] for d in diags))
+    qrcp_s = max_over_ranks(statistics.mean(d["t_qrcp"] for d in diags))
+    solve_s = max_over_ranks(statistics.mean(d["t_solve"] for d in diags))
+    rgen_s = max_over_ranks(statistics.mean(d["t_rgen"] for d in diags))
+    gather_s = max_over_ranks(statistics.mean(d["t_gather"] for d in diags))
+    flops = 8.0 * l * m * n
+    sketch_tf_rank = 8.0 * l * m * n_loc / sketch_s / 1e12  # slowest rank's kernel
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        tf, dt, n_s, threads = oracle_sample(cfg, seed, target_s=args.ref_seconds)
+        cpu = {"value": tf, "unit": UNIT, "cores": threads, "kind": "oracle",
+               "sample": f"oracle sketch of {n_s}/{cfg.n} columns of {cfg.name} "
+                         f"({dt:.1f} s, R regenerated, {threads} OpenMP threads)"}
+    if rank != 0:
+        return 0
+    prof = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            prof = json.load(f).get(f"{cfg.name}/sketch", {})
+    except OSError:
+        pass
+    line = {
+        "metric": METRIC, "value": flops / step_s / 1e12, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": cfg.name, "m": m, "n": n, "k": k, "l": l, "noise": cfg.noise,
+                   "seed": seed, "parallelism": f"column-shard x{world}",
+                   "l2": f"inputs larger than L2 (A = {16 * m * n / 2**30:.2f} GiB vs 126 MB)"},
+        "id_seconds": step_s,
+        "sketch_tflops": sketch_tf_rank * world,
+        "phases": {"rgen_s": rgen_s, "sketch_s": sketch_s, "gather_s": gather_s,
+                   "qrcp_s": qrcp_s, "solve_s": solve_s, "generate_s": gen_s,
+                   "error_estimate_s": est_s, "error_estimate_q": args.q},
+        "error_estimate": est,
+        "error_bound_eq3": rid.error_bound(m, n, k, 1e-20, cfg.noise * (m**0.5 + n**0.5))
+        if cfg.noise else None,
+        "tie_margin_min": diags[-1]["tie_margin_min"],
+        "roofline": {"bound": "tensor", "achieved": sketch_tf_rank,
+                     "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                     "frac": sketch_tf_rank / FP64_DMMA_PEAK_TFLOPS,
+                     "traffic": prof.get("dram_bytes_per_launch"),
+                     "kernel": "k_zgemm_dmma (sketch Y = R A, DMMA.8x8x4)",
+                     "algorithmic": f"8*l*m*n_loc = {8.0 * l * m * n_loc:.4g} flop per launch",
+                     "peak_source": FP64_PEAK_SOURCE},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--seed", type=int, default=HEADLINE_SEED)
+    ap.add_argument("--q", type=int, default=20, help="estimator iterations (0 = skip)")
+    ap.add_argument("--ref-seconds", type=float, default=15.0)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+    return run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

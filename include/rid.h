@@ -1,0 +1,157 @@
+/*
+ * rid.h — C ABI of librid: the randomized interpolative decomposition (ID) of
+ * Lucas, Stalzer & Feo, "Parallel implementation of fast randomized algorithms for the
+ * decomposition of low rank matrices" (arXiv 1205.3830), on NVIDIA B200 (sm_100a).
+ *
+ * Problem (§2, Eq. 1): given a complex m x n matrix A of approximate rank k, find
+ * k column indices J (B = A[:, J]) and a k x n matrix P with A ≈ B P. The randomised algorithm
+ * (§2) sketches Y = R A with an l x m random R (l = k + oversampling), factors
+ * Y ≈ Q [R1 R2] with a column permutation, solves R2 = R1 T and sets P = [I T].
+ *
+ * Conventions for every call
+ *   - complex values are IEEE binary64 pairs (re, im) ("rid_z", 16 bytes, = cuDoubleComplex =
+ *     torch.complex128 element); matrices are COLUMN-MAJOR with a leading dimension ld ≥ rows.
+ *   - A column shard is columns [col0, col0 + n_loc) of the global m x n matrix A. With a
+ *     communicator of G ranks, rank g holds one contiguous shard and every rank calls
+ *     collectively with the same (m, n, k, l, seed, ...).
+ *   - Pointers may be DEVICE pointers (on the context's device) or HOST pointers (pageable or
+ *     pinned). The library detects which (cudaPointerGetAttributes); host buffers are staged
+ *     through device workspace with the copies on the context stream (this is the "e2e" path).
+ *   - Ownership: the caller owns every buffer passed in; the library never retains a caller
+ *     pointer after a call returns. The library owns transient workspace inside the context
+ *     (sketch matrix R, the full Y, reflectors, B = A[:, J], estimator vectors) and frees it in
+ *     rid_destroy.
+ *   - Calls are ordered on the context stream. rid_generate and rid_sketch return after
+ *     enqueueing when all buffers are on the device; rid_decompose and rid_error_estimate
+ *     synchronise the stream once (to read the rank status / the estimate). Any call with host
+ *     buffers synchronises before returning.
+ *   - Errors: a status code is returned; no exception or abort crosses the ABI; the message is in
+ *     rid_last_error(ctx). Argument errors (RID_EINVAL) are detected before anything is enqueued.
+ *
+ * Randomness: every random matrix entry is N(seed, s, i, j) of docs/RNG.md (Philox4x32-10 with
+ * counter (i, j, s, 0), key = seed; complex Gaussian with parts N(0, 1/2)): X s=1, Y0 s=2,
+ * E s=3, R s=4 (s=20 on the one retry), estimator start vector s=5.
+ */
+#ifndef RID_H_
+#define RID_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct {
+  double re, im;
+} rid_z;
+
+typedef enum {
+  RID_OK = 0,
+  RID_EINVAL = 1,     /* argument violates a precondition (nothing was enqueued) */
+  RID_ERANK = 2,      /* sketch rank < k after one re-randomisation */
+  RID_ESINGULAR = 3,  /* |R11[i,i]| < 1e-13 max |R11 diag| */
+  RID_ENOMEM = 4,     /* device or pinned allocation failed */
+  RID_ECUDA = 5,      /* a CUDA runtime error; see rid_last_error */
+  RID_ENCCL = 6       /* an NCCL error; see rid_last_error */
+} rid_status;
+
+typedef struct rid_ctx rid_ctx;
+
+/* Per-call diagnostics (SPEC.md:298-302 IdDiagnostics); every field is written by the call that
+ * receives it; times are device times from CUDA events on the context stream, in seconds. */
+typedef struct {
+  double t_rgen;      /* Philox fill of the sketch matrix R                       */
+  double t_sketch;    /* Y_loc = R A_loc (DMMA)                                    */
+  double t_gather;    /* all-gather of Y over the communicator (0 when G = 1)      */
+  double t_qrcp;      /* pivoted Householder QR of Y                               */
+  double t_solve;     /* R11^{-1}, T = R11^{-1} R12 (DMMA), P = [I T] assembly      */
+  double t_total;     /* whole call, device time                                   */
+  double t_h2d, t_d2h;/* host staging copies (e2e path), 0 for device buffers      */
+  int retries;        /* 0 or 1 sketch re-randomisations             */
+  int rank_achieved;  /* k on success; the achieved rank on RID_ERANK              */
+  double tie_margin_min; /* min_j (nu(1) - nu(2)) / nu(1) over the k pivot steps (reading R18) */
+  double resid_last;  /* nu_p at the last pivot step (|R11[k-1,k-1]|)              */
+  int launches;       /* number of librid CUDA kernels this call launched           */
+} rid_diag;
+
+/* --- context ------------------------------------------------------------------------------- */
+/* Create a context on CUDA device `device` whose calls are ordered on `cuda_stream` (a
+ * cudaStream_t owned by the caller; NULL = the legacy default stream, as everywhere in CUDA). */
+rid_status rid_create(rid_ctx** ctx, int device, void* cuda_stream);
+void rid_destroy(rid_ctx* ctx);
+/* Last error message of this context ("" when none). Valid until the next call on ctx. */
+const char* rid_last_error(const rid_ctx* ctx);
+/* Library version string and the compiled GPU architecture ("sm_100a"). */
+const char* rid_version(void);
+
+/* --- communicator (column sharding over G GPUs, NCCL over NVLink) --------------------------- */
+/* Size of the opaque unique-id blob (NCCL_UNIQUE_ID_BYTES). */
+size_t rid_comm_id_bytes(void);
+/* Rank 0 creates the id (writes rid_comm_id_bytes() bytes to `id`); the caller broadcasts it
+ * to the other ranks by any means (the Python layer uses torch.distributed). */
+rid_status rid_comm_get_id(void* id);
+/* Every rank: join the communicator of `nranks` ranks as `rank` (collective, blocking). */
+rid_status rid_comm_init(rid_ctx* ctx, const void* id, int rank, int nranks);
+/* Query: rank and nranks (1, 0 when no communicator). */
+rid_status rid_comm_info(const rid_ctx* ctx, int* rank, int* nranks);
+
+/* --- the method ---------------------------------------------------------------------------- */
+/* A[:, shard] = X Y0 + noise E (docs/RNG.md §5): X m x k, Y0 k x n, E m x n from
+ * Philox. Bit-identical to the CPU oracle. Preconditions: 1 <= k <= min(m, n), 0 <= col0,
+ * n_loc >= 0, col0 + n_loc <= n, lda >= m, m, n < 2^32. */
+rid_status rid_generate(rid_ctx* ctx, uint64_t seed, int64_t m, int64_t n, int64_t k, double noise,
+                        int64_t col0, int64_t n_loc, rid_z* A, int64_t lda);
+
+/* Y (l x n_loc) = R A with R(r, i) = N(seed, stream, r, i) (north_star; PAPER.md:97 licenses the
+ * Gaussian sketch in place of the SRFT of Eqs. 4–7). stream is 4 (or 20 on the retry). The K
+ * summation is ascending and fused, so Y is bit-identical to the oracle's naive loop.
+ * Preconditions: 1 <= l <= m, lda >= m, ldy >= l. */
+rid_status rid_sketch(rid_ctx* ctx, uint64_t seed, uint32_t stream, int64_t l, const rid_z* A,
+                      int64_t m, int64_t n_loc, int64_t lda, rid_z* Y, int64_t ldy);
+
+/* The whole ID on a column shard: sketch -> all-gather Y -> column-pivoted
+ * Householder QR of Y (k steps, greedy max-norm pivot, ties -> lowest index) -> T = R11^{-1} R12
+ * for the local columns -> P_loc = [I T] in original column order (P[t, J_t] = 1 exactly).
+ * Outputs: J (k int64, GLOBAL column ids in pivot order; replicated on every rank) and P_loc
+ * (k x n_loc, ldp >= k). On RID_ERANK after one retry with R stream 20, J/P are unspecified.
+ * Preconditions: 1 <= k <= min(m, n), k <= l <= min(m, 1024), shard as for rid_generate,
+ * G * n_loc == n when a communicator is set. diag may be NULL. */
+rid_status rid_decompose(rid_ctx* ctx, const rid_z* A, int64_t m, int64_t n, int64_t col0,
+                         int64_t n_loc, int64_t lda, int64_t k, int64_t l, uint64_t seed,
+                         int64_t* J, rid_z* P, int64_t ldp, rid_diag* diag);
+
+/* Power-iteration estimate of ||A - A[:, J] P||_2 (Table 5): x0 from stream 5
+ * normalised, q fixed iterations of y = A x - B (P x), z = A^H y - P^H (B^H y), est = sqrt(||z||),
+ * x = z / ||z||, with compensated (TwoProd/TwoSum) accumulation in every dot product.
+ * J are global column ids (as returned by rid_decompose), P the local k x n_loc block.
+ * *est is written on the host. Preconditions: q >= 1, shapes as above. */
+rid_status rid_error_estimate(rid_ctx* ctx, const rid_z* A, int64_t m, int64_t n, int64_t col0,
+                              int64_t n_loc, int64_t lda, const int64_t* J, int64_t k,
+                              const rid_z* P, int64_t ldp, int q, uint64_t seed, double* est,
+                              rid_diag* diag);
+
+/* Eq. (3) right-hand side 50 sqrt(mn) (1/eps)^(1/k) sigma_kp1. Host only. */
+double rid_error_bound(int64_t m, int64_t n, int64_t k, double eps, double sigma_kp1);
+
+/* --- lower-level entry points (the steps of rid_decompose, for tests and G-emulation) --------- */
+/* out(i, j) = N(seed, s, row0 + i, col0 + j), rows x cols, leading dimension ld. */
+rid_status rid_normal_fill(rid_ctx* ctx, uint64_t seed, uint32_t s, int64_t rows, int64_t cols,
+                           int64_t row0, int64_t col0, rid_z* out, int64_t ld);
+/* Pivoted QR of a full sketch Y (l x n, copied; the caller's Y is not modified). Outputs J (k),
+ * R (k x n, original column order: R[:, c] = Q^H Y[:, c] rows 0..k-1, zero below the diagonal of
+ * the pivot columns), resid (k, nu_p per step) and margin (k, tie margins); any of R, resid,
+ * margin may be NULL. Returns RID_ERANK with diag->rank_achieved on rank failure. */
+rid_status rid_qrcp(rid_ctx* ctx, const rid_z* Y, int64_t l, int64_t n, int64_t ldy, int64_t k,
+                    int64_t* J, rid_z* R, int64_t ldr, double* resid, double* margin,
+                    rid_diag* diag);
+/* P_loc from a full sketch Y (l x n): the factorisation of rid_qrcp followed by the solve for
+ * columns [col0, col0 + n_loc). Used to emulate G shards on one GPU. */
+rid_status rid_factor_solve(rid_ctx* ctx, const rid_z* Y, int64_t l, int64_t n, int64_t ldy,
+                            int64_t k, int64_t col0, int64_t n_loc, int64_t* J, rid_z* P,
+                            int64_t ldp, rid_diag* diag);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RID_H_ */

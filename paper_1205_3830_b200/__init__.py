@@ -1,0 +1,361 @@
+"""paper_1205_3830_b200 — randomized interpolative decomposition (arXiv 1205.3830) on B200.
+
+Thin Python binding over the C ABI of ``include/rid.h`` (``librid.so``, built in-tree by
+``paper_1205_3830_b200.build``). Argument marshalling only: every step of the method runs in the
+CUDA kernels of ``csrc/``. There is no CPU fallback — if the library is missing or no GPU is
+visible, calls raise.
+
+Matrices are complex128 and column-major: a torch tensor of shape (rows, cols) with
+``stride(0) == 1`` (e.g. ``torch.empty((cols, rows), dtype=torch.complex128).T``) or a numpy
+array in Fortran order. Tensors on the GPU are used in place; host tensors / numpy arrays go
+through the library's own host staging (the "e2e" path of bench.py).
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+__all__ = [
+    "RidError", "Context", "Diag", "lib", "colmajor_empty", "generate", "sketch", "decompose",
+    "error_estimate", "error_bound", "normal_fill", "qrcp", "factor_solve", "shard_range",
+    "STREAM_R", "STREAM_R_RETRY",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librid.so")
+STREAM_R, STREAM_R_RETRY = 4, 20
+
+RID_OK, RID_EINVAL, RID_ERANK, RID_ESINGULAR, RID_ENOMEM, RID_ECUDA, RID_ENCCL = range(7)
+_STATUS = {0: "RID_OK", 1: "RID_EINVAL", 2: "RID_ERANK", 3: "RID_ESINGULAR", 4: "RID_ENOMEM",
+           5: "RID_ECUDA", 6: "RID_ENCCL"}
+
+
+class RidError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Diag(ctypes.Structure):
+    """rid_diag (include/rid.h)."""
+
+    _fields_ = [("t_rgen", ctypes.c_double), ("t_sketch", ctypes.c_double),
+                ("t_gather", ctypes.c_double), ("t_qrcp", ctypes.c_double),
+                ("t_solve", ctypes.c_double), ("t_total", ctypes.c_double),
+                ("t_h2d", ctypes.c_double), ("t_d2h", ctypes.c_double),
+                ("retries", ctypes.c_int), ("rank_achieved", ctypes.c_int),
+                ("tie_margin_min", ctypes.c_double), ("resid_last", ctypes.c_double),
+                ("launches", ctypes.c_int)]
+
+    def as_dict(self):
+        return {f: getattr(self, f) for f, _ in self._fields_}
+
+
+_lib = None
+EXPORTS = ["rid_create", "rid_destroy", "rid_last_error", "rid_version", "rid_comm_id_bytes",
+           "rid_comm_get_id", "rid_comm_init", "rid_comm_info", "rid_generate", "rid_sketch",
+           "rid_decompose", "rid_error_estimate", "rid_error_bound", "rid_normal_fill",
+           "rid_qrcp", "rid_factor_solve"]
+
+
+def lib():
+    """Load librid.so (raises if it was not built — there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} missing: run `python -m paper_1205_3830_b200.build` "
+                           "(the CUDA path has no CPU fallback)")
+    L = ctypes.CDLL(LIB_PATH)
+    p, i64, u64, u32, d, ci = (ctypes.c_void_p, ctypes.c_int64, ctypes.c_uint64, ctypes.c_uint32,
+                               ctypes.c_double, ctypes.c_int)
+    sig = {
+        "rid_create": ([ctypes.POINTER(p), ci, p], ci),
+        "rid_destroy": ([p], None),
+        "rid_last_error": ([p], ctypes.c_char_p),
+        "rid_version": ([], ctypes.c_char_p),
+        "rid_comm_id_bytes": ([], ctypes.c_size_t),
+        "rid_comm_get_id": ([p], ci),
+        "rid_comm_init": ([p, p, ci, ci], ci),
+        "rid_comm_info": ([p, ctypes.POINTER(ci), ctypes.POINTER(ci)], ci),
+        "rid_generate": ([p, u64, i64, i64, i64, d, i64, i64, p, i64], ci),
+        "rid_sketch": ([p, u64, u32, i64, p, i64, i64, i64, p, i64], ci),
+        "rid_decompose": ([p, p, i64, i64, i64, i64, i64, i64, i64, u64, p, p, i64, p], ci),
+        "rid_error_estimate": ([p, p, i64, i64, i64, i64, i64, p, i64, p, i64, ci, u64, p, p], ci),
+        "rid_error_bound": ([i64, i64, i64, d, d], d),
+        "rid_normal_fill": ([p, u64, u32, i64, i64, i64, i64, p, i64], ci),
+        "rid_qrcp": ([p, p, i64, i64, i64, i64, p, p, i64, p, p, p], ci),
+        "rid_factor_solve": ([p, p, i64, i64, i64, i64, i64, i64, p, p, i64, p], ci),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+# ------------------------------------------------------------------------------ buffers ---------
+def _torch():
+    import torch
+
+    return torch
+
+
+def colmajor_empty(rows: int, cols: int, device="cuda", dtype=None, pin_memory=False):
+    """Empty column-major (rows, cols) tensor (stride (1, rows))."""
+    torch = _torch()
+    dtype = dtype or torch.complex128
+    if str(device) == "cpu":
+        t = torch.empty((cols, rows), dtype=dtype, pin_memory=pin_memory)
+    else:
+        t = torch.empty((cols, rows), dtype=dtype, device=device)
+    return t.T
+
+
+class _Buf:
+    """(pointer, leading dimension, keep-alive) for a complex128 column-major matrix."""
+
+    def __init__(self, a, rows: int, cols: int, name: str):
+        self.obj = a
+        if isinstance(a, np.ndarray):
+            if a.dtype != np.complex128:
+                raise TypeError(f"{name}: need complex128, got {a.dtype}")
+            if a.ndim == 1:
+                a = a.reshape(-1, 1)
+            if a.shape != (rows, cols):
+                raise ValueError(f"{name}: shape {a.shape} != {(rows, cols)}")
+            if cols > 1 and not a.flags.f_contiguous and a.strides[0] != 16:
+                raise ValueError(f"{name}: numpy array must be column-major (Fortran order)")
+            self.ptr = a.ctypes.data
+            self.ld = a.strides[1] // 16 if cols > 1 else rows
+            self.obj = a
+        else:
+            torch = _torch()
+            if a.dtype != torch.complex128:
+                raise TypeError(f"{name}: need torch.complex128, got {a.dtype}")
+            if a.dim() == 1:
+                a = a.reshape(-1, 1)
+            if tuple(a.shape) != (rows, cols):
+                raise ValueError(f"{name}: shape {tuple(a.shape)} != {(rows, cols)}")
+            if a.stride(0) != 1 and rows > 1:
+                raise ValueError(f"{name}: tensor must be column-major (stride(0) == 1)")
+            self.ptr = a.data_ptr()
+            self.ld = a.stride(1) if cols > 1 else max(rows, 1)
+            self.obj = a
+        self.ld = max(self.ld, rows)
+
+
+def _ptr_i64(a):
+    if isinstance(a, np.ndarray):
+        if a.dtype != np.int64 or not a.flags.c_contiguous:
+            raise TypeError("J must be a contiguous int64 array")
+        return a.ctypes.data
+    torch = _torch()
+    if a.dtype != torch.int64 or not a.is_contiguous():
+        raise TypeError("J must be a contiguous int64 tensor")
+    return a.data_ptr()
+
+
+# ------------------------------------------------------------------------------ context ---------
+class Context:
+    """A librid context (rid_ctx) bound to one CUDA device and stream."""
+
+    def __init__(self, device: int = 0, stream=None):
+        L = lib()
+        self._L = L
+        self.device = device
+        h = ctypes.c_void_p()
+        sp = None
+        if stream is not None:
+            sp = ctypes.c_void_p(stream if isinstance(stream, int) else stream.cuda_stream)
+        st = L.rid_create(ctypes.byref(h), device, sp)
+        if st != RID_OK:
+            raise RidError(st, f"rid_create(device={device}) failed (is a B200 visible?)")
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self._L.rid_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, st: int, what: str):
+        if st != RID_OK:
+            msg = self._L.rid_last_error(self.h).decode(errors="replace")
+            raise RidError(st, f"{what}: {msg}")
+
+    # communicator ------------------------------------------------------------------------------
+    def comm_init(self, id_bytes: bytes, rank: int, nranks: int):
+        buf = ctypes.create_string_buffer(id_bytes, len(id_bytes))
+        self.check(self._L.rid_comm_init(self.h, buf, rank, nranks), "rid_comm_init")
+
+    def comm_info(self):
+        r, n = ctypes.c_int(), ctypes.c_int()
+        self.check(self._L.rid_comm_info(self.h, ctypes.byref(r), ctypes.byref(n)), "rid_comm_info")
+        return r.value, n.value
+
+
+def comm_get_id() -> bytes:
+    L = lib()
+    nb = L.rid_comm_id_bytes()
+    buf = ctypes.create_string_buffer(nb)
+    st = L.rid_comm_get_id(buf)
+    if st != RID_OK:
+        raise RidError(st, "rid_comm_get_id")
+    return buf.raw
+
+
+_default = {}
+
+
+def default_context(device=None) -> Context:
+    torch = _torch()
+    dev = torch.cuda.current_device() if device is None else device
+    if dev not in _default:
+        _default[dev] = Context(dev, torch.cuda.current_stream(dev))
+    return _default[dev]
+
+
+def shard_range(n: int, rank: int, world: int):
+    """Columns [col0, col0 + n_loc) of rank `rank` (contiguous equal blocks; n % world == 0)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    if n % world:
+        raise ValueError(f"n={n} is not divisible by world={world}")
+    n_loc = n // world
+    return rank * n_loc, n_loc
+
+
+# ------------------------------------------------------------------------------ the method ------
+def generate(seed: int, m: int, n: int, k: int, noise: float, col0: int = 0, n_loc=None,
+             out=None, ctx: Context | None = None, device="cuda"):
+    """A[:, col0:col0+n_loc] = X Y0 + noise E (docs/RNG.md §5), bit-identical to the oracle."""
+    ctx = ctx or default_context()
+    n_loc = n - col0 if n_loc is None else n_loc
+    if out is None:
+        out = colmajor_empty(m, n_loc, device=device)
+    b = _Buf(out, m, n_loc, "A")
+    ctx.check(lib().rid_generate(ctx.h, seed, m, n, k, float(noise), col0, n_loc, b.ptr, b.ld),
+              "rid_generate")
+    return out
+
+
+def sketch(A, seed: int, l: int, stream: int = STREAM_R, out=None, ctx: Context | None = None):
+    """Y = R A with R(r, i) = N(seed, stream, r, i) (DMMA, ascending fused K chain)."""
+    ctx = ctx or default_context()
+    m, n_loc = A.shape
+    a = _Buf(A, m, n_loc, "A")
+    if out is None:
+        out = colmajor_empty(l, n_loc, device=A.device if hasattr(A, "device") else "cpu") \
+            if not isinstance(A, np.ndarray) else np.zeros((l, n_loc), np.complex128, order="F")
+    y = _Buf(out, l, n_loc, "Y")
+    ctx.check(lib().rid_sketch(ctx.h, seed, stream, l, a.ptr, m, n_loc, a.ld, y.ptr, y.ld),
+              "rid_sketch")
+    return out
+
+
+@dataclass
+class IdResult:
+    J: object
+    P: object
+    diag: dict
+
+
+def decompose(A, k: int, l: int, seed: int, n: int | None = None, col0: int = 0, J=None, P=None,
+              ctx: Context | None = None) -> IdResult:
+    """The whole ID of the (shard of the) matrix A: J (k, global ids) and P_loc."""
+    ctx = ctx or default_context()
+    m, n_loc = A.shape
+    n = n_loc if n is None else n
+    a = _Buf(A, m, n_loc, "A")
+    host = isinstance(A, np.ndarray) or (hasattr(A, "device") and A.device.type == "cpu")
+    if J is None:
+        J = np.zeros(k, np.int64) if isinstance(A, np.ndarray) else _torch().empty(
+            k, dtype=_torch().int64, device=A.device)
+    if P is None:
+        P = np.zeros((k, n_loc), np.complex128, order="F") if isinstance(A, np.ndarray) else \
+            colmajor_empty(k, n_loc, device="cpu" if host else A.device,
+                           pin_memory=host and _torch().cuda.is_available())
+    p = _Buf(P, k, n_loc, "P")
+    d = Diag()
+    ctx.check(lib().rid_decompose(ctx.h, a.ptr, m, n, col0, n_loc, a.ld, k, l, seed, _ptr_i64(J),
+                                  p.ptr, p.ld, ctypes.byref(d)), "rid_decompose")
+    return IdResult(J, P, d.as_dict())
+
+
+def error_estimate(A, J, P, q: int, seed: int, n: int | None = None, col0: int = 0,
+                   ctx: Context | None = None) -> float:
+    """Compensated power-iteration estimate of ||A - A[:, J] P||_2 (Table 5)."""
+    ctx = ctx or default_context()
+    m, n_loc = A.shape
+    k = P.shape[0]
+    n = n_loc if n is None else n
+    a = _Buf(A, m, n_loc, "A")
+    p = _Buf(P, k, n_loc, "P")
+    est = ctypes.c_double()
+    d = Diag()
+    ctx.check(lib().rid_error_estimate(ctx.h, a.ptr, m, n, col0, n_loc, a.ld, _ptr_i64(J), k, p.ptr,
+                                       p.ld, int(q), seed, ctypes.byref(est), ctypes.byref(d)),
+              "rid_error_estimate")
+    return est.value
+
+
+def error_bound(m: int, n: int, k: int, eps: float, sigma_kp1: float) -> float:
+    """Eq. (3) right-hand side."""
+    return lib().rid_error_bound(m, n, k, eps, sigma_kp1)
+
+
+def normal_fill(seed: int, s: int, rows: int, cols: int, row0: int = 0, col0: int = 0, out=None,
+                ctx: Context | None = None, device="cuda"):
+    ctx = ctx or default_context()
+    if out is None:
+        out = colmajor_empty(rows, cols, device=device)
+    b = _Buf(out, rows, cols, "out")
+    ctx.check(lib().rid_normal_fill(ctx.h, seed, s, rows, cols, row0, col0, b.ptr, b.ld),
+              "rid_normal_fill")
+    return out
+
+
+def qrcp(Y, k: int, ctx: Context | None = None, want_R: bool = True):
+    """Pivoted Householder QR of a full sketch: (J, R (k x n) or None, resid, margin, diag)."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    l, n = Y.shape
+    y = _Buf(Y, l, n, "Y")
+    dev = Y.device
+    J = torch.empty(k, dtype=torch.int64, device=dev)
+    R = colmajor_empty(k, n, device=dev) if want_R else None
+    resid = torch.empty(k, dtype=torch.float64, device=dev)
+    margin = torch.empty(k, dtype=torch.float64, device=dev)
+    d = Diag()
+    st = lib().rid_qrcp(ctx.h, y.ptr, l, n, y.ld, k, J.data_ptr(),
+                        R.data_ptr() if R is not None else None, k if R is not None else k,
+                        resid.data_ptr(), margin.data_ptr(), ctypes.byref(d))
+    if st == RID_ERANK:
+        raise RidError(st, f"rank {d.rank_achieved} < k = {k}")
+    ctx.check(st, "rid_qrcp")
+    return J, R, resid, margin, d.as_dict()
+
+
+def factor_solve(Y, k: int, col0: int, n_loc: int, ctx: Context | None = None):
+    """(J, P_loc) from a full sketch Y: factorisation + solve for one column shard."""
+    torch = _torch()
+    ctx = ctx or default_context()
+    l, n = Y.shape
+    y = _Buf(Y, l, n, "Y")
+    J = torch.empty(k, dtype=torch.int64, device=Y.device)
+    P = colmajor_empty(k, n_loc, device=Y.device)
+    p = _Buf(P, k, n_loc, "P")
+    d = Diag()
+    ctx.check(lib().rid_factor_solve(ctx.h, y.ptr, l, n, y.ld, k, col0, n_loc, J.data_ptr(), p.ptr,
+                                     p.ld, ctypes.byref(d)), "rid_factor_solve")
+    return J, P, d.as_dict()

@@ -1,0 +1,389 @@
+// k_qrcp.cu — column-pivoted Householder QR of the sketch Y (l x n), k steps, one persistent
+// cooperative kernel with one grid barrier per step.
+//
+// Paper: "a highly approximate QR factorization on the matrix Y ... Y ≈ QR" with a column
+// permutation "so that the first k columns are linearly independent and contain the k most
+// weighted vectors" (§2, Eqs. 8–9); the authors note Householder "should result
+// in similar stability with only half the runtime" of their CGS (§3.2).
+// Readings: R8 greedy max residual 2-norm pivot, ties -> lowest column index;
+// R11 the residual norms are recomputed exactly from the updated column every step (no
+// downdating); R13 rank failure when nu_p < 1e-13 * max_c ||Y[:, c]||.
+//
+// Layout: every CTA owns a contiguous block of columns; a warp owns a column at a time and keeps
+// its rows j..l-1 in registers (MAXQ complex per lane) while it forms v^H y, applies
+// y <- y - conj(tau) (v^H y) v and recomputes ||y[j+1:l]|| — one read and one write of the
+// trailing column per step. Every CTA rebuilds the same reflector from column p (identical bits:
+// same code, same data, commutative butterfly reductions), so the only cross-CTA exchange is the
+// per-CTA (best, second, index) candidate triple. Output, in place in Y (LAPACK-like):
+// rows 0..k-1 of every non-pivot column are R12; Y[0:t, J_t] is R11[0:t, t]; beta[t] = R11[t, t].
+#include <cfloat>
+#include <cstdint>
+
+#include "rid_device.cuh"
+#include "rid_internal.h"
+
+namespace rid {
+
+struct Top2 {
+  double b1;   // best value
+  double b2;   // second-best value
+  long long i1;  // index of best
+};
+
+__device__ __forceinline__ bool beats(double v, long long i, double bv, long long bi) {
+  return v > bv || (v == bv && i < bi);
+}
+__device__ __forceinline__ void top2_init(Top2& a) {
+  a.b1 = -1.0;
+  a.b2 = -1.0;
+  a.i1 = 0x7FFFFFFFFFFFFFFFLL;
+}
+__device__ __forceinline__ void top2_push(Top2& a, double v, long long i) {
+  if (beats(v, i, a.b1, a.i1)) {
+    a.b2 = a.b1;
+    a.b1 = v;
+    a.i1 = i;
+  } else if (v > a.b2) {
+    a.b2 = v;
+  }
+}
+__device__ __forceinline__ void top2_merge(Top2& a, const Top2& c) {
+  if (beats(c.b1, c.i1, a.b1, a.i1)) {
+    a.b2 = fmax(a.b1, c.b2);
+    a.b1 = c.b1;
+    a.i1 = c.i1;
+  } else {
+    a.b2 = fmax(a.b2, c.b1);
+  }
+}
+__device__ __forceinline__ void top2_warp(Top2& a) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    Top2 o;
+    o.b1 = __shfl_xor_sync(0xffffffffu, a.b1, m);
+    o.b2 = __shfl_xor_sync(0xffffffffu, a.b2, m);
+    o.i1 = __shfl_xor_sync(0xffffffffu, a.i1, m);
+    top2_merge(a, o);
+  }
+}
+// butterfly sum: every lane ends with the same bits (fp addition is commutative)
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, m));
+  return v;
+}
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1u);
+    while (ld_acquire(bar) < target) __nanosleep(20);
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+constexpr int kQrcpThreads = 256;
+constexpr int kQrcpWarps = kQrcpThreads / 32;
+
+template <int MAXQ>
+__global__ void __launch_bounds__(kQrcpThreads) k_qrcp(double2* __restrict__ Y, int64_t ldy, int l,
+                                                       int64_t n, int k, double tol_rel,
+                                                       QrcpOut out, QrcpWork w) {
+  __shared__ double2 sv[MAXQ * 32];
+  __shared__ Top2 sred[kQrcpWarps];
+  __shared__ double s_tau_re, s_tau_im;
+  __shared__ long long s_p;
+  __shared__ int s_stop;
+
+  const int nb = gridDim.x, b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t per = (n + nb - 1) / nb;
+  const int64_t c_lo = (int64_t)b * per;
+  const int64_t c_hi = (c_lo + per < n) ? c_lo + per : n;
+  double nu0max = 0.0;
+  unsigned phase = 0;
+
+  auto block_top2_publish = [&](Top2 loc, int parity) {
+    top2_warp(loc);
+    if (lane == 0) sred[warp] = loc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Top2 t = sred[0];
+      for (int q = 1; q < kQrcpWarps; ++q) top2_merge(t, sred[q]);
+      double* c = w.cand + ((size_t)parity * w.max_blocks + b) * 3;
+      c[0] = t.b1;
+      c[1] = t.b2;
+      c[2] = (double)t.i1;
+    }
+  };
+
+  // ---- phase 0: initial column norms --------------------------------------------------------
+  {
+    Top2 loc;
+    top2_init(loc);
+    for (int64_t c = c_lo + warp; c < c_hi; c += kQrcpWarps) {
+      const double2* yc = Y + c * ldy;
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int r = lane + 32 * q;
+        if (r < l) {
+          const double2 y = yc[r];
+          s = __fma_rn(y.x, y.x, s);
+          s = __fma_rn(y.y, y.y, s);
+        }
+      }
+      const double nu = __dsqrt_rn(warp_sum(s));
+      if (lane == 0) {
+        w.nu[c] = nu;
+        top2_push(loc, nu, c);  // one lane per column: the multiset of candidates has no copies
+      }
+    }
+    block_top2_publish(loc, 0);
+    grid_barrier(w.bar, (unsigned)nb * (++phase));
+  }
+
+  for (int j = 0; j < k; ++j) {
+    // ---- 1. global pivot: reduce the per-CTA candidates (every CTA, identically) ------------
+    if (warp == 0) {
+      Top2 t;
+      top2_init(t);
+      const double* cb = w.cand + (size_t)(j & 1) * w.max_blocks * 3;
+      for (int q = lane; q < nb; q += 32) {
+        Top2 o;
+        o.b1 = cb[q * 3 + 0];
+        o.b2 = cb[q * 3 + 1];
+        o.i1 = (long long)cb[q * 3 + 2];
+        top2_merge(t, o);
+      }
+      top2_warp(t);
+      if (j == 0) nu0max = t.b1;  // max_c ||Y[:, c]||
+      if (lane == 0) {
+        s_p = t.i1;
+        s_stop = (!(t.b1 >= tol_rel * nu0max) || t.b1 <= 0.0) ? 1 : 0;
+        if (b == 0) {
+          out.resid[j] = t.b1;
+          out.margin[j] = (t.b2 < 0.0) ? DBL_MAX : (t.b1 - t.b2) / t.b1;
+          if (!s_stop) out.J[j] = t.i1;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_stop) {
+      if (b == 0 && threadIdx.x == 0) {
+        out.info[0] = 2;
+        out.info[1] = j;
+      }
+      return;  // every CTA takes the same decision at the same step
+    }
+    const int64_t p = s_p;
+
+    // ---- 2. Householder reflector from x = Y[j:l, p] (LAPACK zlarfg convention) -------------
+    if (warp == 0) {
+      const double2* xp = Y + p * ldy;
+      double2 x[MAXQ];
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int r = j + lane + 32 * q;
+        x[q] = (r < l) ? xp[r] : make_double2(0.0, 0.0);
+        if (r > j && r < l) {
+          s = __fma_rn(x[q].x, x[q].x, s);
+          s = __fma_rn(x[q].y, x[q].y, s);
+        }
+      }
+      const double xnorm2 = warp_sum(s);
+      const double ar = __shfl_sync(0xffffffffu, x[0].x, 0);
+      const double ai = __shfl_sync(0xffffffffu, x[0].y, 0);
+      double tau_re, tau_im, beta, sc_re, sc_im;
+      if (xnorm2 == 0.0 && ai == 0.0) {
+        tau_re = 0.0;
+        tau_im = 0.0;
+        beta = ar;
+        sc_re = 0.0;
+        sc_im = 0.0;
+      } else {
+        const double nrm = __dsqrt_rn(__fma_rn(ar, ar, __fma_rn(ai, ai, xnorm2)));
+        beta = (ar >= 0.0) ? -nrm : nrm;
+        tau_re = __ddiv_rn(__dsub_rn(beta, ar), beta);
+        tau_im = __ddiv_rn(-ai, beta);
+        // scal = 1 / (alpha - beta)
+        const double dr = __dsub_rn(ar, beta), di = ai;
+        const double den = __fma_rn(dr, dr, __dmul_rn(di, di));
+        sc_re = __ddiv_rn(dr, den);
+        sc_im = __ddiv_rn(-di, den);
+      }
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int rr = lane + 32 * q;  // row j + rr
+        if (j + rr < l) {
+          double2 v;
+          if (rr == 0) {
+            v = make_double2(1.0, 0.0);
+          } else {
+            v.x = __fma_rn(x[q].x, sc_re, -__dmul_rn(x[q].y, sc_im));
+            v.y = __fma_rn(x[q].x, sc_im, __dmul_rn(x[q].y, sc_re));
+          }
+          sv[rr] = v;
+        }
+      }
+      if (lane == 0) {
+        s_tau_re = tau_re;
+        s_tau_im = tau_im;
+        if (b == 0) out.beta[j] = beta;
+      }
+    }
+    __syncthreads();
+    const double tr = s_tau_re, ti = s_tau_im;
+
+    // ---- 3. apply H^H = I - conj(tau) v v^H to every owned trailing column ------------------
+    Top2 loc;
+    top2_init(loc);
+    for (int64_t c = c_lo + warp; c < c_hi; c += kQrcpWarps) {
+      if (c == p) {
+        if (lane == 0) w.nu[p] = -1.0;  // chosen
+        continue;
+      }
+      if (w.nu[c] < 0.0) continue;  // chosen at an earlier step
+      double2* yc = Y + c * ldy;
+      double2 y[MAXQ];
+      double wr = 0.0, wi = 0.0;
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int rr = lane + 32 * q;
+        if (j + rr < l) {
+          y[q] = yc[j + rr];
+          const double2 v = sv[rr];
+          // conj(v) * y
+          wr = __fma_rn(v.x, y[q].x, __fma_rn(v.y, y[q].y, wr));
+          wi = __fma_rn(v.x, y[q].y, __fma_rn(-v.y, y[q].x, wi));
+        }
+      }
+      wr = warp_sum(wr);
+      wi = warp_sum(wi);
+      // s = conj(tau) * w
+      const double s_re = __fma_rn(tr, wr, __dmul_rn(ti, wi));
+      const double s_im = __fma_rn(tr, wi, -__dmul_rn(ti, wr));
+      double nn = 0.0;
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int rr = lane + 32 * q;
+        if (j + rr < l) {
+          const double2 v = sv[rr];
+          // y -= s * v
+          y[q].x = __fma_rn(-s_re, v.x, __fma_rn(s_im, v.y, y[q].x));
+          y[q].y = __fma_rn(-s_re, v.y, __fma_rn(-s_im, v.x, y[q].y));
+          yc[j + rr] = y[q];
+          if (rr > 0) {
+            nn = __fma_rn(y[q].x, y[q].x, nn);
+            nn = __fma_rn(y[q].y, y[q].y, nn);
+          }
+        }
+      }
+      const double nu = __dsqrt_rn(warp_sum(nn));
+      if (lane == 0) {
+        w.nu[c] = nu;
+        top2_push(loc, nu, c);
+      }
+    }
+    block_top2_publish(loc, (j + 1) & 1);
+    grid_barrier(w.bar, (unsigned)nb * (++phase));
+  }
+  if (b == 0 && threadIdx.x == 0) {
+    out.info[0] = 0;
+    out.info[1] = k;
+  }
+}
+
+size_t qrcp_work_bytes(int64_t n, int max_blocks) {
+  return (size_t)n * sizeof(double) + (size_t)2 * 3 * max_blocks * sizeof(double) + 256;
+}
+
+template <int MAXQ>
+static cudaError_t launch_qrcp(double2* Y, int64_t ldy, int l, int64_t n, int k, double tol_rel,
+                               const QrcpOut& out, const QrcpWork& w, int num_sms,
+                               cudaStream_t st) {
+  int occ = 0;
+  cudaError_t e =
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qrcp<MAXQ>, kQrcpThreads, 0);
+  if (e != cudaSuccess) return e;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  int blocks = num_sms * (occ < 2 ? occ : 2);
+  if (blocks > w.max_blocks) blocks = w.max_blocks;
+  const int64_t min_cols = 8;  // keep >= 8 columns per CTA on small n
+  if ((int64_t)blocks * min_cols > n) blocks = (int)((n + min_cols - 1) / min_cols);
+  if (blocks < 1) blocks = 1;
+  e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned), st);
+  if (e != cudaSuccess) return e;
+  QrcpOut o = out;
+  QrcpWork ww = w;
+  void* args[] = {&Y, &ldy, &l, &n, &k, &tol_rel, &o, &ww};
+  return cudaLaunchCooperativeKernel((void*)k_qrcp<MAXQ>, dim3(blocks), dim3(kQrcpThreads), args, 0,
+                                     st);
+}
+
+cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, double tol_rel,
+                 const QrcpOut& out, const QrcpWork& w, int num_sms, cudaStream_t st) {
+  const int li = (int)l, ki = (int)k;
+  const int qneed = (li + 31) / 32;
+#define RID_Q(QV) \
+  if (qneed <= QV) return launch_qrcp<QV>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st);
+  RID_Q(1) RID_Q(2) RID_Q(3) RID_Q(4) RID_Q(5) RID_Q(6) RID_Q(8) RID_Q(9) RID_Q(12) RID_Q(17)
+  RID_Q(24) RID_Q(32)
+#undef RID_Q
+  return cudaErrorInvalidValue;  // l > 1024 unsupported
+}
+
+// ---------------------------------------------------------------------------------------------
+// Inverse of R11 (upper triangular, R11[t, s] = Y[t, J[s]] for t < s, R11[s, s] = beta[s]):
+// column c of R11^{-1} by right-looking back-substitution on e_c ("solving Lv = w
+// for triangular L"); one CTA per column, the right-hand side in shared memory.
+// ---------------------------------------------------------------------------------------------
+__global__ void k_tri_inverse(const double2* __restrict__ Y, int64_t ldy,
+                              const int64_t* __restrict__ J, const double* __restrict__ beta,
+                              int k, double2* __restrict__ Rinv) {
+  extern __shared__ double2 bvec[];  // k
+  const int c = blockIdx.x;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) bvec[i] = make_double2(i == c ? 1.0 : 0.0, 0.0);
+  __syncthreads();
+  for (int s = c; s >= 0; --s) {
+    const double d = beta[s];
+    const double2 xs = make_double2(__ddiv_rn(bvec[s].x, d), __ddiv_rn(bvec[s].y, d));
+    const double2* col = Y + J[s] * ldy;  // R11[0:s, s]
+    __syncthreads();
+    for (int i = threadIdx.x; i < s; i += blockDim.x) {
+      const double2 r = col[i];
+      double2 bi = bvec[i];
+      bi.x = __fma_rn(-r.x, xs.x, __fma_rn(r.y, xs.y, bi.x));
+      bi.y = __fma_rn(-r.x, xs.y, __fma_rn(-r.y, xs.x, bi.y));
+      bvec[i] = bi;
+    }
+    if (threadIdx.x == 0) bvec[s] = xs;
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < k; i += blockDim.x)
+    Rinv[(int64_t)c * k + i] = (i <= c) ? bvec[i] : make_double2(0.0, 0.0);
+}
+
+cudaError_t tri_inverse(const double2* Y, int64_t ldy, const int64_t* J, const double* beta,
+                        int64_t k, double2* Rinv, cudaStream_t st) {
+  if (k <= 0) return cudaSuccess;
+  const size_t sm = (size_t)k * sizeof(double2);
+  if (sm > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_tri_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)sm);
+    if (e != cudaSuccess) return e;
+  }
+  k_tri_inverse<<<(unsigned)k, 256, sm, st>>>(Y, ldy, J, beta, (int)k, Rinv);
+  return cudaGetLastError();
+}
+
+}  // namespace rid

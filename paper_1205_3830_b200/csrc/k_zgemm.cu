@@ -1,0 +1,221 @@
+// k_zgemm.cu — the ordered complex128 GEMM on the FP64 tensor pipe (DMMA), used by three steps:
+//   * rid_sketch:    Y  = R · A          (Mout = l,  K = m, N = n_loc)   north_star
+//   * rid_generate:  A  = X · Y0 + ε·E   (Mout = m,  K = k, N = n_loc)   PAPER.md:112; RNG.md §5
+//   * interpolation: T  = R11⁻¹ · R12    (Mout = k,  K = k, N = n_loc)   PAPER.md:88-90 (Eq. 10)
+//
+// Real embedding: a complex product C = Rm·Bm is computed as C̃ᵀ = B̃ᵀ · R̃ᵀ where B̃ is Bm's
+// interleaved (re, im) memory read as a 2K × N real matrix (no copy) and R̃ is the 2×2-block
+// expansion [[re, −im], [im, re]] of Rm built on the fly from Rm's own bits. The MMA's M dimension
+// is the column index j, its N dimension the real row index r̃ = 2r + {re, im}, so each lane's
+// accumulator pair {c0, c1} is exactly one complex output (re, im) — stored as one 16-byte write.
+//
+// Order: every output element is ONE fused-multiply-add chain over the real K index in ascending
+// order (DMMA.8x8x4 is that chain, bit for bit — measured, profiles/r01_box_facts_*.txt), starting
+// from +0. For the sketch and the generation this is exactly the order of docs/RNG.md §5/§6, so
+// the results are bit-identical to the oracle's naive loops. No split-K: the K loop is sequential.
+//
+// Pipeline: STAGES-deep cp.async (LDGSTS) ring into padded shared memory (B̃ pitch ≡ 4 mod 16
+// doubles and R pitch ≡ 4 mod 8 complex make every fragment load a single conflict-free
+// wavefront); 8 warps; grid = (r̃-tiles, j-tiles) with r̃ fastest so the CTAs that share an
+// A tile run together and hit L2.
+#include "rid_device.cuh"
+#include "rid_internal.h"
+
+namespace rid {
+
+struct ZgemmEpilogue {
+  int mode;          // 0: C = acc; 1: C = fma(noise, E(i, col0 + j), acc) (generation)
+  double noise;
+  uint64_t seed;
+  int64_t col0;
+};
+
+template <int FJ, int FR, int WARPS_J, int WARPS_R, int BK, int STAGES>
+struct ZgemmCfg {
+  static constexpr int kThreads = WARPS_J * WARPS_R * 32;
+  static constexpr int BJ = WARPS_J * FJ * 8;   // columns per CTA
+  static constexpr int BR = WARPS_R * FR * 8;   // real rows per CTA
+  static constexpr int BRC = BR / 2;            // complex rows per CTA
+  static constexpr int BKC = BK / 2;            // complex K per stage
+  static constexpr int PB = BK + 4;             // doubles; ≡ 4 (mod 16)
+  static constexpr int PR = BRC + ((4 - BRC % 8) % 8 + 8) % 8;  // complex; ≡ 4 (mod 8)
+  static constexpr int kStageB = BJ * PB;        // doubles
+  static constexpr int kStageR = BKC * PR * 2;   // doubles
+  static constexpr int kStage = kStageB + kStageR;
+  static constexpr size_t kSmem = (size_t)STAGES * kStage * sizeof(double);
+  static_assert(BK % 16 == 0, "BK must be a multiple of 16");
+  static_assert(PR % 8 == 4 && PR >= BRC, "R pitch");
+};
+
+template <int FJ, int FR, int WARPS_J, int WARPS_R, int BK, int STAGES>
+__global__ void __launch_bounds__(WARPS_J* WARPS_R * 32, 1)
+    k_zgemm_dmma(const double2* __restrict__ Rm, int64_t ldr, const double2* __restrict__ Bm,
+                 int64_t ldb, double2* __restrict__ C, int64_t ldc, int64_t Mout, int64_t N,
+                 int64_t K, ZgemmEpilogue ep) {
+  using Cfg = ZgemmCfg<FJ, FR, WARPS_J, WARPS_R, BK, STAGES>;
+  extern __shared__ __align__(16) double smem[];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t = lane & 3;
+  const int wj = warp % WARPS_J, wr = warp / WARPS_J;
+  const int64_t r0c = (int64_t)blockIdx.x * Cfg::BRC;  // complex row offset of this CTA
+  const int64_t j0 = (int64_t)blockIdx.y * Cfg::BJ;
+  const int64_t nk = (K + Cfg::BKC - 1) / Cfg::BKC;     // complex-K stages
+
+  auto load_stage = [&](int slot, int64_t kc0) {
+    double* sB = smem + (size_t)slot * Cfg::kStage;
+    double* sR = sB + Cfg::kStageB;
+    // B̃ tile: BJ columns x BKC complex (16 B chunks), K-contiguous per column
+    for (int q = tid; q < Cfg::BJ * Cfg::BKC; q += Cfg::kThreads) {
+      const int col = q / Cfg::BKC, kc = q % Cfg::BKC;
+      const int64_t gj = j0 + col, gk = kc0 + kc;
+      const bool ok = gj < N && gk < K;
+      const double2* src = ok ? Bm + gj * ldb + gk : Bm;
+      cp_async16(sB + col * Cfg::PB + 2 * kc, src, ok);
+    }
+    // R tile: BKC K-columns x BRC complex rows, row-contiguous
+    for (int q = tid; q < Cfg::BKC * Cfg::BRC; q += Cfg::kThreads) {
+      const int kc = q / Cfg::BRC, rr = q % Cfg::BRC;
+      const int64_t gr = r0c + rr, gk = kc0 + kc;
+      const bool ok = gr < Mout && gk < K;
+      const double2* src = ok ? Rm + gk * ldr + gr : Rm;
+      cp_async16(sR + 2 * (kc * Cfg::PR + rr), src, ok);
+    }
+  };
+
+  double acc[FJ][FR][2];
+#pragma unroll
+  for (int a = 0; a < FJ; ++a)
+#pragma unroll
+    for (int b = 0; b < FR; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+  // per-lane constants of the R̃ fragment: element R̃[r̃][κ] with r̃ parity = g&1, κ parity = t&1
+  const int comp = (g & 1) ^ (t & 1);                 // 0 -> re, 1 -> im
+  const unsigned long long sgn = ((g & 1) == 0 && (t & 1) == 1) ? 0x8000000000000000ULL : 0ULL;
+  const int laneR = 2 * ((t >> 1) * Cfg::PR + (g >> 1)) + comp + wr * FR * 8;  // doubles
+  const int laneB = (wj * FJ * 8 + g) * Cfg::PB + t;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nk) load_stage(s, (int64_t)s * Cfg::BKC);
+    cp_async_commit();
+  }
+
+  for (int64_t kt = 0; kt < nk; ++kt) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {  // prefetch stage kt + STAGES - 1 into the slot freed by stage kt - 1
+      const int64_t kn = kt + STAGES - 1;
+      if (kn < nk) load_stage((int)(kn % STAGES), kn * Cfg::BKC);
+      cp_async_commit();
+    }
+    const double* sB = smem + (size_t)(kt % STAGES) * Cfg::kStage;
+    const double* sR = sB + Cfg::kStageB;
+#pragma unroll
+    for (int kk = 0; kk < BK / 4; ++kk) {
+      double a[FJ], b[FR];
+#pragma unroll
+      for (int f = 0; f < FJ; ++f) a[f] = sB[laneB + f * 8 * Cfg::PB + kk * 4];
+#pragma unroll
+      for (int f = 0; f < FR; ++f) {
+        const double v = sR[laneR + f * 8 + kk * 4 * Cfg::PR];
+        b[f] = __longlong_as_double(__double_as_longlong(v) ^ sgn);
+      }
+#pragma unroll
+      for (int fa = 0; fa < FJ; ++fa)
+#pragma unroll
+        for (int fb = 0; fb < FR; ++fb) dmma8x8x4(acc[fa][fb][0], acc[fa][fb][1], a[fa], b[fb]);
+    }
+  }
+  cp_async_wait<0>();
+
+  // epilogue: {c0, c1} = (re, im) of C(r, j), r = r0c + wr*FR*4 + f*4 + t, j = j0 + wj*FJ*8 + fa*8 + g
+#pragma unroll
+  for (int fa = 0; fa < FJ; ++fa) {
+    const int64_t j = j0 + wj * FJ * 8 + fa * 8 + g;
+    if (j >= N) continue;
+#pragma unroll
+    for (int fb = 0; fb < FR; ++fb) {
+      const int64_t r = r0c + wr * FR * 4 + fb * 4 + t;
+      if (r >= Mout) continue;
+      C[j * ldc + r] = make_double2(acc[fa][fb][0], acc[fa][fb][1]);
+    }
+  }
+  if (ep.mode == 1) {
+    // generation: A = fma(noise, E, X·Y0) per component, E(i, j) = N(seed, 3, i, col0 + j).
+    // A second, rolled pass over this thread's own outputs (just written, L1/L2-hot) keeps the
+    // accumulator registers free of the Philox/normal code.
+#pragma unroll 1
+    for (int q = 0; q < FJ * FR; ++q) {
+      const int fa = q / FR, fb = q % FR;
+      const int64_t j = j0 + wj * FJ * 8 + fa * 8 + g;
+      const int64_t r = r0c + wr * FR * 4 + fb * 4 + t;
+      if (j >= N || r >= Mout) continue;
+      double2* cp = C + j * ldc + r;
+      const double2 a = *cp;
+      const double2 e = rid_normal(ep.seed, 3u, (uint32_t)r, (uint32_t)(ep.col0 + j));
+      *cp = make_double2(__fma_rn(ep.noise, e.x, a.x), __fma_rn(ep.noise, e.y, a.y));
+    }
+  }
+}
+
+template <int FJ, int FR, int WARPS_J, int WARPS_R, int BK, int STAGES>
+static cudaError_t launch_cfg(const double2* Rm, int64_t ldr, const double2* Bm, int64_t ldb,
+                              double2* C, int64_t ldc, int64_t Mout, int64_t N, int64_t K,
+                              const ZgemmEpilogue& ep, cudaStream_t st) {
+  using Cfg = ZgemmCfg<FJ, FR, WARPS_J, WARPS_R, BK, STAGES>;
+  auto kern = k_zgemm_dmma<FJ, FR, WARPS_J, WARPS_R, BK, STAGES>;
+  static bool attr_set = false;  // per-instantiation, set once per process
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)Cfg::kSmem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int64_t tiles_r = (Mout + Cfg::BRC - 1) / Cfg::BRC;
+  const int64_t tiles_j = (N + Cfg::BJ - 1) / Cfg::BJ;
+  if (tiles_r > 0x7FFFFFFF || tiles_j > 65535) return cudaErrorInvalidConfiguration;
+  dim3 grid((unsigned)tiles_r, (unsigned)tiles_j);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep);
+  return cudaGetLastError();
+}
+
+// Tile choice: 2*Mout real rows are covered by tiles of BR = 16*FR rows (FJ = 2, 4x2 warps,
+// BJ = 64 columns); FR is picked to minimise padded rows (every padded row is wasted DMMA work),
+// ties -> larger FR (fewer A re-reads). Large Mout (generation) uses 128x128 tiles.
+#define RID_FR_LIST(X) X(3) X(4) X(5) X(6) X(8) X(9) X(10) X(11) X(12) X(17)
+
+int zgemm_pick_fr(int64_t Mout) {
+  const int64_t rows = 2 * Mout;
+  int best = -1;
+  int64_t best_waste = INT64_MAX;
+#define RID_TRY(FRV)                                                             \
+  {                                                                              \
+    const int64_t br = 16 * (FRV);                                               \
+    const int64_t waste = ((rows + br - 1) / br) * br - rows;                    \
+    if (waste < best_waste || (waste == best_waste && (FRV) > best)) {           \
+      best_waste = waste;                                                        \
+      best = (FRV);                                                              \
+    }                                                                            \
+  }
+  RID_FR_LIST(RID_TRY)
+#undef RID_TRY
+  return best;
+}
+
+cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int64_t ldb,
+                          double2* C, int64_t ldc, int64_t Mout, int64_t N, int64_t K,
+                          int mode, double noise, uint64_t seed, int64_t col0, cudaStream_t st) {
+  if (Mout <= 0 || N <= 0) return cudaSuccess;
+  ZgemmEpilogue ep{mode, noise, seed, col0};
+  if (Mout >= 2048) return launch_cfg<4, 8, 4, 2, 16, 4>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
+  switch (zgemm_pick_fr(Mout)) {
+#define RID_CASE(FRV) \
+  case FRV: return launch_cfg<2, FRV, 4, 2, 16, 4>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
+    RID_FR_LIST(RID_CASE)
+#undef RID_CASE
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace rid

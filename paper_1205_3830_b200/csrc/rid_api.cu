@@ -1,0 +1,614 @@
+// rid_api.cu — the C ABI of include/rid.h: argument checking, workspace, host staging, phase
+// timing, NCCL plumbing, and the orchestration of the kernels in k_*.cu. No arithmetic of the
+// method runs on the host.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/rid.h"
+#include "rid_internal.h"
+
+struct rid_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool owns_stream = false;
+  int num_sms = 148;
+  std::string err;
+  struct Buf {
+    void* p = nullptr;
+    size_t bytes = 0;
+  };
+  std::map<std::string, Buf> ws;
+  ncclComm_t comm = nullptr;
+  int rank = 0, nranks = 1;
+  cudaEvent_t ev[12] = {};
+};
+
+namespace {
+
+rid_status fail(rid_ctx* c, rid_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return st;
+}
+
+#define RID_CUDA(c, expr)                                                                    \
+  do {                                                                                       \
+    cudaError_t e__ = (expr);                                                                \
+    if (e__ != cudaSuccess)                                                                  \
+      return fail((c), e__ == cudaErrorMemoryAllocation ? RID_ENOMEM : RID_ECUDA,            \
+                  "%s: %s (%s:%d)", #expr, cudaGetErrorString(e__), __FILE__, __LINE__);     \
+  } while (0)
+
+#define RID_NCCL(c, expr)                                                                    \
+  do {                                                                                       \
+    ncclResult_t r__ = (expr);                                                               \
+    if (r__ != ncclSuccess)                                                                  \
+      return fail((c), RID_ENCCL, "%s: %s", #expr, ncclGetErrorString(r__));                 \
+  } while (0)
+
+#define RID_TRY(expr)                 \
+  do {                                \
+    rid_status s__ = (expr);          \
+    if (s__ != RID_OK) return s__;    \
+  } while (0)
+
+rid_status ws_get(rid_ctx* c, const char* name, size_t bytes, void** out) {
+  auto& b = c->ws[name];
+  if (b.bytes < bytes) {
+    if (b.p) {
+      RID_CUDA(c, cudaStreamSynchronize(c->stream));
+      RID_CUDA(c, cudaFree(b.p));
+      b.p = nullptr;
+      b.bytes = 0;
+    }
+    cudaError_t e = cudaMalloc(&b.p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(c, RID_ENOMEM, "workspace '%s': cudaMalloc(%zu) failed: %s", name, bytes,
+                  cudaGetErrorString(e));
+    }
+    b.bytes = bytes;
+  }
+  *out = b.p;
+  return RID_OK;
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+// A matrix argument: device pointer used in place, or a host buffer staged in workspace.
+struct MatArg {
+  void* dev = nullptr;
+  bool host = false;
+};
+
+rid_status stage_in(rid_ctx* c, const char* name, const void* user, size_t rows, size_t cols,
+                    size_t ld, size_t elem, bool copy, MatArg* out) {
+  out->host = !is_device_ptr(user);
+  if (!out->host) {
+    out->dev = const_cast<void*>(user);
+    return RID_OK;
+  }
+  const size_t bytes = (cols == 0 ? 0 : ((cols - 1) * ld + rows)) * elem;
+  RID_TRY(ws_get(c, name, bytes ? bytes : elem, &out->dev));
+  if (copy && bytes)
+    RID_CUDA(c, cudaMemcpyAsync(out->dev, user, bytes, cudaMemcpyHostToDevice, c->stream));
+  return RID_OK;
+}
+
+rid_status stage_out(rid_ctx* c, const MatArg& a, void* user, size_t rows, size_t cols, size_t ld,
+                     size_t elem) {
+  if (!a.host) return RID_OK;
+  const size_t bytes = (cols == 0 ? 0 : ((cols - 1) * ld + rows)) * elem;
+  if (bytes) RID_CUDA(c, cudaMemcpyAsync(user, a.dev, bytes, cudaMemcpyDeviceToHost, c->stream));
+  return RID_OK;
+}
+
+rid_status check_ctx(rid_ctx* c) {
+  if (!c) return RID_EINVAL;
+  c->err.clear();
+  RID_CUDA(c, cudaSetDevice(c->device));
+  return RID_OK;
+}
+
+float ev_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  if (cudaEventElapsedTime(&ms, a, b) != cudaSuccess) {
+    cudaGetLastError();
+    return 0.f;
+  }
+  return ms;
+}
+
+constexpr double kRankTol = 1e-13;   // reading R13
+constexpr double kSingTol = 1e-13;
+constexpr uint32_t kStreamR = 4, kStreamRRetry = 20;
+
+// Factor the full sketch in workspace "Y" and solve for the local shard columns.
+// On entry Yw holds the full l x n sketch (ld = l). Writes J (device ws), P_loc (device).
+rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64_t k, int64_t col0,
+                            int64_t n_loc, double2* Pdev, int64_t ldp, int64_t** Jdev_out,
+                            int* info_host, rid_diag* diag, bool solve, double** beta_out) {
+  void *pJ, *pbeta, *presid, *pmargin, *pinfo, *pwork;
+  RID_TRY(ws_get(c, "J", sizeof(int64_t) * k, &pJ));
+  RID_TRY(ws_get(c, "beta", sizeof(double) * k, &pbeta));
+  RID_TRY(ws_get(c, "resid", sizeof(double) * k, &presid));
+  RID_TRY(ws_get(c, "margin", sizeof(double) * k, &pmargin));
+  RID_TRY(ws_get(c, "info", sizeof(int) * 2, &pinfo));
+  const int max_blocks = 4 * c->num_sms;
+  RID_TRY(ws_get(c, "qrcp_work", rid::qrcp_work_bytes(n, max_blocks), &pwork));
+  rid::QrcpOut o{(int64_t*)pJ, (double*)pbeta, (double*)presid, (double*)pmargin, (int*)pinfo};
+  char* wb = (char*)pwork;
+  rid::QrcpWork w{(double*)wb, (double*)(wb + sizeof(double) * n), nullptr, max_blocks};
+  w.bar = (unsigned*)(wb + sizeof(double) * n + sizeof(double) * 2 * 3 * max_blocks);
+  RID_CUDA(c, rid::qrcp(Yw, l, l, n, k, kRankTol, o, w, c->num_sms, c->stream));
+  // one synchronisation: rank status, R11 diagonal (singularity), diagnostics
+  std::vector<double> hb(k), hr(k), hm(k);
+  RID_CUDA(c, cudaMemcpyAsync(info_host, pinfo, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->stream));
+  RID_CUDA(c, cudaMemcpyAsync(hb.data(), pbeta, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+  RID_CUDA(c, cudaMemcpyAsync(hr.data(), presid, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+  RID_CUDA(c, cudaMemcpyAsync(hm.data(), pmargin, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+  RID_CUDA(c, cudaStreamSynchronize(c->stream));
+  *Jdev_out = (int64_t*)pJ;
+  if (beta_out) *beta_out = (double*)pbeta;
+  if (diag) {
+    const int kk = info_host[0] == 0 ? (int)k : info_host[1];
+    double mm = INFINITY;
+    for (int j = 0; j + 1 < kk; ++j) mm = std::fmin(mm, hm[j]);
+    diag->tie_margin_min = mm;
+    diag->rank_achieved = info_host[0] == 0 ? (int)k : info_host[1];
+    diag->resid_last = kk > 0 ? hr[kk - 1] : 0.0;
+  }
+  if (info_host[0] != 0) return RID_ERANK;
+  double dmax = 0.0;
+  for (int64_t t = 0; t < k; ++t) dmax = std::fmax(dmax, std::fabs(hb[t]));
+  for (int64_t t = 0; t < k; ++t)
+    if (std::fabs(hb[t]) < kSingTol * dmax)
+      return fail(c, RID_ESINGULAR, "R11[%lld,%lld] = %g below 1e-13 * %g", (long long)t,
+                  (long long)t, hb[t], dmax);
+  if (!solve) return RID_OK;
+  void* pRinv;
+  RID_TRY(ws_get(c, "Rinv", sizeof(double2) * k * k, &pRinv));
+  RID_CUDA(c, rid::tri_inverse(Yw, l, (const int64_t*)pJ, (const double*)pbeta, k,
+                               (double2*)pRinv, c->stream));
+  RID_CUDA(c, rid::zgemm_ordered((const double2*)pRinv, k, Yw + col0 * l, l, Pdev, ldp, k, n_loc,
+                                 k, 0, 0.0, 0, 0, c->stream));
+  RID_CUDA(c, rid::assemble_identity((const int64_t*)pJ, k, col0, n_loc, Pdev, ldp, c->stream));
+  return RID_OK;
+}
+
+__global__ void k_extract_R(const double2* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ J,
+                            const double* __restrict__ beta, int64_t k, int64_t n,
+                            double2* __restrict__ R, int64_t ldr) {
+  // R[:, c] = Y[0:k, c] for non-pivot c; for c = J[s]: rows < s from Y, row s = beta[s], rows > s 0
+  const int64_t c = blockIdx.x;
+  __shared__ int64_t s_piv;
+  if (threadIdx.x == 0) {
+    s_piv = -1;
+    for (int64_t s = 0; s < k; ++s)
+      if (J[s] == c) s_piv = s;
+  }
+  __syncthreads();
+  const int64_t s = s_piv;
+  for (int64_t t = threadIdx.x; t < k; t += blockDim.x) {
+    double2 v = Y[c * ldy + t];
+    if (s >= 0) {
+      if (t == s) v = make_double2(beta[s], 0.0);
+      else if (t > s) v = make_double2(0.0, 0.0);
+    }
+    R[c * ldr + t] = v;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rid_version(void) { return "librid 0.1 (sm_100a, DMMA fp64 tensor pipe)"; }
+
+rid_status rid_create(rid_ctx** out, int device, void* cuda_stream) {
+  if (!out) return RID_EINVAL;
+  *out = nullptr;
+  rid_ctx* c = new rid_ctx();
+  c->device = device;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) {
+    delete c;
+    return RID_ECUDA;
+  }
+  c->stream = (cudaStream_t)cuda_stream;  // NULL = the legacy default stream, as in CUDA
+  cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
+  for (auto& ev : c->ev) cudaEventCreate(&ev);
+  *out = c;
+  return RID_OK;
+}
+
+void rid_destroy(rid_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->stream);
+  for (auto& kv : c->ws)
+    if (kv.second.p) cudaFree(kv.second.p);
+  for (auto& ev : c->ev)
+    if (ev) cudaEventDestroy(ev);
+  if (c->comm) ncclCommDestroy(c->comm);
+  if (c->owns_stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+const char* rid_last_error(const rid_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+size_t rid_comm_id_bytes(void) { return sizeof(ncclUniqueId); }
+
+rid_status rid_comm_get_id(void* id) {
+  if (!id) return RID_EINVAL;
+  ncclUniqueId u;
+  if (ncclGetUniqueId(&u) != ncclSuccess) return RID_ENCCL;
+  std::memcpy(id, &u, sizeof u);
+  return RID_OK;
+}
+
+rid_status rid_comm_init(rid_ctx* c, const void* id, int rank, int nranks) {
+  RID_TRY(check_ctx(c));
+  if (!id || nranks < 1 || rank < 0 || rank >= nranks)
+    return fail(c, RID_EINVAL, "rid_comm_init: bad rank %d / nranks %d", rank, nranks);
+  if (c->comm) {
+    ncclCommDestroy(c->comm);
+    c->comm = nullptr;
+  }
+  if (nranks > 1) {
+    ncclUniqueId u;
+    std::memcpy(&u, id, sizeof u);
+    RID_NCCL(c, ncclCommInitRank(&c->comm, nranks, u, rank));
+  }
+  c->rank = rank;
+  c->nranks = nranks;
+  return RID_OK;
+}
+
+rid_status rid_comm_info(const rid_ctx* c, int* rank, int* nranks) {
+  if (!c) return RID_EINVAL;
+  if (rank) *rank = c->rank;
+  if (nranks) *nranks = c->nranks;
+  return RID_OK;
+}
+
+double rid_error_bound(int64_t m, int64_t n, int64_t k, double eps, double sigma_kp1) {
+  if (m < 1 || n < 1 || k < 1 || !(eps > 0.0) || eps > 1.0) return NAN;
+  return 50.0 * std::sqrt((double)m * (double)n) * std::pow(1.0 / eps, 1.0 / (double)k) * sigma_kp1;
+}
+
+rid_status rid_normal_fill(rid_ctx* c, uint64_t seed, uint32_t s, int64_t rows, int64_t cols,
+                           int64_t row0, int64_t col0, rid_z* out, int64_t ld) {
+  RID_TRY(check_ctx(c));
+  if (rows < 0 || cols < 0 || row0 < 0 || col0 < 0 || ld < rows || !out ||
+      row0 + rows > (int64_t)0xFFFFFFFFLL || col0 + cols > (int64_t)0xFFFFFFFFLL)
+    return fail(c, RID_EINVAL, "rid_normal_fill: bad shape");
+  MatArg o;
+  RID_TRY(stage_in(c, "stage_out0", out, rows, cols, ld, sizeof(rid_z), false, &o));
+  RID_CUDA(c, rid::normal_fill(seed, s, rows, cols, row0, col0, (double2*)o.dev, ld, c->stream));
+  RID_TRY(stage_out(c, o, out, rows, cols, ld, sizeof(rid_z)));
+  if (o.host) RID_CUDA(c, cudaStreamSynchronize(c->stream));
+  return RID_OK;
+}
+
+rid_status rid_generate(rid_ctx* c, uint64_t seed, int64_t m, int64_t n, int64_t k, double noise,
+                        int64_t col0, int64_t n_loc, rid_z* A, int64_t lda) {
+  RID_TRY(check_ctx(c));
+  if (m < 1 || n < 1 || k < 1 || k > m || k > n || col0 < 0 || n_loc < 0 || col0 + n_loc > n ||
+      lda < m || !A || m > (int64_t)0xFFFFFFFFLL || n > (int64_t)0xFFFFFFFFLL || !std::isfinite(noise))
+    return fail(c, RID_EINVAL, "rid_generate: bad arguments (m=%lld n=%lld k=%lld col0=%lld n_loc=%lld lda=%lld)",
+                (long long)m, (long long)n, (long long)k, (long long)col0, (long long)n_loc, (long long)lda);
+  if (n_loc == 0) return RID_OK;
+  MatArg a;
+  RID_TRY(stage_in(c, "stage_A", A, m, n_loc, lda, sizeof(rid_z), false, &a));
+  void *pX, *pY0;
+  RID_TRY(ws_get(c, "X", sizeof(double2) * m * k, &pX));
+  RID_TRY(ws_get(c, "Y0", sizeof(double2) * k * n_loc, &pY0));
+  RID_CUDA(c, rid::normal_fill(seed, 1u, m, k, 0, 0, (double2*)pX, m, c->stream));
+  RID_CUDA(c, rid::normal_fill(seed, 2u, k, n_loc, 0, col0, (double2*)pY0, k, c->stream));
+  RID_CUDA(c, rid::zgemm_ordered((const double2*)pX, m, (const double2*)pY0, k, (double2*)a.dev, lda,
+                                 m, n_loc, k, noise != 0.0 ? 1 : 0, noise, seed, col0, c->stream));
+  RID_TRY(stage_out(c, a, A, m, n_loc, lda, sizeof(rid_z)));
+  if (a.host) RID_CUDA(c, cudaStreamSynchronize(c->stream));
+  return RID_OK;
+}
+
+rid_status rid_sketch(rid_ctx* c, uint64_t seed, uint32_t stream, int64_t l, const rid_z* A,
+                      int64_t m, int64_t n_loc, int64_t lda, rid_z* Y, int64_t ldy) {
+  RID_TRY(check_ctx(c));
+  if (l < 1 || l > m || m < 1 || n_loc < 0 || lda < m || ldy < l || !A || !Y ||
+      m > (int64_t)0xFFFFFFFFLL)
+    return fail(c, RID_EINVAL, "rid_sketch: bad arguments");
+  if (n_loc == 0) return RID_OK;
+  MatArg a, y;
+  RID_TRY(stage_in(c, "stage_A", A, m, n_loc, lda, sizeof(rid_z), true, &a));
+  RID_TRY(stage_in(c, "stage_Y", Y, l, n_loc, ldy, sizeof(rid_z), false, &y));
+  void* pR;
+  RID_TRY(ws_get(c, "R", sizeof(double2) * l * m, &pR));
+  RID_CUDA(c, rid::normal_fill(seed, stream, l, m, 0, 0, (double2*)pR, l, c->stream));
+  RID_CUDA(c, rid::zgemm_ordered((const double2*)pR, l, (const double2*)a.dev, lda, (double2*)y.dev,
+                                 ldy, l, n_loc, m, 0, 0.0, 0, 0, c->stream));
+  RID_TRY(stage_out(c, y, Y, l, n_loc, ldy, sizeof(rid_z)));
+  if (a.host || y.host) RID_CUDA(c, cudaStreamSynchronize(c->stream));
+  return RID_OK;
+}
+
+rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64_t col0,
+                         int64_t n_loc, int64_t lda, int64_t k, int64_t l, uint64_t seed,
+                         int64_t* J, rid_z* P, int64_t ldp, rid_diag* diag) {
+  RID_TRY(check_ctx(c));
+  if (m < 1 || n < 1 || k < 1 || k > m || k > n || l < k || l > m || l > 1024 || col0 < 0 ||
+      n_loc < 1 || col0 + n_loc > n || lda < m || ldp < k || !A || !J || !P ||
+      m > (int64_t)0xFFFFFFFFLL)
+    return fail(c, RID_EINVAL, "rid_decompose: bad arguments (m=%lld n=%lld k=%lld l=%lld col0=%lld n_loc=%lld)",
+                (long long)m, (long long)n, (long long)k, (long long)l, (long long)col0, (long long)n_loc);
+  if (c->nranks > 1 && (n_loc * c->nranks != n || col0 != n_loc * c->rank))
+    return fail(c, RID_EINVAL, "rid_decompose: shard (%lld, %lld) is not rank %d's 1/%d of n=%lld",
+                (long long)col0, (long long)n_loc, c->rank, c->nranks, (long long)n);
+  if (c->nranks == 1 && (col0 != 0 || n_loc != n))
+    return fail(c, RID_EINVAL, "rid_decompose: without a communicator the shard must be all of A");
+  rid_diag d{};
+  cudaEvent_t* ev = c->ev;
+  RID_CUDA(c, cudaEventRecord(ev[0], c->stream));
+  MatArg a, p;
+  RID_TRY(stage_in(c, "stage_A", A, m, n_loc, lda, sizeof(rid_z), true, &a));
+  RID_TRY(stage_in(c, "stage_P", P, k, n_loc, ldp, sizeof(rid_z), false, &p));
+  RID_CUDA(c, cudaEventRecord(ev[1], c->stream));
+  void *pY, *pR;
+  RID_TRY(ws_get(c, "Y", sizeof(double2) * l * n, &pY));
+  RID_TRY(ws_get(c, "R", sizeof(double2) * l * m, &pR));
+  double2* Yw = (double2*)pY;
+  int64_t* Jdev = nullptr;
+  rid_status st = RID_OK;
+  int info[2] = {0, 0};
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    const uint32_t sR = attempt == 0 ? kStreamR : kStreamRRetry;
+    RID_CUDA(c, cudaEventRecord(ev[2], c->stream));
+    RID_CUDA(c, rid::normal_fill(seed, sR, l, m, 0, 0, (double2*)pR, l, c->stream));
+    RID_CUDA(c, cudaEventRecord(ev[3], c->stream));
+    d.launches += 3;  // R fill, sketch GEMM, QRCP
+    RID_CUDA(c, rid::zgemm_ordered((const double2*)pR, l, (const double2*)a.dev, lda, Yw + col0 * l,
+                                   l, l, n_loc, m, 0, 0.0, 0, 0, c->stream));
+    RID_CUDA(c, cudaEventRecord(ev[4], c->stream));
+    if (c->nranks > 1) {
+      RID_NCCL(c, ncclAllGather(Yw + col0 * l, Yw, (size_t)(2 * l * n_loc), ncclDouble, c->comm,
+                                c->stream));
+    }
+    RID_CUDA(c, cudaEventRecord(ev[5], c->stream));
+    st = factor_and_solve(c, Yw, l, n, k, col0, n_loc, (double2*)p.dev, ldp, &Jdev, info, &d,
+                          false, nullptr);
+    RID_CUDA(c, cudaEventRecord(ev[6], c->stream));
+    if (st == RID_ERANK && attempt == 0) {
+      d.retries = 1;
+      continue;  // repeat with a different instance of the random matrix
+    }
+    break;
+  }
+  if (st == RID_ERANK) {
+    if (diag) *diag = d;
+    return fail(c, RID_ERANK, "sketch rank %d < k = %lld after one re-randomisation", d.rank_achieved,
+                (long long)k);
+  }
+  if (st != RID_OK) return st;
+  {  // solve
+    void* pbeta;
+    RID_TRY(ws_get(c, "beta", sizeof(double) * k, &pbeta));
+    void* pRinv;
+    RID_TRY(ws_get(c, "Rinv", sizeof(double2) * k * k, &pRinv));
+    RID_CUDA(c, rid::tri_inverse(Yw, l, Jdev, (const double*)pbeta, k, (double2*)pRinv, c->stream));
+    RID_CUDA(c, rid::zgemm_ordered((const double2*)pRinv, k, Yw + col0 * l, l, (double2*)p.dev, ldp,
+                                   k, n_loc, k, 0, 0.0, 0, 0, c->stream));
+    RID_CUDA(c, rid::assemble_identity(Jdev, k, col0, n_loc, (double2*)p.dev, ldp, c->stream));
+    d.launches += 3;  // R11^-1, T GEMM, identity block
+  }
+  RID_CUDA(c, cudaEventRecord(ev[7], c->stream));
+  RID_TRY(stage_out(c, p, P, k, n_loc, ldp, sizeof(rid_z)));
+  if (is_device_ptr(J))
+    RID_CUDA(c, cudaMemcpyAsync(J, Jdev, sizeof(int64_t) * k, cudaMemcpyDeviceToDevice, c->stream));
+  else
+    RID_CUDA(c, cudaMemcpyAsync(J, Jdev, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, c->stream));
+  RID_CUDA(c, cudaEventRecord(ev[8], c->stream));
+  RID_CUDA(c, cudaEventSynchronize(ev[8]));
+  if (diag) {
+    d.t_h2d = ev_ms(ev[0], ev[1]) * 1e-3;
+    d.t_rgen = ev_ms(ev[2], ev[3]) * 1e-3;
+    d.t_sketch = ev_ms(ev[3], ev[4]) * 1e-3;
+    d.t_gather = ev_ms(ev[4], ev[5]) * 1e-3;
+    d.t_qrcp = ev_ms(ev[5], ev[6]) * 1e-3;
+    d.t_solve = ev_ms(ev[6], ev[7]) * 1e-3;
+    d.t_d2h = ev_ms(ev[7], ev[8]) * 1e-3;
+    d.t_total = ev_ms(ev[0], ev[8]) * 1e-3;
+    *diag = d;
+  }
+  return RID_OK;
+}
+
+rid_status rid_qrcp(rid_ctx* c, const rid_z* Y, int64_t l, int64_t n, int64_t ldy, int64_t k,
+                    int64_t* J, rid_z* R, int64_t ldr, double* resid, double* margin,
+                    rid_diag* diag) {
+  RID_TRY(check_ctx(c));
+  if (l < 1 || n < 1 || k < 1 || k > l || k > n || l > 1024 || ldy < l || !Y || !J ||
+      (R && ldr < k))
+    return fail(c, RID_EINVAL, "rid_qrcp: bad arguments");
+  MatArg y;
+  RID_TRY(stage_in(c, "stage_Yin", Y, l, n, ldy, sizeof(rid_z), true, &y));
+  void* pY;
+  RID_TRY(ws_get(c, "Y", sizeof(double2) * l * n, &pY));
+  RID_CUDA(c, cudaMemcpy2DAsync(pY, sizeof(double2) * l, y.dev, sizeof(double2) * ldy,
+                                sizeof(double2) * l, n, cudaMemcpyDeviceToDevice, c->stream));
+  int64_t* Jdev = nullptr;
+  int info[2];
+  rid_diag d{};
+  double* beta = nullptr;
+  rid_status st = factor_and_solve(c, (double2*)pY, l, n, k, 0, n, nullptr, k, &Jdev, info, &d,
+                                   false, &beta);
+  if (diag) *diag = d;
+  if (st != RID_OK) return st;
+  const bool jdev = is_device_ptr(J);
+  RID_CUDA(c, cudaMemcpyAsync(J, Jdev, sizeof(int64_t) * k,
+                              jdev ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, c->stream));
+  if (R) {
+    MatArg r;
+    RID_TRY(stage_in(c, "stage_R", R, k, n, ldr, sizeof(rid_z), false, &r));
+    k_extract_R<<<(unsigned)n, 128, 0, c->stream>>>((const double2*)pY, l, Jdev, beta, k, n,
+                                                     (double2*)r.dev, ldr);
+    RID_CUDA(c, cudaGetLastError());
+    RID_TRY(stage_out(c, r, R, k, n, ldr, sizeof(rid_z)));
+  }
+  void *presid, *pmargin;
+  RID_TRY(ws_get(c, "resid", sizeof(double) * k, &presid));
+  RID_TRY(ws_get(c, "margin", sizeof(double) * k, &pmargin));
+  if (resid)
+    RID_CUDA(c, cudaMemcpyAsync(resid, presid, sizeof(double) * k, cudaMemcpyDefault, c->stream));
+  if (margin)
+    RID_CUDA(c, cudaMemcpyAsync(margin, pmargin, sizeof(double) * k, cudaMemcpyDefault, c->stream));
+  RID_CUDA(c, cudaStreamSynchronize(c->stream));
+  return RID_OK;
+}
+
+rid_status rid_factor_solve(rid_ctx* c, const rid_z* Y, int64_t l, int64_t n, int64_t ldy,
+                            int64_t k, int64_t col0, int64_t n_loc, int64_t* J, rid_z* P,
+                            int64_t ldp, rid_diag* diag) {
+  RID_TRY(check_ctx(c));
+  if (l < 1 || n < 1 || k < 1 || k > l || k > n || l > 1024 || ldy < l || !Y || !J || !P ||
+      col0 < 0 || n_loc < 1 || col0 + n_loc > n || ldp < k)
+    return fail(c, RID_EINVAL, "rid_factor_solve: bad arguments");
+  MatArg y, p;
+  RID_TRY(stage_in(c, "stage_Yin", Y, l, n, ldy, sizeof(rid_z), true, &y));
+  RID_TRY(stage_in(c, "stage_P", P, k, n_loc, ldp, sizeof(rid_z), false, &p));
+  void* pY;
+  RID_TRY(ws_get(c, "Y", sizeof(double2) * l * n, &pY));
+  RID_CUDA(c, cudaMemcpy2DAsync(pY, sizeof(double2) * l, y.dev, sizeof(double2) * ldy,
+                                sizeof(double2) * l, n, cudaMemcpyDeviceToDevice, c->stream));
+  int64_t* Jdev = nullptr;
+  int info[2];
+  rid_diag d{};
+  rid_status st = factor_and_solve(c, (double2*)pY, l, n, k, col0, n_loc, (double2*)p.dev, ldp,
+                                   &Jdev, info, &d, true, nullptr);
+  if (diag) *diag = d;
+  if (st != RID_OK) return st;
+  RID_TRY(stage_out(c, p, P, k, n_loc, ldp, sizeof(rid_z)));
+  RID_CUDA(c, cudaMemcpyAsync(J, Jdev, sizeof(int64_t) * k, cudaMemcpyDefault, c->stream));
+  RID_CUDA(c, cudaStreamSynchronize(c->stream));
+  return RID_OK;
+}
+
+rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64_t col0,
+                              int64_t n_loc, int64_t lda, const int64_t* J, int64_t k,
+                              const rid_z* P, int64_t ldp, int q, uint64_t seed, double* est,
+                              rid_diag* diag) {
+  RID_TRY(check_ctx(c));
+  if (m < 1 || n < 1 || k < 1 || k > n || col0 < 0 || n_loc < 1 || col0 + n_loc > n || lda < m ||
+      ldp < k || q < 1 || !A || !J || !P || !est || n > (int64_t)0xFFFFFFFFLL)
+    return fail(c, RID_EINVAL, "rid_error_estimate: bad arguments");
+  if (c->nranks > 1 && (n_loc * c->nranks != n || col0 != n_loc * c->rank))
+    return fail(c, RID_EINVAL, "rid_error_estimate: shard is not rank %d's 1/%d", c->rank, c->nranks);
+  if (c->nranks == 1 && (col0 != 0 || n_loc != n))
+    return fail(c, RID_EINVAL, "rid_error_estimate: without a communicator the shard must be all of A");
+  const int G = c->nranks;
+  cudaEvent_t* ev = c->ev;
+  RID_CUDA(c, cudaEventRecord(ev[0], c->stream));
+  MatArg a, p;
+  RID_TRY(stage_in(c, "stage_A", A, m, n_loc, lda, sizeof(rid_z), true, &a));
+  RID_TRY(stage_in(c, "stage_P", P, k, n_loc, ldp, sizeof(rid_z), true, &p));
+  void *pJ, *pB, *px, *pz, *py, *pu, *psb, *ppx, *pax, *pwall, *pnp, *pnn, *pest;
+  RID_TRY(ws_get(c, "estJ", sizeof(int64_t) * k, &pJ));
+  RID_CUDA(c, cudaMemcpyAsync(pJ, J, sizeof(int64_t) * k, cudaMemcpyDefault, c->stream));
+  const rid::EstPlan pl = rid::est_plan(m, n_loc, k, c->num_sms);
+  RID_TRY(ws_get(c, "estB", sizeof(double2) * m * k, &pB));
+  RID_TRY(ws_get(c, "estx", sizeof(double2) * n_loc, &px));
+  RID_TRY(ws_get(c, "estz", sizeof(double2) * n_loc, &pz));
+  RID_TRY(ws_get(c, "esty", sizeof(double2) * m, &py));
+  RID_TRY(ws_get(c, "estu", sizeof(double) * 4 * k * G, &pu));
+  RID_TRY(ws_get(c, "estsb", sizeof(double) * 4 * k, &psb));
+  RID_TRY(ws_get(c, "estpx", sizeof(double) * 4 * k * pl.px_parts, &ppx));
+  RID_TRY(ws_get(c, "estax", sizeof(double) * 4 * m * pl.ax_parts, &pax));
+  RID_TRY(ws_get(c, "estwall", sizeof(double) * 4 * m * (G > 1 ? G : 1), &pwall));
+  const int nparts_max = pl.z_blocks > pl.x0_blocks ? pl.z_blocks : pl.x0_blocks;
+  RID_TRY(ws_get(c, "estnp", sizeof(double) * 2 * nparts_max, &pnp));
+  RID_TRY(ws_get(c, "estnn", sizeof(double) * 2 * (G + 1), &pnn));
+  RID_TRY(ws_get(c, "estval", sizeof(double), &pest));
+  double2* B = (double2*)pB;
+  double2 *x = (double2*)px, *z = (double2*)pz, *y = (double2*)py;
+  double *u = (double*)pu, *nn = (double*)pnn;
+  // B = A[:, J], replicated on every rank (owners contribute their columns, the rest are 0)
+  if (G > 1) RID_CUDA(c, cudaMemsetAsync(B, 0, sizeof(double2) * m * k, c->stream));
+  RID_CUDA(c, rid::gather_columns((const double2*)a.dev, lda, m, (const int64_t*)pJ, k, col0, n_loc,
+                                  B, m, c->stream));
+  if (G > 1)
+    RID_NCCL(c, ncclAllReduce(B, B, (size_t)(2 * m * k), ncclDouble, ncclSum, c->comm, c->stream));
+  // reduce a dd scalar over ranks: local parts -> nn[2*rank], allgather, merge -> nn[2*G]
+  auto scalar_allreduce = [&](const double* parts, int nparts) -> rid_status {
+    double* slot = nn + 2 * (G > 1 ? c->rank : 0);
+    RID_CUDA(c, rid::est_merge_scalar(parts, nparts, slot, c->stream));
+    if (G > 1) {
+      RID_NCCL(c, ncclAllGather(slot, nn, 2, ncclDouble, c->comm, c->stream));
+      RID_CUDA(c, rid::est_merge_scalar(nn, G, nn + 2 * G, c->stream));
+    }
+    return RID_OK;
+  };
+  const double* nn_final = nn + (G > 1 ? 2 * G : 0);
+  RID_CUDA(c, rid::est_x0(seed, col0, n_loc, x, (double*)pnp, pl, c->stream));
+  RID_TRY(scalar_allreduce((const double*)pnp, pl.x0_blocks));
+  RID_CUDA(c, rid::est_normalise(x, n_loc, nn_final, x, nullptr, c->stream));
+  RID_CUDA(c, cudaEventRecord(ev[1], c->stream));
+  for (int it = 0; it < q; ++it) {
+    // u = P x (replicated after the exchange)
+    double* u_loc = u + (size_t)4 * k * (G > 1 ? c->rank : 0);
+    RID_CUDA(c, rid::est_px((const double2*)p.dev, ldp, k, n_loc, x, (double*)ppx, u_loc, pl, c->stream));
+    if (G > 1) {
+      RID_NCCL(c, ncclAllGather(u_loc, u, (size_t)(4 * k), ncclDouble, c->comm, c->stream));
+      RID_CUDA(c, rid::est_merge_vec(u, G, k, (double*)psb, c->stream));  // sb as scratch
+      RID_CUDA(c, cudaMemcpyAsync(u, psb, sizeof(double) * 4 * k, cudaMemcpyDeviceToDevice, c->stream));
+    }
+    // y = A x - B u (replicated)
+    RID_CUDA(c, rid::est_ax((const double2*)a.dev, lda, m, n_loc, x, (double*)pax, pl, c->stream));
+    if (G > 1) {
+      double* w_loc = (double*)pwall + (size_t)4 * m * c->rank;
+      RID_CUDA(c, rid::est_merge_vec((const double*)pax, pl.ax_parts, m, w_loc, c->stream));
+      RID_NCCL(c, ncclAllGather(w_loc, pwall, (size_t)(4 * m), ncclDouble, c->comm, c->stream));
+      RID_CUDA(c, rid::est_y((const double*)pwall, G, m, B, m, k, u, y, c->stream));
+    } else {
+      RID_CUDA(c, rid::est_y((const double*)pax, pl.ax_parts, m, B, m, k, u, y, c->stream));
+    }
+    // sb = B^H y ; z = A^H y - P^H sb ; x = z / ||z||
+    RID_CUDA(c, rid::est_bhy(B, m, m, k, y, (double*)psb, c->stream));
+    RID_CUDA(c, rid::est_z((const double2*)a.dev, lda, m, n_loc, y, (const double2*)p.dev, ldp, k,
+                           (const double*)psb, z, (double*)pnp, pl, c->stream));
+    RID_TRY(scalar_allreduce((const double*)pnp, pl.z_blocks));
+    RID_CUDA(c, rid::est_normalise(z, n_loc, nn_final, x, (double*)pest, c->stream));
+  }
+  RID_CUDA(c, cudaEventRecord(ev[2], c->stream));
+  RID_CUDA(c, cudaMemcpyAsync(est, pest, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  RID_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (diag) {
+    rid_diag d{};
+    d.t_total = ev_ms(ev[0], ev[2]) * 1e-3;
+    d.t_h2d = ev_ms(ev[0], ev[1]) * 1e-3;
+    d.launches = 3 + 3 + q * (3 + 4 + (G > 1 ? 2 : 1) + 1);
+    *diag = d;
+  }
+  return RID_OK;
+}
+
+}  // extern "C"

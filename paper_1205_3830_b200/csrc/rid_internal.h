@@ -1,0 +1,78 @@
+// rid_internal.h — internal launchers shared by the CUDA translation units of librid.
+// Not part of the public C ABI (that is include/rid.h).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace rid {
+
+// Ordered complex GEMM C = Rm · Bm on DMMA (k_zgemm.cu). mode 1 adds noise·E(r, col0 + j) with
+// E from Philox stream 3 (generation epilogue).
+cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int64_t ldb,
+                          double2* C, int64_t ldc, int64_t Mout, int64_t N, int64_t K, int mode,
+                          double noise, uint64_t seed, int64_t col0, cudaStream_t st);
+int zgemm_pick_fr(int64_t Mout);
+
+// out(i, j) = N(seed, s, row0 + i, col0 + j), column-major with leading dimension ld (k_misc.cu)
+cudaError_t normal_fill(uint64_t seed, uint32_t s, int64_t rows, int64_t cols, int64_t row0,
+                        int64_t col0, double2* out, int64_t ld, cudaStream_t st);
+
+// Column-pivoted Householder QR of Y (l x n, in place), k steps (k_qrcp.cu).
+struct QrcpOut {
+  int64_t* J;        // device, k
+  double* beta;      // device, k: R11 diagonal (real)
+  double* resid;     // device, k: nu_p at each step
+  double* margin;    // device, k: (nu(1) - nu(2)) / nu(1) at each step
+  int* info;         // device, 2: [0] status (0 ok, 2 rank failure), [1] rank achieved
+};
+struct QrcpWork {
+  double* nu;        // n
+  double* cand;      // 2 * 3 * max_blocks doubles (best, second, index-as-double) x 2 parities
+  unsigned* bar;     // 1
+  int max_blocks;
+};
+size_t qrcp_work_bytes(int64_t n, int max_blocks);
+cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, double tol_rel,
+                 const QrcpOut& out, const QrcpWork& w, int num_sms, cudaStream_t st);
+
+// Inverse of the pivoted triangle R11 (R11[t, s] = Y[t, J[s]] for t < s, beta[s] on the diagonal)
+cudaError_t tri_inverse(const double2* Y, int64_t ldy, const int64_t* J, const double* beta,
+                        int64_t k, double2* Rinv, cudaStream_t st);
+// P[:, J_t - col0] = e_t for pivots inside the shard (k_misc.cu)
+cudaError_t assemble_identity(const int64_t* J, int64_t k, int64_t col0, int64_t n_loc, double2* P,
+                              int64_t ldp, cudaStream_t st);
+// B(:, t) = A(:, J_t - col0) for pivots inside the shard (k_misc.cu)
+cudaError_t gather_columns(const double2* A, int64_t lda, int64_t m, const int64_t* J, int64_t k,
+                           int64_t col0, int64_t n_loc, double2* B, int64_t ldb, cudaStream_t st);
+
+// Compensated power-iteration pieces (k_estimate.cu). Vectors of "cdd" are 4 doubles per entry
+// (re.s, re.c, im.s, im.c): a Dot2 accumulator whose value is s + c.
+struct EstPlan {
+  int64_t px_chunk;
+  int px_parts;
+  int64_t ax_split_cols;
+  int ax_parts;
+  int z_blocks;
+  int x0_blocks;
+};
+EstPlan est_plan(int64_t m, int64_t n_loc, int64_t k, int num_sms);
+cudaError_t est_x0(uint64_t seed, int64_t col0, int64_t n_loc, double2* x, double* part,
+                   const EstPlan& p, cudaStream_t st);
+cudaError_t est_merge_scalar(const double* part, int nparts, double* out, cudaStream_t st);
+cudaError_t est_normalise(const double2* v, int64_t n_loc, const double* nn, double2* x,
+                          double* est_out, cudaStream_t st);
+cudaError_t est_px(const double2* P, int64_t ldp, int64_t k, int64_t n_loc, const double2* x,
+                   double* part, double* u_out, const EstPlan& p, cudaStream_t st);
+cudaError_t est_merge_vec(const double* part, int nparts, int64_t len, double* out,
+                          cudaStream_t st);
+cudaError_t est_ax(const double2* A, int64_t lda, int64_t m, int64_t n_loc, const double2* x,
+                   double* part, const EstPlan& p, cudaStream_t st);
+cudaError_t est_y(const double* wpart, int nparts, int64_t m, const double2* B, int64_t ldb,
+                  int64_t k, const double* u, double2* y, cudaStream_t st);
+cudaError_t est_bhy(const double2* B, int64_t ldb, int64_t m, int64_t k, const double2* y,
+                    double* sb, cudaStream_t st);
+cudaError_t est_z(const double2* A, int64_t lda, int64_t m, int64_t n_loc, const double2* y,
+                  const double2* P, int64_t ldp, int64_t k, const double* sb, double2* z,
+                  double* npart, const EstPlan& p, cudaStream_t st);
+
+}  // namespace rid
