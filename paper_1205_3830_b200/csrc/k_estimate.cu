@@ -93,13 +93,29 @@ __global__ void k_x0(uint64_t seed, int64_t col0, int64_t n_loc, double2* __rest
   }
 }
 
-// merge nparts dd scalars (fixed order) -> out[0..1]
-__global__ void k_merge_scalar(const double* __restrict__ part, int nparts, double* __restrict__ out) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  dd t = {part[0], part[1]};
-  for (int q = 1; q < nparts; ++q) dd_merge(t, dd{part[2 * q], part[2 * q + 1]});
-  out[0] = t.s;
-  out[1] = t.c;
+// merge nparts dd scalars -> out[0..1]; thread i merges parts i, i+256, ... in order, then a
+// fixed-shape tree over the 256 threads (deterministic for a given nparts)
+__global__ void __launch_bounds__(256) k_merge_scalar(const double* __restrict__ part, int nparts,
+                                                      double* __restrict__ out) {
+  __shared__ double ss[256], sc[256];
+  dd t = {0.0, 0.0};
+  for (int q = threadIdx.x; q < nparts; q += 256) dd_merge(t, dd{part[2 * q], part[2 * q + 1]});
+  ss[threadIdx.x] = t.s;
+  sc[threadIdx.x] = t.c;
+  __syncthreads();
+  for (int h = 128; h >= 1; h >>= 1) {
+    if (threadIdx.x < h) {
+      dd a = {ss[threadIdx.x], sc[threadIdx.x]};
+      dd_merge(a, dd{ss[threadIdx.x + h], sc[threadIdx.x + h]});
+      ss[threadIdx.x] = a.s;
+      sc[threadIdx.x] = a.c;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    out[0] = ss[0];
+    out[1] = sc[0];
+  }
 }
 
 // x *= 1 / ||v|| where the norm^2 is the dd in nn[0..1] (x = v / ||v||, one division each)
@@ -254,7 +270,7 @@ __global__ void __launch_bounds__(256) k_z(const double2* __restrict__ A, int64_
 // ------------------------------------------------------------------------------ launchers ------
 EstPlan est_plan(int64_t m, int64_t n_loc, int64_t k, int num_sms) {
   EstPlan p;
-  p.px_chunk = 256;
+  p.px_chunk = 64;
   p.px_parts = (int)((n_loc + p.px_chunk - 1) / p.px_chunk);
   const int64_t row_blocks = (m + 255) / 256;
   int64_t splits = (8 * num_sms + row_blocks - 1) / row_blocks;
@@ -276,7 +292,7 @@ cudaError_t est_x0(uint64_t seed, int64_t col0, int64_t n_loc, double2* x, doubl
   return cudaGetLastError();
 }
 cudaError_t est_merge_scalar(const double* part, int nparts, double* out, cudaStream_t st) {
-  k_merge_scalar<<<1, 32, 0, st>>>(part, nparts, out);
+  k_merge_scalar<<<1, 256, 0, st>>>(part, nparts, out);
   return cudaGetLastError();
 }
 cudaError_t est_normalise(const double2* v, int64_t n_loc, const double* nn, double2* x,
@@ -289,7 +305,7 @@ cudaError_t est_normalise(const double2* v, int64_t n_loc, const double* nn, dou
 }
 cudaError_t est_px(const double2* P, int64_t ldp, int64_t k, int64_t n_loc, const double2* x,
                    double* part, double* u_out, const EstPlan& p, cudaStream_t st) {
-  k_px<<<p.px_parts, 128, 0, st>>>(P, ldp, k, n_loc, x, p.px_chunk, part);
+  k_px<<<p.px_parts, 256, 0, st>>>(P, ldp, k, n_loc, x, p.px_chunk, part);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   k_merge_vec<<<(unsigned)((k + 127) / 128), 128, 0, st>>>(part, p.px_parts, k, u_out);

@@ -9,12 +9,15 @@
 // R11 the residual norms are recomputed exactly from the updated column every step (no
 // downdating); R13 rank failure when nu_p < 1e-13 * max_c ||Y[:, c]||.
 //
-// Layout: every CTA owns a contiguous block of columns; a warp owns a column at a time and keeps
-// its rows j..l-1 in registers (MAXQ complex per lane) while it forms v^H y, applies
-// y <- y - conj(tau) (v^H y) v and recomputes ||y[j+1:l]|| — one read and one write of the
-// trailing column per step. Every CTA rebuilds the same reflector from column p (identical bits:
-// same code, same data, commutative butterfly reductions), so the only cross-CTA exchange is the
-// per-CTA (best, second, index) candidate triple. Output, in place in Y (LAPACK-like):
+// Layout: every CTA owns a contiguous block of columns. A column's trailing segment rows j..l-1
+// is handled by a group of `lpc` lanes (32, 16, 8 or 4 — chosen per step so that each lane holds
+// at most MAXQ rows in registers): while the trailing block shrinks, a warp works on 32/lpc
+// columns at once, so the bytes in flight per warp stay ~constant and late (short) steps do not
+// become latency-bound. Per column: w = v^H y (butterfly within the group), y <- y - conj(tau) w v,
+// nu = ||y[j+1:l]|| recomputed exactly — one read and one write of the trailing segment per step.
+// Every CTA rebuilds the same reflector from column p (identical bits: same code, same data,
+// commutative butterfly reductions), so the only cross-CTA exchange is the per-CTA
+// (best, second, index) candidate triple. Output, in place in Y (LAPACK-like):
 // rows 0..k-1 of every non-pivot column are R12; Y[0:t, J_t] is R11[0:t, t]; beta[t] = R11[t, t].
 #include <cfloat>
 #include <cstdint>
@@ -25,8 +28,8 @@
 namespace rid {
 
 struct Top2 {
-  double b1;   // best value
-  double b2;   // second-best value
+  double b1;     // best value
+  double b2;     // second-best value
   long long i1;  // index of best
 };
 
@@ -66,10 +69,12 @@ __device__ __forceinline__ void top2_warp(Top2& a) {
     top2_merge(a, o);
   }
 }
-// butterfly sum: every lane ends with the same bits (fp addition is commutative)
-__device__ __forceinline__ double warp_sum(double v) {
+// butterfly sum over groups of `lpc` lanes (lpc a power of two): every lane of a group ends with
+// the same bits (fp addition is commutative)
+__device__ __forceinline__ double group_sum(double v, int lpc) {
 #pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, m));
+  for (int m = 16; m >= 1; m >>= 1)
+    if (m < lpc) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, m));
   return v;
 }
 
@@ -93,10 +98,18 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
 constexpr int kQrcpThreads = 256;
 constexpr int kQrcpWarps = kQrcpThreads / 32;
 
+// lanes per column for a trailing segment of `rows` rows: the smallest group that keeps every
+// lane at <= MAXQ rows (more columns per warp as the segment shrinks)
+__device__ __forceinline__ int pick_lpc(int rows, int maxq) {
+  int lpc = 32;
+  while (lpc > 4 && rows <= (lpc / 2) * maxq) lpc >>= 1;
+  return lpc;
+}
+
 template <int MAXQ>
-__global__ void __launch_bounds__(kQrcpThreads) k_qrcp(double2* __restrict__ Y, int64_t ldy, int l,
-                                                       int64_t n, int k, double tol_rel,
-                                                       QrcpOut out, QrcpWork w) {
+__global__ void __launch_bounds__(kQrcpThreads, 2)
+    k_qrcp(double2* __restrict__ Y, int64_t ldy, int l, int64_t n, int k, double tol_rel,
+           QrcpOut out, QrcpWork w) {
   __shared__ double2 sv[MAXQ * 32];
   __shared__ Top2 sred[kQrcpWarps];
   __shared__ double s_tau_re, s_tau_im;
@@ -127,22 +140,26 @@ __global__ void __launch_bounds__(kQrcpThreads) k_qrcp(double2* __restrict__ Y, 
 
   // ---- phase 0: initial column norms --------------------------------------------------------
   {
+    const int lpc = pick_lpc(l, MAXQ);
+    const int cpw = 32 / lpc, sg = lane / lpc, sl = lane % lpc;
     Top2 loc;
     top2_init(loc);
-    for (int64_t c = c_lo + warp; c < c_hi; c += kQrcpWarps) {
+    for (int64_t c0 = c_lo + (int64_t)warp * cpw; c0 < c_hi; c0 += (int64_t)kQrcpWarps * cpw) {
+      const int64_t c = c0 + sg;
+      const bool live = c < c_hi;
       const double2* yc = Y + c * ldy;
       double s = 0.0;
 #pragma unroll
       for (int q = 0; q < MAXQ; ++q) {
-        const int r = lane + 32 * q;
-        if (r < l) {
+        const int r = sl + lpc * q;
+        if (live && r < l) {
           const double2 y = yc[r];
           s = __fma_rn(y.x, y.x, s);
           s = __fma_rn(y.y, y.y, s);
         }
       }
-      const double nu = __dsqrt_rn(warp_sum(s));
-      if (lane == 0) {
+      const double nu = __dsqrt_rn(group_sum(s, lpc));
+      if (live && sl == 0) {
         w.nu[c] = nu;
         top2_push(loc, nu, c);  // one lane per column: the multiset of candidates has no copies
       }
@@ -185,24 +202,23 @@ __global__ void __launch_bounds__(kQrcpThreads) k_qrcp(double2* __restrict__ Y, 
       return;  // every CTA takes the same decision at the same step
     }
     const int64_t p = s_p;
+    const int rows = l - j;
 
     // ---- 2. Householder reflector from x = Y[j:l, p] (LAPACK zlarfg convention) -------------
     if (warp == 0) {
-      const double2* xp = Y + p * ldy;
-      double2 x[MAXQ];
+      const double2* xp = Y + p * ldy + j;
       double s = 0.0;
-#pragma unroll
-      for (int q = 0; q < MAXQ; ++q) {
-        const int r = j + lane + 32 * q;
-        x[q] = (r < l) ? xp[r] : make_double2(0.0, 0.0);
-        if (r > j && r < l) {
-          s = __fma_rn(x[q].x, x[q].x, s);
-          s = __fma_rn(x[q].y, x[q].y, s);
+      for (int rr = lane; rr < rows; rr += 32) {
+        const double2 x = xp[rr];
+        sv[rr] = x;
+        if (rr > 0) {
+          s = __fma_rn(x.x, x.x, s);
+          s = __fma_rn(x.y, x.y, s);
         }
       }
-      const double xnorm2 = warp_sum(s);
-      const double ar = __shfl_sync(0xffffffffu, x[0].x, 0);
-      const double ai = __shfl_sync(0xffffffffu, x[0].y, 0);
+      const double xnorm2 = group_sum(s, 32);
+      __syncwarp();
+      const double ar = sv[0].x, ai = sv[0].y;
       double tau_re, tau_im, beta, sc_re, sc_im;
       if (xnorm2 == 0.0 && ai == 0.0) {
         tau_re = 0.0;
@@ -221,19 +237,17 @@ __global__ void __launch_bounds__(kQrcpThreads) k_qrcp(double2* __restrict__ Y, 
         sc_re = __ddiv_rn(dr, den);
         sc_im = __ddiv_rn(-di, den);
       }
-#pragma unroll
-      for (int q = 0; q < MAXQ; ++q) {
-        const int rr = lane + 32 * q;  // row j + rr
-        if (j + rr < l) {
-          double2 v;
-          if (rr == 0) {
-            v = make_double2(1.0, 0.0);
-          } else {
-            v.x = __fma_rn(x[q].x, sc_re, -__dmul_rn(x[q].y, sc_im));
-            v.y = __fma_rn(x[q].x, sc_im, __dmul_rn(x[q].y, sc_re));
-          }
-          sv[rr] = v;
+      __syncwarp();
+      for (int rr = lane; rr < rows; rr += 32) {
+        double2 v;
+        if (rr == 0) {
+          v = make_double2(1.0, 0.0);
+        } else {
+          const double2 x = sv[rr];
+          v.x = __fma_rn(x.x, sc_re, -__dmul_rn(x.y, sc_im));
+          v.y = __fma_rn(x.x, sc_im, __dmul_rn(x.y, sc_re));
         }
+        sv[rr] = v;
       }
       if (lane == 0) {
         s_tau_re = tau_re;
@@ -245,51 +259,62 @@ __global__ void __launch_bounds__(kQrcpThreads) k_qrcp(double2* __restrict__ Y, 
     const double tr = s_tau_re, ti = s_tau_im;
 
     // ---- 3. apply H^H = I - conj(tau) v v^H to every owned trailing column ------------------
+    const int lpc = pick_lpc(rows, MAXQ);
+    const int cpw = 32 / lpc, sg = lane / lpc, sl = lane % lpc;
     Top2 loc;
     top2_init(loc);
-    for (int64_t c = c_lo + warp; c < c_hi; c += kQrcpWarps) {
-      if (c == p) {
-        if (lane == 0) w.nu[p] = -1.0;  // chosen
-        continue;
+    for (int64_t c0 = c_lo + (int64_t)warp * cpw; c0 < c_hi; c0 += (int64_t)kQrcpWarps * cpw) {
+      const int64_t c = c0 + sg;
+      // a lane group works only on a live, unchosen, non-pivot column; the shuffles below are
+      // executed by the whole warp regardless (dead groups carry zeros)
+      bool live = c < c_hi;
+      if (live && c == p) {
+        if (sl == 0) w.nu[p] = -1.0;  // chosen
+        live = false;
       }
-      if (w.nu[c] < 0.0) continue;  // chosen at an earlier step
-      double2* yc = Y + c * ldy;
+      if (live && w.nu[c] < 0.0) live = false;  // chosen at an earlier step
+      double2* yc = Y + c * ldy + j;
       double2 y[MAXQ];
       double wr = 0.0, wi = 0.0;
 #pragma unroll
       for (int q = 0; q < MAXQ; ++q) {
-        const int rr = lane + 32 * q;
-        if (j + rr < l) {
-          y[q] = yc[j + rr];
+        const int rr = sl + lpc * q;
+        y[q] = make_double2(0.0, 0.0);
+        if (live && rr < rows) y[q] = yc[rr];
+      }
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int rr = sl + lpc * q;
+        if (rr < rows) {
           const double2 v = sv[rr];
           // conj(v) * y
           wr = __fma_rn(v.x, y[q].x, __fma_rn(v.y, y[q].y, wr));
           wi = __fma_rn(v.x, y[q].y, __fma_rn(-v.y, y[q].x, wi));
         }
       }
-      wr = warp_sum(wr);
-      wi = warp_sum(wi);
+      wr = group_sum(wr, lpc);
+      wi = group_sum(wi, lpc);
       // s = conj(tau) * w
       const double s_re = __fma_rn(tr, wr, __dmul_rn(ti, wi));
       const double s_im = __fma_rn(tr, wi, -__dmul_rn(ti, wr));
       double nn = 0.0;
 #pragma unroll
       for (int q = 0; q < MAXQ; ++q) {
-        const int rr = lane + 32 * q;
-        if (j + rr < l) {
+        const int rr = sl + lpc * q;
+        if (rr < rows) {
           const double2 v = sv[rr];
           // y -= s * v
           y[q].x = __fma_rn(-s_re, v.x, __fma_rn(s_im, v.y, y[q].x));
           y[q].y = __fma_rn(-s_re, v.y, __fma_rn(-s_im, v.x, y[q].y));
-          yc[j + rr] = y[q];
+          if (live) yc[rr] = y[q];
           if (rr > 0) {
             nn = __fma_rn(y[q].x, y[q].x, nn);
             nn = __fma_rn(y[q].y, y[q].y, nn);
           }
         }
       }
-      const double nu = __dsqrt_rn(warp_sum(nn));
-      if (lane == 0) {
+      const double nu = __dsqrt_rn(group_sum(nn, lpc));
+      if (live && sl == 0) {
         w.nu[c] = nu;
         top2_push(loc, nu, c);
       }

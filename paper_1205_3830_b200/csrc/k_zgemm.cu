@@ -18,6 +18,8 @@
 // doubles and R pitch ≡ 4 mod 8 complex make every fragment load a single conflict-free
 // wavefront); 8 warps; grid = (r̃-tiles, j-tiles) with r̃ fastest so the CTAs that share an
 // A tile run together and hit L2.
+#include <cstdlib>
+
 #include "rid_device.cuh"
 #include "rid_internal.h"
 
@@ -47,8 +49,8 @@ struct ZgemmCfg {
   static_assert(PR % 8 == 4 && PR >= BRC, "R pitch");
 };
 
-template <int FJ, int FR, int WARPS_J, int WARPS_R, int BK, int STAGES>
-__global__ void __launch_bounds__(WARPS_J* WARPS_R * 32, 1)
+template <int FJ, int FR, int WARPS_J, int WARPS_R, int BK, int STAGES, int MINB>
+__global__ void __launch_bounds__(WARPS_J* WARPS_R * 32, MINB)
     k_zgemm_dmma(const double2* __restrict__ Rm, int64_t ldr, const double2* __restrict__ Bm,
                  int64_t ldb, double2* __restrict__ C, int64_t ldc, int64_t Mout, int64_t N,
                  int64_t K, ZgemmEpilogue ep) {
@@ -62,24 +64,54 @@ __global__ void __launch_bounds__(WARPS_J* WARPS_R * 32, 1)
   const int64_t j0 = (int64_t)blockIdx.y * Cfg::BJ;
   const int64_t nk = (K + Cfg::BKC - 1) / Cfg::BKC;     // complex-K stages
 
+  // Per-thread copy plan, fixed for the whole K loop: chunk q of the B̃ tile is (column q / BKC,
+  // complex K q % BKC), chunk q of the R tile is (K q / BRC, row q % BRC). Only the K offset
+  // changes from stage to stage, so each stage is a handful of 64-bit adds and LDGSTS.
+  constexpr int kChB = (Cfg::BJ * Cfg::BKC + Cfg::kThreads - 1) / Cfg::kThreads;
+  constexpr int kChR = (Cfg::BKC * Cfg::BRC + Cfg::kThreads - 1) / Cfg::kThreads;
+  const double2* srcB[kChB];
+  int dstB[kChB], kcB[kChB];
+  bool okB[kChB];
+#pragma unroll
+  for (int i = 0; i < kChB; ++i) {
+    const int q = tid + i * Cfg::kThreads;
+    const int col = q / Cfg::BKC, kc = q % Cfg::BKC;
+    okB[i] = q < Cfg::BJ * Cfg::BKC && j0 + col < N;
+    srcB[i] = okB[i] ? Bm + (j0 + col) * ldb + kc : Bm;
+    dstB[i] = col * Cfg::PB + 2 * kc;
+    kcB[i] = q < Cfg::BJ * Cfg::BKC ? kc : 0;
+  }
+  const double2* srcR[kChR];
+  int dstR[kChR], kcR[kChR];
+  bool okR[kChR], inR[kChR];
+#pragma unroll
+  for (int i = 0; i < kChR; ++i) {
+    const int q = tid + i * Cfg::kThreads;
+    const int kc = q / Cfg::BRC, rr = q % Cfg::BRC;
+    inR[i] = q < Cfg::BKC * Cfg::BRC;
+    okR[i] = inR[i] && r0c + rr < Mout;
+    srcR[i] = okR[i] ? Rm + kc * ldr + r0c + rr : Rm;
+    dstR[i] = 2 * (kc * Cfg::PR + rr);
+    kcR[i] = inR[i] ? kc : 0;
+  }
   auto load_stage = [&](int slot, int64_t kc0) {
     double* sB = smem + (size_t)slot * Cfg::kStage;
     double* sR = sB + Cfg::kStageB;
-    // B̃ tile: BJ columns x BKC complex (16 B chunks), K-contiguous per column
-    for (int q = tid; q < Cfg::BJ * Cfg::BKC; q += Cfg::kThreads) {
-      const int col = q / Cfg::BKC, kc = q % Cfg::BKC;
-      const int64_t gj = j0 + col, gk = kc0 + kc;
-      const bool ok = gj < N && gk < K;
-      const double2* src = ok ? Bm + gj * ldb + gk : Bm;
-      cp_async16(sB + col * Cfg::PB + 2 * kc, src, ok);
+    const bool full = kc0 + Cfg::BKC <= K;  // only the last stage has a K tail
+#pragma unroll
+    for (int i = 0; i < kChB; ++i) {
+      if (tid + i * Cfg::kThreads < Cfg::BJ * Cfg::BKC) {
+        const bool ok = okB[i] && (full || kc0 + kcB[i] < K);
+        cp_async16(sB + dstB[i], ok ? srcB[i] + kc0 : Bm, ok);
+      }
     }
-    // R tile: BKC K-columns x BRC complex rows, row-contiguous
-    for (int q = tid; q < Cfg::BKC * Cfg::BRC; q += Cfg::kThreads) {
-      const int kc = q / Cfg::BRC, rr = q % Cfg::BRC;
-      const int64_t gr = r0c + rr, gk = kc0 + kc;
-      const bool ok = gr < Mout && gk < K;
-      const double2* src = ok ? Rm + gk * ldr + gr : Rm;
-      cp_async16(sR + 2 * (kc * Cfg::PR + rr), src, ok);
+    const int64_t roff = kc0 * ldr;
+#pragma unroll
+    for (int i = 0; i < kChR; ++i) {
+      if (inR[i]) {
+        const bool ok = okR[i] && (full || kc0 + kcR[i] < K);
+        cp_async16(sR + dstR[i], ok ? srcR[i] + roff : Rm, ok);
+      }
     }
   };
 
@@ -159,12 +191,12 @@ __global__ void __launch_bounds__(WARPS_J* WARPS_R * 32, 1)
   }
 }
 
-template <int FJ, int FR, int WARPS_J, int WARPS_R, int BK, int STAGES>
+template <int FJ, int FR, int WARPS_J, int WARPS_R, int BK, int STAGES, int MINB = 1>
 static cudaError_t launch_cfg(const double2* Rm, int64_t ldr, const double2* Bm, int64_t ldb,
                               double2* C, int64_t ldc, int64_t Mout, int64_t N, int64_t K,
                               const ZgemmEpilogue& ep, cudaStream_t st) {
   using Cfg = ZgemmCfg<FJ, FR, WARPS_J, WARPS_R, BK, STAGES>;
-  auto kern = k_zgemm_dmma<FJ, FR, WARPS_J, WARPS_R, BK, STAGES>;
+  auto kern = k_zgemm_dmma<FJ, FR, WARPS_J, WARPS_R, BK, STAGES, MINB>;
   static bool attr_set = false;  // per-instantiation, set once per process
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -180,25 +212,36 @@ static cudaError_t launch_cfg(const double2* Rm, int64_t ldr, const double2* Bm,
   return cudaGetLastError();
 }
 
-// Tile choice: 2*Mout real rows are covered by tiles of BR = 16*FR rows (FJ = 2, 4x2 warps,
-// BJ = 64 columns); FR is picked to minimise padded rows (every padded row is wasted DMMA work),
-// ties -> larger FR (fewer A re-reads). Large Mout (generation) uses 128x128 tiles.
-#define RID_FR_LIST(X) X(3) X(4) X(5) X(6) X(8) X(9) X(10) X(11) X(12) X(17)
+// Tile choice (tuned on B200, tools/tune_sketch.py / tune_gen.py, profiles/r01_tune_*.log):
+// every config runs 3 cp.async stages and 2 CTAs per SM (16 warps/SM hide the DMMA, LDS and
+// barrier latencies that 8 warps could not). The 2*Mout real rows are covered by tiles of BR rows;
+// the candidate minimising padded rows (every padded row is wasted DMMA work) wins, ties -> the
+// larger BR (fewer re-reads of A). FR <= 11: 2 x 4 warps (BJ = 64, BR = 16 FR); FR = 12, 17:
+// 8 warps along j (BJ = 64, BR = 8 FR, fits 128 registers). Generation (Mout >= 2048): 64 x 64
+// tiles, 3 CTAs per SM. Measured: C4 sketch 34.7 TF/s, C5 33.6, generation C4 30.9.
+#define RID_FR_A(X) X(3) X(4) X(5) X(6) X(8) X(9) X(10) X(11)
+#define RID_FR_B(X) X(12) X(17)
 
 int zgemm_pick_fr(int64_t Mout) {
   const int64_t rows = 2 * Mout;
   int best = -1;
-  int64_t best_waste = INT64_MAX;
-#define RID_TRY(FRV)                                                             \
+  int64_t best_waste = INT64_MAX, best_br = 0;
+#define RID_TRY(FRV, BRV)                                                        \
   {                                                                              \
-    const int64_t br = 16 * (FRV);                                               \
+    const int64_t br = (BRV);                                                    \
     const int64_t waste = ((rows + br - 1) / br) * br - rows;                    \
-    if (waste < best_waste || (waste == best_waste && (FRV) > best)) {           \
+    if (waste < best_waste || (waste == best_waste && br > best_br)) {           \
       best_waste = waste;                                                        \
+      best_br = br;                                                              \
       best = (FRV);                                                              \
     }                                                                            \
   }
-  RID_FR_LIST(RID_TRY)
+#define RID_TRY_A(FRV) RID_TRY(FRV, 16 * (FRV))
+#define RID_TRY_B(FRV) RID_TRY(FRV, 8 * (FRV))
+  RID_FR_A(RID_TRY_A)
+  RID_FR_B(RID_TRY_B)
+#undef RID_TRY_A
+#undef RID_TRY_B
 #undef RID_TRY
   return best;
 }
@@ -208,12 +251,27 @@ cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int
                           int mode, double noise, uint64_t seed, int64_t col0, cudaStream_t st) {
   if (Mout <= 0 || N <= 0) return cudaSuccess;
   ZgemmEpilogue ep{mode, noise, seed, col0};
-  if (Mout >= 2048) return launch_cfg<4, 8, 4, 2, 16, 4>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
+  if (const char* v = getenv("RID_ZGEMM_VARIANT")) {  // tile experiments (tools/tune_*.py)
+    const int id = atoi(v);
+#define RID_V(ID, ...) \
+  if (id == ID) return launch_cfg<__VA_ARGS__>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
+    RID_V(1, 2, 11, 4, 2, 16, 4, 1)   // round-1 first version
+    RID_V(2, 1, 11, 8, 1, 16, 3, 3)
+    RID_V(3, 1, 17, 8, 1, 16, 4, 2)
+    RID_V(4, 1, 3, 8, 1, 16, 3, 4)
+    RID_V(5, 4, 8, 4, 2, 16, 4, 1)    // round-1 first generation tile
+#undef RID_V
+  }
+  if (Mout >= 2048) return launch_cfg<1, 8, 8, 1, 16, 3, 3>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
   switch (zgemm_pick_fr(Mout)) {
-#define RID_CASE(FRV) \
-  case FRV: return launch_cfg<2, FRV, 4, 2, 16, 4>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
-    RID_FR_LIST(RID_CASE)
-#undef RID_CASE
+#define RID_CASE_A(FRV) \
+  case FRV: return launch_cfg<2, FRV, 4, 2, 16, 3, 2>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
+#define RID_CASE_B(FRV) \
+  case FRV: return launch_cfg<1, FRV, 8, 1, 16, 3, 2>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
+    RID_FR_A(RID_CASE_A)
+    RID_FR_B(RID_CASE_B)
+#undef RID_CASE_A
+#undef RID_CASE_B
     default: return cudaErrorInvalidValue;
   }
 }
