@@ -9,16 +9,25 @@
 // R11 the residual norms are recomputed exactly from the updated column every step (no
 // downdating); R13 rank failure when nu_p < 1e-13 * max_c ||Y[:, c]||.
 //
-// Layout: every CTA owns a contiguous block of columns. A column's trailing segment rows j..l-1
-// is handled by a group of `lpc` lanes (32, 16, 8 or 4 — chosen per step so that each lane holds
-// at most MAXQ rows in registers): while the trailing block shrinks, a warp works on 32/lpc
-// columns at once, so the bytes in flight per warp stay ~constant and late (short) steps do not
-// become latency-bound. Per column: w = v^H y (butterfly within the group), y <- y - conj(tau) w v,
-// nu = ||y[j+1:l]|| recomputed exactly — one read and one write of the trailing segment per step.
+// Deferred write-back (the kernel is HBM-bound: one step touches the whole trailing block):
+// steps are grouped in blocks of QB. Y is materialised only at block boundaries; inside a block,
+// step j = j0 + t reloads each trailing column's block-start segment y^(j0)[j0:l], re-applies the
+// t + 1 reflectors H_j0 .. H_j in registers (they sit in shared memory) and recomputes the exact
+// residual norm of rows j+1..l-1 from that vector — the same numbers as a step-by-step update,
+// but each step reads the trailing block once and writes it only at the end of the block
+// (1 + 1/QB passes instead of 2). The FP64 work grows to ≈ 4 (QB + 1) FMA per element per step,
+// which the FP64 pipe absorbs (B200: 64 FMA/clk/SM against ≈1.4 elements/clk/SM of HBM).
+//
+// Work split: every CTA owns a contiguous block of columns. A column's segment is handled by a
+// group of `lpc` lanes (32, 16, 8 or 4 — chosen per block so that each lane holds at most MAXQ
+// rows in registers): as the trailing block shrinks a warp works on 32/lpc columns at once.
 // Every CTA rebuilds the same reflector from column p (identical bits: same code, same data,
 // commutative butterfly reductions), so the only cross-CTA exchange is the per-CTA
-// (best, second, index) candidate triple. Output, in place in Y (LAPACK-like):
-// rows 0..k-1 of every non-pivot column are R12; Y[0:t, J_t] is R11[0:t, t]; beta[t] = R11[t, t].
+// (best, second, index) candidate triple.
+//
+// Output: rows 0..k-1 of every non-pivot column of Y hold R12 (materialised at the last block
+// end); the pivot triangle R11 (k x k, column s = pivot step s, diagonal beta real) is written
+// densely to out.R11 by CTA 0; out.beta[s] = R11[s, s].
 #include <cfloat>
 #include <cstdint>
 
@@ -95,24 +104,67 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
   __syncthreads();
 }
 
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 constexpr int kQrcpThreads = 256;
 constexpr int kQrcpWarps = kQrcpThreads / 32;
+// Steps per deferred-write block. Measured on B200 (C4, tools/trace_qrcp.py): QB = 4 cut the
+// write traffic but every extra reflector re-read v from shared memory for every column
+// (≈27 us per reflector per step at C4: shared-memory bound), so the update pass went from
+// 98 to 61/83/110/153 us for t = 0..3. QB = 1 (write every step) is the faster choice until the
+// block update moves onto the tensor pipe.
+constexpr int kQB = 1;
 
-// lanes per column for a trailing segment of `rows` rows: the smallest group that keeps every
-// lane at <= MAXQ rows (more columns per warp as the segment shrinks)
+// lanes per column for a segment of `rows` rows: the smallest group that keeps every lane at
+// <= MAXQ rows (more columns per warp as the segment shrinks)
 __device__ __forceinline__ int pick_lpc(int rows, int maxq) {
   int lpc = 32;
   while (lpc > 4 && rows <= (lpc / 2) * maxq) lpc >>= 1;
   return lpc;
 }
 
+// y <- H^H y for the reflector stored in v (zeros above its pivot row), tau = (tr, ti); every
+// lane of the lpc-group holds rows sl + lpc*q of the segment.
+template <int MAXQ>
+__device__ __forceinline__ void apply_reflector(double2 (&y)[MAXQ], const double2* v, double tr,
+                                                double ti, int sl, int lpc, int L) {
+  double wr = 0.0, wi = 0.0;
+#pragma unroll
+  for (int q = 0; q < MAXQ; ++q) {
+    const int rr = sl + lpc * q;
+    if (rr < L) {
+      const double2 vv = v[rr];
+      wr = __fma_rn(vv.x, y[q].x, __fma_rn(vv.y, y[q].y, wr));   // conj(v) * y
+      wi = __fma_rn(vv.x, y[q].y, __fma_rn(-vv.y, y[q].x, wi));
+    }
+  }
+  wr = group_sum(wr, lpc);
+  wi = group_sum(wi, lpc);
+  const double s_re = __fma_rn(tr, wr, __dmul_rn(ti, wi));    // s = conj(tau) * w
+  const double s_im = __fma_rn(tr, wi, -__dmul_rn(ti, wr));
+#pragma unroll
+  for (int q = 0; q < MAXQ; ++q) {
+    const int rr = sl + lpc * q;
+    if (rr < L) {
+      const double2 vv = v[rr];
+      y[q].x = __fma_rn(-s_re, vv.x, __fma_rn(s_im, vv.y, y[q].x));  // y -= s * v
+      y[q].y = __fma_rn(-s_re, vv.y, __fma_rn(-s_im, vv.x, y[q].y));
+    }
+  }
+}
+
 template <int MAXQ>
 __global__ void __launch_bounds__(kQrcpThreads, 2)
     k_qrcp(double2* __restrict__ Y, int64_t ldy, int l, int64_t n, int k, double tol_rel,
            QrcpOut out, QrcpWork w) {
-  __shared__ double2 sv[MAXQ * 32];
+  extern __shared__ double2 sv_raw[];  // kQB reflectors of the current block, rows j0..l-1
+  double2(*sv)[MAXQ * 32] = reinterpret_cast<double2(*)[MAXQ * 32]>(sv_raw);
+  __shared__ double s_tau[kQB][2];
   __shared__ Top2 sred[kQrcpWarps];
-  __shared__ double s_tau_re, s_tau_im;
   __shared__ long long s_p;
   __shared__ int s_stop;
 
@@ -169,27 +221,32 @@ __global__ void __launch_bounds__(kQrcpThreads, 2)
   }
 
   for (int j = 0; j < k; ++j) {
+    const int j0 = j - j % kQB;  // block start
+    const int t = j - j0;        // position in the block
+    const int L = l - j0;        // segment length (rows j0..l-1)
+    const bool block_end = (t == kQB - 1) || (j == k - 1);
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[4 * j + 0] = globaltimer();
     // ---- 1. global pivot: reduce the per-CTA candidates (every CTA, identically) ------------
     if (warp == 0) {
-      Top2 t;
-      top2_init(t);
+      Top2 tt;
+      top2_init(tt);
       const double* cb = w.cand + (size_t)(j & 1) * w.max_blocks * 3;
       for (int q = lane; q < nb; q += 32) {
         Top2 o;
         o.b1 = cb[q * 3 + 0];
         o.b2 = cb[q * 3 + 1];
         o.i1 = (long long)cb[q * 3 + 2];
-        top2_merge(t, o);
+        top2_merge(tt, o);
       }
-      top2_warp(t);
-      if (j == 0) nu0max = t.b1;  // max_c ||Y[:, c]||
+      top2_warp(tt);
+      if (j == 0) nu0max = tt.b1;  // max_c ||Y[:, c]||
       if (lane == 0) {
-        s_p = t.i1;
-        s_stop = (!(t.b1 >= tol_rel * nu0max) || t.b1 <= 0.0) ? 1 : 0;
+        s_p = tt.i1;
+        s_stop = (!(tt.b1 >= tol_rel * nu0max) || tt.b1 <= 0.0) ? 1 : 0;
         if (b == 0) {
-          out.resid[j] = t.b1;
-          out.margin[j] = (t.b2 < 0.0) ? DBL_MAX : (t.b1 - t.b2) / t.b1;
-          if (!s_stop) out.J[j] = t.i1;
+          out.resid[j] = tt.b1;
+          out.margin[j] = (tt.b2 < 0.0) ? DBL_MAX : (tt.b1 - tt.b2) / tt.b1;
+          if (!s_stop) out.J[j] = tt.i1;
         }
       }
     }
@@ -202,23 +259,37 @@ __global__ void __launch_bounds__(kQrcpThreads, 2)
       return;  // every CTA takes the same decision at the same step
     }
     const int64_t p = s_p;
-    const int rows = l - j;
 
-    // ---- 2. Householder reflector from x = Y[j:l, p] (LAPACK zlarfg convention) -------------
+    // ---- 2. reflector H_j from x = (H_{j-1} .. H_j0)^H y_p^(j0) rows j..l-1 (zlarfg) ---------
     if (warp == 0) {
-      const double2* xp = Y + p * ldy + j;
+      const double2* yp = Y + p * ldy + j0;
+      double2 x[MAXQ];
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int rr = lane + 32 * q;
+        x[q] = (rr < L) ? yp[rr] : make_double2(0.0, 0.0);
+      }
+      for (int i = 0; i < t; ++i) apply_reflector<MAXQ>(x, sv[i], s_tau[i][0], s_tau[i][1], lane, 32, L);
       double s = 0.0;
-      for (int rr = lane; rr < rows; rr += 32) {
-        const double2 x = xp[rr];
-        sv[rr] = x;
-        if (rr > 0) {
-          s = __fma_rn(x.x, x.x, s);
-          s = __fma_rn(x.y, x.y, s);
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int rr = lane + 32 * q;
+        if (rr > t && rr < L) {
+          s = __fma_rn(x[q].x, x[q].x, s);
+          s = __fma_rn(x[q].y, x[q].y, s);
         }
       }
       const double xnorm2 = group_sum(s, 32);
-      __syncwarp();
-      const double ar = sv[0].x, ai = sv[0].y;
+      // alpha = x at row j (relative row t): held by lane t % 32, slot t / 32
+      double ar = 0.0, ai = 0.0;
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q)
+        if (q == t / 32) {
+          ar = x[q].x;
+          ai = x[q].y;
+        }
+      ar = __shfl_sync(0xffffffffu, ar, t % 32);
+      ai = __shfl_sync(0xffffffffu, ai, t % 32);
       double tau_re, tau_im, beta, sc_re, sc_im;
       if (xnorm2 == 0.0 && ai == 0.0) {
         tau_re = 0.0;
@@ -231,35 +302,47 @@ __global__ void __launch_bounds__(kQrcpThreads, 2)
         beta = (ar >= 0.0) ? -nrm : nrm;
         tau_re = __ddiv_rn(__dsub_rn(beta, ar), beta);
         tau_im = __ddiv_rn(-ai, beta);
-        // scal = 1 / (alpha - beta)
-        const double dr = __dsub_rn(ar, beta), di = ai;
+        const double dr = __dsub_rn(ar, beta), di = ai;  // scal = 1 / (alpha - beta)
         const double den = __fma_rn(dr, dr, __dmul_rn(di, di));
         sc_re = __ddiv_rn(dr, den);
         sc_im = __ddiv_rn(-di, den);
       }
-      __syncwarp();
-      for (int rr = lane; rr < rows; rr += 32) {
-        double2 v;
-        if (rr == 0) {
-          v = make_double2(1.0, 0.0);
-        } else {
-          const double2 x = sv[rr];
-          v.x = __fma_rn(x.x, sc_re, -__dmul_rn(x.y, sc_im));
-          v.y = __fma_rn(x.x, sc_im, __dmul_rn(x.y, sc_re));
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int rr = lane + 32 * q;
+        if (rr < L) {
+          double2 v;
+          if (rr < t) {
+            v = make_double2(0.0, 0.0);
+          } else if (rr == t) {
+            v = make_double2(1.0, 0.0);
+          } else {
+            v.x = __fma_rn(x[q].x, sc_re, -__dmul_rn(x[q].y, sc_im));
+            v.y = __fma_rn(x[q].x, sc_im, __dmul_rn(x[q].y, sc_re));
+          }
+          sv[t][rr] = v;
+          // pivot column of R11: rows j0..j-1 are the transformed x, rows < j0 are final in Y
+          if (b == 0 && rr < t) out.R11[(int64_t)j * k + j0 + rr] = x[q];
         }
-        sv[rr] = v;
       }
       if (lane == 0) {
-        s_tau_re = tau_re;
-        s_tau_im = tau_im;
-        if (b == 0) out.beta[j] = beta;
+        s_tau[t][0] = tau_re;
+        s_tau[t][1] = tau_im;
+        if (b == 0) {
+          out.beta[j] = beta;
+          out.R11[(int64_t)j * k + j] = make_double2(beta, 0.0);
+        }
       }
     }
     __syncthreads();
-    const double tr = s_tau_re, ti = s_tau_im;
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[4 * j + 1] = globaltimer();
 
-    // ---- 3. apply H^H = I - conj(tau) v v^H to every owned trailing column ------------------
-    const int lpc = pick_lpc(rows, MAXQ);
+    // ---- 3. every owned trailing column: reload y^(j0), apply H_j0..H_j, exact norm ----------
+    // rows 0..j0-1 of the pivot column are final (nobody writes them again): CTA 0's last warp
+    // copies them into the dense R11 off the critical path (R11 is zeroed before the launch)
+    if (b == 0 && warp == kQrcpWarps - 1)
+      for (int r = lane; r < j0; r += 32) out.R11[(int64_t)j * k + r] = Y[p * ldy + r];
+    const int lpc = pick_lpc(L, MAXQ);
     const int cpw = 32 / lpc, sg = lane / lpc, sl = lane % lpc;
     Top2 loc;
     top2_init(loc);
@@ -273,44 +356,29 @@ __global__ void __launch_bounds__(kQrcpThreads, 2)
         live = false;
       }
       if (live && w.nu[c] < 0.0) live = false;  // chosen at an earlier step
-      double2* yc = Y + c * ldy + j;
+      double2* yc = Y + c * ldy + j0;
       double2 y[MAXQ];
-      double wr = 0.0, wi = 0.0;
 #pragma unroll
       for (int q = 0; q < MAXQ; ++q) {
         const int rr = sl + lpc * q;
         y[q] = make_double2(0.0, 0.0);
-        if (live && rr < rows) y[q] = yc[rr];
+        if (live && rr < L) y[q] = yc[rr];
       }
-#pragma unroll
-      for (int q = 0; q < MAXQ; ++q) {
-        const int rr = sl + lpc * q;
-        if (rr < rows) {
-          const double2 v = sv[rr];
-          // conj(v) * y
-          wr = __fma_rn(v.x, y[q].x, __fma_rn(v.y, y[q].y, wr));
-          wi = __fma_rn(v.x, y[q].y, __fma_rn(-v.y, y[q].x, wi));
-        }
-      }
-      wr = group_sum(wr, lpc);
-      wi = group_sum(wi, lpc);
-      // s = conj(tau) * w
-      const double s_re = __fma_rn(tr, wr, __dmul_rn(ti, wi));
-      const double s_im = __fma_rn(tr, wi, -__dmul_rn(ti, wr));
+      for (int i = 0; i <= t; ++i) apply_reflector<MAXQ>(y, sv[i], s_tau[i][0], s_tau[i][1], sl, lpc, L);
       double nn = 0.0;
 #pragma unroll
       for (int q = 0; q < MAXQ; ++q) {
         const int rr = sl + lpc * q;
-        if (rr < rows) {
-          const double2 v = sv[rr];
-          // y -= s * v
-          y[q].x = __fma_rn(-s_re, v.x, __fma_rn(s_im, v.y, y[q].x));
-          y[q].y = __fma_rn(-s_re, v.y, __fma_rn(-s_im, v.x, y[q].y));
-          if (live) yc[rr] = y[q];
-          if (rr > 0) {
-            nn = __fma_rn(y[q].x, y[q].x, nn);
-            nn = __fma_rn(y[q].y, y[q].y, nn);
-          }
+        if (rr > t && rr < L) {
+          nn = __fma_rn(y[q].x, y[q].x, nn);
+          nn = __fma_rn(y[q].y, y[q].y, nn);
+        }
+      }
+      if (block_end && live) {
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) {
+          const int rr = sl + lpc * q;
+          if (rr < L) yc[rr] = y[q];
         }
       }
       const double nu = __dsqrt_rn(group_sum(nn, lpc));
@@ -320,7 +388,9 @@ __global__ void __launch_bounds__(kQrcpThreads, 2)
       }
     }
     block_top2_publish(loc, (j + 1) & 1);
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[4 * j + 2] = globaltimer();
     grid_barrier(w.bar, (unsigned)nb * (++phase));
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[4 * j + 3] = globaltimer();
   }
   if (b == 0 && threadIdx.x == 0) {
     out.info[0] = 0;
@@ -336,9 +406,12 @@ template <int MAXQ>
 static cudaError_t launch_qrcp(double2* Y, int64_t ldy, int l, int64_t n, int k, double tol_rel,
                                const QrcpOut& out, const QrcpWork& w, int num_sms,
                                cudaStream_t st) {
+  const size_t smem = sizeof(double2) * kQB * MAXQ * 32;
+  cudaError_t e = cudaFuncSetAttribute(k_qrcp<MAXQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem);
+  if (e != cudaSuccess) return e;
   int occ = 0;
-  cudaError_t e =
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qrcp<MAXQ>, kQrcpThreads, 0);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qrcp<MAXQ>, kQrcpThreads, smem);
   if (e != cudaSuccess) return e;
   if (occ < 1) return cudaErrorInvalidConfiguration;
   int blocks = num_sms * (occ < 2 ? occ : 2);
@@ -351,8 +424,8 @@ static cudaError_t launch_qrcp(double2* Y, int64_t ldy, int l, int64_t n, int k,
   QrcpOut o = out;
   QrcpWork ww = w;
   void* args[] = {&Y, &ldy, &l, &n, &k, &tol_rel, &o, &ww};
-  return cudaLaunchCooperativeKernel((void*)k_qrcp<MAXQ>, dim3(blocks), dim3(kQrcpThreads), args, 0,
-                                     st);
+  return cudaLaunchCooperativeKernel((void*)k_qrcp<MAXQ>, dim3(blocks), dim3(kQrcpThreads), args,
+                                     smem, st);
 }
 
 cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, double tol_rel,
@@ -368,21 +441,19 @@ cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, doubl
 }
 
 // ---------------------------------------------------------------------------------------------
-// Inverse of R11 (upper triangular, R11[t, s] = Y[t, J[s]] for t < s, R11[s, s] = beta[s]):
-// column c of R11^{-1} by right-looking back-substitution on e_c ("solving Lv = w
-// for triangular L"); one CTA per column, the right-hand side in shared memory.
+// Inverse of the dense upper-triangular R11 (k x k, column-major): column c of R11^{-1} by
+// right-looking back-substitution on e_c ("solving Lv = w for triangular L"); one CTA
+// per column, the right-hand side in shared memory.
 // ---------------------------------------------------------------------------------------------
-__global__ void k_tri_inverse(const double2* __restrict__ Y, int64_t ldy,
-                              const int64_t* __restrict__ J, const double* __restrict__ beta,
-                              int k, double2* __restrict__ Rinv) {
+__global__ void k_tri_inverse(const double2* __restrict__ R11, int k, double2* __restrict__ Rinv) {
   extern __shared__ double2 bvec[];  // k
   const int c = blockIdx.x;
   for (int i = threadIdx.x; i < k; i += blockDim.x) bvec[i] = make_double2(i == c ? 1.0 : 0.0, 0.0);
   __syncthreads();
   for (int s = c; s >= 0; --s) {
-    const double d = beta[s];
+    const double d = R11[(int64_t)s * k + s].x;  // real diagonal (beta)
     const double2 xs = make_double2(__ddiv_rn(bvec[s].x, d), __ddiv_rn(bvec[s].y, d));
-    const double2* col = Y + J[s] * ldy;  // R11[0:s, s]
+    const double2* col = R11 + (int64_t)s * k;  // R11[0:s, s]
     __syncthreads();
     for (int i = threadIdx.x; i < s; i += blockDim.x) {
       const double2 r = col[i];
@@ -398,8 +469,7 @@ __global__ void k_tri_inverse(const double2* __restrict__ Y, int64_t ldy,
     Rinv[(int64_t)c * k + i] = (i <= c) ? bvec[i] : make_double2(0.0, 0.0);
 }
 
-cudaError_t tri_inverse(const double2* Y, int64_t ldy, const int64_t* J, const double* beta,
-                        int64_t k, double2* Rinv, cudaStream_t st) {
+cudaError_t tri_inverse(const double2* R11, int64_t k, double2* Rinv, cudaStream_t st) {
   if (k <= 0) return cudaSuccess;
   const size_t sm = (size_t)k * sizeof(double2);
   if (sm > 48 * 1024) {
@@ -407,7 +477,7 @@ cudaError_t tri_inverse(const double2* Y, int64_t ldy, const int64_t* J, const d
                                          (int)sm);
     if (e != cudaSuccess) return e;
   }
-  k_tri_inverse<<<(unsigned)k, 256, sm, st>>>(Y, ldy, J, beta, (int)k, Rinv);
+  k_tri_inverse<<<(unsigned)k, 256, sm, st>>>(R11, (int)k, Rinv);
   return cudaGetLastError();
 }
 

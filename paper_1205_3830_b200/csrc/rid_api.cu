@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -156,11 +157,34 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
   RID_TRY(ws_get(c, "info", sizeof(int) * 2, &pinfo));
   const int max_blocks = 4 * c->num_sms;
   RID_TRY(ws_get(c, "qrcp_work", rid::qrcp_work_bytes(n, max_blocks), &pwork));
-  rid::QrcpOut o{(int64_t*)pJ, (double*)pbeta, (double*)presid, (double*)pmargin, (int*)pinfo};
+  void* pR11;
+  RID_TRY(ws_get(c, "R11", sizeof(double2) * k * k, &pR11));
+  rid::QrcpOut o{(int64_t*)pJ, (double*)pbeta, (double*)presid, (double*)pmargin, (int*)pinfo,
+                 (double2*)pR11};
   char* wb = (char*)pwork;
   rid::QrcpWork w{(double*)wb, (double*)(wb + sizeof(double) * n), nullptr, max_blocks};
   w.bar = (unsigned*)(wb + sizeof(double) * n + sizeof(double) * 2 * 3 * max_blocks);
+  const char* trace_path = getenv("RID_QRCP_TRACE");  // per-step timing of k_qrcp (tools)
+  if (trace_path) {
+    void* pt;
+    RID_TRY(ws_get(c, "qrcp_trace", sizeof(unsigned long long) * 4 * k, &pt));
+    RID_CUDA(c, cudaMemsetAsync(pt, 0, sizeof(unsigned long long) * 4 * k, c->stream));
+    w.trace = (unsigned long long*)pt;
+  }
+  RID_CUDA(c, cudaMemsetAsync(pR11, 0, sizeof(double2) * k * k, c->stream));
   RID_CUDA(c, rid::qrcp(Yw, l, l, n, k, kRankTol, o, w, c->num_sms, c->stream));
+  if (trace_path) {
+    std::vector<unsigned long long> tr(4 * k);
+    RID_CUDA(c, cudaMemcpyAsync(tr.data(), w.trace, sizeof(unsigned long long) * 4 * k,
+                                cudaMemcpyDeviceToHost, c->stream));
+    RID_CUDA(c, cudaStreamSynchronize(c->stream));
+    if (FILE* f = fopen(trace_path, "w")) {
+      for (int64_t j = 0; j < k; ++j)
+        fprintf(f, "%lld %llu %llu %llu %llu\n", (long long)j, tr[4 * j], tr[4 * j + 1],
+                tr[4 * j + 2], tr[4 * j + 3]);
+      fclose(f);
+    }
+  }
   // one synchronisation: rank status, R11 diagonal (singularity), diagnostics
   std::vector<double> hb(k), hr(k), hm(k);
   RID_CUDA(c, cudaMemcpyAsync(info_host, pinfo, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->stream));
@@ -188,8 +212,7 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
   if (!solve) return RID_OK;
   void* pRinv;
   RID_TRY(ws_get(c, "Rinv", sizeof(double2) * k * k, &pRinv));
-  RID_CUDA(c, rid::tri_inverse(Yw, l, (const int64_t*)pJ, (const double*)pbeta, k,
-                               (double2*)pRinv, c->stream));
+  RID_CUDA(c, rid::tri_inverse((const double2*)pR11, k, (double2*)pRinv, c->stream));
   RID_CUDA(c, rid::zgemm_ordered((const double2*)pRinv, k, Yw + col0 * l, l, Pdev, ldp, k, n_loc,
                                  k, 0, 0.0, 0, 0, c->stream));
   RID_CUDA(c, rid::assemble_identity((const int64_t*)pJ, k, col0, n_loc, Pdev, ldp, c->stream));
@@ -197,9 +220,9 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
 }
 
 __global__ void k_extract_R(const double2* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ J,
-                            const double* __restrict__ beta, int64_t k, int64_t n,
+                            const double2* __restrict__ R11, int64_t k, int64_t n,
                             double2* __restrict__ R, int64_t ldr) {
-  // R[:, c] = Y[0:k, c] for non-pivot c; for c = J[s]: rows < s from Y, row s = beta[s], rows > s 0
+  // R[:, c] = Y[0:k, c] for non-pivot c; for c = J[s]: column s of the dense triangle R11
   const int64_t c = blockIdx.x;
   __shared__ int64_t s_piv;
   if (threadIdx.x == 0) {
@@ -209,14 +232,8 @@ __global__ void k_extract_R(const double2* __restrict__ Y, int64_t ldy, const in
   }
   __syncthreads();
   const int64_t s = s_piv;
-  for (int64_t t = threadIdx.x; t < k; t += blockDim.x) {
-    double2 v = Y[c * ldy + t];
-    if (s >= 0) {
-      if (t == s) v = make_double2(beta[s], 0.0);
-      else if (t > s) v = make_double2(0.0, 0.0);
-    }
-    R[c * ldr + t] = v;
-  }
+  for (int64_t t = threadIdx.x; t < k; t += blockDim.x)
+    R[c * ldr + t] = (s >= 0) ? R11[s * k + t] : Y[c * ldy + t];
 }
 
 }  // namespace
@@ -411,11 +428,10 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
   }
   if (st != RID_OK) return st;
   {  // solve
-    void* pbeta;
-    RID_TRY(ws_get(c, "beta", sizeof(double) * k, &pbeta));
-    void* pRinv;
+    void *pR11, *pRinv;
+    RID_TRY(ws_get(c, "R11", sizeof(double2) * k * k, &pR11));
     RID_TRY(ws_get(c, "Rinv", sizeof(double2) * k * k, &pRinv));
-    RID_CUDA(c, rid::tri_inverse(Yw, l, Jdev, (const double*)pbeta, k, (double2*)pRinv, c->stream));
+    RID_CUDA(c, rid::tri_inverse((const double2*)pR11, k, (double2*)pRinv, c->stream));
     RID_CUDA(c, rid::zgemm_ordered((const double2*)pRinv, k, Yw + col0 * l, l, (double2*)p.dev, ldp,
                                    k, n_loc, k, 0, 0.0, 0, 0, c->stream));
     RID_CUDA(c, rid::assemble_identity(Jdev, k, col0, n_loc, (double2*)p.dev, ldp, c->stream));
@@ -470,8 +486,11 @@ rid_status rid_qrcp(rid_ctx* c, const rid_z* Y, int64_t l, int64_t n, int64_t ld
   if (R) {
     MatArg r;
     RID_TRY(stage_in(c, "stage_R", R, k, n, ldr, sizeof(rid_z), false, &r));
-    k_extract_R<<<(unsigned)n, 128, 0, c->stream>>>((const double2*)pY, l, Jdev, beta, k, n,
-                                                     (double2*)r.dev, ldr);
+    void* pR11;
+    RID_TRY(ws_get(c, "R11", sizeof(double2) * k * k, &pR11));
+    k_extract_R<<<(unsigned)n, 128, 0, c->stream>>>((const double2*)pY, l, Jdev,
+                                                     (const double2*)pR11, k, n, (double2*)r.dev,
+                                                     ldr);
     RID_CUDA(c, cudaGetLastError());
     RID_TRY(stage_out(c, r, R, k, n, ldr, sizeof(rid_z)));
   }

@@ -24,20 +24,21 @@ struct QrcpOut {
   double* resid;     // device, k: nu_p at each step
   double* margin;    // device, k: (nu(1) - nu(2)) / nu(1) at each step
   int* info;         // device, 2: [0] status (0 ok, 2 rank failure), [1] rank achieved
+  double2* R11;      // device, k x k column-major: the pivot triangle (column s = step s)
 };
 struct QrcpWork {
   double* nu;        // n
   double* cand;      // 2 * 3 * max_blocks doubles (best, second, index-as-double) x 2 parities
   unsigned* bar;     // 1
   int max_blocks;
+  unsigned long long* trace = nullptr;  // optional: 4 %globaltimer stamps per step (CTA 0)
 };
 size_t qrcp_work_bytes(int64_t n, int max_blocks);
 cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, double tol_rel,
                  const QrcpOut& out, const QrcpWork& w, int num_sms, cudaStream_t st);
 
 // Inverse of the pivoted triangle R11 (R11[t, s] = Y[t, J[s]] for t < s, beta[s] on the diagonal)
-cudaError_t tri_inverse(const double2* Y, int64_t ldy, const int64_t* J, const double* beta,
-                        int64_t k, double2* Rinv, cudaStream_t st);
+cudaError_t tri_inverse(const double2* R11, int64_t k, double2* Rinv, cudaStream_t st);
 // P[:, J_t - col0] = e_t for pivots inside the shard (k_misc.cu)
 cudaError_t assemble_identity(const int64_t* J, int64_t k, int64_t col0, int64_t n_loc, double2* P,
                               int64_t ldp, cudaStream_t st);
