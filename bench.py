@@ -111,13 +111,20 @@ def oracle_sample(cfg, seed: int, target_s: float = 15.0):
     import oracle
 
     threads = oracle.set_threads(os.cpu_count() or 1)
-    n_s = 8
-    A = oracle.generate(seed, cfg.m, cfg.n, cfg.k, cfg.noise, 0, n_s)
-    t0 = time.perf_counter()
-    oracle.sketch(A, seed, cfg.l)
-    dt = time.perf_counter() - t0
-    n_s = max(threads, min(cfg.n, int(n_s * target_s / max(dt, 1e-3))))
-    n_s = max(threads, (n_s // threads) * threads)
+
+    def timed(ncols):
+        A = oracle.generate(seed, cfg.m, cfg.n, cfg.k, cfg.noise, 0, ncols)
+        t0 = time.perf_counter()
+        oracle.sketch(A, seed, cfg.l)
+        return time.perf_counter() - t0
+
+    # two-point calibration: fixed cost (R regeneration) + per-column cost
+    n1, n2 = threads, 4 * threads
+    t1, t2 = timed(n1), timed(n2)
+    per_col = max((t2 - t1) / (n2 - n1), 1e-9)
+    fixed = max(t1 - n1 * per_col, 0.0)
+    n_s = int((target_s - fixed) / per_col)
+    n_s = max(threads, min(cfg.n, (n_s // threads) * threads))
     A = oracle.generate(seed, cfg.m, cfg.n, cfg.k, cfg.noise, 0, n_s)
     t0 = time.perf_counter()
     oracle.sketch(A, seed, cfg.l)

@@ -30,6 +30,9 @@ struct rid_ctx {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
   cudaEvent_t ev[12] = {};
+  // host-A streaming (e2e path): a copy stream and double-buffer events, created on first use
+  cudaStream_t copy_stream = nullptr;
+  cudaEvent_t ev_copied[2] = {}, ev_used[2] = {}, ev_copy0 = nullptr, ev_copy1 = nullptr;
 };
 
 namespace {
@@ -219,6 +222,55 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
   return RID_OK;
 }
 
+// Y[:, 0:n_loc] = R A for a HOST A (the e2e path): A is streamed to the device in column chunks
+// of ~1 GiB on a copy stream, double-buffered, each chunk's sketch overlapping the copy of the
+// next. The sketch of a column does not depend on the chunking, so Y is bit-identical to the
+// device-resident call. The device never holds more than two chunks of A.
+rid_status sketch_streamed(rid_ctx* c, const double2* R, const rid_z* hostA, int64_t m,
+                           int64_t n_loc, int64_t lda, int64_t l, double2* Y, int* launches,
+                           double* t_h2d) {
+  if (!c->copy_stream) {
+    RID_CUDA(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      RID_CUDA(c, cudaEventCreateWithFlags(&c->ev_copied[b], cudaEventDisableTiming));
+      RID_CUDA(c, cudaEventCreateWithFlags(&c->ev_used[b], cudaEventDisableTiming));
+    }
+    RID_CUDA(c, cudaEventCreate(&c->ev_copy0));
+    RID_CUDA(c, cudaEventCreate(&c->ev_copy1));
+  }
+  int64_t chunk = (int64_t)(1 << 30) / (16 * m);
+  if (chunk < 64) chunk = 64;
+  if (chunk > n_loc) chunk = n_loc;
+  void* buf[2];
+  RID_TRY(ws_get(c, "streamA0", sizeof(double2) * m * chunk, &buf[0]));
+  RID_TRY(ws_get(c, "streamA1", sizeof(double2) * m * chunk, &buf[1]));
+  // the copy stream must not overwrite a buffer before the previous call's kernels used it
+  RID_CUDA(c, cudaEventRecord(c->ev_used[0], c->stream));
+  RID_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->ev_used[0], 0));
+  RID_CUDA(c, cudaEventRecord(c->ev_copy0, c->copy_stream));
+  int i = 0;
+  for (int64_t j0 = 0; j0 < n_loc; j0 += chunk, ++i) {
+    const int b = i & 1;
+    const int64_t nc = (j0 + chunk <= n_loc) ? chunk : n_loc - j0;
+    if (i >= 2) RID_CUDA(c, cudaStreamWaitEvent(c->copy_stream, c->ev_used[b], 0));
+    RID_CUDA(c, cudaMemcpy2DAsync(buf[b], sizeof(double2) * m, hostA + j0 * lda,
+                                  sizeof(double2) * lda, sizeof(double2) * m, nc,
+                                  cudaMemcpyHostToDevice, c->copy_stream));
+    RID_CUDA(c, cudaEventRecord(c->ev_copied[b], c->copy_stream));
+    RID_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0));
+    RID_CUDA(c, rid::zgemm_ordered(R, l, (const double2*)buf[b], m, Y + j0 * l, l, l, nc, m, 0,
+                                   0.0, 0, 0, c->stream));
+    RID_CUDA(c, cudaEventRecord(c->ev_used[b], c->stream));
+    ++*launches;
+  }
+  RID_CUDA(c, cudaEventRecord(c->ev_copy1, c->copy_stream));
+  if (t_h2d) {
+    RID_CUDA(c, cudaEventSynchronize(c->ev_copy1));
+    *t_h2d += ev_ms(c->ev_copy0, c->ev_copy1) * 1e-3;
+  }
+  return RID_OK;
+}
+
 __global__ void k_extract_R(const double2* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ J,
                             const double2* __restrict__ R11, int64_t k, int64_t n,
                             double2* __restrict__ R, int64_t ldr) {
@@ -268,6 +320,16 @@ void rid_destroy(rid_ctx* c) {
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->copy_stream) {
+    cudaStreamSynchronize(c->copy_stream);
+    cudaStreamDestroy(c->copy_stream);
+    for (int b = 0; b < 2; ++b) {
+      cudaEventDestroy(c->ev_copied[b]);
+      cudaEventDestroy(c->ev_used[b]);
+    }
+    cudaEventDestroy(c->ev_copy0);
+    cudaEventDestroy(c->ev_copy1);
+  }
   if (c->owns_stream) cudaStreamDestroy(c->stream);
   delete c;
 }
@@ -388,7 +450,8 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
   cudaEvent_t* ev = c->ev;
   RID_CUDA(c, cudaEventRecord(ev[0], c->stream));
   MatArg a, p;
-  RID_TRY(stage_in(c, "stage_A", A, m, n_loc, lda, sizeof(rid_z), true, &a));
+  const bool a_host = !is_device_ptr(A);  // host A is streamed chunk by chunk under the sketch
+  if (!a_host) RID_TRY(stage_in(c, "stage_A", A, m, n_loc, lda, sizeof(rid_z), true, &a));
   RID_TRY(stage_in(c, "stage_P", P, k, n_loc, ldp, sizeof(rid_z), false, &p));
   RID_CUDA(c, cudaEventRecord(ev[1], c->stream));
   void *pY, *pR;
@@ -403,9 +466,15 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
     RID_CUDA(c, cudaEventRecord(ev[2], c->stream));
     RID_CUDA(c, rid::normal_fill(seed, sR, l, m, 0, 0, (double2*)pR, l, c->stream));
     RID_CUDA(c, cudaEventRecord(ev[3], c->stream));
-    d.launches += 3;  // R fill, sketch GEMM, QRCP
-    RID_CUDA(c, rid::zgemm_ordered((const double2*)pR, l, (const double2*)a.dev, lda, Yw + col0 * l,
-                                   l, l, n_loc, m, 0, 0.0, 0, 0, c->stream));
+    d.launches += 2;  // R fill, QRCP
+    if (a_host) {
+      RID_TRY(sketch_streamed(c, (const double2*)pR, A, m, n_loc, lda, l, Yw + col0 * l,
+                              &d.launches, nullptr));
+    } else {
+      RID_CUDA(c, rid::zgemm_ordered((const double2*)pR, l, (const double2*)a.dev, lda,
+                                     Yw + col0 * l, l, l, n_loc, m, 0, 0.0, 0, 0, c->stream));
+      d.launches += 1;
+    }
     RID_CUDA(c, cudaEventRecord(ev[4], c->stream));
     if (c->nranks > 1) {
       RID_NCCL(c, ncclAllGather(Yw + col0 * l, Yw, (size_t)(2 * l * n_loc), ncclDouble, c->comm,
@@ -446,7 +515,8 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
   RID_CUDA(c, cudaEventRecord(ev[8], c->stream));
   RID_CUDA(c, cudaEventSynchronize(ev[8]));
   if (diag) {
-    d.t_h2d = ev_ms(ev[0], ev[1]) * 1e-3;
+    // host A: the streamed copies overlap the sketch (t_sketch then includes copy stalls)
+    d.t_h2d = a_host ? ev_ms(c->ev_copy0, c->ev_copy1) * 1e-3 : ev_ms(ev[0], ev[1]) * 1e-3;
     d.t_rgen = ev_ms(ev[2], ev[3]) * 1e-3;
     d.t_sketch = ev_ms(ev[3], ev[4]) * 1e-3;
     d.t_gather = ev_ms(ev[4], ev[5]) * 1e-3;
