@@ -354,7 +354,9 @@ rid_status rid_comm_init(rid_ctx* c, const void* id, int rank, int nranks) {
     ncclCommDestroy(c->comm);
     c->comm = nullptr;
   }
-  if (nranks > 1) {
+  // a 1-rank communicator is created only on request (RID_FORCE_NCCL=1): it routes a single
+  // GPU through the collective code path (tests/test_gpu_collective.py)
+  if (nranks > 1 || getenv("RID_FORCE_NCCL")) {
     ncclUniqueId u;
     std::memcpy(&u, id, sizeof u);
     RID_NCCL(c, ncclCommInitRank(&c->comm, nranks, u, rank));
@@ -476,7 +478,7 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
       d.launches += 1;
     }
     RID_CUDA(c, cudaEventRecord(ev[4], c->stream));
-    if (c->nranks > 1) {
+    if (c->comm) {
       RID_NCCL(c, ncclAllGather(Yw + col0 * l, Yw, (size_t)(2 * l * n_loc), ncclDouble, c->comm,
                                 c->stream));
     }
@@ -615,6 +617,7 @@ rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, 
   if (c->nranks == 1 && (col0 != 0 || n_loc != n))
     return fail(c, RID_EINVAL, "rid_error_estimate: without a communicator the shard must be all of A");
   const int G = c->nranks;
+  const bool coll = c->comm != nullptr;  // collective path (G > 1, or forced for testing)
   cudaEvent_t* ev = c->ev;
   RID_CUDA(c, cudaEventRecord(ev[0], c->stream));
   MatArg a, p;
@@ -632,7 +635,7 @@ rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, 
   RID_TRY(ws_get(c, "estsb", sizeof(double) * 4 * k, &psb));
   RID_TRY(ws_get(c, "estpx", sizeof(double) * 4 * k * pl.px_parts, &ppx));
   RID_TRY(ws_get(c, "estax", sizeof(double) * 4 * m * pl.ax_parts, &pax));
-  RID_TRY(ws_get(c, "estwall", sizeof(double) * 4 * m * (G > 1 ? G : 1), &pwall));
+  RID_TRY(ws_get(c, "estwall", sizeof(double) * 4 * m * (coll ? G : 1), &pwall));
   const int nparts_max = pl.z_blocks > pl.x0_blocks ? pl.z_blocks : pl.x0_blocks;
   RID_TRY(ws_get(c, "estnp", sizeof(double) * 2 * nparts_max, &pnp));
   RID_TRY(ws_get(c, "estnn", sizeof(double) * 2 * (G + 1), &pnn));
@@ -641,38 +644,38 @@ rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, 
   double2 *x = (double2*)px, *z = (double2*)pz, *y = (double2*)py;
   double *u = (double*)pu, *nn = (double*)pnn;
   // B = A[:, J], replicated on every rank (owners contribute their columns, the rest are 0)
-  if (G > 1) RID_CUDA(c, cudaMemsetAsync(B, 0, sizeof(double2) * m * k, c->stream));
+  if (coll) RID_CUDA(c, cudaMemsetAsync(B, 0, sizeof(double2) * m * k, c->stream));
   RID_CUDA(c, rid::gather_columns((const double2*)a.dev, lda, m, (const int64_t*)pJ, k, col0, n_loc,
                                   B, m, c->stream));
-  if (G > 1)
+  if (coll)
     RID_NCCL(c, ncclAllReduce(B, B, (size_t)(2 * m * k), ncclDouble, ncclSum, c->comm, c->stream));
   // reduce a dd scalar over ranks: local parts -> nn[2*rank], allgather, merge -> nn[2*G]
   auto scalar_allreduce = [&](const double* parts, int nparts) -> rid_status {
-    double* slot = nn + 2 * (G > 1 ? c->rank : 0);
+    double* slot = nn + 2 * (coll ? c->rank : 0);
     RID_CUDA(c, rid::est_merge_scalar(parts, nparts, slot, c->stream));
-    if (G > 1) {
+    if (coll) {
       RID_NCCL(c, ncclAllGather(slot, nn, 2, ncclDouble, c->comm, c->stream));
       RID_CUDA(c, rid::est_merge_scalar(nn, G, nn + 2 * G, c->stream));
     }
     return RID_OK;
   };
-  const double* nn_final = nn + (G > 1 ? 2 * G : 0);
+  const double* nn_final = nn + (coll ? 2 * G : 0);
   RID_CUDA(c, rid::est_x0(seed, col0, n_loc, x, (double*)pnp, pl, c->stream));
   RID_TRY(scalar_allreduce((const double*)pnp, pl.x0_blocks));
   RID_CUDA(c, rid::est_normalise(x, n_loc, nn_final, x, nullptr, c->stream));
   RID_CUDA(c, cudaEventRecord(ev[1], c->stream));
   for (int it = 0; it < q; ++it) {
     // u = P x (replicated after the exchange)
-    double* u_loc = u + (size_t)4 * k * (G > 1 ? c->rank : 0);
+    double* u_loc = u + (size_t)4 * k * (coll ? c->rank : 0);
     RID_CUDA(c, rid::est_px((const double2*)p.dev, ldp, k, n_loc, x, (double*)ppx, u_loc, pl, c->stream));
-    if (G > 1) {
+    if (coll) {
       RID_NCCL(c, ncclAllGather(u_loc, u, (size_t)(4 * k), ncclDouble, c->comm, c->stream));
       RID_CUDA(c, rid::est_merge_vec(u, G, k, (double*)psb, c->stream));  // sb as scratch
       RID_CUDA(c, cudaMemcpyAsync(u, psb, sizeof(double) * 4 * k, cudaMemcpyDeviceToDevice, c->stream));
     }
     // y = A x - B u (replicated)
     RID_CUDA(c, rid::est_ax((const double2*)a.dev, lda, m, n_loc, x, (double*)pax, pl, c->stream));
-    if (G > 1) {
+    if (coll) {
       double* w_loc = (double*)pwall + (size_t)4 * m * c->rank;
       RID_CUDA(c, rid::est_merge_vec((const double*)pax, pl.ax_parts, m, w_loc, c->stream));
       RID_NCCL(c, ncclAllGather(w_loc, pwall, (size_t)(4 * m), ncclDouble, c->comm, c->stream));
@@ -694,7 +697,7 @@ rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, 
     rid_diag d{};
     d.t_total = ev_ms(ev[0], ev[2]) * 1e-3;
     d.t_h2d = ev_ms(ev[0], ev[1]) * 1e-3;
-    d.launches = 3 + 3 + q * (3 + 4 + (G > 1 ? 2 : 1) + 1);
+    d.launches = 3 + 3 + q * (3 + 4 + (coll ? 2 : 1) + 1);
     *diag = d;
   }
   return RID_OK;
