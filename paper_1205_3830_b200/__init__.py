@@ -58,7 +58,7 @@ _lib = None
 EXPORTS = ["rid_create", "rid_destroy", "rid_last_error", "rid_version", "rid_comm_id_bytes",
            "rid_comm_get_id", "rid_comm_init", "rid_comm_info", "rid_generate", "rid_sketch",
            "rid_decompose", "rid_error_estimate", "rid_error_bound", "rid_normal_fill",
-           "rid_qrcp", "rid_factor_solve"]
+           "rid_qrcp", "rid_factor_solve", "rid_sketch_splits"]
 
 
 def lib():
@@ -82,7 +82,8 @@ def lib():
         "rid_comm_init": ([p, p, ci, ci], ci),
         "rid_comm_info": ([p, ctypes.POINTER(ci), ctypes.POINTER(ci)], ci),
         "rid_generate": ([p, u64, i64, i64, i64, d, i64, i64, p, i64], ci),
-        "rid_sketch": ([p, u64, u32, i64, p, i64, i64, i64, p, i64], ci),
+        "rid_sketch": ([p, u64, u32, i64, p, i64, i64, i64, i64, p, i64], ci),
+        "rid_sketch_splits": ([p, i64, i64, i64], ci),
         "rid_decompose": ([p, p, i64, i64, i64, i64, i64, i64, i64, u64, p, p, i64, p], ci),
         "rid_error_estimate": ([p, p, i64, i64, i64, i64, i64, p, i64, p, i64, ci, u64, p, p], ci),
         "rid_error_bound": ([i64, i64, i64, d, d], d),
@@ -249,18 +250,27 @@ def generate(seed: int, m: int, n: int, k: int, noise: float, col0: int = 0, n_l
     return out
 
 
-def sketch(A, seed: int, l: int, stream: int = STREAM_R, out=None, ctx: Context | None = None):
-    """Y = R A with R(r, i) = N(seed, stream, r, i) (DMMA, ascending fused K chain)."""
+def sketch(A, seed: int, l: int, stream: int = STREAM_R, out=None, n: int | None = None,
+           ctx: Context | None = None):
+    """Y = R A with R(r, i) = N(seed, stream, r, i) on the DMMA pipe. A may be a column block of
+    an n-column matrix (n defaults to A's own width); n fixes the K-split (sketch_splits)."""
     ctx = ctx or default_context()
     m, n_loc = A.shape
+    n = n_loc if n is None else n
     a = _Buf(A, m, n_loc, "A")
     if out is None:
         out = colmajor_empty(l, n_loc, device=A.device if hasattr(A, "device") else "cpu") \
             if not isinstance(A, np.ndarray) else np.zeros((l, n_loc), np.complex128, order="F")
     y = _Buf(out, l, n_loc, "Y")
-    ctx.check(lib().rid_sketch(ctx.h, seed, stream, l, a.ptr, m, n_loc, a.ld, y.ptr, y.ld),
+    ctx.check(lib().rid_sketch(ctx.h, seed, stream, l, a.ptr, m, n, n_loc, a.ld, y.ptr, y.ld),
               "rid_sketch")
     return out
+
+
+def sketch_splits(m: int, l: int, n: int, ctx: Context | None = None) -> int:
+    """K slices of the sketch of an m x n matrix (1: bit-identical to the oracle's chain)."""
+    ctx = ctx or default_context()
+    return lib().rid_sketch_splits(ctx.h, m, l, n)
 
 
 @dataclass

@@ -30,6 +30,8 @@ struct ZgemmEpilogue {
   double noise;
   uint64_t seed;
   int64_t col0;
+  int64_t kchunk;    // complex K per blockIdx.z slice (K when there is no split)
+  int64_t zstride;   // elements between the partial outputs of consecutive slices
 };
 
 template <int FJ, int FR, int WARPS_J, int WARPS_R, int BK, int STAGES>
@@ -62,7 +64,11 @@ __global__ void __launch_bounds__(WARPS_J* WARPS_R * 32, MINB)
   const int wj = warp % WARPS_J, wr = warp / WARPS_J;
   const int64_t r0c = (int64_t)blockIdx.x * Cfg::BRC;  // complex row offset of this CTA
   const int64_t j0 = (int64_t)blockIdx.y * Cfg::BJ;
-  const int64_t nk = (K + Cfg::BKC - 1) / Cfg::BKC;     // complex-K stages
+  // K slice of this CTA (split-K: blockIdx.z; the slice's partial goes to its own output)
+  const int64_t kbeg = (int64_t)blockIdx.z * ep.kchunk;
+  K = (kbeg + ep.kchunk < K) ? kbeg + ep.kchunk : K;   // end of the slice
+  C += (int64_t)blockIdx.z * ep.zstride;
+  const int64_t nk = (K - kbeg + Cfg::BKC - 1) / Cfg::BKC;  // complex-K stages
 
   // Per-thread copy plan, fixed for the whole K loop: chunk q of the B̃ tile is (column q / BKC,
   // complex K q % BKC), chunk q of the R tile is (K q / BRC, row q % BRC). Only the K offset
@@ -129,7 +135,7 @@ __global__ void __launch_bounds__(WARPS_J* WARPS_R * 32, MINB)
 
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_stage(s, (int64_t)s * Cfg::BKC);
+    if (s < nk) load_stage(s, kbeg + (int64_t)s * Cfg::BKC);
     cp_async_commit();
   }
 
@@ -138,7 +144,7 @@ __global__ void __launch_bounds__(WARPS_J* WARPS_R * 32, MINB)
     __syncthreads();
     {  // prefetch stage kt + STAGES - 1 into the slot freed by stage kt - 1
       const int64_t kn = kt + STAGES - 1;
-      if (kn < nk) load_stage((int)(kn % STAGES), kn * Cfg::BKC);
+      if (kn < nk) load_stage((int)(kn % STAGES), kbeg + kn * Cfg::BKC);
       cp_async_commit();
     }
     const double* sB = smem + (size_t)(kt % STAGES) * Cfg::kStage;
@@ -191,10 +197,27 @@ __global__ void __launch_bounds__(WARPS_J* WARPS_R * 32, MINB)
   }
 }
 
+// Split-K combine: C(r, j) = ((P_0 + P_1) + P_2) + ... in slice order (deterministic).
+__global__ void k_splitk_reduce(const double2* __restrict__ part, int S, int64_t Mout, int64_t N,
+                                double2* __restrict__ C, int64_t ldc) {
+  const int64_t total = Mout * N, zs = Mout * N;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    double2 a = part[q];
+    for (int z = 1; z < S; ++z) {
+      const double2 b = part[z * zs + q];
+      a = make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+    }
+    const int64_t r = q % Mout, j = q / Mout;
+    C[j * ldc + r] = a;
+  }
+}
+
 template <int FJ, int FR, int WARPS_J, int WARPS_R, int BK, int STAGES, int MINB = 1>
 static cudaError_t launch_cfg(const double2* Rm, int64_t ldr, const double2* Bm, int64_t ldb,
                               double2* C, int64_t ldc, int64_t Mout, int64_t N, int64_t K,
-                              const ZgemmEpilogue& ep, cudaStream_t st) {
+                              const ZgemmEpilogue& ep, cudaStream_t st, int ksplit = 1,
+                              double2* partial = nullptr) {
   using Cfg = ZgemmCfg<FJ, FR, WARPS_J, WARPS_R, BK, STAGES>;
   auto kern = k_zgemm_dmma<FJ, FR, WARPS_J, WARPS_R, BK, STAGES, MINB>;
   static bool attr_set = false;  // per-instantiation, set once per process
@@ -206,9 +229,31 @@ static cudaError_t launch_cfg(const double2* Rm, int64_t ldr, const double2* Bm,
   }
   const int64_t tiles_r = (Mout + Cfg::BRC - 1) / Cfg::BRC;
   const int64_t tiles_j = (N + Cfg::BJ - 1) / Cfg::BJ;
-  if (tiles_r > 0x7FFFFFFF || tiles_j > 65535) return cudaErrorInvalidConfiguration;
-  dim3 grid((unsigned)tiles_r, (unsigned)tiles_j);
-  kern<<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep);
+  ZgemmEpilogue e2 = ep;
+  double2* Cout = C;
+  int64_t ldo = ldc;
+  int S = 1;
+  e2.kchunk = K > 0 ? K : 1;
+  e2.zstride = 0;
+  if (ksplit > 1 && partial && ep.mode == 0) {
+    int64_t kc = (K + ksplit - 1) / ksplit;
+    kc = ((kc + Cfg::BKC - 1) / Cfg::BKC) * Cfg::BKC;
+    S = (int)((K + kc - 1) / kc);
+    if (S > 1) {
+      e2.kchunk = kc;
+      e2.zstride = Mout * N;
+      Cout = partial;
+      ldo = Mout;
+    }
+  }
+  if (tiles_r > 0x7FFFFFFF || tiles_j > 65535 || S > 65535) return cudaErrorInvalidConfiguration;
+  dim3 grid((unsigned)tiles_r, (unsigned)tiles_j, (unsigned)S);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(Rm, ldr, Bm, ldb, Cout, ldo, Mout, N, K, e2);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || S == 1) return e;
+  int64_t blocks = (Mout * N + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_splitk_reduce<<<(unsigned)blocks, 256, 0, st>>>(partial, S, Mout, N, C, ldc);
   return cudaGetLastError();
 }
 
@@ -246,15 +291,43 @@ int zgemm_pick_fr(int64_t Mout) {
   return best;
 }
 
+// Split-K policy for the sketch (K = m long, few output tiles): every rank of a G <= 8 column
+// sharding must see enough CTAs, and every column must be computed identically for any G, so the
+// slice count depends only on (Mout, K, n_ref) with n_ref = n_global / 8 (the smallest shard an
+// 8-GPU box runs): S = ceil(2 * SMs / tiles(n_ref)), each slice >= 512 complex K, S <= 64.
+// C4 (n_ref = 4096 -> 384 tiles) keeps S = 1 and with it the bit-identity to the oracle's single
+// ascending chain; C2, C3, C5 split (their Y then agrees with the oracle to rounding, ~1e-16).
+int zgemm_ksplit(int64_t Mout, int64_t K, int64_t n_ref, int num_sms) {
+  if (const char* v = getenv("RID_SKETCH_SPLIT")) {  // tests: force a slice count (1 = unsplit)
+    const int s = atoi(v);
+    if (s >= 1) return s;
+  }
+  if (Mout >= 2048 || n_ref <= 0 || K <= 0) return 1;
+  const int fr = zgemm_pick_fr(Mout);
+  int64_t br = 16 * fr;
+#define RID_B_BR(FRV) \
+  if (fr == (FRV)) br = 8 * (FRV);
+  RID_FR_B(RID_B_BR)
+#undef RID_B_BR
+  const int64_t tiles = ((n_ref + 63) / 64) * ((2 * Mout + br - 1) / br);
+  int64_t s = (2 * (int64_t)num_sms + tiles - 1) / tiles;
+  const int64_t smax = K / 512 > 1 ? K / 512 : 1;
+  if (s > smax) s = smax;
+  if (s > 64) s = 64;
+  return s < 1 ? 1 : (int)s;
+}
+
 cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int64_t ldb,
                           double2* C, int64_t ldc, int64_t Mout, int64_t N, int64_t K,
-                          int mode, double noise, uint64_t seed, int64_t col0, cudaStream_t st) {
+                          int mode, double noise, uint64_t seed, int64_t col0, cudaStream_t st,
+                          int ksplit, double2* partial) {
   if (Mout <= 0 || N <= 0) return cudaSuccess;
-  ZgemmEpilogue ep{mode, noise, seed, col0};
+  ZgemmEpilogue ep{mode, noise, seed, col0, K, 0};
   if (const char* v = getenv("RID_ZGEMM_VARIANT")) {  // tile experiments (tools/tune_*.py)
     const int id = atoi(v);
 #define RID_V(ID, ...) \
-  if (id == ID) return launch_cfg<__VA_ARGS__>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
+  if (id == ID)        \
+    return launch_cfg<__VA_ARGS__>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st, ksplit, partial);
     RID_V(1, 2, 11, 4, 2, 16, 4, 1)   // round-1 first version
     RID_V(2, 1, 11, 8, 1, 16, 3, 3)
     RID_V(3, 1, 17, 8, 1, 16, 4, 2)
@@ -262,12 +335,17 @@ cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int
     RID_V(5, 4, 8, 4, 2, 16, 4, 1)    // round-1 first generation tile
 #undef RID_V
   }
-  if (Mout >= 2048) return launch_cfg<1, 8, 8, 1, 16, 3, 3>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
+  if (Mout >= 2048)
+    return launch_cfg<1, 8, 8, 1, 16, 3, 3>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
   switch (zgemm_pick_fr(Mout)) {
-#define RID_CASE_A(FRV) \
-  case FRV: return launch_cfg<2, FRV, 4, 2, 16, 3, 2>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
-#define RID_CASE_B(FRV) \
-  case FRV: return launch_cfg<1, FRV, 8, 1, 16, 3, 2>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
+#define RID_CASE_A(FRV)                                                                        \
+  case FRV:                                                                                    \
+    return launch_cfg<2, FRV, 4, 2, 16, 3, 2>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st,    \
+                                              ksplit, partial);
+#define RID_CASE_B(FRV)                                                                        \
+  case FRV:                                                                                    \
+    return launch_cfg<1, FRV, 8, 1, 16, 3, 2>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st,    \
+                                              ksplit, partial);
     RID_FR_A(RID_CASE_A)
     RID_FR_B(RID_CASE_B)
 #undef RID_CASE_A

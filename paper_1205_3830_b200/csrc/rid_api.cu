@@ -228,7 +228,7 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
 // device-resident call. The device never holds more than two chunks of A.
 rid_status sketch_streamed(rid_ctx* c, const double2* R, const rid_z* hostA, int64_t m,
                            int64_t n_loc, int64_t lda, int64_t l, double2* Y, int* launches,
-                           double* t_h2d) {
+                           double* t_h2d, int ksplit, double2* partial) {
   if (!c->copy_stream) {
     RID_CUDA(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     for (int b = 0; b < 2; ++b) {
@@ -259,9 +259,9 @@ rid_status sketch_streamed(rid_ctx* c, const double2* R, const rid_z* hostA, int
     RID_CUDA(c, cudaEventRecord(c->ev_copied[b], c->copy_stream));
     RID_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0));
     RID_CUDA(c, rid::zgemm_ordered(R, l, (const double2*)buf[b], m, Y + j0 * l, l, l, nc, m, 0,
-                                   0.0, 0, 0, c->stream));
+                                   0.0, 0, 0, c->stream, ksplit, partial));
     RID_CUDA(c, cudaEventRecord(c->ev_used[b], c->stream));
-    ++*launches;
+    *launches += ksplit > 1 ? 2 : 1;
   }
   RID_CUDA(c, cudaEventRecord(c->ev_copy1, c->copy_stream));
   if (t_h2d) {
@@ -414,21 +414,28 @@ rid_status rid_generate(rid_ctx* c, uint64_t seed, int64_t m, int64_t n, int64_t
   return RID_OK;
 }
 
+int rid_sketch_splits(const rid_ctx* c, int64_t m, int64_t l, int64_t n) {
+  if (!c || m < 1 || l < 1 || n < 1) return 1;
+  return rid::zgemm_ksplit(l, m, n / 8, c->num_sms);
+}
+
 rid_status rid_sketch(rid_ctx* c, uint64_t seed, uint32_t stream, int64_t l, const rid_z* A,
-                      int64_t m, int64_t n_loc, int64_t lda, rid_z* Y, int64_t ldy) {
+                      int64_t m, int64_t n, int64_t n_loc, int64_t lda, rid_z* Y, int64_t ldy) {
   RID_TRY(check_ctx(c));
-  if (l < 1 || l > m || m < 1 || n_loc < 0 || lda < m || ldy < l || !A || !Y ||
+  if (l < 1 || l > m || m < 1 || n_loc < 0 || n < n_loc || lda < m || ldy < l || !A || !Y ||
       m > (int64_t)0xFFFFFFFFLL)
     return fail(c, RID_EINVAL, "rid_sketch: bad arguments");
   if (n_loc == 0) return RID_OK;
   MatArg a, y;
   RID_TRY(stage_in(c, "stage_A", A, m, n_loc, lda, sizeof(rid_z), true, &a));
   RID_TRY(stage_in(c, "stage_Y", Y, l, n_loc, ldy, sizeof(rid_z), false, &y));
-  void* pR;
+  void *pR, *pS = nullptr;
   RID_TRY(ws_get(c, "R", sizeof(double2) * l * m, &pR));
+  const int S = rid::zgemm_ksplit(l, m, n / 8, c->num_sms);
+  if (S > 1) RID_TRY(ws_get(c, "splitk", sizeof(double2) * S * l * n_loc, &pS));
   RID_CUDA(c, rid::normal_fill(seed, stream, l, m, 0, 0, (double2*)pR, l, c->stream));
   RID_CUDA(c, rid::zgemm_ordered((const double2*)pR, l, (const double2*)a.dev, lda, (double2*)y.dev,
-                                 ldy, l, n_loc, m, 0, 0.0, 0, 0, c->stream));
+                                 ldy, l, n_loc, m, 0, 0.0, 0, 0, c->stream, S, (double2*)pS));
   RID_TRY(stage_out(c, y, Y, l, n_loc, ldy, sizeof(rid_z)));
   if (a.host || y.host) RID_CUDA(c, cudaStreamSynchronize(c->stream));
   return RID_OK;
@@ -460,6 +467,14 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
   RID_TRY(ws_get(c, "Y", sizeof(double2) * l * n, &pY));
   RID_TRY(ws_get(c, "R", sizeof(double2) * l * m, &pR));
   double2* Yw = (double2*)pY;
+  // K-split of the sketch: a function of (m, l, n) only, so Y is identical for every sharding
+  const int S = rid::zgemm_ksplit(l, m, n / 8, c->num_sms);
+  void* pS = nullptr;
+  if (S > 1) {
+    const int64_t cols = a_host ? std::min<int64_t>(n_loc, std::max<int64_t>(64, (int64_t)(1 << 30) / (16 * m)))
+                                : n_loc;
+    RID_TRY(ws_get(c, "splitk", sizeof(double2) * S * l * cols, &pS));
+  }
   int64_t* Jdev = nullptr;
   rid_status st = RID_OK;
   int info[2] = {0, 0};
@@ -471,11 +486,12 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
     d.launches += 2;  // R fill, QRCP
     if (a_host) {
       RID_TRY(sketch_streamed(c, (const double2*)pR, A, m, n_loc, lda, l, Yw + col0 * l,
-                              &d.launches, nullptr));
+                              &d.launches, nullptr, S, (double2*)pS));
     } else {
       RID_CUDA(c, rid::zgemm_ordered((const double2*)pR, l, (const double2*)a.dev, lda,
-                                     Yw + col0 * l, l, l, n_loc, m, 0, 0.0, 0, 0, c->stream));
-      d.launches += 1;
+                                     Yw + col0 * l, l, l, n_loc, m, 0, 0.0, 0, 0, c->stream, S,
+                                     (double2*)pS));
+      d.launches += S > 1 ? 2 : 1;
     }
     RID_CUDA(c, cudaEventRecord(ev[4], c->stream));
     if (c->comm) {

@@ -8,10 +8,14 @@ namespace rid {
 
 // Ordered complex GEMM C = Rm · Bm on DMMA (k_zgemm.cu). mode 1 adds noise·E(r, col0 + j) with
 // E from Philox stream 3 (generation epilogue).
+// ksplit > 1 splits K into slices summed by a fixed-order combine (partial: ksplit*Mout*N elems).
 cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int64_t ldb,
                           double2* C, int64_t ldc, int64_t Mout, int64_t N, int64_t K, int mode,
-                          double noise, uint64_t seed, int64_t col0, cudaStream_t st);
+                          double noise, uint64_t seed, int64_t col0, cudaStream_t st,
+                          int ksplit = 1, double2* partial = nullptr);
 int zgemm_pick_fr(int64_t Mout);
+// K slices for a sketch of Mout rows, K = m, chosen from n_ref = n_global / 8 only (G-invariant)
+int zgemm_ksplit(int64_t Mout, int64_t K, int64_t n_ref, int num_sms);
 
 // out(i, j) = N(seed, s, row0 + i, col0 + j), column-major with leading dimension ld (k_misc.cu)
 cudaError_t normal_fill(uint64_t seed, uint32_t s, int64_t rows, int64_t cols, int64_t row0,

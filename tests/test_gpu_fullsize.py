@@ -70,8 +70,14 @@ def test_fullsize_against_oracle_golden(rid, orc, name):
         assert np.array_equal(bits(A[:, j].cpu().numpy()), bits(a_o[:, 0])), f"A[:, {j}]"
     # sketch: sampled columns bitwise, Frobenius norm
     Y = rid.sketch(A, seed, c.l)
+    S = rid.sketch_splits(c.m, c.l, c.n)
     for j in cols:
-        assert np.array_equal(bits(Y[:, j].cpu().numpy()), bits(unhex(g["Y_cols"][str(j)]))), f"Y[:, {j}]"
+        y_o = unhex(g["Y_cols"][str(j)])
+        y_g = Y[:, j].cpu().numpy()
+        if S == 1:  # one ascending fused chain: bit-identical
+            assert np.array_equal(bits(y_g), bits(y_o)), f"Y[:, {j}]"
+        else:  # S fixed-order slice sums
+            assert np.linalg.norm(y_g - y_o) <= 1e-13 * np.linalg.norm(y_o), f"Y[:, {j}]"
     yf = float(torch.linalg.norm(Y))
     assert abs(yf - g["Y_fro"]) <= 1e-12 * g["Y_fro"]
     del Y

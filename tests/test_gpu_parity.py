@@ -94,13 +94,24 @@ SKETCH_CASES = [  # (seed, m, n, k, noise, l)
 
 
 @pytest.mark.parametrize("seed,m,n,k,noise,l", SKETCH_CASES)
-def test_sketch_bitexact(rid, orc, seed, m, n, k, noise, l):
+def test_sketch_bitexact(rid, orc, seed, m, n, k, noise, l, monkeypatch):
     A_g = rid.generate(seed, m, n, k, noise)
-    Y_g = np_(rid.sketch(A_g, seed, l))
     A_o = orc.generate(seed, m, n, k, noise)
     Y_o = orc.sketch(A_o, seed, l)
-    assert relf(Y_g, Y_o) <= 1e-12  # the north-star bar ...
-    assert bits_equal(Y_g, Y_o)      # ... and in fact bit-identical (same fused order)
+    # the default launch (K split into S slices when the tile count is small): the north-star bar
+    S = rid.sketch_splits(m, l, n)
+    Y_g = np_(rid.sketch(A_g, seed, l))
+    assert relf(Y_g, Y_o) <= 1e-12
+    if S == 1:
+        assert bits_equal(Y_g, Y_o)
+    # one slice: the single ascending fused chain, bit-identical to the oracle's naive loop
+    monkeypatch.setenv("RID_SKETCH_SPLIT", "1")
+    Y_1 = np_(rid.sketch(A_g, seed, l))
+    assert bits_equal(Y_1, Y_o)
+    # an explicit 3-slice split: fixed-order slice sums, within rounding
+    monkeypatch.setenv("RID_SKETCH_SPLIT", "3")
+    Y_3 = np_(rid.sketch(A_g, seed, l))
+    assert relf(Y_3, Y_o) <= 1e-14
 
 
 def test_sketch_retry_stream_and_ld(rid, orc):
@@ -177,7 +188,7 @@ def test_g_emulation_bitwise(rid):
             col0, nl = rid.shard_range(n, g, G)
             A_g = rid.generate(seed, m, n, k, noise, col0, nl)
             assert torch.equal(A_g.contiguous(), A[:, col0:col0 + nl].contiguous())
-            Ys.append(rid.sketch(A_g, seed, l))
+            Ys.append(rid.sketch(A_g, seed, l, n=n))  # the same K-split as the whole matrix
         Y = torch.cat([y.T for y in Ys]).T  # column-major concatenation
         for g in range(G):
             col0, nl = rid.shard_range(n, g, G)
