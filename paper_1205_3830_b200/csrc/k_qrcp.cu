@@ -346,7 +346,10 @@ __global__ void __launch_bounds__(kQrcpThreads, 2)
     const int cpw = 32 / lpc, sg = lane / lpc, sl = lane % lpc;
     Top2 loc;
     top2_init(loc);
-    for (int64_t c0 = c_lo + (int64_t)warp * cpw; c0 < c_hi; c0 += (int64_t)kQrcpWarps * cpw) {
+    // (a one-iteration-ahead cp.async prefetch of the next column segment was measured: no gain
+    // — the early steps already stream at ~5.9 TB/s of read+write — so loads stay direct)
+    const int64_t cstride = (int64_t)kQrcpWarps * cpw;
+    for (int64_t c0 = c_lo + (int64_t)warp * cpw; c0 < c_hi; c0 += cstride) {
       const int64_t c = c0 + sg;
       // a lane group works only on a live, unchosen, non-pivot column; the shuffles below are
       // executed by the whole warp regardless (dead groups carry zeros)
