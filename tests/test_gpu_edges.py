@@ -1,0 +1,98 @@
+"""Edge cases and determinism of the CUDA path (through the C ABI), against the oracle.
+
+- degenerate shapes: k = l, k = n (P a permutation), l = m, k = 1, a single column, n_loc not a
+  multiple of any tile, m not a multiple of 8;
+- run-to-run determinism: two calls give bitwise identical J, P, Y and estimate (a race canary);
+- the rank-failure retry path (one re-randomisation with R stream 20);
+- host P with device A, and J returned to a host array.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def rid():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1205_3830_b200 import build
+
+    build.build()
+    import paper_1205_3830_b200 as rid
+
+    return rid
+
+
+def np_(t):
+    return t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t)
+
+
+def relf(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+EDGE = [  # (name, seed, m, n, k, l, noise)
+    ("k=l", 1, 500, 300, 24, 24, 1e-9),
+    ("k=n", 2, 300, 40, 40, 48, 0.0),
+    ("l=m", 3, 40, 200, 8, 40, 1e-7),
+    ("k=1", 4, 256, 100, 1, 9, 1e-6),
+    ("one column", 5, 128, 1, 1, 4, 0.0),
+    ("ragged", 6, 1001, 777, 13, 29, 1e-8),
+]
+
+
+@pytest.mark.parametrize("name,seed,m,n,k,l,noise", EDGE)
+def test_edge_shapes(rid, orc, name, seed, m, n, k, l, noise):
+    A_o = orc.generate(seed, m, n, k, noise)
+    d = orc.decompose(A_o, k, l, seed)
+    A = rid.generate(seed, m, n, k, noise)
+    r = rid.decompose(A, k, l, seed)
+    J, P = np_(r.J), np_(r.P)
+    if k > 1 and d.tie_margins[:-1].min() < 1e-10:
+        pytest.skip(f"{name}: tie-ambiguous (margin {d.tie_margins[:-1].min():.2e})")
+    assert J.tolist() == d.J.tolist()
+    assert np.array_equal(P[:, J], np.eye(k, dtype=complex))
+    assert relf(P, d.P) <= 1e-10
+    if n == k:  # P is a permutation matrix, exactly
+        assert np.array_equal(np.abs(P), np.abs(P).round()) and np.allclose(P.sum(0), 1)
+
+
+def test_run_to_run_determinism(rid):
+    m, n, k, l, noise, seed = 4096, 2048, 96, 112, 1e-10, 9
+    A = rid.generate(seed, m, n, k, noise)
+    outs = []
+    for _ in range(2):
+        Y = rid.sketch(A, seed, l)
+        r = rid.decompose(A, k, l, seed)
+        e = rid.error_estimate(A, r.J, r.P, 4, seed)
+        outs.append((np_(Y), np_(r.J), np_(r.P), e))
+    (Y0, J0, P0, e0), (Y1, J1, P1, e1) = outs
+    assert np.array_equal(np.ascontiguousarray(Y0).view(np.uint64),
+                          np.ascontiguousarray(Y1).view(np.uint64))
+    assert np.array_equal(J0, J1)
+    assert np.array_equal(np.ascontiguousarray(P0).view(np.uint64),
+                          np.ascontiguousarray(P1).view(np.uint64))
+    assert e0 == e1
+
+
+def test_retry_path(rid, orc):
+    """A matrix of exact rank k - 1 < k makes the first sketch rank-deficient: the library retries
+    once with R stream 20 and then reports RID_ERANK with the achieved rank."""
+    A = rid.generate(3, 300, 120, 5, 0.0)
+    with pytest.raises(rid.RidError) as e:
+        rid.decompose(A, 6, 12, 3)
+    assert e.value.status == rid.RID_ERANK
+    assert "rank 5" in str(e.value)
+
+
+def test_host_outputs(rid, orc):
+    m, n, k, l = 600, 150, 10, 20
+    A = rid.generate(4, m, n, k, 1e-9)
+    J = np.zeros(k, np.int64)
+    P = np.zeros((k, n), np.complex128, order="F")
+    r = rid.decompose(A, k, l, 4, J=J, P=P)
+    ref = rid.decompose(A, k, l, 4)
+    assert J.tolist() == np_(ref.J).tolist()
+    assert np.array_equal(P, np_(ref.P))
