@@ -32,6 +32,7 @@ struct ZgemmEpilogue {
   int64_t col0;
   int64_t kchunk;    // complex K per blockIdx.z slice (K when there is no split)
   int64_t zstride;   // elements between the partial outputs of consecutive slices
+  int regen_stream;  // REGEN kernels: Philox stream of R
 };
 
 template <int FJ, int FR, int WARPS_J, int WARPS_R, int BK, int STAGES>
@@ -51,7 +52,10 @@ struct ZgemmCfg {
   static_assert(PR % 8 == 4 && PR >= BRC, "R pitch");
 };
 
-template <int FJ, int FR, int WARPS_J, int WARPS_R, int BK, int STAGES, int MINB>
+// REGEN = 1: the R tile is regenerated from Philox inside the kernel (R(r, i) = N(seed,
+// ep.regen_stream, r, i), the north star's literal design) instead of streamed from the
+// pre-generated R in HBM/L2 — kept as the measured alternative.
+template <int FJ, int FR, int WARPS_J, int WARPS_R, int BK, int STAGES, int MINB, int REGEN = 0>
 __global__ void __launch_bounds__(WARPS_J* WARPS_R * 32, MINB)
     k_zgemm_dmma(const double2* __restrict__ Rm, int64_t ldr, const double2* __restrict__ Bm,
                  int64_t ldb, double2* __restrict__ C, int64_t ldc, int64_t Mout, int64_t N,
@@ -116,7 +120,16 @@ __global__ void __launch_bounds__(WARPS_J* WARPS_R * 32, MINB)
     for (int i = 0; i < kChR; ++i) {
       if (inR[i]) {
         const bool ok = okR[i] && (full || kc0 + kcR[i] < K);
-        cp_async16(sR + dstR[i], ok ? srcR[i] + roff : Rm, ok);
+        if (REGEN) {
+          const int q = tid + i * Cfg::kThreads;
+          const int64_t gr = r0c + q % Cfg::BRC, gk = kc0 + kcR[i];
+          const double2 v = ok ? rid_normal(ep.seed, (uint32_t)ep.regen_stream, (uint32_t)gr,
+                                            (uint32_t)gk)
+                               : make_double2(0.0, 0.0);
+          *reinterpret_cast<double2*>(sR + dstR[i]) = v;
+        } else {
+          cp_async16(sR + dstR[i], ok ? srcR[i] + roff : Rm, ok);
+        }
       }
     }
   };
@@ -213,13 +226,13 @@ __global__ void k_splitk_reduce(const double2* __restrict__ part, int S, int64_t
   }
 }
 
-template <int FJ, int FR, int WARPS_J, int WARPS_R, int BK, int STAGES, int MINB = 1>
+template <int FJ, int FR, int WARPS_J, int WARPS_R, int BK, int STAGES, int MINB = 1, int REGEN = 0>
 static cudaError_t launch_cfg(const double2* Rm, int64_t ldr, const double2* Bm, int64_t ldb,
                               double2* C, int64_t ldc, int64_t Mout, int64_t N, int64_t K,
                               const ZgemmEpilogue& ep, cudaStream_t st, int ksplit = 1,
                               double2* partial = nullptr) {
   using Cfg = ZgemmCfg<FJ, FR, WARPS_J, WARPS_R, BK, STAGES>;
-  auto kern = k_zgemm_dmma<FJ, FR, WARPS_J, WARPS_R, BK, STAGES, MINB>;
+  auto kern = k_zgemm_dmma<FJ, FR, WARPS_J, WARPS_R, BK, STAGES, MINB, REGEN>;
   static bool attr_set = false;  // per-instantiation, set once per process
   if (!attr_set) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -322,7 +335,7 @@ cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int
                           int mode, double noise, uint64_t seed, int64_t col0, cudaStream_t st,
                           int ksplit, double2* partial) {
   if (Mout <= 0 || N <= 0) return cudaSuccess;
-  ZgemmEpilogue ep{mode, noise, seed, col0, K, 0};
+  ZgemmEpilogue ep{mode, noise, seed, col0, K, 0, 0};
   if (const char* v = getenv("RID_ZGEMM_VARIANT")) {  // tile experiments (tools/tune_*.py)
     const int id = atoi(v);
 #define RID_V(ID, ...) \
@@ -334,6 +347,16 @@ cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int
     RID_V(4, 1, 3, 8, 1, 16, 3, 4)
     RID_V(5, 4, 8, 4, 2, 16, 4, 1)    // round-1 first generation tile
 #undef RID_V
+    // in-kernel Philox regeneration of R (REGEN): ep.seed / regen_stream from RID_REGEN_STREAM
+    if (id >= 10 && id <= 11) {
+      ep.seed = seed;
+      ep.regen_stream = getenv("RID_REGEN_STREAM") ? atoi(getenv("RID_REGEN_STREAM")) : 4;
+      if (id == 10)
+        return launch_cfg<2, 11, 4, 2, 16, 3, 2, 1>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st,
+                                                     ksplit, partial);
+      return launch_cfg<1, 17, 8, 1, 16, 3, 2, 1>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st,
+                                                   ksplit, partial);
+    }
   }
   if (Mout >= 2048)
     return launch_cfg<1, 8, 8, 1, 16, 3, 3>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);

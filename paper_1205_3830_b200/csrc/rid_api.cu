@@ -435,7 +435,7 @@ rid_status rid_sketch(rid_ctx* c, uint64_t seed, uint32_t stream, int64_t l, con
   if (S > 1) RID_TRY(ws_get(c, "splitk", sizeof(double2) * S * l * n_loc, &pS));
   RID_CUDA(c, rid::normal_fill(seed, stream, l, m, 0, 0, (double2*)pR, l, c->stream));
   RID_CUDA(c, rid::zgemm_ordered((const double2*)pR, l, (const double2*)a.dev, lda, (double2*)y.dev,
-                                 ldy, l, n_loc, m, 0, 0.0, 0, 0, c->stream, S, (double2*)pS));
+                                 ldy, l, n_loc, m, 0, 0.0, seed, 0, c->stream, S, (double2*)pS));
   RID_TRY(stage_out(c, y, Y, l, n_loc, ldy, sizeof(rid_z)));
   if (a.host || y.host) RID_CUDA(c, cudaStreamSynchronize(c->stream));
   return RID_OK;
@@ -489,7 +489,7 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
                               &d.launches, nullptr, S, (double2*)pS));
     } else {
       RID_CUDA(c, rid::zgemm_ordered((const double2*)pR, l, (const double2*)a.dev, lda,
-                                     Yw + col0 * l, l, l, n_loc, m, 0, 0.0, 0, 0, c->stream, S,
+                                     Yw + col0 * l, l, l, n_loc, m, 0, 0.0, seed, 0, c->stream, S,
                                      (double2*)pS));
       d.launches += S > 1 ? 2 : 1;
     }
