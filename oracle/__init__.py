@@ -27,6 +27,7 @@ _LIB = os.path.join(_HERE, "librid_oracle.so")
 
 RID_OK, RID_EINVAL, RID_ERANK, RID_ESINGULAR, RID_ENOMEM = 0, 1, 2, 3, 4
 STREAM_X, STREAM_Y0, STREAM_E, STREAM_R, STREAM_X0, STREAM_R_RETRY = 1, 2, 3, 4, 5, 20
+STREAM_PHASE, STREAM_SAMPLE, STREAM_PHASE_RETRY, STREAM_SAMPLE_RETRY = 6, 7, 22, 23
 
 
 class OracleError(RuntimeError):
@@ -90,6 +91,10 @@ def lib():
         L.orc_error_bound.restype = d
         L.orc_noise_floor.argtypes = [i64, i64, d]
         L.orc_noise_floor.restype = d
+        L.orc_srft_plan.argtypes = [u64, u32, u32, i64, i64, p, p]
+        L.orc_srft_plan.restype = ctypes.c_int
+        L.orc_srft_apply.argtypes = [p, p, i64, i64, i64, p, i64, p, i64]
+        L.orc_srft_apply.restype = ctypes.c_int
         L.orc_set_threads.argtypes = [ctypes.c_int]
         L.orc_set_threads.restype = ctypes.c_int
         _lib = L
@@ -216,15 +221,49 @@ class Decomposition:
     extra: dict = field(default_factory=dict)
 
 
-def decompose(A, k: int, l: int, seed: int) -> Decomposition:
-    """The whole ID: sketch -> pivoted CGS2 (one retry on stream 20) -> back-substitution."""
+def srft_plan(seed: int, m: int, l: int, retry: bool = False):
+    """SRFT plan (docs/RNG.md §7): phases d (m complex, |d| = 1) and row samples s (l ints)."""
+    d = np.zeros(m, np.complex128)
+    s = np.zeros(l, np.int64)
+    sp, ss = (STREAM_PHASE_RETRY, STREAM_SAMPLE_RETRY) if retry else (STREAM_PHASE, STREAM_SAMPLE)
+    st = lib().orc_srft_plan(seed, sp, ss, m, l, _ptr(d), _ptr(s))
+    if st:
+        raise OracleError(st, "srft_plan")
+    return d, s
+
+
+def srft_apply(d, s, A):
+    """Y = S F D A for an explicit plan (Eqs. 4-7), direct ascending sums."""
+    A = _fortran_c128(A)
+    m, n_loc = A.shape
+    d = np.ascontiguousarray(d, np.complex128)
+    s = np.ascontiguousarray(s, np.int64)
+    l = s.size
+    Y = np.zeros((l, n_loc), np.complex128, order="F")
+    st = lib().orc_srft_apply(_ptr(d), _ptr(s), l, m, n_loc, _ptr(A), m, _ptr(Y), l)
+    if st:
+        raise OracleError(st, "srft_apply")
+    return Y
+
+
+def srft_sketch(A, seed: int, l: int, retry: bool = False):
+    A = _fortran_c128(A)
+    d, s = srft_plan(seed, A.shape[0], l, retry)
+    return srft_apply(d, s, A)
+
+
+def decompose(A, k: int, l: int, seed: int, sketch_kind: str = "gaussian") -> Decomposition:
+    """The whole ID: sketch -> pivoted CGS2 (one retry: stream 20, or 22/23 for the SRFT) ->
+    back-substitution. sketch_kind 'gaussian' (north star) or 'srft'."""
     A = _fortran_c128(A)
     retries = 0
-    Y = sketch(A, seed, l, STREAM_R)
+    mk = (lambda retry: sketch(A, seed, l, STREAM_R_RETRY if retry else STREAM_R)) \
+        if sketch_kind == "gaussian" else (lambda retry: srft_sketch(A, seed, l, retry))
+    Y = mk(False)
     qr = pivoted_qr(Y, k)
     if qr.status == RID_ERANK:  # PAPER.md:80 re-randomise once (SPEC.md:333)
         retries = 1
-        Y = sketch(A, seed, l, STREAM_R_RETRY)
+        Y = mk(True)
         qr = pivoted_qr(Y, k)
         if qr.status == RID_ERANK:
             raise OracleError(RID_ERANK, f"decompose (rank {qr.rank_achieved})")

@@ -23,6 +23,7 @@
  *   orc_backsolve       PAPER.md:88-93 (§2, Eqs. 10–11: R2 = R1 T, P = [I T])
  *   orc_error_estimate  PAPER.md:262-277 (Table 5, ||A − BP||_2), readings R15/R16
  *   orc_error_bound     PAPER.md:60-63 (§2, Eq. 3)
+ *   orc_srft_plan, orc_srft_apply   PAPER.md:69-80 (§2, Eqs. 4–7: Y = S F D A), docs/RNG.md §7
  *
  * Parity-pinned by tests/test_oracle_*.py (curand Philox, libm, LAPACK ZGEQP3, scipy ID,
  * lstsq, dense SVD, brute force, closed forms).
@@ -563,6 +564,79 @@ double orc_error_bound(int64_t m, int64_t n, int64_t k, double eps, double sigma
 double orc_noise_floor(int64_t m, int64_t n, double delta) {
   double mn = (double)(m < n ? m : n);
   return sqrt(2.0 * mn) * delta;
+}
+
+/* ------------------------------------------------------------------------------------------ */
+/* SRFT randomisation Y = S F D A (§2, Eqs. 4–7; docs/RNG.md §7).             */
+/* Plan: phases d_i = e^{2 pi i phi_i}, phi_i = u1 of Philox (i, 0, s_phase, 0); samples         */
+/* s_k = x0 & (m-1) of Philox (k, 0, s_sample, 0). m must be a power of two.                     */
+/* ------------------------------------------------------------------------------------------ */
+static int is_pow2(int64_t m) { return m > 0 && (m & (m - 1)) == 0; }
+
+int orc_srft_plan(uint64_t seed, uint32_t s_phase, uint32_t s_sample, int64_t m, int64_t l,
+                  double* d, int64_t* samples) {
+  if (!is_pow2(m) || l < 1 || m > ((int64_t)1 << 32)) return RID_EINVAL;
+  const uint32_t key[2] = {(uint32_t)(seed & 0xFFFFFFFFu), (uint32_t)(seed >> 32)};
+  for (int64_t i = 0; i < m; ++i) {
+    uint32_t ctr[4] = {(uint32_t)i, 0u, s_phase, 0u}, x[4];
+    orc_philox4x32_10(ctr, key, x);
+    double c, s;
+    orc_rid_sincos2pi(uniform_from(x[0], x[1]), &c, &s);
+    d[2 * i] = c;
+    d[2 * i + 1] = s;
+  }
+  for (int64_t k = 0; k < l; ++k) {
+    uint32_t ctr[4] = {(uint32_t)k, 0u, s_sample, 0u}, x[4];
+    orc_philox4x32_10(ctr, key, x);
+    samples[k] = (int64_t)(x[0] & (uint32_t)(m - 1));
+  }
+  return RID_OK;
+}
+
+/* Y(k, c) = sum_{i ascending} F[s_k, i] * (d_i * A(i, c)), F[t, i] = e^{-2 pi i (t i mod m) / m}
+ * (Eq. 6, unnormalised) evaluated through the spec'd sincos on u = ((t i) mod m) / m (exact). The
+ * plan (d, samples) is an input so tests can pin the transform with chosen plans. */
+int orc_srft_apply(const double* d, const int64_t* samples, int64_t l, int64_t m, int64_t n_loc,
+                   const double* A, int64_t lda, double* Y, int64_t ldy) {
+  if (!is_pow2(m) || l < 1 || n_loc < 0 || lda < m || ldy < l) return RID_EINVAL;
+  double* tw = (double*)malloc(sizeof(double) * 2 * (size_t)m); /* F entries e^{-2 pi i t / m} */
+  if (!tw) return RID_ENOMEM;
+  for (int64_t t = 0; t < m; ++t) {
+    double c, s;
+    orc_rid_sincos2pi((double)t / (double)m, &c, &s);
+    tw[2 * t] = c;
+    tw[2 * t + 1] = -s;
+  }
+#pragma omp parallel
+  {
+    double* b = (double*)malloc(sizeof(double) * 2 * (size_t)m);
+#pragma omp for schedule(static)
+    for (int64_t c = 0; c < n_loc; ++c) {
+      const double* a = &A[2 * c * lda];
+      for (int64_t i = 0; i < m; ++i) { /* b = D a */
+        const double dr = d[2 * i], di = d[2 * i + 1], ar = a[2 * i], ai = a[2 * i + 1];
+        b[2 * i] = fma(dr, ar, -(di * ai));
+        b[2 * i + 1] = fma(di, ar, dr * ai);
+      }
+      for (int64_t k = 0; k < l; ++k) {
+        const uint64_t sk = (uint64_t)samples[k];
+        double yr = 0.0, yi = 0.0;
+        for (int64_t i = 0; i < m; ++i) {
+          const uint64_t t = (sk * (uint64_t)i) & (uint64_t)(m - 1);
+          const double wr = tw[2 * t], wi = tw[2 * t + 1];
+          yr = fma(wr, b[2 * i], yr);
+          yr = fma(-wi, b[2 * i + 1], yr);
+          yi = fma(wi, b[2 * i], yi);
+          yi = fma(wr, b[2 * i + 1], yi);
+        }
+        Y[2 * (k + c * ldy)] = yr;
+        Y[2 * (k + c * ldy) + 1] = yi;
+      }
+    }
+    free(b);
+  }
+  free(tw);
+  return RID_OK;
 }
 
 int orc_set_threads(int nthreads) {
