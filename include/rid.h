@@ -58,6 +58,12 @@ typedef enum {
 
 typedef struct rid_ctx rid_ctx;
 
+/* Randomisation used by rid_decompose (rid_set_sketch). */
+typedef enum {
+  RID_SKETCH_GAUSSIAN = 0, /* Y = R A, R l x m complex Gaussian (north star; default)            */
+  RID_SKETCH_SRFT = 1      /* Y = S F D A (Eqs. 4–7); m a power of two >= 16     */
+} rid_sketch_kind;
+
 /* Per-call diagnostics (SPEC.md:298-302 IdDiagnostics); every field is written by the call that
  * receives it; times are device times from CUDA events on the context stream, in seconds. */
 typedef struct {
@@ -112,6 +118,16 @@ rid_status rid_generate(rid_ctx* ctx, uint64_t seed, int64_t m, int64_t n, int64
  * order (agreement to rounding). Preconditions: 1 <= l <= m, n_loc <= n, lda >= m, ldy >= l. */
 rid_status rid_sketch(rid_ctx* ctx, uint64_t seed, uint32_t stream, int64_t l, const rid_z* A,
                       int64_t m, int64_t n, int64_t n_loc, int64_t lda, rid_z* Y, int64_t ldy);
+/* The paper's own randomisation Y = S F D A (§2, Eqs. 4–7; docs/RNG.md §7):
+ * D random unit phases (Philox stream 6), F the unnormalised DFT (Eq. 6), S l row samples with
+ * replacement (stream 7); retry != 0 uses streams 22/23. Computed as a 16-point DFT
+ * pass plus 16 small DMMA GEMMs (8 l m n / 16 flops); agrees with the direct sum to rounding.
+ * Preconditions: m a power of two, 16 <= m < 2^32, 1 <= l, n_loc <= n, lda >= m, ldy >= l. */
+rid_status rid_sketch_srft(rid_ctx* ctx, uint64_t seed, int retry, int64_t l, const rid_z* A,
+                           int64_t m, int64_t n, int64_t n_loc, int64_t lda, rid_z* Y,
+                           int64_t ldy);
+/* Select the randomisation of subsequent rid_decompose calls on ctx (default GAUSSIAN). */
+rid_status rid_set_sketch(rid_ctx* ctx, int kind);
 /* Number of K slices S the sketch of an m-row, n-column matrix uses (1 = unsplit): chosen so that
  * the n/8-column shard of an 8-GPU run still fills the GPU, a function of (m, l, n) only. */
 int rid_sketch_splits(const rid_ctx* ctx, int64_t m, int64_t l, int64_t n);

@@ -58,7 +58,9 @@ _lib = None
 EXPORTS = ["rid_create", "rid_destroy", "rid_last_error", "rid_version", "rid_comm_id_bytes",
            "rid_comm_get_id", "rid_comm_init", "rid_comm_info", "rid_generate", "rid_sketch",
            "rid_decompose", "rid_error_estimate", "rid_error_bound", "rid_normal_fill",
-           "rid_qrcp", "rid_factor_solve", "rid_sketch_splits"]
+           "rid_qrcp", "rid_factor_solve", "rid_sketch_splits", "rid_sketch_srft",
+           "rid_set_sketch"]
+SKETCH_GAUSSIAN, SKETCH_SRFT = 0, 1
 
 
 def lib():
@@ -84,6 +86,8 @@ def lib():
         "rid_generate": ([p, u64, i64, i64, i64, d, i64, i64, p, i64], ci),
         "rid_sketch": ([p, u64, u32, i64, p, i64, i64, i64, i64, p, i64], ci),
         "rid_sketch_splits": ([p, i64, i64, i64], ci),
+        "rid_sketch_srft": ([p, u64, ci, i64, p, i64, i64, i64, i64, p, i64], ci),
+        "rid_set_sketch": ([p, ci], ci),
         "rid_decompose": ([p, p, i64, i64, i64, i64, i64, i64, i64, u64, p, p, i64, p], ci),
         "rid_error_estimate": ([p, p, i64, i64, i64, i64, i64, p, i64, p, i64, ci, u64, p, p], ci),
         "rid_error_bound": ([i64, i64, i64, d, d], d),
@@ -267,6 +271,22 @@ def sketch(A, seed: int, l: int, stream: int = STREAM_R, out=None, n: int | None
     return out
 
 
+def sketch_srft(A, seed: int, l: int, retry: bool = False, out=None, n: int | None = None,
+                ctx: Context | None = None):
+    """Y = S F D A, the paper's SRFT randomisation; m a power of two >= 16."""
+    ctx = ctx or default_context()
+    m, n_loc = A.shape
+    n = n_loc if n is None else n
+    a = _Buf(A, m, n_loc, "A")
+    if out is None:
+        out = colmajor_empty(l, n_loc, device=A.device if hasattr(A, "device") else "cpu") \
+            if not isinstance(A, np.ndarray) else np.zeros((l, n_loc), np.complex128, order="F")
+    y = _Buf(out, l, n_loc, "Y")
+    ctx.check(lib().rid_sketch_srft(ctx.h, seed, int(retry), l, a.ptr, m, n, n_loc, a.ld, y.ptr,
+                                    y.ld), "rid_sketch_srft")
+    return out
+
+
 def sketch_splits(m: int, l: int, n: int, ctx: Context | None = None) -> int:
     """K slices of the sketch of an m x n matrix (1: bit-identical to the oracle's chain)."""
     ctx = ctx or default_context()
@@ -281,9 +301,12 @@ class IdResult:
 
 
 def decompose(A, k: int, l: int, seed: int, n: int | None = None, col0: int = 0, J=None, P=None,
-              ctx: Context | None = None) -> IdResult:
-    """The whole ID of the (shard of the) matrix A: J (k, global ids) and P_loc."""
+              ctx: Context | None = None, sketch: str = "gaussian") -> IdResult:
+    """The whole ID of the (shard of the) matrix A: J (k, global ids) and P_loc.
+    sketch: 'gaussian' (north star, default) or 'srft' (the paper's Y = S F D A)."""
     ctx = ctx or default_context()
+    kind = {"gaussian": SKETCH_GAUSSIAN, "srft": SKETCH_SRFT}[sketch]
+    ctx.check(lib().rid_set_sketch(ctx.h, kind), "rid_set_sketch")
     m, n_loc = A.shape
     n = n_loc if n is None else n
     a = _Buf(A, m, n_loc, "A")

@@ -33,6 +33,7 @@ struct rid_ctx {
   // host-A streaming (e2e path): a copy stream and double-buffer events, created on first use
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {}, ev_used[2] = {}, ev_copy0 = nullptr, ev_copy1 = nullptr;
+  int sketch_kind = 0;  // RID_SKETCH_GAUSSIAN (north star) or RID_SKETCH_SRFT
 };
 
 namespace {
@@ -271,6 +272,26 @@ rid_status sketch_streamed(rid_ctx* c, const double2* R, const rid_z* hostA, int
   return RID_OK;
 }
 
+// SRFT sketch of a device A (a_dev) or a host A (host_A, staged whole) into Y (device, ldy).
+rid_status srft_into(rid_ctx* c, uint64_t seed, bool retry, int64_t l, const rid_z* host_A,
+                     const void* a_dev, int64_t m, int64_t n, int64_t n_loc, int64_t lda,
+                     double2* Y, int64_t ldy, int* launches) {
+  if (m < 16 || (m & (m - 1)) != 0)
+    return fail(c, RID_EINVAL, "SRFT sketch: m = %lld must be a power of two >= 16", (long long)m);
+  if (!a_dev) {
+    MatArg a;
+    RID_TRY(stage_in(c, "stage_A", host_A, m, n_loc, lda, sizeof(rid_z), true, &a));
+    a_dev = a.dev;
+  }
+  void *pw, *ps;
+  RID_TRY(ws_get(c, "srft_work", rid::srft_work_bytes(m, l, n_loc), &pw));
+  const size_t split_elems = (size_t)8 * (size_t)l * 4096;  // bounded split-K workspace
+  RID_TRY(ws_get(c, "srft_splitk", sizeof(double2) * split_elems, &ps));
+  RID_CUDA(c, rid::srft_sketch(seed, retry, l, (const double2*)a_dev, m, n, n_loc, lda, Y, ldy, pw,
+                               (double2*)ps, split_elems, c->num_sms, c->stream, launches));
+  return RID_OK;
+}
+
 __global__ void k_extract_R(const double2* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ J,
                             const double2* __restrict__ R11, int64_t k, int64_t n,
                             double2* __restrict__ R, int64_t ldr) {
@@ -414,6 +435,33 @@ rid_status rid_generate(rid_ctx* c, uint64_t seed, int64_t m, int64_t n, int64_t
   return RID_OK;
 }
 
+rid_status rid_set_sketch(rid_ctx* c, int kind) {
+  if (!c) return RID_EINVAL;
+  if (kind != RID_SKETCH_GAUSSIAN && kind != RID_SKETCH_SRFT)
+    return fail(c, RID_EINVAL, "rid_set_sketch: unknown kind %d", kind);
+  c->sketch_kind = kind;
+  return RID_OK;
+}
+
+rid_status rid_sketch_srft(rid_ctx* c, uint64_t seed, int retry, int64_t l, const rid_z* A,
+                           int64_t m, int64_t n, int64_t n_loc, int64_t lda, rid_z* Y,
+                           int64_t ldy) {
+  RID_TRY(check_ctx(c));
+  if (l < 1 || m < 16 || (m & (m - 1)) != 0 || n_loc < 0 || n < n_loc || lda < m || ldy < l ||
+      !A || !Y || m > (int64_t)0xFFFFFFFFLL || n_loc > 0xFFFFFFFFLL)
+    return fail(c, RID_EINVAL, "rid_sketch_srft: bad arguments (m must be a power of two >= 16)");
+  if (n_loc == 0) return RID_OK;
+  MatArg a, y;
+  RID_TRY(stage_in(c, "stage_A", A, m, n_loc, lda, sizeof(rid_z), true, &a));
+  RID_TRY(stage_in(c, "stage_Y", Y, l, n_loc, ldy, sizeof(rid_z), false, &y));
+  int launches = 0;
+  RID_TRY(srft_into(c, seed, retry != 0, l, nullptr, a.dev, m, n, n_loc, lda, (double2*)y.dev, ldy,
+                    &launches));
+  RID_TRY(stage_out(c, y, Y, l, n_loc, ldy, sizeof(rid_z)));
+  if (a.host || y.host) RID_CUDA(c, cudaStreamSynchronize(c->stream));
+  return RID_OK;
+}
+
 int rid_sketch_splits(const rid_ctx* c, int64_t m, int64_t l, int64_t n) {
   if (!c || m < 1 || l < 1 || n < 1) return 1;
   return rid::zgemm_ksplit(l, m, n / 8, c->num_sms);
@@ -481,6 +529,12 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
   for (int attempt = 0; attempt < 2; ++attempt) {
     const uint32_t sR = attempt == 0 ? kStreamR : kStreamRRetry;
     RID_CUDA(c, cudaEventRecord(ev[2], c->stream));
+    if (c->sketch_kind == RID_SKETCH_SRFT) {  // the paper's own randomisation
+      RID_CUDA(c, cudaEventRecord(ev[3], c->stream));
+      d.launches += 1;  // QRCP
+      RID_TRY(srft_into(c, seed, attempt == 1, l, A, a_host ? nullptr : a.dev, m, n, n_loc, lda,
+                        Yw + col0 * l, l, &d.launches));
+    } else {
     RID_CUDA(c, rid::normal_fill(seed, sR, l, m, 0, 0, (double2*)pR, l, c->stream));
     RID_CUDA(c, cudaEventRecord(ev[3], c->stream));
     d.launches += 2;  // R fill, QRCP
@@ -492,6 +546,7 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
                                      Yw + col0 * l, l, l, n_loc, m, 0, 0.0, seed, 0, c->stream, S,
                                      (double2*)pS));
       d.launches += S > 1 ? 2 : 1;
+    }
     }
     RID_CUDA(c, cudaEventRecord(ev[4], c->stream));
     if (c->comm) {

@@ -81,3 +81,12 @@ cudaError_t est_z(const double2* A, int64_t lda, int64_t m, int64_t n_loc, const
                   double* npart, const EstPlan& p, cudaStream_t st);
 
 }  // namespace rid
+
+namespace rid {
+// SRFT randomisation Y = S F D A (k_srft.cu). m a power of two, m >= 16.
+size_t srft_work_bytes(int64_t m, int64_t l, int64_t n_loc);
+cudaError_t srft_sketch(uint64_t seed, bool retry, int64_t l, const double2* A, int64_t m,
+                        int64_t n, int64_t n_loc, int64_t lda, double2* Y, int64_t ldy, void* work,
+                        double2* splitk, size_t splitk_elems, int num_sms, cudaStream_t st,
+                        int* launches);
+}  // namespace rid
