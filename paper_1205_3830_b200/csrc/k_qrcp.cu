@@ -30,6 +30,10 @@
 // densely to out.R11 by CTA 0; out.beta[s] = R11[s, s].
 #include <cfloat>
 #include <cstdint>
+#include <cstdlib>
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "rid_device.cuh"
 #include "rid_internal.h"
@@ -401,42 +405,620 @@ __global__ void __launch_bounds__(kQrcpThreads, 2)
   }
 }
 
-size_t qrcp_work_bytes(int64_t n, int max_blocks) {
-  return (size_t)n * sizeof(double) + (size_t)2 * 3 * max_blocks * sizeof(double) + 256;
+// =============================================================================================
+// Blocked variant (default): LAPACK zlaqps-style panels of nb <= kNB reflectors.
+//
+// The exact-recompute kernel above reads AND writes the whole trailing block every step (C4:
+// ≈146 GB over 512 steps). Inside a panel starting at step j0 this kernel never rewrites the
+// trailing block: with y^(j0)_c the column at the panel start and f_s(c) = conj(τ_s)·v_sᴴ y^(j0+s)_c,
+//     y^(j+1)_c = y^(j0)_c − Σ_{s<=t} v_s f_s(c),         t = j − j0,
+//     f_t(c)   = conj(τ_t)·( v_tᴴ y^(j0)_c − Σ_{s<t} (v_tᴴ v_s) f_s(c) ),
+//     R(j, c)  = y^(j0)_c[j] − Σ_{s<=t} V[j, s] f_s(c),
+// so step j reads rows j..l−1 of every trailing column once (the GEMV v_tᴴ y^(j0)), writes one
+// element (R(j, c)) and one f per column, and downdates the residual norm
+//     ν_c² ← ν_c² − |R(j, c)|²          (H_j is unitary on rows j..l−1)
+// with the LAPACK safeguard: when (ν_new/ν_ref)² <= kRecompTol (ν_ref = the last exact value) the
+// norm is recomputed exactly from y^(j0) (still in registers) minus the pending reflectors. The
+// downdate's relative error is bounded by ≈ j·u/kRecompTol ≈ 6e-10 at j = 512 — four orders below
+// the smallest top-2 pivot gap measured on C2–C5 (1.8e-6), so J is unaffected (R11').
+// After each panel the trailing rows j0+nb..l−1 are updated in one tensor-core GEMM,
+// Y −= V·F (k_zgemm.cu mode 2, K = nb): read + write once per nb steps instead of every step.
+// =============================================================================================
+constexpr int kNB = 16;
+constexpr double kRecompTol = 1e-4;
+constexpr int kRingThreads = 512;
+constexpr int kRingWarps = kRingThreads / 32;
+constexpr int kMaxSlots = 64;
+constexpr int kCH = 16;  // rows per streamed box (a box is kCH rows x 32 columns, 8 KB)
+
+__device__ __forceinline__ void cmac_sub(double2& x, const double2 v, const double2 f) {  // x -= v f
+  x.x = __fma_rn(-v.x, f.x, __fma_rn(v.y, f.y, x.x));
+  x.y = __fma_rn(-v.x, f.y, __fma_rn(-v.y, f.x, x.y));
+}
+__device__ __forceinline__ void cmac_add(double& ar, double& ai, const double2 g, const double2 f) {
+  ar = __fma_rn(g.x, f.x, __fma_rn(-g.y, f.y, ar));  // a += g f
+  ai = __fma_rn(g.x, f.y, __fma_rn(g.y, f.x, ai));
+}
+
+// ---- PTX helpers: mbarrier + bulk async copy (TMA engine, no tensor map) -------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void tma_box_g2s(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(b))
+      : "memory");
+}
+__device__ __forceinline__ void consumers_sync() {  // warps 1..15 only
+  asm volatile("bar.sync 1, %0;\n" ::"n"((kRingWarps - 1) * 32) : "memory");
+}
+
+// One CTA per SM, 16 warps. Warp 0: the pivot reduction. Warps 1..15:
+// the reflector; then the first `ncw` of them each stream their own share of the trailing
+// columns through a private ring of D shared-memory slots: lane 0 issues one cp.async.bulk per
+// column segment (rows j..l−1 = 16·(l−j) contiguous bytes, TMA engine, completion on the slot's
+// mbarrier) D − 1 columns ahead of the one being reduced (GEMV from shared memory, f_t, R(j, c),
+// the downdated norm). Columns are visited in alternating order from step to step, so the
+// segments read last in step j — still in the 126 MB L2 — are read first in step j + 1.
+template <int MAXQ>
+__global__ void __launch_bounds__(kRingThreads, 1)
+    k_qrcp_ring(double2* __restrict__ Y, int64_t ldy, int l, int64_t n, int k, int j0, int jend,
+                double tol_rel, QrcpOut out, QrcpWork w, int ncw, int D, int per, int slot_elems,
+                int flags, const __grid_constant__ CUtensorMap tmap) {
+  constexpr int kCW = kRingWarps - 1;  // consumer warps in the reflector phase
+  constexpr int kRQ = (MAXQ * 32 + kCW * 32 - 1) / (kCW * 32);
+  extern __shared__ __align__(128) unsigned char ring_smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(ring_smem);                 // kMaxSlots
+  double2* sv = reinterpret_cast<double2*>(full + kMaxSlots);              // MAXQ*32
+  double2* ring = reinterpret_cast<double2*>(                              // ncw*D*32*kCH
+      (reinterpret_cast<uintptr_t>(sv + MAXQ * 32 + 32) + 127) & ~(uintptr_t)127);  // TMA: 128 B
+  __shared__ double2 s_vrow[kNB], s_g[kNB], s_fp[kNB];
+  __shared__ double s_red[kRingWarps];
+  __shared__ double s_par[2];  // alpha re/im
+  __shared__ Top2 sred[kRingWarps];
+  __shared__ long long s_p;
+  __shared__ int s_stop;
+
+  if (out.info[0] == 2) return;  // an earlier panel stopped on rank failure (uniform)
+  const int nbk = gridDim.x, b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c_lo = (int64_t)b * per;
+  const int64_t c_hi = (c_lo + per < n) ? c_lo + per : n;
+  const int64_t ldv = l;
+  double nu0max = (j0 > 0) ? w.scal[0] : 0.0;
+  unsigned phase = 0;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < ncw * D; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (j0 == 0) {  // ---- initial exact column norms (one pass, direct loads) -------------------
+    const int lpc = pick_lpc(l, MAXQ);
+    const int cpw = 32 / lpc, sg = lane / lpc, sl = lane % lpc;
+    Top2 loc;
+    top2_init(loc);
+    for (int64_t c0 = c_lo + (int64_t)warp * cpw; c0 < c_hi; c0 += (int64_t)kRingWarps * cpw) {
+      const int64_t c = c0 + sg;
+      const bool live = c < c_hi;
+      const double2* yc = Y + c * ldy;
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int r = sl + lpc * q;
+        if (live && r < l) {
+          const double2 y = yc[r];
+          s = __fma_rn(y.x, y.x, s);
+          s = __fma_rn(y.y, y.y, s);
+        }
+      }
+      const double nu = __dsqrt_rn(group_sum(s, lpc));
+      if (live && sl == 0) {
+        w.nu[c] = nu;
+        w.nuref[c] = nu;
+        top2_push(loc, nu, c);
+      }
+    }
+    top2_warp(loc);
+    if (lane == 0) sred[warp] = loc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Top2 tt = sred[0];
+      for (int q = 1; q < kRingWarps; ++q) top2_merge(tt, sred[q]);
+      double* c = w.cand + (size_t)b * 3;  // parity 0
+      c[0] = tt.b1;
+      c[1] = tt.b2;
+      c[2] = (double)tt.i1;
+    }
+    grid_barrier(w.bar, (unsigned)nbk * (++phase));
+  }
+
+  unsigned ubase = 0;  // items this warp streamed in earlier steps of this launch (ring parity)
+  for (int j = j0; j < jend; ++j) {
+    const int t = j - j0;
+    const int L = l - j;  // rows j..l-1
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[4 * j + 0] = globaltimer();
+    // ---- 1. global pivot (every CTA, identically); the owner drops it from its list ---------
+    if (warp == 0) {
+      Top2 tt;
+      top2_init(tt);
+      const double* cb = w.cand + (size_t)(j & 1) * w.max_blocks * 3;
+      for (int q = lane; q < nbk; q += 32) {
+        Top2 o;
+        o.b1 = cb[q * 3 + 0];
+        o.b2 = cb[q * 3 + 1];
+        o.i1 = (long long)cb[q * 3 + 2];
+        top2_merge(tt, o);
+      }
+      top2_warp(tt);
+      if (j == 0) nu0max = tt.b1;  // max_c ||Y[:, c]||
+      const bool stop = !(tt.b1 >= tol_rel * nu0max) || tt.b1 <= 0.0 || tt.i1 < 0 || tt.i1 >= n;
+      const int64_t p = tt.i1;
+      if (lane == 0) {
+        s_p = p;
+        s_stop = stop ? 1 : 0;
+        if (b == 0) {
+          if (j == 0) w.scal[0] = nu0max;
+          out.resid[j] = tt.b1;
+          out.margin[j] = (tt.b2 < 0.0) ? DBL_MAX : (tt.b1 - tt.b2) / tt.b1;
+          if (!stop) out.J[j] = p;
+        }
+      }
+      if (!stop && p >= c_lo && p < c_hi && lane == 0) w.nu[p] = -1.0;  // the owner: chosen
+    }
+    __syncthreads();
+    if (s_stop) {
+      if (b == 0 && threadIdx.x == 0) {
+        out.info[0] = 2;
+        out.info[1] = j;
+      }
+      return;  // no copy is in flight: every item of the previous step was consumed
+    }
+    const int64_t p = s_p;
+    const bool rev = (j & 1) != 0;  // alternate the batch and row order (L2 reuse across steps)
+
+    if (warp > 0) {
+      const int cw = warp - 1, idx = cw * 32 + lane;
+      // the CTA's columns are cut into batches of 32 consecutive columns (lane i <-> column i of
+      // the batch; chosen columns leave their lane idle); streaming warp cw takes batches cw,
+      // cw + ncw, ... and streams each batch's rows j..l-1 as 32-row x 32-column boxes (one 2D TMA
+      // copy of 16 KB per box, rows past l zero-filled) through its D ring slots
+      const int nbat = (int)((c_hi - c_lo + 31) / 32);
+      const int mybat = (cw < ncw && nbat > cw) ? (nbat - cw + ncw - 1) / ncw : 0;
+      const int nch = (L + kCH - 1) / kCH;
+      const int nitems = mybat * nch;
+      auto issue = [&](int u) {  // item u = (batch u / nch, chunk u % nch) into its slot
+        const int q = u / nch, ch0 = u - q * nch;
+        const int ch = rev ? nch - 1 - ch0 : ch0;  // odd steps stream bottom-up
+        const int bi = cw + ncw * q;
+        const int bb = rev ? nbat - 1 - bi : bi;
+        const int s = cw * D + (int)((ubase + (unsigned)u) % (unsigned)D);
+        if (lane == 0) {
+          if (!(flags & 1)) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          mbar_expect_tx(&full[s], (unsigned)(32 * kCH * sizeof(double2)));
+          tma_box_g2s(ring + (size_t)s * 32 * kCH, &tmap, 2 * (j + ch * kCH),
+                      (int)(c_lo + 32 * bb), &full[s]);
+        }
+      };
+      // ---- 2a. prologue: this warp's first D boxes start streaming now ---------------------
+      for (int u = 0; u < nitems && u < D; ++u) issue(u);
+      // ---- 2b. reflector H_j from x = y^(j0)_p[j:l] − Σ_{s<t} V[j:l, s] f_s(p) --------------
+      if (cw == 0 && lane < t) {
+        s_fp[lane] = w.F[p * kNB + lane];
+        s_vrow[lane] = w.V[(int64_t)lane * ldv + j];
+      }
+      consumers_sync();
+      double2 x[kRQ];
+      double s2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < kRQ; ++q) {
+        const int rr = idx + kCW * 32 * q;
+        x[q] = make_double2(0.0, 0.0);
+        if (rr < L) {
+          x[q] = Y[p * ldy + j + rr];
+#pragma unroll
+          for (int s0 = 0; s0 < kNB; s0 += 8) {  // 8 loads in flight (L2), then their fmas
+            double2 vv[8];
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+              if (s0 + s < t) vv[s] = w.V[(int64_t)(s0 + s) * ldv + j + rr];
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+              if (s0 + s < t) cmac_sub(x[q], vv[s], s_fp[s0 + s]);
+          }
+          if (rr > 0) {
+            s2 = __fma_rn(x[q].x, x[q].x, s2);
+            s2 = __fma_rn(x[q].y, x[q].y, s2);
+          }
+        }
+      }
+      s2 = group_sum(s2, 32);
+      if (lane == 0) s_red[cw] = s2;
+      if (idx == 0) {
+        s_par[0] = x[0].x;
+        s_par[1] = x[0].y;
+      }
+      consumers_sync();
+      double xnorm2 = 0.0;
+      for (int q = 0; q < kCW; ++q) xnorm2 = __dadd_rn(xnorm2, s_red[q]);  // fixed order
+      const double ar = s_par[0], ai = s_par[1];
+      double tr, ti, beta, sc_re, sc_im;
+      if (xnorm2 == 0.0 && ai == 0.0) {
+        tr = 0.0;
+        ti = 0.0;
+        beta = ar;
+        sc_re = 0.0;
+        sc_im = 0.0;
+      } else {
+        const double nrm = __dsqrt_rn(__fma_rn(ar, ar, __fma_rn(ai, ai, xnorm2)));
+        beta = (ar >= 0.0) ? -nrm : nrm;
+        tr = __ddiv_rn(__dsub_rn(beta, ar), beta);
+        ti = __ddiv_rn(-ai, beta);
+        const double dr = __dsub_rn(ar, beta), di = ai;  // scal = 1 / (alpha - beta)
+        const double den = __fma_rn(dr, dr, __dmul_rn(di, di));
+        sc_re = __ddiv_rn(dr, den);
+        sc_im = __ddiv_rn(-di, den);
+      }
+#pragma unroll
+      for (int q = 0; q < kRQ; ++q) {
+        const int rr = idx + kCW * 32 * q;
+        if (rr < L) {
+          double2 v;
+          if (rr == 0) {
+            v = make_double2(1.0, 0.0);
+          } else {
+            v.x = __fma_rn(x[q].x, sc_re, -__dmul_rn(x[q].y, sc_im));
+            v.y = __fma_rn(x[q].x, sc_im, __dmul_rn(x[q].y, sc_re));
+          }
+          sv[rr] = v;
+          if (b == 0) w.V[(int64_t)t * ldv + j + rr] = v;
+        }
+      }
+      if (idx < 32) sv[L + idx] = make_double2(0.0, 0.0);  // the last box reads up to L + 31
+      if (b == 0) {
+        if (idx == 0) {
+          out.beta[j] = beta;
+          out.R11[(int64_t)j * k + j] = make_double2(beta, 0.0);
+        }
+        // rows 0..j-1 of the pivot column are final R entries
+        for (int r = idx; r < j; r += kCW * 32) out.R11[(int64_t)j * k + r] = Y[p * ldy + r];
+      }
+      consumers_sync();
+      // s_g[s] = v_tᴴ v_s for s < t (one warp per s)
+      for (int s = cw; s < t; s += kCW) {
+        const double2* vs = w.V + (int64_t)s * ldv + j;
+        double gr = 0.0, gi = 0.0;
+#pragma unroll
+        for (int q = 0; q < MAXQ; ++q) {
+          const int rr = lane + 32 * q;
+          if (rr < L) {
+            const double2 a = sv[rr], v = vs[rr];
+            gr = __fma_rn(a.x, v.x, __fma_rn(a.y, v.y, gr));  // conj(a) v
+            gi = __fma_rn(a.x, v.y, __fma_rn(-a.y, v.x, gi));
+          }
+        }
+        gr = group_sum(gr, 32);
+        gi = group_sum(gi, 32);
+        if (lane == 0) s_g[s] = make_double2(gr, gi);
+      }
+      consumers_sync();
+      if (w.trace && b == 0 && idx == 0) w.trace[4 * j + 1] = globaltimer();
+
+      // ---- 3. this warp's batches: lane = column, rows streamed box by box -------------------
+      Top2 loc;
+      top2_init(loc);
+      bool live = false;
+      int64_t c = 0;
+      double nu_old = 0.0, ref = 0.0, hr = 0.0, hi = 0.0, rsr = 0.0, rsi = 0.0;
+      double a0r = 0.0, a0i = 0.0, a1r = 0.0, a1i = 0.0;
+      double2 yj = make_double2(0.0, 0.0);
+      for (int u = 0; u < nitems; ++u) {
+        const int q = u / nch, ch0 = u - q * nch;
+        const int ch = rev ? nch - 1 - ch0 : ch0;
+        if (ch0 == 0) {  // batch start: this lane's column, its norms and pending-reflector terms
+          const int bi = cw + ncw * q;
+          const int bb = rev ? nbat - 1 - bi : bi;
+          c = c_lo + 32 * bb + lane;
+          nu_old = c < c_hi ? w.nu[c] : -1.0;
+          live = nu_old >= 0.0;  // chosen columns (and p) carry -1
+          ref = live ? w.nuref[c] : 0.0;
+          // h = Σ_{s<t} g_s f_s,  rs = Σ_{s<t} V[j, s] f_s
+          hr = hi = rsr = rsi = 0.0;
+#pragma unroll
+          for (int s0 = 0; s0 < kNB; s0 += 8) {
+            double2 f[8];
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+              f[s] = (live && s0 + s < t) ? w.F[c * kNB + s0 + s] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int s = 0; s < 8; ++s)
+              if (s0 + s < t) {
+                cmac_add(hr, hi, s_g[s0 + s], f[s]);
+                cmac_add(rsr, rsi, s_vrow[s0 + s], f[s]);
+              }
+          }
+          a0r = a0i = a1r = a1i = 0.0;
+        }
+        const unsigned U = ubase + (unsigned)u;
+        const int s = cw * D + (int)(U % (unsigned)D);
+        mbar_wait(&full[s], (U / (unsigned)D) & 1);
+        const double2* sy = ring + (size_t)s * 32 * kCH + lane * kCH;  // this lane's column
+        if (ch == 0) yj = sy[0];
+        const double2* vv = sv + ch * kCH;
+        // rows visited in a lane-rotated order: conflict-free shared-memory wavefronts
+#pragma unroll
+        for (int rr = 0; rr < kCH; rr += 2) {
+          const int r0 = (rr + lane) & (kCH - 1), r1 = (rr + 1 + lane) & (kCH - 1);
+          const double2 v0 = vv[r0], y0 = sy[r0], v1 = vv[r1], y1 = sy[r1];
+          a0r = __fma_rn(v0.x, y0.x, __fma_rn(v0.y, y0.y, a0r));  // conj(v) y
+          a0i = __fma_rn(v0.x, y0.y, __fma_rn(-v0.y, y0.x, a0i));
+          a1r = __fma_rn(v1.x, y1.x, __fma_rn(v1.y, y1.y, a1r));
+          a1i = __fma_rn(v1.x, y1.y, __fma_rn(-v1.y, y1.x, a1i));
+        }
+        __syncwarp();  // every lane is done with the slot
+        if (u + D < nitems) issue(u + D);
+        if (ch0 == nch - 1 && live) {  // ---- this lane's column is complete -----------------
+          const double dr = __dsub_rn(__dadd_rn(a0r, a1r), hr);  // d = v_tᴴ y − h
+          const double di = __dsub_rn(__dadd_rn(a0i, a1i), hi);
+          const double2 ft = make_double2(__fma_rn(tr, dr, __dmul_rn(ti, di)),  // conj(tau) d
+                                          __fma_rn(tr, di, -__dmul_rn(ti, dr)));
+          const double2 Rj = make_double2(__dsub_rn(__dsub_rn(yj.x, rsr), ft.x),
+                                          __dsub_rn(__dsub_rn(yj.y, rsi), ft.y));
+          // downdate ν² ← ν² − |R(j, c)|²; exact recompute when it has cancelled below
+          // kRecompTol·ν_ref² (LAPACK zlaqps safeguard)
+          const double d2 =
+              __fma_rn(-Rj.x, Rj.x, __fma_rn(-Rj.y, Rj.y, __dmul_rn(nu_old, nu_old)));
+          const bool need = !(nu_old > 0.0) || !(d2 > kRecompTol * __dmul_rn(ref, ref));
+          double nu_new = __dsqrt_rn(d2 > 0.0 ? d2 : 0.0);
+          if (need) {  // rare, this lane alone: rows j+1..l-1 of y^(j+1) from global memory
+            double nn = 0.0;
+            for (int rr = 1; rr < L; ++rr) {
+              double2 z = Y[c * ldy + j + rr];
+              for (int uu = 0; uu < t; ++uu)
+                cmac_sub(z, w.V[(int64_t)uu * ldv + j + rr], w.F[c * kNB + uu]);
+              cmac_sub(z, sv[rr], ft);
+              nn = __fma_rn(z.x, z.x, nn);
+              nn = __fma_rn(z.y, z.y, nn);
+            }
+            nu_new = __dsqrt_rn(nn);
+          }
+          w.F[c * kNB + t] = ft;
+          Y[c * ldy + j] = Rj;
+          w.nu[c] = nu_new;
+          if (need) w.nuref[c] = nu_new;
+          top2_push(loc, nu_new, c);
+        }
+      }
+      ubase += (unsigned)nitems;
+      top2_warp(loc);
+      if (lane == 0) sred[warp] = loc;
+    } else if (lane == 0) {
+      Top2 z;
+      top2_init(z);
+      sred[0] = z;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Top2 tt = sred[0];
+      for (int q = 1; q < kRingWarps; ++q) top2_merge(tt, sred[q]);
+      double* cc = w.cand + ((size_t)((j + 1) & 1) * w.max_blocks + b) * 3;
+      cc[0] = tt.b1;
+      cc[1] = tt.b2;
+      cc[2] = (double)tt.i1;
+    }
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[4 * j + 2] = globaltimer();
+    if (j + 1 < jend) grid_barrier(w.bar, (unsigned)nbk * (++phase));
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[4 * j + 3] = globaltimer();
+  }
+  if (b == 0 && threadIdx.x == 0) out.info[1] = jend;
+}
+
+size_t qrcp_work_bytes(int64_t n, int64_t l, int max_blocks) {
+  return (size_t)2 * n * sizeof(double) + (size_t)2 * 3 * max_blocks * sizeof(double) +
+         (size_t)l * kNB * sizeof(double2) + (size_t)kNB * n * sizeof(double2) + 512;
+}
+
+QrcpWork qrcp_work_carve(void* buf, int64_t n, int64_t l, int max_blocks) {
+  char* p = (char*)buf;
+  QrcpWork w{};
+  w.max_blocks = max_blocks;
+  w.V = (double2*)p;  // 16-byte aligned first
+  p += (size_t)l * kNB * sizeof(double2);
+  w.F = (double2*)p;
+  p += (size_t)kNB * n * sizeof(double2);
+  w.nu = (double*)p;
+  p += (size_t)n * sizeof(double);
+  w.nuref = (double*)p;
+  p += (size_t)n * sizeof(double);
+  w.cand = (double*)p;
+  p += (size_t)2 * 3 * max_blocks * sizeof(double);
+  w.scal = (double*)p;
+  p += 64;
+  w.bar = (unsigned*)p;
+  return w;
+}
+
+static int qrcp_blocks(const void* kern, size_t smem, int num_sms, int max_blocks, int64_t n,
+                       cudaError_t* err) {
+  int occ = 0;
+  *err = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kQrcpThreads, smem);
+  if (*err != cudaSuccess) return 0;
+  if (occ < 1) {
+    *err = cudaErrorInvalidConfiguration;
+    return 0;
+  }
+  int blocks = num_sms * (occ < 2 ? occ : 2);
+  if (blocks > max_blocks) blocks = max_blocks;
+  const int64_t min_cols = 8;  // keep >= 8 columns per CTA on small n
+  if ((int64_t)blocks * min_cols > n) blocks = (int)((n + min_cols - 1) / min_cols);
+  return blocks < 1 ? 1 : blocks;
 }
 
 template <int MAXQ>
 static cudaError_t launch_qrcp(double2* Y, int64_t ldy, int l, int64_t n, int k, double tol_rel,
                                const QrcpOut& out, const QrcpWork& w, int num_sms,
-                               cudaStream_t st) {
+                               cudaStream_t st, int* launches) {
   const size_t smem = sizeof(double2) * kQB * MAXQ * 32;
   cudaError_t e = cudaFuncSetAttribute(k_qrcp<MAXQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
-  int occ = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_qrcp<MAXQ>, kQrcpThreads, smem);
+  const int blocks = qrcp_blocks((const void*)k_qrcp<MAXQ>, smem, num_sms, w.max_blocks, n, &e);
   if (e != cudaSuccess) return e;
-  if (occ < 1) return cudaErrorInvalidConfiguration;
-  int blocks = num_sms * (occ < 2 ? occ : 2);
-  if (blocks > w.max_blocks) blocks = w.max_blocks;
-  const int64_t min_cols = 8;  // keep >= 8 columns per CTA on small n
-  if ((int64_t)blocks * min_cols > n) blocks = (int)((n + min_cols - 1) / min_cols);
-  if (blocks < 1) blocks = 1;
   e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned), st);
   if (e != cudaSuccess) return e;
   QrcpOut o = out;
   QrcpWork ww = w;
   void* args[] = {&Y, &ldy, &l, &n, &k, &tol_rel, &o, &ww};
+  *launches += 1;
   return cudaLaunchCooperativeKernel((void*)k_qrcp<MAXQ>, dim3(blocks), dim3(kQrcpThreads), args,
                                      smem, st);
 }
 
+// Panels of nb steps (k_qrcp_ring), each followed by the tensor-core trailing update
+// Y[jend:l, :] -= V[jend:l, 0:nb] · F[0:nb, :] (k_zgemm.cu mode 2).
+template <int MAXQ>
+static cudaError_t launch_qrcp_blocked(double2* Y, int64_t ldy, int l, int64_t n, int k,
+                                       double tol_rel, const QrcpOut& out, const QrcpWork& w,
+                                       int num_sms, cudaStream_t st, int* launches, int nbw) {
+  auto kern = k_qrcp_ring<MAXQ>;
+  cudaError_t e;
+  int dev = 0, optin = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
+    return e;
+  cudaFuncAttributes fa;
+  if ((e = cudaFuncGetAttributes(&fa, (const void*)kern)) != cudaSuccess) return e;
+  int blocks = num_sms;
+  if ((int64_t)blocks * 8 > n) blocks = (int)((n + 7) / 8);
+  if (blocks > w.max_blocks) blocks = w.max_blocks;
+  if (blocks < 1) blocks = 1;
+  const int per = (int)((n + blocks - 1) / blocks);
+  blocks = (int)((n + per - 1) / per);
+  const int slot_elems = 0;  // (unused: slots are 32 lanes x kLS rows)
+  const size_t fixed = (size_t)kMaxSlots * 8 + (size_t)(MAXQ * 32 + 32) * sizeof(double2) + 128;
+  const size_t avail = (size_t)optin - fa.sharedSizeBytes - 1024;
+  const size_t slot_bytes = (size_t)32 * kCH * sizeof(double2);
+  if (avail < fixed + 2 * slot_bytes) return cudaErrorInvalidConfiguration;
+  int slots = (int)((avail - fixed) / slot_bytes);
+  if (slots > kMaxSlots) slots = kMaxSlots;
+  // ncw streaming warps with D slots each: D >= 2 keeps a chunk in flight while one is reduced
+  // one batch of 32 columns per streaming warp where possible (the critical path of a step is
+  // the busiest warp), each with D >= 2 boxes in flight
+  const int nbat = (per + 31) / 32;
+  int ncw = kRingWarps - 1;
+  if (ncw > nbat) ncw = nbat;
+  if (ncw > slots / 2) ncw = slots / 2;
+  if (const char* v = getenv("RID_QRCP_NCW")) {  // experiments
+    const int x = atoi(v);
+    if (x >= 1 && x <= slots / 2) ncw = x;
+  }
+  int D = slots / ncw;
+  if (D > 4) D = 4;
+  if (const char* v = getenv("RID_QRCP_D")) {  // ring-depth experiments
+    const int x = atoi(v);
+    if (x >= 2 && x * ncw <= slots) D = x;
+  }
+  const size_t smem = fixed + (size_t)ncw * D * slot_bytes;
+  if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+    return e;
+  // 2D tensor map of Y as a (2l doubles) x n matrix, boxes of kCH complex rows x 32 columns
+  static PFN_cuTensorMapEncodeTiled encode = nullptr;
+  if (!encode) {
+    cudaDriverEntryPointQueryResult qr;
+    if ((e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault,
+                                     &qr)) != cudaSuccess)
+      return e;
+    if (qr != cudaDriverEntryPointSuccess || !encode) return cudaErrorSymbolNotFound;
+  }
+  CUtensorMap tmap;
+  const cuuint64_t gdim[2] = {(cuuint64_t)(2 * l), (cuuint64_t)n};
+  const cuuint64_t gstride[1] = {(cuuint64_t)ldy * sizeof(double2)};
+  const cuuint32_t box[2] = {(cuuint32_t)(2 * kCH), 32u};
+  const cuuint32_t estr[2] = {1u, 1u};
+  if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)Y, gdim, gstride, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  if ((e = cudaMemsetAsync(out.info, 0, 2 * sizeof(int), st)) != cudaSuccess) return e;
+  if ((e = cudaMemsetAsync(w.F, 0, (size_t)kNB * n * sizeof(double2), st)) != cudaSuccess) return e;
+  for (int j0 = 0; j0 < k; j0 += nbw) {
+    const int jend = (j0 + nbw < k) ? j0 + nbw : k;
+    if ((e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+    QrcpOut o = out;
+    QrcpWork ww = w;
+    int j0v = j0, jendv = jend, ncwv = ncw, Dv = D, perv = per, sev = slot_elems;
+    int flags = getenv("RID_QRCP_FLAGS") ? atoi(getenv("RID_QRCP_FLAGS")) : 0;
+    void* args[] = {&Y, &ldy, &l, &n, &k, &j0v, &jendv, &tol_rel, &o, &ww, &ncwv, &Dv, &perv, &sev,
+                    &flags, &tmap};
+    e = cudaLaunchCooperativeKernel((void*)kern, dim3(blocks), dim3(kRingThreads), args, smem, st);
+    if (e != cudaSuccess) return e;
+    *launches += 1;
+    if (jend < k) {  // trailing rows jend..l-1 of every column
+      e = zgemm_ordered(w.V + jend, l, w.F, kNB, Y + jend, ldy, l - jend, n, jend - j0, 2, 0.0, 0,
+                        0, st);
+      if (e != cudaSuccess) return e;
+      *launches += 1;
+    }
+  }
+  return cudaSuccess;
+}
+
 cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, double tol_rel,
-                 const QrcpOut& out, const QrcpWork& w, int num_sms, cudaStream_t st) {
+                 const QrcpOut& out, const QrcpWork& w, int num_sms, cudaStream_t st,
+                 int* launches, int variant) {
   const int li = (int)l, ki = (int)k;
   const int qneed = (li + 31) / 32;
-#define RID_Q(QV) \
-  if (qneed <= QV) return launch_qrcp<QV>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st);
+  // Blocked panels pay off once the sketch no longer fits in L2 (C4: 34.2 -> 21.1 ms, C5: 9.2 ->
+  // 6.6 ms); small sketches (C2/C3, ~10 MB) are latency-bound and the single persistent kernel
+  // is faster there (C2: 0.68 vs 1.04 ms). Measured on B200, tools/trace_qrcp.py.
+  if (variant < 0) {
+    variant = (16.0 * (double)l * (double)n >= 64.0 * (1 << 20)) ? 1 : 0;
+    if (const char* v = getenv("RID_QRCP_VARIANT")) variant = atoi(v);
+  }
+  int nbw = kNB;
+  if (const char* v = getenv("RID_QRCP_NB")) nbw = atoi(v);  // panel-width experiments
+  if (nbw < 1 || nbw > kNB) nbw = kNB;
+  int dummy = 0;
+  if (!launches) launches = &dummy;
+#define RID_Q(QV)                                                                              \
+  if (qneed <= QV)                                                                             \
+    return variant == 0                                                                        \
+               ? launch_qrcp<QV>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st, launches)    \
+               : launch_qrcp_blocked<QV>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st,      \
+                                         launches, nbw);
   RID_Q(1) RID_Q(2) RID_Q(3) RID_Q(4) RID_Q(5) RID_Q(6) RID_Q(8) RID_Q(9) RID_Q(12) RID_Q(17)
   RID_Q(24) RID_Q(32)
 #undef RID_Q

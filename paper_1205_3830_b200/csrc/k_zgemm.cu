@@ -26,7 +26,8 @@
 namespace rid {
 
 struct ZgemmEpilogue {
-  int mode;          // 0: C = acc; 1: C = fma(noise, E(i, col0 + j), acc) (generation)
+  int mode;          // 0: C = acc; 1: C = fma(noise, E(i, col0 + j), acc) (generation);
+                     // 2: C = C - acc (QRCP trailing update)
   double noise;
   uint64_t seed;
   int64_t col0;
@@ -189,7 +190,12 @@ __global__ void __launch_bounds__(WARPS_J* WARPS_R * 32, MINB)
     for (int fb = 0; fb < FR; ++fb) {
       const int64_t r = r0c + wr * FR * 4 + fb * 4 + t;
       if (r >= Mout) continue;
-      C[j * ldc + r] = make_double2(acc[fa][fb][0], acc[fa][fb][1]);
+      double2 o = make_double2(acc[fa][fb][0], acc[fa][fb][1]);
+      if (ep.mode == 2) {  // QRCP trailing update: C = C - Rm·Bm
+        const double2 c = C[j * ldc + r];
+        o = make_double2(__dsub_rn(c.x, o.x), __dsub_rn(c.y, o.y));
+      }
+      C[j * ldc + r] = o;
     }
   }
   if (ep.mode == 1) {

@@ -160,14 +160,12 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
   RID_TRY(ws_get(c, "margin", sizeof(double) * k, &pmargin));
   RID_TRY(ws_get(c, "info", sizeof(int) * 2, &pinfo));
   const int max_blocks = 4 * c->num_sms;
-  RID_TRY(ws_get(c, "qrcp_work", rid::qrcp_work_bytes(n, max_blocks), &pwork));
+  RID_TRY(ws_get(c, "qrcp_work", rid::qrcp_work_bytes(n, l, max_blocks), &pwork));
   void* pR11;
   RID_TRY(ws_get(c, "R11", sizeof(double2) * k * k, &pR11));
   rid::QrcpOut o{(int64_t*)pJ, (double*)pbeta, (double*)presid, (double*)pmargin, (int*)pinfo,
                  (double2*)pR11};
-  char* wb = (char*)pwork;
-  rid::QrcpWork w{(double*)wb, (double*)(wb + sizeof(double) * n), nullptr, max_blocks};
-  w.bar = (unsigned*)(wb + sizeof(double) * n + sizeof(double) * 2 * 3 * max_blocks);
+  rid::QrcpWork w = rid::qrcp_work_carve(pwork, n, l, max_blocks);
   const char* trace_path = getenv("RID_QRCP_TRACE");  // per-step timing of k_qrcp (tools)
   if (trace_path) {
     void* pt;
@@ -176,7 +174,8 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
     w.trace = (unsigned long long*)pt;
   }
   RID_CUDA(c, cudaMemsetAsync(pR11, 0, sizeof(double2) * k * k, c->stream));
-  RID_CUDA(c, rid::qrcp(Yw, l, l, n, k, kRankTol, o, w, c->num_sms, c->stream));
+  RID_CUDA(c, rid::qrcp(Yw, l, l, n, k, kRankTol, o, w, c->num_sms, c->stream,
+                        diag ? &diag->launches : nullptr));
   if (trace_path) {
     std::vector<unsigned long long> tr(4 * k);
     RID_CUDA(c, cudaMemcpyAsync(tr.data(), w.trace, sizeof(unsigned long long) * 4 * k,
@@ -531,13 +530,12 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
     RID_CUDA(c, cudaEventRecord(ev[2], c->stream));
     if (c->sketch_kind == RID_SKETCH_SRFT) {  // the paper's own randomisation
       RID_CUDA(c, cudaEventRecord(ev[3], c->stream));
-      d.launches += 1;  // QRCP
       RID_TRY(srft_into(c, seed, attempt == 1, l, A, a_host ? nullptr : a.dev, m, n, n_loc, lda,
                         Yw + col0 * l, l, &d.launches));
     } else {
     RID_CUDA(c, rid::normal_fill(seed, sR, l, m, 0, 0, (double2*)pR, l, c->stream));
     RID_CUDA(c, cudaEventRecord(ev[3], c->stream));
-    d.launches += 2;  // R fill, QRCP
+    d.launches += 1;  // R fill
     if (a_host) {
       RID_TRY(sketch_streamed(c, (const double2*)pR, A, m, n_loc, lda, l, Yw + col0 * l,
                               &d.launches, nullptr, S, (double2*)pS));

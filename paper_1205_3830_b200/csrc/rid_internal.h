@@ -7,7 +7,8 @@
 namespace rid {
 
 // Ordered complex GEMM C = Rm · Bm on DMMA (k_zgemm.cu). mode 1 adds noise·E(r, col0 + j) with
-// E from Philox stream 3 (generation epilogue).
+// E from Philox stream 3 (generation epilogue); mode 2 computes C = C − Rm · Bm (QRCP trailing
+// update).
 // ksplit > 1 splits K into slices summed by a fixed-order combine (partial: ksplit*Mout*N elems).
 cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int64_t ldb,
                           double2* C, int64_t ldc, int64_t Mout, int64_t N, int64_t K, int mode,
@@ -31,15 +32,25 @@ struct QrcpOut {
   double2* R11;      // device, k x k column-major: the pivot triangle (column s = step s)
 };
 struct QrcpWork {
-  double* nu;        // n
+  double* nu;        // n: current residual norms (-1 = chosen)
   double* cand;      // 2 * 3 * max_blocks doubles (best, second, index-as-double) x 2 parities
   unsigned* bar;     // 1
   int max_blocks;
   unsigned long long* trace = nullptr;  // optional: 4 %globaltimer stamps per step (CTA 0)
+  // blocked variant (k_qrcp_panel)
+  double* nuref = nullptr;  // n: norm at the last exact computation (downdating safeguard)
+  double* scal = nullptr;   // 1: max_c ||Y[:, c]||
+  double2* V = nullptr;     // l x kNB: the panel's reflectors (column-major, ld = l)
+  double2* F = nullptr;     // kNB x n: f_s(c) (column-major, ld = kNB)
 };
-size_t qrcp_work_bytes(int64_t n, int max_blocks);
+// one workspace buffer of qrcp_work_bytes(n, l, max_blocks) bytes, carved by qrcp_work_carve
+size_t qrcp_work_bytes(int64_t n, int64_t l, int max_blocks);
+QrcpWork qrcp_work_carve(void* buf, int64_t n, int64_t l, int max_blocks);
+// variant: 1 = blocked panels + tensor-core trailing update (default), 0 = exact recompute
+// every step (one persistent kernel). *launches += kernels enqueued.
 cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, double tol_rel,
-                 const QrcpOut& out, const QrcpWork& w, int num_sms, cudaStream_t st);
+                 const QrcpOut& out, const QrcpWork& w, int num_sms, cudaStream_t st,
+                 int* launches, int variant = -1);
 
 // Inverse of the pivoted triangle R11 (R11[t, s] = Y[t, J[s]] for t < s, beta[s] on the diagonal)
 cudaError_t tri_inverse(const double2* R11, int64_t k, double2* Rinv, cudaStream_t st);

@@ -1,22 +1,41 @@
-"""Per-step timing of the QRCP kernel (RID_QRCP_TRACE) on a config's sketch."""
-import os, sys
+"""Per-step timing of the QRCP kernels (RID_QRCP_TRACE) on a config's sketch.
+
+    python tools/trace_qrcp.py C4 [variant]      variant: 1 blocked (default), 0 exact recompute
+Stamps per step (CTA 0, %globaltimer): start, reflector ready, own pass + publish done, barrier
+passed. For the blocked variant the time between the last step of a panel and the first of the
+next (the tensor-core trailing update + launch) is reported as "panel gap"."""
+import os
+import sys
+
 sys.path.insert(0, os.getcwd())
-import numpy as np, torch
-import paper_1205_3830_b200 as rid
-from paper_1205_3830_b200.configs import CONFIGS
+import numpy as np  # noqa: E402
+
+import paper_1205_3830_b200 as rid  # noqa: E402
+from paper_1205_3830_b200.configs import CONFIGS  # noqa: E402
+
 c = CONFIGS[sys.argv[1] if len(sys.argv) > 1 else "C4"]
+variant = sys.argv[2] if len(sys.argv) > 2 else "1"
+os.environ["RID_QRCP_VARIANT"] = variant
 A = rid.generate(1, c.m, c.n, c.k, c.noise)
-path = f"gpurun_out/qrcp_trace_{c.name}.txt"
+rid.decompose(A, c.k, c.l, 1)  # warm
+path = f"gpurun_out/qrcp_trace_{c.name}_v{variant}.txt"
 os.environ["RID_QRCP_TRACE"] = path
 r = rid.decompose(A, c.k, c.l, 1)
+del os.environ["RID_QRCP_TRACE"]
 t = np.loadtxt(path, dtype=np.float64)
-t0 = t[0, 1]
 d_piv = (t[:, 2] - t[:, 1]) / 1e3  # pivot reduce + Householder (us)
-d_upd = (t[:, 3] - t[:, 2]) / 1e3  # update pass + publish
+d_upd = (t[:, 3] - t[:, 2]) / 1e3  # pass + publish
 d_bar = (t[:, 4] - t[:, 3]) / 1e3  # grid barrier
+gap = (t[1:, 1] - t[:-1, 4]) / 1e3  # between steps (kernel boundary for the blocked variant)
 tot = (t[-1, 4] - t[0, 1]) / 1e6
-print(f"{c.name}: qrcp total {tot:.2f} ms (diag {r.diag['t_qrcp']*1e3:.2f} ms)")
-for a, b in [(0, 64), (64, 128), (128, 256), (256, 384), (384, c.k)]:
-    if a >= c.k: break
+print(f"{c.name} variant {variant}: qrcp traced span {tot:.2f} ms (diag t_qrcp {r.diag['t_qrcp']*1e3:.2f} ms)"
+      f"; sum pivot+hh {d_piv.sum()/1e3:.2f} ms, pass {d_upd.sum()/1e3:.2f} ms, barrier {d_bar.sum()/1e3:.2f} ms,"
+      f" gaps {gap.sum()/1e3:.2f} ms")
+edges = [0, 16, 64, 128, 256, 384, 512, 1024]
+for a, b in zip(edges[:-1], edges[1:]):
+    if a >= c.k:
+        break
     b = min(b, c.k)
-    print(f" steps {a:4d}-{b:4d}: pivot+hh {d_piv[a:b].mean():7.2f} us  update {d_upd[a:b].mean():8.2f} us  barrier {d_bar[a:b].mean():6.2f} us  (rows {c.l-a}..{c.l-b+1})")
+    print(f" steps {a:4d}-{b:4d}: pivot+hh {d_piv[a:b].mean():7.2f} us  pass {d_upd[a:b].mean():8.2f} us"
+          f"  barrier {d_bar[a:b].mean():6.2f} us  gap {gap[a:b-1].mean() if b - 1 > a else 0:7.2f} us"
+          f"  (rows {c.l-a}..{c.l-b+1})")
