@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 2)
     const int t = j - j0;        // position in the block
     const int L = l - j0;        // segment length (rows j0..l-1)
     const bool block_end = (t == kQB - 1) || (j == k - 1);
-    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[4 * j + 0] = globaltimer();
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 0] = globaltimer();
     // ---- 1. global pivot: reduce the per-CTA candidates (every CTA, identically) ------------
     if (warp == 0) {
       Top2 tt;
@@ -339,7 +339,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 2)
       }
     }
     __syncthreads();
-    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[4 * j + 1] = globaltimer();
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 1] = globaltimer();
 
     // ---- 3. every owned trailing column: reload y^(j0), apply H_j0..H_j, exact norm ----------
     // rows 0..j0-1 of the pivot column are final (nobody writes them again): CTA 0's last warp
@@ -395,9 +395,9 @@ __global__ void __launch_bounds__(kQrcpThreads, 2)
       }
     }
     block_top2_publish(loc, (j + 1) & 1);
-    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[4 * j + 2] = globaltimer();
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 2] = globaltimer();
     grid_barrier(w.bar, (unsigned)nb * (++phase));
-    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[4 * j + 3] = globaltimer();
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 3] = globaltimer();
   }
   if (b == 0 && threadIdx.x == 0) {
     out.info[0] = 0;
@@ -424,9 +424,10 @@ __global__ void __launch_bounds__(kQrcpThreads, 2)
 // After each panel the trailing rows j0+nb..l−1 are updated in one tensor-core GEMM,
 // Y −= V·F (k_zgemm.cu mode 2, K = nb): read + write once per nb steps instead of every step.
 // =============================================================================================
-constexpr int kNB = 16;
+constexpr int kNB = 16;         // max reflectors per panel (storage)
+constexpr int kNBDefault = 16;  // panel width (measured on B200: nb = 24, 32 are slower at C4/C5)
 constexpr double kRecompTol = 1e-4;
-constexpr int kRingThreads = 512;
+constexpr int kRingThreads = 256;
 constexpr int kRingWarps = kRingThreads / 32;
 constexpr int kMaxSlots = 64;
 constexpr int kCH = 16;  // rows per streamed box (a box is kCH rows x 32 columns, 8 KB)
@@ -481,6 +482,25 @@ __device__ __forceinline__ void tma_box_g2s(void* dst, const CUtensorMap* map, i
       "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(b))
       : "memory");
 }
+// the same with an L2 eviction-priority policy (createpolicy) for the box's lines
+__device__ __forceinline__ void tma_box_g2s_hint(void* dst, const CUtensorMap* map, int x, int y,
+                                                 uint64_t* b, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(b)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void consumers_sync() {  // warps 1..15 only
   asm volatile("bar.sync 1, %0;\n" ::"n"((kRingWarps - 1) * 32) : "memory");
 }
@@ -496,7 +516,7 @@ template <int MAXQ>
 __global__ void __launch_bounds__(kRingThreads, 1)
     k_qrcp_ring(double2* __restrict__ Y, int64_t ldy, int l, int64_t n, int k, int j0, int jend,
                 double tol_rel, QrcpOut out, QrcpWork w, int ncw, int D, int per, int slot_elems,
-                int flags, const __grid_constant__ CUtensorMap tmap) {
+                int flags, double l2_keep, const __grid_constant__ CUtensorMap tmap) {
   constexpr int kCW = kRingWarps - 1;  // consumer warps in the reflector phase
   constexpr int kRQ = (MAXQ * 32 + kCW * 32 - 1) / (kCW * 32);
   extern __shared__ __align__(128) unsigned char ring_smem[];
@@ -570,7 +590,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
   for (int j = j0; j < jend; ++j) {
     const int t = j - j0;
     const int L = l - j;  // rows j..l-1
-    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[4 * j + 0] = globaltimer();
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 0] = globaltimer();
     // ---- 1. global pivot (every CTA, identically); the owner drops it from its list ---------
     if (warp == 0) {
       Top2 tt;
@@ -608,6 +628,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
       return;  // no copy is in flight: every item of the previous step was consumed
     }
     const int64_t p = s_p;
+    if (w.trace && b == 0 && threadIdx.x == 32) w.trace[8 * j + 4] = globaltimer();
     const bool rev = (j & 1) != 0;  // alternate the batch and row order (L2 reuse across steps)
 
     if (warp > 0) {
@@ -620,49 +641,80 @@ __global__ void __launch_bounds__(kRingThreads, 1)
       const int mybat = (cw < ncw && nbat > cw) ? (nbat - cw + ncw - 1) / ncw : 0;
       const int nch = (L + kCH - 1) / kCH;
       const int nitems = mybat * nch;
-      auto issue = [&](int u) {  // item u = (batch u / nch, chunk u % nch) into its slot
-        const int q = u / nch, ch0 = u - q * nch;
-        const int ch = rev ? nch - 1 - ch0 : ch0;  // odd steps stream bottom-up
-        const int bi = cw + ncw * q;
+      // L2 residency: the first nkeep batches of every CTA (≈ l2_keep bytes of the trailing
+      // block over the whole grid) are re-read from L2 at every step
+      const double blk = 16.0 * (double)L * (double)n;
+      const int nkeep = blk <= l2_keep ? nbat : (int)((double)nbat * l2_keep / blk);
+      const uint64_t pol_first = policy_evict_first();
+      // boxes are issued in consumption order, D ahead: (iq, ich) = batch and chunk of the next
+      int iq = 0, ich = 0, isl = (int)(ubase % (unsigned)D), issued = 0;
+      auto issue_next = [&]() {
+        const int ch = rev ? nch - 1 - ich : ich;  // odd steps stream bottom-up
+        const int bi = cw + ncw * iq;
         const int bb = rev ? nbat - 1 - bi : bi;
-        const int s = cw * D + (int)((ubase + (unsigned)u) % (unsigned)D);
+        const int s = cw * D + isl;
         if (lane == 0) {
-          if (!(flags & 1)) asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
           mbar_expect_tx(&full[s], (unsigned)(32 * kCH * sizeof(double2)));
-          tma_box_g2s(ring + (size_t)s * 32 * kCH, &tmap, 2 * (j + ch * kCH),
-                      (int)(c_lo + 32 * bb), &full[s]);
+          // batches below nkeep stay in L2 from step to step; the rest stream with evict_first
+          if (bb < nkeep)
+            tma_box_g2s(ring + (size_t)s * 32 * kCH, &tmap, 2 * (j + ch * kCH),
+                        (int)(c_lo + 32 * bb), &full[s]);
+          else
+            tma_box_g2s_hint(ring + (size_t)s * 32 * kCH, &tmap, 2 * (j + ch * kCH),
+                             (int)(c_lo + 32 * bb), &full[s], pol_first);
         }
+        if (++ich == nch) {
+          ich = 0;
+          ++iq;
+        }
+        if (++isl == D) isl = 0;
       };
       // ---- 2a. prologue: this warp's first D boxes start streaming now ---------------------
-      for (int u = 0; u < nitems && u < D; ++u) issue(u);
+      if (!(flags & 4))
+        for (; issued < nitems && issued < D; ++issued) issue_next();
       // ---- 2b. reflector H_j from x = y^(j0)_p[j:l] − Σ_{s<t} V[j:l, s] f_s(p) --------------
-      if (cw == 0 && lane < t) {
-        s_fp[lane] = w.F[p * kNB + lane];
-        s_vrow[lane] = w.V[(int64_t)lane * ldv + j];
-      }
-      consumers_sync();
+      // all loads of a round are issued before their fmas: the pivot column's rows, then the
+      // pending reflectors V[j:l, s] (8 columns per round) and f_s(p) (a broadcast)
       double2 x[kRQ];
+#pragma unroll
+      for (int q = 0; q < kRQ; ++q) {
+        const int rr = idx + kCW * 32 * q;
+        x[q] = rr < L ? Y[p * ldy + j + rr] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int s0 = 0; s0 < kNB; s0 += 8) {
+        if (s0 < t) {
+          double2 vv[kRQ][8], fp[8];
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {
+            fp[s] = s0 + s < t ? w.F[p * kNB + s0 + s] : make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < kRQ; ++q) {
+              const int rr = idx + kCW * 32 * q;
+              vv[q][s] = (s0 + s < t && rr < L) ? w.V[(int64_t)(s0 + s) * ldv + j + rr]
+                                                : make_double2(0.0, 0.0);
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < 8; ++s) {
+            if (s0 + s < t) {
+#pragma unroll
+              for (int q = 0; q < kRQ; ++q) cmac_sub(x[q], vv[q][s], fp[s]);
+              if (idx == 0) {  // row j: V[j, s] and f_s(p) for the column pass
+                s_vrow[s0 + s] = vv[0][s];
+                s_fp[s0 + s] = fp[s];
+              }
+            }
+          }
+        }
+      }
       double s2 = 0.0;
 #pragma unroll
       for (int q = 0; q < kRQ; ++q) {
         const int rr = idx + kCW * 32 * q;
-        x[q] = make_double2(0.0, 0.0);
-        if (rr < L) {
-          x[q] = Y[p * ldy + j + rr];
-#pragma unroll
-          for (int s0 = 0; s0 < kNB; s0 += 8) {  // 8 loads in flight (L2), then their fmas
-            double2 vv[8];
-#pragma unroll
-            for (int s = 0; s < 8; ++s)
-              if (s0 + s < t) vv[s] = w.V[(int64_t)(s0 + s) * ldv + j + rr];
-#pragma unroll
-            for (int s = 0; s < 8; ++s)
-              if (s0 + s < t) cmac_sub(x[q], vv[s], s_fp[s0 + s]);
-          }
-          if (rr > 0) {
-            s2 = __fma_rn(x[q].x, x[q].x, s2);
-            s2 = __fma_rn(x[q].y, x[q].y, s2);
-          }
+        if (rr > 0 && rr < L) {
+          s2 = __fma_rn(x[q].x, x[q].x, s2);
+          s2 = __fma_rn(x[q].y, x[q].y, s2);
         }
       }
       s2 = group_sum(s2, 32);
@@ -672,6 +724,9 @@ __global__ void __launch_bounds__(kRingThreads, 1)
         s_par[1] = x[0].y;
       }
       consumers_sync();
+      if (w.trace && b == 0 && idx == 0) w.trace[8 * j + 5] = globaltimer();
+      if (flags & 4)  // experiment: the prologue after the pivot column is built
+        for (; issued < nitems && issued < D; ++issued) issue_next();
       double xnorm2 = 0.0;
       for (int q = 0; q < kCW; ++q) xnorm2 = __dadd_rn(xnorm2, s_red[q]);  // fixed order
       const double ar = s_par[0], ai = s_par[1];
@@ -717,6 +772,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
         for (int r = idx; r < j; r += kCW * 32) out.R11[(int64_t)j * k + r] = Y[p * ldy + r];
       }
       consumers_sync();
+      if (w.trace && b == 0 && idx == 0) w.trace[8 * j + 6] = globaltimer();
       // s_g[s] = v_tᴴ v_s for s < t (one warp per s)
       for (int s = cw; s < t; s += kCW) {
         const double2* vs = w.V + (int64_t)s * ldv + j;
@@ -735,26 +791,33 @@ __global__ void __launch_bounds__(kRingThreads, 1)
         if (lane == 0) s_g[s] = make_double2(gr, gi);
       }
       consumers_sync();
-      if (w.trace && b == 0 && idx == 0) w.trace[4 * j + 1] = globaltimer();
+      if (w.trace && b == 0 && idx == 0) w.trace[8 * j + 1] = globaltimer();
 
-      // ---- 3. this warp's batches: lane = column, rows streamed box by box -------------------
+      // ---- 3. this warp's batches. Inside a box lane = (row rl, column parity half): each lane
+      // accumulates conj(v[row])·y over its row of 16 of the batch's columns (a register per
+      // column, v in a register, one conflict-free 512 B shared-memory wavefront group per
+      // column pair); at the end of a batch the partials are transposed through the consumed
+      // slot and lane i sums column i's 16 row-partials in a fixed order. ------------------------
+      const int rl = lane & (kCH - 1), half = lane >> 4;
       Top2 loc;
       top2_init(loc);
       bool live = false;
       int64_t c = 0;
       double nu_old = 0.0, ref = 0.0, hr = 0.0, hi = 0.0, rsr = 0.0, rsi = 0.0;
-      double a0r = 0.0, a0i = 0.0, a1r = 0.0, a1i = 0.0;
       double2 yj = make_double2(0.0, 0.0);
+      double2 acc[16];
+      int cq = 0, cch = 0, csl = (int)(ubase % (unsigned)D);
+      unsigned cph = (ubase / (unsigned)D) & 1u;
       for (int u = 0; u < nitems; ++u) {
-        const int q = u / nch, ch0 = u - q * nch;
-        const int ch = rev ? nch - 1 - ch0 : ch0;
-        if (ch0 == 0) {  // batch start: this lane's column, its norms and pending-reflector terms
-          const int bi = cw + ncw * q;
+        const int ch = rev ? nch - 1 - cch : cch;
+        if (cch == 0) {  // batch start: lane i's column, its norms, row j, pending-reflector terms
+          const int bi = cw + ncw * cq;
           const int bb = rev ? nbat - 1 - bi : bi;
           c = c_lo + 32 * bb + lane;
           nu_old = c < c_hi ? w.nu[c] : -1.0;
           live = nu_old >= 0.0;  // chosen columns (and p) carry -1
           ref = live ? w.nuref[c] : 0.0;
+          yj = live ? Y[c * ldy + j] : make_double2(0.0, 0.0);
           // h = Σ_{s<t} g_s f_s,  rs = Σ_{s<t} V[j, s] f_s
           hr = hi = rsr = rsi = 0.0;
 #pragma unroll
@@ -770,29 +833,49 @@ __global__ void __launch_bounds__(kRingThreads, 1)
                 cmac_add(rsr, rsi, s_vrow[s0 + s], f[s]);
               }
           }
-          a0r = a0i = a1r = a1i = 0.0;
-        }
-        const unsigned U = ubase + (unsigned)u;
-        const int s = cw * D + (int)(U % (unsigned)D);
-        mbar_wait(&full[s], (U / (unsigned)D) & 1);
-        const double2* sy = ring + (size_t)s * 32 * kCH + lane * kCH;  // this lane's column
-        if (ch == 0) yj = sy[0];
-        const double2* vv = sv + ch * kCH;
-        // rows visited in a lane-rotated order: conflict-free shared-memory wavefronts
 #pragma unroll
-        for (int rr = 0; rr < kCH; rr += 2) {
-          const int r0 = (rr + lane) & (kCH - 1), r1 = (rr + 1 + lane) & (kCH - 1);
-          const double2 v0 = vv[r0], y0 = sy[r0], v1 = vv[r1], y1 = sy[r1];
-          a0r = __fma_rn(v0.x, y0.x, __fma_rn(v0.y, y0.y, a0r));  // conj(v) y
-          a0i = __fma_rn(v0.x, y0.y, __fma_rn(-v0.y, y0.x, a0i));
-          a1r = __fma_rn(v1.x, y1.x, __fma_rn(v1.y, y1.y, a1r));
-          a1i = __fma_rn(v1.x, y1.y, __fma_rn(-v1.y, y1.x, a1i));
+          for (int cc = 0; cc < 16; ++cc) acc[cc] = make_double2(0.0, 0.0);
         }
-        __syncwarp();  // every lane is done with the slot
-        if (u + D < nitems) issue(u + D);
-        if (ch0 == nch - 1 && live) {  // ---- this lane's column is complete -----------------
-          const double dr = __dsub_rn(__dadd_rn(a0r, a1r), hr);  // d = v_tᴴ y − h
-          const double di = __dsub_rn(__dadd_rn(a0i, a1i), hi);
+        const int s = cw * D + csl;
+        mbar_wait(&full[s], cph);
+        double2* box = ring + (size_t)s * 32 * kCH;  // [32 columns][kCH rows]
+        const double2 v = sv[ch * kCH + rl];
+#pragma unroll
+        for (int cc = 0; cc < 16; ++cc) {
+          const double2 y = box[(2 * cc + half) * kCH + rl];
+          acc[cc].x = __fma_rn(v.x, y.x, __fma_rn(v.y, y.y, acc[cc].x));  // conj(v) y
+          acc[cc].y = __fma_rn(v.x, y.y, __fma_rn(-v.y, y.x, acc[cc].y));
+        }
+        const bool last = cch == nch - 1;
+        double dr = 0.0, di = 0.0;
+        __syncwarp();
+        if (last) {  // transpose through the consumed slot: lane i sums column i
+#pragma unroll
+          for (int cc = 0; cc < 16; ++cc) box[(2 * cc + half) * kCH + rl] = acc[cc];
+          __syncwarp();
+          double e0r = 0.0, e0i = 0.0, e1r = 0.0, e1i = 0.0;
+#pragma unroll
+          for (int r = 0; r < kCH; r += 2) {
+            const double2 p0 = box[lane * kCH + ((r + lane) & (kCH - 1))];
+            const double2 p1 = box[lane * kCH + ((r + 1 + lane) & (kCH - 1))];
+            e0r = __dadd_rn(e0r, p0.x);
+            e0i = __dadd_rn(e0i, p0.y);
+            e1r = __dadd_rn(e1r, p1.x);
+            e1i = __dadd_rn(e1i, p1.y);
+          }
+          dr = __dadd_rn(e0r, e1r);
+          di = __dadd_rn(e0i, e1i);
+          __syncwarp();
+        }
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");  // generic -> TMA (WAR)
+        __syncwarp();
+        if (issued < nitems) {  // refill the slot D boxes ahead
+          issue_next();
+          ++issued;
+        }
+        if (last && live) {  // ---- lane i's column is complete --------------------------------
+          dr = __dsub_rn(dr, hr);  // d = v_tᴴ y − h
+          di = __dsub_rn(di, hi);
           const double2 ft = make_double2(__fma_rn(tr, dr, __dmul_rn(ti, di)),  // conj(tau) d
                                           __fma_rn(tr, di, -__dmul_rn(ti, dr)));
           const double2 Rj = make_double2(__dsub_rn(__dsub_rn(yj.x, rsr), ft.x),
@@ -821,6 +904,14 @@ __global__ void __launch_bounds__(kRingThreads, 1)
           if (need) w.nuref[c] = nu_new;
           top2_push(loc, nu_new, c);
         }
+        if (++cch == nch) {
+          cch = 0;
+          ++cq;
+        }
+        if (++csl == D) {
+          csl = 0;
+          cph ^= 1u;
+        }
       }
       ubase += (unsigned)nitems;
       top2_warp(loc);
@@ -839,9 +930,9 @@ __global__ void __launch_bounds__(kRingThreads, 1)
       cc[1] = tt.b2;
       cc[2] = (double)tt.i1;
     }
-    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[4 * j + 2] = globaltimer();
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 2] = globaltimer();
     if (j + 1 < jend) grid_barrier(w.bar, (unsigned)nbk * (++phase));
-    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[4 * j + 3] = globaltimer();
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 3] = globaltimer();
   }
   if (b == 0 && threadIdx.x == 0) out.info[1] = jend;
 }
@@ -981,8 +1072,10 @@ static cudaError_t launch_qrcp_blocked(double2* Y, int64_t ldy, int l, int64_t n
     QrcpWork ww = w;
     int j0v = j0, jendv = jend, ncwv = ncw, Dv = D, perv = per, sev = slot_elems;
     int flags = getenv("RID_QRCP_FLAGS") ? atoi(getenv("RID_QRCP_FLAGS")) : 0;
+    double l2_keep = 80.0 * (1 << 20);  // bytes of the trailing block kept in L2 (126 MB L2)
+    if (const char* v = getenv("RID_QRCP_L2KEEP_MB")) l2_keep = atof(v) * (1 << 20);
     void* args[] = {&Y, &ldy, &l, &n, &k, &j0v, &jendv, &tol_rel, &o, &ww, &ncwv, &Dv, &perv, &sev,
-                    &flags, &tmap};
+                    &flags, &l2_keep, &tmap};
     e = cudaLaunchCooperativeKernel((void*)kern, dim3(blocks), dim3(kRingThreads), args, smem, st);
     if (e != cudaSuccess) return e;
     *launches += 1;
@@ -1008,9 +1101,9 @@ cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, doubl
     variant = (16.0 * (double)l * (double)n >= 64.0 * (1 << 20)) ? 1 : 0;
     if (const char* v = getenv("RID_QRCP_VARIANT")) variant = atoi(v);
   }
-  int nbw = kNB;
+  int nbw = kNBDefault;
   if (const char* v = getenv("RID_QRCP_NB")) nbw = atoi(v);  // panel-width experiments
-  if (nbw < 1 || nbw > kNB) nbw = kNB;
+  if (nbw < 1 || nbw > kNB) nbw = kNBDefault;
   int dummy = 0;
   if (!launches) launches = &dummy;
 #define RID_Q(QV)                                                                              \

@@ -169,22 +169,24 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
   const char* trace_path = getenv("RID_QRCP_TRACE");  // per-step timing of k_qrcp (tools)
   if (trace_path) {
     void* pt;
-    RID_TRY(ws_get(c, "qrcp_trace", sizeof(unsigned long long) * 4 * k, &pt));
-    RID_CUDA(c, cudaMemsetAsync(pt, 0, sizeof(unsigned long long) * 4 * k, c->stream));
+    RID_TRY(ws_get(c, "qrcp_trace", sizeof(unsigned long long) * 8 * k, &pt));
+    RID_CUDA(c, cudaMemsetAsync(pt, 0, sizeof(unsigned long long) * 8 * k, c->stream));
     w.trace = (unsigned long long*)pt;
   }
   RID_CUDA(c, cudaMemsetAsync(pR11, 0, sizeof(double2) * k * k, c->stream));
   RID_CUDA(c, rid::qrcp(Yw, l, l, n, k, kRankTol, o, w, c->num_sms, c->stream,
                         diag ? &diag->launches : nullptr));
   if (trace_path) {
-    std::vector<unsigned long long> tr(4 * k);
-    RID_CUDA(c, cudaMemcpyAsync(tr.data(), w.trace, sizeof(unsigned long long) * 4 * k,
+    std::vector<unsigned long long> tr(8 * k);
+    RID_CUDA(c, cudaMemcpyAsync(tr.data(), w.trace, sizeof(unsigned long long) * 8 * k,
                                 cudaMemcpyDeviceToHost, c->stream));
     RID_CUDA(c, cudaStreamSynchronize(c->stream));
     if (FILE* f = fopen(trace_path, "w")) {
-      for (int64_t j = 0; j < k; ++j)
-        fprintf(f, "%lld %llu %llu %llu %llu\n", (long long)j, tr[4 * j], tr[4 * j + 1],
-                tr[4 * j + 2], tr[4 * j + 3]);
+      for (int64_t j = 0; j < k; ++j) {
+        fprintf(f, "%lld", (long long)j);
+        for (int q = 0; q < 8; ++q) fprintf(f, " %llu", tr[8 * j + q]);
+        fprintf(f, "\n");
+      }
       fclose(f);
     }
   }

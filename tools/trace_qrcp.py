@@ -31,6 +31,13 @@ tot = (t[-1, 4] - t[0, 1]) / 1e6
 print(f"{c.name} variant {variant}: qrcp traced span {tot:.2f} ms (diag t_qrcp {r.diag['t_qrcp']*1e3:.2f} ms)"
       f"; sum pivot+hh {d_piv.sum()/1e3:.2f} ms, pass {d_upd.sum()/1e3:.2f} ms, barrier {d_bar.sum()/1e3:.2f} ms,"
       f" gaps {gap.sum()/1e3:.2f} ms")
+if t.shape[1] > 5 and t[:, 5].any():  # ring kernel: pivot | x-build | zlarfg + sv | G
+    d_a = (t[:, 5] - t[:, 1]) / 1e3
+    d_b = (t[:, 6] - t[:, 5]) / 1e3
+    d_c = (t[:, 7] - t[:, 6]) / 1e3
+    d_d = (t[:, 2] - t[:, 7]) / 1e3
+    print(f" reflector phase split (mean us): pivot reduce {d_a.mean():.2f}, x-build {d_b.mean():.2f},"
+          f" zlarfg+v {d_c.mean():.2f}, G {d_d.mean():.2f}")
 edges = [0, 16, 64, 128, 256, 384, 512, 1024]
 for a, b in zip(edges[:-1], edges[1:]):
     if a >= c.k:
