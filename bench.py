@@ -264,7 +264,9 @@ def run_ours(args, cfg):
     rgen_s = max_over_ranks(statistics.mean(d["t_rgen"] for d in diags))
     gather_s = max_over_ranks(statistics.mean(d["t_gather"] for d in diags))
     flops = 8.0 * l * m * n
-    sketch_tf_rank = 8.0 * l * m * n_loc / sketch_s / 1e12  # slowest rank's kernel
+    sketch_tf_rank = 8.0 * l * m * n_loc / sketch_s / 1e12  # slowest rank's kernel (8lmn)
+    mults = rid.sketch_mults()  # 3: Gauss's three real products (6lmn executed), 4: real embedding
+    sketch_exec_tf = sketch_tf_rank * mults / 4.0
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         tf, dt, n_s, threads = oracle_sample(cfg, seed, target_s=args.ref_seconds)
@@ -291,7 +293,8 @@ def run_ours(args, cfg):
         # every §8(a) row once (a1 generate + a2-a5 the ID + a6 the q-iteration estimate); the
         # headline value times the ID itself (a2-a5), the metric's "end-to-end ID"
         "all_rows_seconds": (gen_s + step_s + est_s) if est_s is not None else None,
-        "sketch_tflops": sketch_tf_rank * world,
+        "sketch_tflops": sketch_tf_rank * world,  # 8lmn convention (the metric's)
+        "sketch_mults": mults,
         "phases": {"rgen_s": rgen_s, "sketch_s": sketch_s, "gather_s": gather_s,
                    "qrcp_s": qrcp_s, "solve_s": solve_s, "generate_s": gen_s,
                    "error_estimate_s": est_s, "error_estimate_q": args.q},
@@ -299,12 +302,15 @@ def run_ours(args, cfg):
         "error_bound_eq3": rid.error_bound(m, n, k, 1e-20, cfg.noise * (m**0.5 + n**0.5))
         if cfg.noise else None,
         "tie_margin_min": diags[-1]["tie_margin_min"],
-        "roofline": {"bound": "tensor", "achieved": sketch_tf_rank,
+        "roofline": {"bound": "tensor", "achieved": sketch_exec_tf,
                      "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": sketch_tf_rank / FP64_DMMA_PEAK_TFLOPS,
+                     "frac": sketch_exec_tf / FP64_DMMA_PEAK_TFLOPS,
                      "traffic": prof.get("dram_bytes_per_launch"),
-                     "kernel": "k_zgemm_dmma (sketch Y = R A, DMMA.8x8x4)",
-                     "algorithmic": f"8*l*m*n_loc = {8.0 * l * m * n_loc:.4g} flop per launch",
+                     "kernel": ("k_zgemm3m (sketch Y = R A, Gauss 3M, DMMA.8x8x4)" if mults == 3
+                                else "k_zgemm_dmma (sketch Y = R A, real embedding, DMMA.8x8x4)"),
+                     "algorithmic": (f"{2 * mults}*l*m*n_loc = {2.0 * mults * l * m * n_loc:.4g} "
+                                     f"flop per launch ({mults} real products per complex "
+                                     f"multiply-add; the metric counts 8*l*m*n)"),
                      "peak_source": FP64_PEAK_SOURCE},
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -113,9 +113,13 @@ rid_status rid_generate(rid_ctx* ctx, uint64_t seed, int64_t m, int64_t n, int64
  * Gaussian sketch in place of the SRFT of Eqs. 4–7). stream is 4 (or 20 on the retry).
  * A is a block of n_loc columns of an m x n matrix (n = n_loc for a whole matrix): n fixes the
  * K-split of the DMMA product (rid_sketch_splits), so the columns of Y are bit-identical for
- * every sharding of the same n. With one slice the K summation is the ascending fused chain and
- * Y is bit-identical to the oracle's naive loop; with S slices the slice sums are added in slice
- * order (agreement to rounding). Preconditions: 1 <= l <= m, n_loc <= n, lda >= m, ldy >= l. */
+ * every sharding of the same n. The complex products use Gauss's three real multiplications
+ * (rid_sketch_mults() == 3, default; R31): Y agrees with the oracle's ascending chain
+ * to rounding (north-star bar 1e-12 relative). With RID_SKETCH_4M=1 in the environment the
+ * real embedding with four (rid_sketch_mults() == 4) is used: with one slice its K summation is
+ * the ascending fused chain and Y is bit-identical to the oracle's naive loop; with S slices the
+ * slice sums are added in slice order. Preconditions: 1 <= l <= m, n_loc <= n, lda >= m,
+ * ldy >= l. */
 rid_status rid_sketch(rid_ctx* ctx, uint64_t seed, uint32_t stream, int64_t l, const rid_z* A,
                       int64_t m, int64_t n, int64_t n_loc, int64_t lda, rid_z* Y, int64_t ldy);
 /* The paper's own randomisation Y = S F D A (§2, Eqs. 4–7; docs/RNG.md §7):
@@ -131,6 +135,9 @@ rid_status rid_set_sketch(rid_ctx* ctx, int kind);
 /* Number of K slices S the sketch of an m-row, n-column matrix uses (1 = unsplit): chosen so that
  * the n/8-column shard of an 8-GPU run still fills the GPU, a function of (m, l, n) only. */
 int rid_sketch_splits(const rid_ctx* ctx, int64_t m, int64_t l, int64_t n);
+/* Real multiplications per complex multiply-add in the sketch kernel: 3 (Gauss, 6 l m n flops,
+ * default) or 4 (real embedding, 8 l m n flops, bit-exact ordered chain; RID_SKETCH_4M=1). */
+int rid_sketch_mults(void);
 
 /* The whole ID on a column shard: sketch -> all-gather Y -> column-pivoted
  * Householder QR of Y (k steps, greedy max-norm pivot, ties -> lowest index) -> T = R11^{-1} R12

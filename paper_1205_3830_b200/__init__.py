@@ -59,7 +59,7 @@ EXPORTS = ["rid_create", "rid_destroy", "rid_last_error", "rid_version", "rid_co
            "rid_comm_get_id", "rid_comm_init", "rid_comm_info", "rid_generate", "rid_sketch",
            "rid_decompose", "rid_error_estimate", "rid_error_bound", "rid_normal_fill",
            "rid_qrcp", "rid_factor_solve", "rid_sketch_splits", "rid_sketch_srft",
-           "rid_set_sketch"]
+           "rid_set_sketch", "rid_sketch_mults"]
 SKETCH_GAUSSIAN, SKETCH_SRFT = 0, 1
 
 
@@ -86,6 +86,7 @@ def lib():
         "rid_generate": ([p, u64, i64, i64, i64, d, i64, i64, p, i64], ci),
         "rid_sketch": ([p, u64, u32, i64, p, i64, i64, i64, i64, p, i64], ci),
         "rid_sketch_splits": ([p, i64, i64, i64], ci),
+        "rid_sketch_mults": ([], ci),
         "rid_sketch_srft": ([p, u64, ci, i64, p, i64, i64, i64, i64, p, i64], ci),
         "rid_set_sketch": ([p, ci], ci),
         "rid_decompose": ([p, p, i64, i64, i64, i64, i64, i64, i64, u64, p, p, i64, p], ci),
@@ -288,9 +289,15 @@ def sketch_srft(A, seed: int, l: int, retry: bool = False, out=None, n: int | No
 
 
 def sketch_splits(m: int, l: int, n: int, ctx: Context | None = None) -> int:
-    """K slices of the sketch of an m x n matrix (1: bit-identical to the oracle's chain)."""
+    """K slices of the sketch of an m x n matrix."""
     ctx = ctx or default_context()
     return lib().rid_sketch_splits(ctx.h, m, l, n)
+
+
+def sketch_mults() -> int:
+    """3: Gauss's three-multiplication sketch (default); 4: the ordered real embedding
+    (RID_SKETCH_4M=1), bit-identical to the oracle's chain when sketch_splits(...) == 1."""
+    return lib().rid_sketch_mults()
 
 
 @dataclass

@@ -224,11 +224,29 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
   return RID_OK;
 }
 
+// R (l x m, stream s) for the sketch, plus Re R + Im R for the 3M kernel. Returns launches.
+rid_status fill_R(rid_ctx* c, uint64_t seed, uint32_t s, int64_t l, int64_t m, double2** R,
+                  double** Rs, int* launches) {
+  void *pR, *pRs = nullptr;
+  RID_TRY(ws_get(c, "R", sizeof(double2) * l * m, &pR));
+  RID_CUDA(c, rid::normal_fill(seed, s, l, m, 0, 0, (double2*)pR, l, c->stream));
+  *launches += 1;
+  if (rid::sketch_mults() == 3) {
+    RID_TRY(ws_get(c, "Rs", sizeof(double) * rid::rsum_ld(l) * m, &pRs));
+    RID_CUDA(c, rid::rsum_fill((const double2*)pR, l, m, l, (double*)pRs, rid::rsum_ld(l),
+                               c->stream));
+    *launches += 1;
+  }
+  *R = (double2*)pR;
+  *Rs = (double*)pRs;
+  return RID_OK;
+}
+
 // Y[:, 0:n_loc] = R A for a HOST A (the e2e path): A is streamed to the device in column chunks
 // of ~1 GiB on a copy stream, double-buffered, each chunk's sketch overlapping the copy of the
 // next. The sketch of a column does not depend on the chunking, so Y is bit-identical to the
 // device-resident call. The device never holds more than two chunks of A.
-rid_status sketch_streamed(rid_ctx* c, const double2* R, const rid_z* hostA, int64_t m,
+rid_status sketch_streamed(rid_ctx* c, const double2* R, const double* Rs, const rid_z* hostA, int64_t m,
                            int64_t n_loc, int64_t lda, int64_t l, double2* Y, int* launches,
                            double* t_h2d, int ksplit, double2* partial) {
   if (!c->copy_stream) {
@@ -260,8 +278,8 @@ rid_status sketch_streamed(rid_ctx* c, const double2* R, const rid_z* hostA, int
                                   cudaMemcpyHostToDevice, c->copy_stream));
     RID_CUDA(c, cudaEventRecord(c->ev_copied[b], c->copy_stream));
     RID_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0));
-    RID_CUDA(c, rid::zgemm_ordered(R, l, (const double2*)buf[b], m, Y + j0 * l, l, l, nc, m, 0,
-                                   0.0, 0, 0, c->stream, ksplit, partial));
+    RID_CUDA(c, rid::sketch_gemm(R, l, Rs, (const double2*)buf[b], m, Y + j0 * l, l, l, nc, m,
+                                 c->stream, ksplit, partial));
     RID_CUDA(c, cudaEventRecord(c->ev_used[b], c->stream));
     *launches += ksplit > 1 ? 2 : 1;
   }
@@ -465,8 +483,10 @@ rid_status rid_sketch_srft(rid_ctx* c, uint64_t seed, int retry, int64_t l, cons
 
 int rid_sketch_splits(const rid_ctx* c, int64_t m, int64_t l, int64_t n) {
   if (!c || m < 1 || l < 1 || n < 1) return 1;
-  return rid::zgemm_ksplit(l, m, n / 8, c->num_sms);
+  return rid::sketch_ksplit(l, m, n / 8, c->num_sms);
 }
+
+int rid_sketch_mults(void) { return rid::sketch_mults(); }
 
 rid_status rid_sketch(rid_ctx* c, uint64_t seed, uint32_t stream, int64_t l, const rid_z* A,
                       int64_t m, int64_t n, int64_t n_loc, int64_t lda, rid_z* Y, int64_t ldy) {
@@ -478,13 +498,15 @@ rid_status rid_sketch(rid_ctx* c, uint64_t seed, uint32_t stream, int64_t l, con
   MatArg a, y;
   RID_TRY(stage_in(c, "stage_A", A, m, n_loc, lda, sizeof(rid_z), true, &a));
   RID_TRY(stage_in(c, "stage_Y", Y, l, n_loc, ldy, sizeof(rid_z), false, &y));
-  void *pR, *pS = nullptr;
-  RID_TRY(ws_get(c, "R", sizeof(double2) * l * m, &pR));
-  const int S = rid::zgemm_ksplit(l, m, n / 8, c->num_sms);
+  void* pS = nullptr;
+  double2* R;
+  double* Rs;
+  int nl = 0;
+  RID_TRY(fill_R(c, seed, stream, l, m, &R, &Rs, &nl));
+  const int S = rid::sketch_ksplit(l, m, n / 8, c->num_sms);
   if (S > 1) RID_TRY(ws_get(c, "splitk", sizeof(double2) * S * l * n_loc, &pS));
-  RID_CUDA(c, rid::normal_fill(seed, stream, l, m, 0, 0, (double2*)pR, l, c->stream));
-  RID_CUDA(c, rid::zgemm_ordered((const double2*)pR, l, (const double2*)a.dev, lda, (double2*)y.dev,
-                                 ldy, l, n_loc, m, 0, 0.0, seed, 0, c->stream, S, (double2*)pS));
+  RID_CUDA(c, rid::sketch_gemm(R, l, Rs, (const double2*)a.dev, lda, (double2*)y.dev, ldy, l,
+                               n_loc, m, c->stream, S, (double2*)pS));
   RID_TRY(stage_out(c, y, Y, l, n_loc, ldy, sizeof(rid_z)));
   if (a.host || y.host) RID_CUDA(c, cudaStreamSynchronize(c->stream));
   return RID_OK;
@@ -517,7 +539,7 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
   RID_TRY(ws_get(c, "R", sizeof(double2) * l * m, &pR));
   double2* Yw = (double2*)pY;
   // K-split of the sketch: a function of (m, l, n) only, so Y is identical for every sharding
-  const int S = rid::zgemm_ksplit(l, m, n / 8, c->num_sms);
+  const int S = rid::sketch_ksplit(l, m, n / 8, c->num_sms);
   void* pS = nullptr;
   if (S > 1) {
     const int64_t cols = a_host ? std::min<int64_t>(n_loc, std::max<int64_t>(64, (int64_t)(1 << 30) / (16 * m)))
@@ -535,16 +557,16 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
       RID_TRY(srft_into(c, seed, attempt == 1, l, A, a_host ? nullptr : a.dev, m, n, n_loc, lda,
                         Yw + col0 * l, l, &d.launches));
     } else {
-    RID_CUDA(c, rid::normal_fill(seed, sR, l, m, 0, 0, (double2*)pR, l, c->stream));
+    double2* Rg;
+    double* Rsg;
+    RID_TRY(fill_R(c, seed, sR, l, m, &Rg, &Rsg, &d.launches));
     RID_CUDA(c, cudaEventRecord(ev[3], c->stream));
-    d.launches += 1;  // R fill
     if (a_host) {
-      RID_TRY(sketch_streamed(c, (const double2*)pR, A, m, n_loc, lda, l, Yw + col0 * l,
-                              &d.launches, nullptr, S, (double2*)pS));
+      RID_TRY(sketch_streamed(c, Rg, Rsg, A, m, n_loc, lda, l, Yw + col0 * l, &d.launches,
+                              nullptr, S, (double2*)pS));
     } else {
-      RID_CUDA(c, rid::zgemm_ordered((const double2*)pR, l, (const double2*)a.dev, lda,
-                                     Yw + col0 * l, l, l, n_loc, m, 0, 0.0, seed, 0, c->stream, S,
-                                     (double2*)pS));
+      RID_CUDA(c, rid::sketch_gemm(Rg, l, Rsg, (const double2*)a.dev, lda, Yw + col0 * l, l, l,
+                                   n_loc, m, c->stream, S, (double2*)pS));
       d.launches += S > 1 ? 2 : 1;
     }
     }

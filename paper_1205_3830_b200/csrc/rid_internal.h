@@ -15,6 +15,22 @@ cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int
                           double noise, uint64_t seed, int64_t col0, cudaStream_t st,
                           int ksplit = 1, double2* partial = nullptr);
 int zgemm_pick_fr(int64_t Mout);
+// The sketch as three real products (Gauss), 6·l·m·n flops (k_zgemm3m.cu); split-K as above.
+// Rs = Re R + Im R (l x m doubles, leading dimension rsum_ld(l), pad rows zero) from rsum_fill.
+cudaError_t zgemm3m(const double2* Rm, int64_t ldr, const double* Rs, int64_t ldrs,
+                    const double2* Bm, int64_t ldb, double2* C, int64_t ldc, int64_t Mout,
+                    int64_t N, int64_t K, cudaStream_t st, int ksplit, double2* partial);
+int zgemm3m_ksplit(int64_t Mout, int64_t K, int64_t n_ref, int num_sms);
+inline int64_t rsum_ld(int64_t l) { return (l + 1) / 2 * 2; }
+cudaError_t rsum_fill(const double2* R, int64_t l, int64_t m, int64_t ldr, double* Rs,
+                      int64_t ldrs, cudaStream_t st);
+// Sketch dispatch: 3 (Gauss, default) or 4 (ordered real embedding, RID_SKETCH_4M=1) real
+// products per complex multiply-add. Rs is only read by the 3M kernel (may be null for 4M).
+int sketch_mults();
+int sketch_ksplit(int64_t l, int64_t m, int64_t n_ref, int num_sms);
+cudaError_t sketch_gemm(const double2* R, int64_t ldr, const double* Rs, const double2* A,
+                        int64_t lda, double2* Y, int64_t ldy, int64_t l, int64_t ncols, int64_t m,
+                        cudaStream_t st, int ksplit, double2* partial);
 // K slices for a sketch of Mout rows, K = m, chosen from n_ref = n_global / 8 only (G-invariant)
 int zgemm_ksplit(int64_t Mout, int64_t K, int64_t n_ref, int num_sms);
 

@@ -74,9 +74,9 @@ def test_fullsize_against_oracle_golden(rid, orc, name):
     for j in cols:
         y_o = unhex(g["Y_cols"][str(j)])
         y_g = Y[:, j].cpu().numpy()
-        if S == 1:  # one ascending fused chain: bit-identical
+        if S == 1 and rid.sketch_mults() == 4:  # one ascending fused chain: bit-identical
             assert np.array_equal(bits(y_g), bits(y_o)), f"Y[:, {j}]"
-        else:  # S fixed-order slice sums
+        else:  # Gauss's three products (R31) and/or S fixed-order slice sums: to rounding
             assert np.linalg.norm(y_g - y_o) <= 1e-13 * np.linalg.norm(y_o), f"Y[:, {j}]"
     yf = float(torch.linalg.norm(Y))
     assert abs(yf - g["Y_fro"]) <= 1e-12 * g["Y_fro"]

@@ -98,20 +98,30 @@ def test_sketch_bitexact(rid, orc, seed, m, n, k, noise, l, monkeypatch):
     A_g = rid.generate(seed, m, n, k, noise)
     A_o = orc.generate(seed, m, n, k, noise)
     Y_o = orc.sketch(A_o, seed, l)
-    # the default launch (K split into S slices when the tile count is small): the north-star bar
-    S = rid.sketch_splits(m, l, n)
+    # the default launch: Gauss's three products (reading R31), K split into S slices when the
+    # tile count is small: the north-star bar, and in practice a few ulps
+    assert rid.sketch_mults() == 3
     Y_g = np_(rid.sketch(A_g, seed, l))
     assert relf(Y_g, Y_o) <= 1e-12
-    if S == 1:
-        assert bits_equal(Y_g, Y_o)
-    # one slice: the single ascending fused chain, bit-identical to the oracle's naive loop
+    # random-walk rounding of an m-term sum, ~u·sqrt(m), times the ~4x cancellation of
+    # Im = P3 - P1 - P2: <= 5e-14 for m <= 8192 (measured 2e-15 .. 1e-14 on these shapes)
+    tol3 = 5e-14
+    assert relf(Y_g, Y_o) <= tol3
     monkeypatch.setenv("RID_SKETCH_SPLIT", "1")
+    assert relf(np_(rid.sketch(A_g, seed, l)), Y_o) <= tol3
+    # the ordered real embedding (4 products): one slice is the single ascending fused chain,
+    # bit-identical to the oracle's naive loop
+    monkeypatch.setenv("RID_SKETCH_4M", "1")
+    assert rid.sketch_mults() == 4
     Y_1 = np_(rid.sketch(A_g, seed, l))
     assert bits_equal(Y_1, Y_o)
     # an explicit 3-slice split: fixed-order slice sums, within rounding
     monkeypatch.setenv("RID_SKETCH_SPLIT", "3")
     Y_3 = np_(rid.sketch(A_g, seed, l))
     assert relf(Y_3, Y_o) <= 1e-14
+    monkeypatch.setenv("RID_SKETCH_4M", "0")
+    Y_33 = np_(rid.sketch(A_g, seed, l))
+    assert relf(Y_33, Y_o) <= tol3
 
 
 def test_sketch_retry_stream_and_ld(rid, orc):
@@ -121,7 +131,11 @@ def test_sketch_retry_stream_and_ld(rid, orc):
     At = torch.from_numpy(big).T.contiguous().T.cuda()[:500]
     assert At.stride() == (1, 520)
     Y = np_(rid.sketch(At, 11, 9, stream=20))
-    assert bits_equal(Y, orc.sketch(A, 11, 9, stream=20))
+    Y_o = orc.sketch(A, 11, 9, stream=20)
+    assert relf(Y, Y_o) <= 5e-14  # Gauss's three products (default), see test_sketch_bitexact
+    with pytest.MonkeyPatch.context() as mp:  # the ordered chain: bitwise
+        mp.setenv("RID_SKETCH_4M", "1")
+        assert bits_equal(np_(rid.sketch(At, 11, 9, stream=20)), Y_o)
 
 
 # ------------------------------------------------------------------------------ decompose ----
