@@ -148,6 +148,22 @@ constexpr double kRankTol = 1e-13;   // reading R13
 constexpr double kSingTol = 1e-13;
 constexpr uint32_t kStreamR = 4, kStreamRRetry = 20;
 
+// T = R11^-1 R12 for the shard's columns (reading R29), on the same complex-product kernel as
+// the sketch (Gauss's three products by default, R31), written straight into P_loc.
+rid_status solve_T(rid_ctx* c, const double2* Rinv, int64_t k, const double2* Y, int64_t ldy,
+                   double2* P, int64_t ldp, int64_t n_loc) {
+  if (rid::sketch_mults() == 3) {
+    void* ps;
+    RID_TRY(ws_get(c, "Rinvs", sizeof(double) * rid::rsum_ld(k) * k, &ps));
+    RID_CUDA(c, rid::rsum_fill(Rinv, k, k, k, (double*)ps, rid::rsum_ld(k), c->stream));
+    RID_CUDA(c, rid::zgemm3m(Rinv, k, (const double*)ps, rid::rsum_ld(k), Y, ldy, P, ldp, k, n_loc,
+                             k, c->stream, 1, nullptr));
+  } else {
+    RID_CUDA(c, rid::zgemm_ordered(Rinv, k, Y, ldy, P, ldp, k, n_loc, k, 0, 0.0, 0, 0, c->stream));
+  }
+  return RID_OK;
+}
+
 // Factor the full sketch in workspace "Y" and solve for the local shard columns.
 // On entry Yw holds the full l x n sketch (ld = l). Writes J (device ws), P_loc (device).
 rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64_t k, int64_t col0,
@@ -218,8 +234,7 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
   void* pRinv;
   RID_TRY(ws_get(c, "Rinv", sizeof(double2) * k * k, &pRinv));
   RID_CUDA(c, rid::tri_inverse((const double2*)pR11, k, (double2*)pRinv, c->stream));
-  RID_CUDA(c, rid::zgemm_ordered((const double2*)pRinv, k, Yw + col0 * l, l, Pdev, ldp, k, n_loc,
-                                 k, 0, 0.0, 0, 0, c->stream));
+  RID_TRY(solve_T(c, (const double2*)pRinv, k, Yw + col0 * l, l, Pdev, ldp, n_loc));
   RID_CUDA(c, rid::assemble_identity((const int64_t*)pJ, k, col0, n_loc, Pdev, ldp, c->stream));
   return RID_OK;
 }
@@ -596,10 +611,9 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
     RID_TRY(ws_get(c, "R11", sizeof(double2) * k * k, &pR11));
     RID_TRY(ws_get(c, "Rinv", sizeof(double2) * k * k, &pRinv));
     RID_CUDA(c, rid::tri_inverse((const double2*)pR11, k, (double2*)pRinv, c->stream));
-    RID_CUDA(c, rid::zgemm_ordered((const double2*)pRinv, k, Yw + col0 * l, l, (double2*)p.dev, ldp,
-                                   k, n_loc, k, 0, 0.0, 0, 0, c->stream));
+    RID_TRY(solve_T(c, (const double2*)pRinv, k, Yw + col0 * l, l, (double2*)p.dev, ldp, n_loc));
     RID_CUDA(c, rid::assemble_identity(Jdev, k, col0, n_loc, (double2*)p.dev, ldp, c->stream));
-    d.launches += 3;  // R11^-1, T GEMM, identity block
+    d.launches += rid::sketch_mults() == 3 ? 4 : 3;  // R11^-1, (sum plane), T GEMM, identity
   }
   RID_CUDA(c, cudaEventRecord(ev[7], c->stream));
   RID_TRY(stage_out(c, p, P, k, n_loc, ldp, sizeof(rid_z)));

@@ -71,7 +71,7 @@ def main(tag, cfg):
             f.write("\n".join(ll) + "\n")
     traffic_path = os.path.join(PROF, "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
-    for kind in ("sketch", "qrcp"):
+    for kind in ("sketch", "qrcp", "update"):
         rep = os.path.join(OUT, f"prof_{kind}_{cfg}.ncu-rep")
         if not os.path.exists(rep):
             continue
