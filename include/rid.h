@@ -144,7 +144,7 @@ int rid_sketch_mults(void);
  * for the local columns -> P_loc = [I T] in original column order (P[t, J_t] = 1 exactly).
  * Outputs: J (k int64, GLOBAL column ids in pivot order; replicated on every rank) and P_loc
  * (k x n_loc, ldp >= k). On RID_ERANK after one retry with R stream 20, J/P are unspecified.
- * Preconditions: 1 <= k <= min(m, n), k <= l <= min(m, 1024), shard as for rid_generate,
+ * Preconditions: 1 <= k <= min(m, n), k <= l <= min(m, 2048), shard as for rid_generate,
  * G * n_loc == n when a communicator is set. diag may be NULL. */
 rid_status rid_decompose(rid_ctx* ctx, const rid_z* A, int64_t m, int64_t n, int64_t col0,
                          int64_t n_loc, int64_t lda, int64_t k, int64_t l, uint64_t seed,

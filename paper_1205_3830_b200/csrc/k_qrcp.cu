@@ -676,6 +676,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
       // all loads of a round are issued before their fmas: the pivot column's rows, then the
       // pending reflectors V[j:l, s] (8 columns per round) and f_s(p) (a broadcast)
       double2 x[kRQ];
+      if constexpr (kRQ <= 3) {
 #pragma unroll
       for (int q = 0; q < kRQ; ++q) {
         const int rr = idx + kCW * 32 * q;
@@ -703,6 +704,32 @@ __global__ void __launch_bounds__(kRingThreads, 1)
               if (idx == 0) {  // row j: V[j, s] and f_s(p) for the column pass
                 s_vrow[s0 + s] = vv[0][s];
                 s_fp[s0 + s] = fp[s];
+              }
+            }
+          }
+        }
+      }
+      } else {  // l > 672: rows one at a time, 8 pending reflectors per round (registers)
+#pragma unroll
+        for (int q = 0; q < kRQ; ++q) {
+          const int rr = idx + kCW * 32 * q;
+          x[q] = rr < L ? Y[p * ldy + j + rr] : make_double2(0.0, 0.0);
+          for (int s0 = 0; s0 < t; s0 += 8) {
+            double2 vv[8], fp[8];
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+              fp[s] = s0 + s < t ? w.F[p * kNB + s0 + s] : make_double2(0.0, 0.0);
+              vv[s] = (s0 + s < t && rr < L) ? w.V[(int64_t)(s0 + s) * ldv + j + rr]
+                                             : make_double2(0.0, 0.0);
+            }
+#pragma unroll
+            for (int s = 0; s < 8; ++s) {
+              if (s0 + s < t) {
+                cmac_sub(x[q], vv[s], fp[s]);
+                if (idx == 0 && q == 0) {
+                  s_vrow[s0 + s] = vv[s];
+                  s_fp[s0 + s] = fp[s];
+                }
               }
             }
           }
@@ -1115,7 +1142,13 @@ cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, doubl
   RID_Q(1) RID_Q(2) RID_Q(3) RID_Q(4) RID_Q(5) RID_Q(6) RID_Q(8) RID_Q(9) RID_Q(12) RID_Q(17)
   RID_Q(24) RID_Q(32)
 #undef RID_Q
-  return cudaErrorInvalidValue;  // l > 1024 unsupported
+  // l up to 2048 (the paper's l = 2k with k = 1000): blocked panels only (the exact kernel holds
+  // a column segment in registers)
+  if (qneed <= 48)
+    return launch_qrcp_blocked<48>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st, launches, nbw);
+  if (qneed <= 64)
+    return launch_qrcp_blocked<64>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st, launches, nbw);
+  return cudaErrorInvalidValue;  // l > 2048 unsupported
 }
 
 // ---------------------------------------------------------------------------------------------

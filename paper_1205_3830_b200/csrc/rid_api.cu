@@ -531,7 +531,7 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
                          int64_t n_loc, int64_t lda, int64_t k, int64_t l, uint64_t seed,
                          int64_t* J, rid_z* P, int64_t ldp, rid_diag* diag) {
   RID_TRY(check_ctx(c));
-  if (m < 1 || n < 1 || k < 1 || k > m || k > n || l < k || l > m || l > 1024 || col0 < 0 ||
+  if (m < 1 || n < 1 || k < 1 || k > m || k > n || l < k || l > m || l > 2048 || col0 < 0 ||
       n_loc < 1 || col0 + n_loc > n || lda < m || ldp < k || !A || !J || !P ||
       m > (int64_t)0xFFFFFFFFLL)
     return fail(c, RID_EINVAL, "rid_decompose: bad arguments (m=%lld n=%lld k=%lld l=%lld col0=%lld n_loc=%lld)",
@@ -642,7 +642,7 @@ rid_status rid_qrcp(rid_ctx* c, const rid_z* Y, int64_t l, int64_t n, int64_t ld
                     int64_t* J, rid_z* R, int64_t ldr, double* resid, double* margin,
                     rid_diag* diag) {
   RID_TRY(check_ctx(c));
-  if (l < 1 || n < 1 || k < 1 || k > l || k > n || l > 1024 || ldy < l || !Y || !J ||
+  if (l < 1 || n < 1 || k < 1 || k > l || k > n || l > 2048 || ldy < l || !Y || !J ||
       (R && ldr < k))
     return fail(c, RID_EINVAL, "rid_qrcp: bad arguments");
   MatArg y;
@@ -688,7 +688,7 @@ rid_status rid_factor_solve(rid_ctx* c, const rid_z* Y, int64_t l, int64_t n, in
                             int64_t k, int64_t col0, int64_t n_loc, int64_t* J, rid_z* P,
                             int64_t ldp, rid_diag* diag) {
   RID_TRY(check_ctx(c));
-  if (l < 1 || n < 1 || k < 1 || k > l || k > n || l > 1024 || ldy < l || !Y || !J || !P ||
+  if (l < 1 || n < 1 || k < 1 || k > l || k > n || l > 2048 || ldy < l || !Y || !J || !P ||
       col0 < 0 || n_loc < 1 || col0 + n_loc > n || ldp < k)
     return fail(c, RID_EINVAL, "rid_factor_solve: bad arguments");
   MatArg y, p;
