@@ -122,3 +122,20 @@ def test_blocked_deterministic_and_matches_exact_variant(rid, monkeypatch):
     assert torch.equal(r0.J, r1.J)
     assert relf(np_(r1.P), np_(r0.P)) <= 1e-12
     assert abs(r0.diag["tie_margin_min"] - r1.diag["tie_margin_min"]) <= 1e-9
+
+
+@pytest.mark.parametrize("name,seed,m,n,k,l,noise", [
+    ("l=1100 (MAXQ 48)", 3, 1500, 1300, 600, 1100, 1e-9),
+    ("l=2000 (MAXQ 64)", 4, 2100, 700, 640, 2000, 0.0),
+])
+def test_large_l_blocked_only(rid, oracle_dec, name, seed, m, n, k, l, noise):
+    """l > 1024 (the paper's l = 2k at k = 1000, NEXT-4) runs only on the blocked kernel (the
+    exact kernel holds a segment in registers): same bar against the oracle."""
+    A_o, d = oracle_dec(seed, m, n, k, l, noise)
+    r = rid.decompose(rid.generate(seed, m, n, k, noise), k, l, seed)
+    if d.tie_margins[:-1].min() < 1e-10:
+        pytest.skip(f"{name}: tie-ambiguous (margin {d.tie_margins[:-1].min():.2e})")
+    J, P = np_(r.J), np_(r.P)
+    assert J.tolist() == d.J.tolist()
+    assert np.array_equal(P[:, J], np.eye(k, dtype=complex))
+    assert relf(P, d.P) <= 1e-10
