@@ -8,8 +8,9 @@
 //   pass 1 (k_srft_pass1): D-scaling and the R-point DFT along i2, one thread per (i1, c), radix-4
 //     x radix-4 in registers, coalesced along i1 — one read of A, one write of Z (HBM-bound);
 //   pass 2: for each residue r, the rows k with s_k mod R = r form one small complex GEMM
-//     Y_r (l_r x n) = W_r (l_r x m1) . Z^(r) (m1 x n) on the ordered DMMA GEMM of k_zgemm.cu —
-//     8 l m n / R real flops instead of the dense 8 l m n.
+//     Y_r (l_r x n) = W_r (l_r x m1) . Z^(r) (m1 x n) on the same complex-product kernel as the
+//     Gaussian sketch (k_zgemm3m.cu, Gauss's three products; the ordered k_zgemm.cu with
+//     RID_SKETCH_4M=1) — 6 (or 8) l m n / R real flops instead of the dense 8 l m n.
 // Plan (docs/RNG.md §7): d_i = (cos, sin)(2 pi u1) of Philox (i, 0, s_phase, 0) via the spec'd
 // sincos, s_k = x0 & (m - 1) of Philox (k, 0, s_sample, 0); W entries from the same sincos on
 // u = ((s_k i1) mod m) / m. Agreement with the oracle's direct ascending sum is to rounding.
@@ -190,10 +191,15 @@ cudaError_t srft_sketch(uint64_t seed, bool retry, int64_t l, const double2* A, 
     for (int r = 0; r < kSrftR; ++r) {
       const int64_t lr = hoffs[r + 1] - hoffs[r];
       if (lr == 0) continue;
-      int S = zgemm_ksplit(lr, m1, n / 8, num_sms);
+      const bool g3 = sketch_mults() == 3;  // Gauss's three products, as the Gaussian sketch
+      int S = g3 ? zgemm3m_ksplit(lr, m1, n / 8, num_sms) : zgemm_ksplit(lr, m1, n / 8, num_sms);
       if ((size_t)S * lr * nc > splitk_elems) S = 1;
-      e = zgemm_ordered(Wg + hoffs[r], l, Z + (int64_t)r * m1 * nc, m1, Yg + hoffs[r], l, lr, nc,
-                        m1, 0, 0.0, 0, 0, st, S, splitk);
+      if (g3)
+        e = zgemm3m(Wg + hoffs[r], l, nullptr, 0, Z + (int64_t)r * m1 * nc, m1, Yg + hoffs[r], l,
+                    lr, nc, m1, st, S, splitk);
+      else
+        e = zgemm_ordered(Wg + hoffs[r], l, Z + (int64_t)r * m1 * nc, m1, Yg + hoffs[r], l, lr,
+                          nc, m1, 0, 0.0, 0, 0, st, S, splitk);
       if (e != cudaSuccess) return e;
       *launches += S > 1 ? 2 : 1;
     }

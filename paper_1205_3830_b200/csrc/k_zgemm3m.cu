@@ -359,6 +359,13 @@ cudaError_t zgemm3m(const double2* Rm, int64_t ldr, const double* Rs, int64_t ld
       default: break;
     }
   }
+  if (!Rs) {  // no Re R + Im R plane (e.g. the SRFT's row-grouped W): sums in registers
+    switch (pick3(Mout)) {
+      case 0: return RID_L3(2, 3, 4, 2, 16, 3, 2, 0, 0);
+      case 1: return RID_L3(1, 5, 8, 1, 16, 3, 2, 0, 0);
+      default: return RID_L3(1, 3, 8, 1, 16, 3, 2, 0, 0);
+    }
+  }
   switch (pick3(Mout)) {
     case 0: return RID_L3(2, 3, 4, 2, 16, 3, 2, 0, 0);
     case 1: return RID_L3(1, 5, 8, 1, 16, 3, 2, 1, 1);

@@ -16,7 +16,8 @@ cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int
                           int ksplit = 1, double2* partial = nullptr);
 int zgemm_pick_fr(int64_t Mout);
 // The sketch as three real products (Gauss), 6·l·m·n flops (k_zgemm3m.cu); split-K as above.
-// Rs = Re R + Im R (l x m doubles, leading dimension rsum_ld(l), pad rows zero) from rsum_fill.
+// Rs = Re R + Im R (l x m doubles, leading dimension rsum_ld(l), pad rows zero) from rsum_fill;
+// Rs == nullptr selects tiles that form the sums in registers.
 cudaError_t zgemm3m(const double2* Rm, int64_t ldr, const double* Rs, int64_t ldrs,
                     const double2* Bm, int64_t ldb, double2* C, int64_t ldc, int64_t Mout,
                     int64_t N, int64_t K, cudaStream_t st, int ksplit, double2* partial);
