@@ -122,6 +122,14 @@ rid_status rid_generate(rid_ctx* ctx, uint64_t seed, int64_t m, int64_t n, int64
  * ldy >= l. */
 rid_status rid_sketch(rid_ctx* ctx, uint64_t seed, uint32_t stream, int64_t l, const rid_z* A,
                       int64_t m, int64_t n, int64_t n_loc, int64_t lda, rid_z* Y, int64_t ldy);
+/* The same for the columns [col0, col0 + n_loc) of the m x n matrix (rid_sketch: col0 = 0).
+ * The global position matters to the kernel plan only: when the unsplit sketch's last wave of
+ * CTAs would be nearly empty, the trailing global columns that fall into it are computed with a
+ * K split (fixed-order slice sums), so every column's bits depend on (m, l, n, its index) alone —
+ * identical for every sharding. Preconditions as rid_sketch, plus 0 <= col0, col0 + n_loc <= n. */
+rid_status rid_sketch_cols(rid_ctx* ctx, uint64_t seed, uint32_t stream, int64_t l,
+                           const rid_z* A, int64_t m, int64_t n, int64_t col0, int64_t n_loc,
+                           int64_t lda, rid_z* Y, int64_t ldy);
 /* The paper's own randomisation Y = S F D A (§2, Eqs. 4–7; docs/RNG.md §7):
  * D random unit phases (Philox stream 6), F the unnormalised DFT (Eq. 6), S l row samples with
  * replacement (stream 7); retry != 0 uses streams 22/23. Computed as a 16-point DFT

@@ -59,7 +59,7 @@ EXPORTS = ["rid_create", "rid_destroy", "rid_last_error", "rid_version", "rid_co
            "rid_comm_get_id", "rid_comm_init", "rid_comm_info", "rid_generate", "rid_sketch",
            "rid_decompose", "rid_error_estimate", "rid_error_bound", "rid_normal_fill",
            "rid_qrcp", "rid_factor_solve", "rid_sketch_splits", "rid_sketch_srft",
-           "rid_set_sketch", "rid_sketch_mults"]
+           "rid_set_sketch", "rid_sketch_mults", "rid_sketch_cols"]
 SKETCH_GAUSSIAN, SKETCH_SRFT = 0, 1
 
 
@@ -87,6 +87,7 @@ def lib():
         "rid_sketch": ([p, u64, u32, i64, p, i64, i64, i64, i64, p, i64], ci),
         "rid_sketch_splits": ([p, i64, i64, i64], ci),
         "rid_sketch_mults": ([], ci),
+        "rid_sketch_cols": ([p, u64, u32, i64, p, i64, i64, i64, i64, i64, p, i64], ci),
         "rid_sketch_srft": ([p, u64, ci, i64, p, i64, i64, i64, i64, p, i64], ci),
         "rid_set_sketch": ([p, ci], ci),
         "rid_decompose": ([p, p, i64, i64, i64, i64, i64, i64, i64, u64, p, p, i64, p], ci),
@@ -256,9 +257,10 @@ def generate(seed: int, m: int, n: int, k: int, noise: float, col0: int = 0, n_l
 
 
 def sketch(A, seed: int, l: int, stream: int = STREAM_R, out=None, n: int | None = None,
-           ctx: Context | None = None):
-    """Y = R A with R(r, i) = N(seed, stream, r, i) on the DMMA pipe. A may be a column block of
-    an n-column matrix (n defaults to A's own width); n fixes the K-split (sketch_splits)."""
+           col0: int = 0, ctx: Context | None = None):
+    """Y = R A with R(r, i) = N(seed, stream, r, i) on the DMMA pipe. A may be the column block
+    [col0, col0 + width) of an n-column matrix (n defaults to A's own width); (n, col0) fix the
+    kernel plan (K split, wave tail), so a block's columns match the whole matrix's bit for bit."""
     ctx = ctx or default_context()
     m, n_loc = A.shape
     n = n_loc if n is None else n
@@ -267,8 +269,8 @@ def sketch(A, seed: int, l: int, stream: int = STREAM_R, out=None, n: int | None
         out = colmajor_empty(l, n_loc, device=A.device if hasattr(A, "device") else "cpu") \
             if not isinstance(A, np.ndarray) else np.zeros((l, n_loc), np.complex128, order="F")
     y = _Buf(out, l, n_loc, "Y")
-    ctx.check(lib().rid_sketch(ctx.h, seed, stream, l, a.ptr, m, n, n_loc, a.ld, y.ptr, y.ld),
-              "rid_sketch")
+    ctx.check(lib().rid_sketch_cols(ctx.h, seed, stream, l, a.ptr, m, n, col0, n_loc, a.ld, y.ptr,
+                                    y.ld), "rid_sketch")
     return out
 
 

@@ -382,12 +382,65 @@ int sketch_ksplit(int64_t l, int64_t m, int64_t n_ref, int num_sms) {
   return sketch_mults() == 4 ? zgemm_ksplit(l, m, n_ref, num_sms)
                              : zgemm3m_ksplit(l, m, n_ref, num_sms);
 }
+// Wave quantisation of the unsplit sketch: R_t row tiles x T column tiles over 2 CTAs per SM.
+// When the last wave would run only a few CTAs (C4: 5632 = 19 x 296 + 8), the trailing global
+// column tiles that fall into it are computed with a K split instead, sized to fill one wave
+// (C4: the last 64 columns in 26 slices). The set depends only on (l, m, n) and the SM count, so
+// every column of Y is still bitwise independent of the sharding.
+SketchTail sketch_tail(int64_t l, int64_t m, int64_t n, int num_sms) {
+  SketchTail t{0, 1};
+  if (sketch_mults() != 3 || getenv("RID_SKETCH_SPLIT") || getenv("RID_SKETCH_NOTAIL")) return t;
+  if (zgemm3m_ksplit(l, m, n / 8, num_sms) != 1) return t;  // already split everywhere
+  const int64_t rt = (l + rows3(pick3(l)) - 1) / rows3(pick3(l));
+  const int64_t T = (n + 63) / 64, slots = 2 * (int64_t)num_sms, total = rt * T;
+  const int64_t rem = total % slots;
+  if (rem == 0 || rem * 2 >= slots) return t;
+  const int64_t q = (rem + rt - 1) / rt;  // trailing column tiles in the split set
+  if (q >= T) return t;
+  int64_t S = slots / (q * rt);
+  const int64_t smax = m / 512 > 1 ? m / 512 : 1;
+  if (S > smax) S = smax;
+  if (S > 64) S = 64;
+  if (S < 2) return t;
+  t.cols = n - (T - q) * 64;
+  t.S = (int)S;
+  return t;
+}
+
+int64_t sketch_partial_elems(int64_t l, int64_t m, int64_t n, int64_t ncols, int num_sms) {
+  const int S = sketch_ksplit(l, m, n / 8, num_sms);
+  const SketchTail t = sketch_tail(l, m, n, num_sms);
+  const int64_t a = S > 1 ? (int64_t)S * l * ncols : 0;
+  const int64_t b = t.cols > 0 ? (int64_t)t.S * l * (t.cols < ncols ? t.cols : ncols) : 0;
+  return a > b ? a : b;
+}
+
 cudaError_t sketch_gemm(const double2* R, int64_t ldr, const double* Rs, const double2* A,
                         int64_t lda, double2* Y, int64_t ldy, int64_t l, int64_t ncols, int64_t m,
-                        cudaStream_t st, int ksplit, double2* partial) {
-  if (sketch_mults() == 4)
+                        cudaStream_t st, int ksplit, double2* partial, int64_t col0, int64_t n,
+                        int num_sms, int* launches) {
+  int dummy = 0;
+  if (!launches) launches = &dummy;
+  if (sketch_mults() == 4) {
+    *launches += ksplit > 1 ? 2 : 1;
     return zgemm_ordered(R, ldr, A, lda, Y, ldy, l, ncols, m, 0, 0.0, 0, 0, st, ksplit, partial);
-  return zgemm3m(R, ldr, Rs, rsum_ld(l), A, lda, Y, ldy, l, ncols, m, st, ksplit, partial);
+  }
+  const SketchTail t = (ksplit == 1 && partial) ? sketch_tail(l, m, n, num_sms) : SketchTail{0, 1};
+  const int64_t tail0 = n - t.cols;  // first global column of the split set
+  int64_t nmain = ncols;
+  if (t.cols > 0 && col0 + ncols > tail0) nmain = tail0 > col0 ? tail0 - col0 : 0;
+  cudaError_t e = cudaSuccess;
+  if (nmain > 0) {
+    e = zgemm3m(R, ldr, Rs, rsum_ld(l), A, lda, Y, ldy, l, nmain, m, st, ksplit, partial);
+    *launches += ksplit > 1 ? 2 : 1;
+    if (e != cudaSuccess) return e;
+  }
+  if (nmain < ncols) {
+    e = zgemm3m(R, ldr, Rs, rsum_ld(l), A + nmain * lda, lda, Y + nmain * ldy, ldy, l,
+                ncols - nmain, m, st, t.S, partial);
+    *launches += 2;
+  }
+  return e;
 }
 
 }  // namespace rid

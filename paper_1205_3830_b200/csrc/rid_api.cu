@@ -261,9 +261,10 @@ rid_status fill_R(rid_ctx* c, uint64_t seed, uint32_t s, int64_t l, int64_t m, d
 // of ~1 GiB on a copy stream, double-buffered, each chunk's sketch overlapping the copy of the
 // next. The sketch of a column does not depend on the chunking, so Y is bit-identical to the
 // device-resident call. The device never holds more than two chunks of A.
-rid_status sketch_streamed(rid_ctx* c, const double2* R, const double* Rs, const rid_z* hostA, int64_t m,
-                           int64_t n_loc, int64_t lda, int64_t l, double2* Y, int* launches,
-                           double* t_h2d, int ksplit, double2* partial) {
+rid_status sketch_streamed(rid_ctx* c, const double2* R, const double* Rs, const rid_z* hostA,
+                           int64_t m, int64_t n, int64_t col0, int64_t n_loc, int64_t lda,
+                           int64_t l, double2* Y, int* launches, double* t_h2d, int ksplit,
+                           double2* partial) {
   if (!c->copy_stream) {
     RID_CUDA(c, cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     for (int b = 0; b < 2; ++b) {
@@ -294,9 +295,8 @@ rid_status sketch_streamed(rid_ctx* c, const double2* R, const double* Rs, const
     RID_CUDA(c, cudaEventRecord(c->ev_copied[b], c->copy_stream));
     RID_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0));
     RID_CUDA(c, rid::sketch_gemm(R, l, Rs, (const double2*)buf[b], m, Y + j0 * l, l, l, nc, m,
-                                 c->stream, ksplit, partial));
+                                 c->stream, ksplit, partial, col0 + j0, n, c->num_sms, launches));
     RID_CUDA(c, cudaEventRecord(c->ev_used[b], c->stream));
-    *launches += ksplit > 1 ? 2 : 1;
   }
   RID_CUDA(c, cudaEventRecord(c->ev_copy1, c->copy_stream));
   if (t_h2d) {
@@ -505,9 +505,15 @@ int rid_sketch_mults(void) { return rid::sketch_mults(); }
 
 rid_status rid_sketch(rid_ctx* c, uint64_t seed, uint32_t stream, int64_t l, const rid_z* A,
                       int64_t m, int64_t n, int64_t n_loc, int64_t lda, rid_z* Y, int64_t ldy) {
+  return rid_sketch_cols(c, seed, stream, l, A, m, n, 0, n_loc, lda, Y, ldy);
+}
+
+rid_status rid_sketch_cols(rid_ctx* c, uint64_t seed, uint32_t stream, int64_t l, const rid_z* A,
+                           int64_t m, int64_t n, int64_t col0, int64_t n_loc, int64_t lda, rid_z* Y,
+                           int64_t ldy) {
   RID_TRY(check_ctx(c));
-  if (l < 1 || l > m || m < 1 || n_loc < 0 || n < n_loc || lda < m || ldy < l || !A || !Y ||
-      m > (int64_t)0xFFFFFFFFLL)
+  if (l < 1 || l > m || m < 1 || n_loc < 0 || col0 < 0 || col0 + n_loc > n || lda < m ||
+      ldy < l || !A || !Y || m > (int64_t)0xFFFFFFFFLL)
     return fail(c, RID_EINVAL, "rid_sketch: bad arguments");
   if (n_loc == 0) return RID_OK;
   MatArg a, y;
@@ -519,9 +525,11 @@ rid_status rid_sketch(rid_ctx* c, uint64_t seed, uint32_t stream, int64_t l, con
   int nl = 0;
   RID_TRY(fill_R(c, seed, stream, l, m, &R, &Rs, &nl));
   const int S = rid::sketch_ksplit(l, m, n / 8, c->num_sms);
-  if (S > 1) RID_TRY(ws_get(c, "splitk", sizeof(double2) * S * l * n_loc, &pS));
+  const int64_t pe = rid::sketch_partial_elems(l, m, n, n_loc, c->num_sms);
+  if (pe > 0) RID_TRY(ws_get(c, "splitk", sizeof(double2) * pe, &pS));
   RID_CUDA(c, rid::sketch_gemm(R, l, Rs, (const double2*)a.dev, lda, (double2*)y.dev, ldy, l,
-                               n_loc, m, c->stream, S, (double2*)pS));
+                               n_loc, m, c->stream, S, (double2*)pS, col0, n, c->num_sms,
+                               nullptr));
   RID_TRY(stage_out(c, y, Y, l, n_loc, ldy, sizeof(rid_z)));
   if (a.host || y.host) RID_CUDA(c, cudaStreamSynchronize(c->stream));
   return RID_OK;
@@ -556,10 +564,11 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
   // K-split of the sketch: a function of (m, l, n) only, so Y is identical for every sharding
   const int S = rid::sketch_ksplit(l, m, n / 8, c->num_sms);
   void* pS = nullptr;
-  if (S > 1) {
+  {
     const int64_t cols = a_host ? std::min<int64_t>(n_loc, std::max<int64_t>(64, (int64_t)(1 << 30) / (16 * m)))
                                 : n_loc;
-    RID_TRY(ws_get(c, "splitk", sizeof(double2) * S * l * cols, &pS));
+    const int64_t pe = rid::sketch_partial_elems(l, m, n, cols, c->num_sms);
+    if (pe > 0) RID_TRY(ws_get(c, "splitk", sizeof(double2) * pe, &pS));
   }
   int64_t* Jdev = nullptr;
   rid_status st = RID_OK;
@@ -577,12 +586,12 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
     RID_TRY(fill_R(c, seed, sR, l, m, &Rg, &Rsg, &d.launches));
     RID_CUDA(c, cudaEventRecord(ev[3], c->stream));
     if (a_host) {
-      RID_TRY(sketch_streamed(c, Rg, Rsg, A, m, n_loc, lda, l, Yw + col0 * l, &d.launches,
-                              nullptr, S, (double2*)pS));
+      RID_TRY(sketch_streamed(c, Rg, Rsg, A, m, n, col0, n_loc, lda, l, Yw + col0 * l,
+                              &d.launches, nullptr, S, (double2*)pS));
     } else {
       RID_CUDA(c, rid::sketch_gemm(Rg, l, Rsg, (const double2*)a.dev, lda, Yw + col0 * l, l, l,
-                                   n_loc, m, c->stream, S, (double2*)pS));
-      d.launches += S > 1 ? 2 : 1;
+                                   n_loc, m, c->stream, S, (double2*)pS, col0, n, c->num_sms,
+                                   &d.launches));
     }
     }
     RID_CUDA(c, cudaEventRecord(ev[4], c->stream));

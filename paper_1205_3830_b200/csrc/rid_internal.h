@@ -29,9 +29,19 @@ cudaError_t rsum_fill(const double2* R, int64_t l, int64_t m, int64_t ldr, doubl
 // products per complex multiply-add. Rs is only read by the 3M kernel (may be null for 4M).
 int sketch_mults();
 int sketch_ksplit(int64_t l, int64_t m, int64_t n_ref, int num_sms);
+// Columns [col0, col0 + ncols) of the global m x n matrix: with ksplit == 1 the trailing global
+// columns of the last, nearly empty wave (sketch_tail) are computed with a K split (partial must
+// hold sketch_partial_elems(...) elements).
+struct SketchTail {
+  int64_t cols;  // trailing global columns computed with the split
+  int S;
+};
+SketchTail sketch_tail(int64_t l, int64_t m, int64_t n, int num_sms);
+int64_t sketch_partial_elems(int64_t l, int64_t m, int64_t n, int64_t ncols, int num_sms);
 cudaError_t sketch_gemm(const double2* R, int64_t ldr, const double* Rs, const double2* A,
                         int64_t lda, double2* Y, int64_t ldy, int64_t l, int64_t ncols, int64_t m,
-                        cudaStream_t st, int ksplit, double2* partial);
+                        cudaStream_t st, int ksplit, double2* partial, int64_t col0, int64_t n,
+                        int num_sms, int* launches);
 // K slices for a sketch of Mout rows, K = m, chosen from n_ref = n_global / 8 only (G-invariant)
 int zgemm_ksplit(int64_t Mout, int64_t K, int64_t n_ref, int num_sms);
 

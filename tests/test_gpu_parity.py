@@ -202,7 +202,7 @@ def test_g_emulation_bitwise(rid):
             col0, nl = rid.shard_range(n, g, G)
             A_g = rid.generate(seed, m, n, k, noise, col0, nl)
             assert torch.equal(A_g.contiguous(), A[:, col0:col0 + nl].contiguous())
-            Ys.append(rid.sketch(A_g, seed, l, n=n))  # the same K-split as the whole matrix
+            Ys.append(rid.sketch(A_g, seed, l, n=n, col0=col0))  # the whole matrix's plan
         Y = torch.cat([y.T for y in Ys]).T  # column-major concatenation
         for g in range(G):
             col0, nl = rid.shard_range(n, g, G)
@@ -282,3 +282,28 @@ def test_estimator_host_path(rid, orc):
     e_h = rid.error_estimate(A_o, d.J, d.P, 5, 2)  # all host buffers
     e_o = orc.error_estimate(A_o, d.J, d.P, 5, 2)
     assert abs(e_h - e_o) <= 1e-10 * e_o
+
+
+def test_sketch_wave_tail_split(rid, orc, monkeypatch):
+    """The trailing global columns of a nearly empty last wave are computed with a K split
+    (rid_sketch_cols, reading R30): those columns agree with the oracle to rounding, every other
+    column is bitwise the unsplit kernel's, and the plan is a function of the global column index
+    — shards reproduce the whole matrix bit for bit."""
+    seed, m, n, k, l, noise = 4, 1024, 13824, 64, 528, 1e-9  # 11 x 216 tiles = 8 over 8 waves
+    A = rid.generate(seed, m, n, k, noise)
+    Y = np_(rid.sketch(A, seed, l))
+    monkeypatch.setenv("RID_SKETCH_NOTAIL", "1")
+    Y0 = np_(rid.sketch(A, seed, l))
+    monkeypatch.delenv("RID_SKETCH_NOTAIL")
+    tail = n - 64
+    assert bits_equal(Y[:, :tail], Y0[:, :tail])
+    assert not bits_equal(Y[:, tail:], Y0[:, tail:])  # the split path ran
+    assert relf(Y[:, tail:], Y0[:, tail:]) <= 5e-14
+    A_o = orc.generate(seed, m, n, k, noise, tail, 64)
+    assert relf(Y[:, tail:], orc.sketch(A_o, seed, l)) <= 5e-14
+    for G in (2, 8):
+        parts = []
+        for g in range(G):
+            col0, nl = rid.shard_range(n, g, G)
+            parts.append(np_(rid.sketch(A[:, col0:col0 + nl], seed, l, n=n, col0=col0)))
+        assert bits_equal(np.concatenate(parts, axis=1), Y)
