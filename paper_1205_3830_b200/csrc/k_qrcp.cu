@@ -453,9 +453,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
                "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
-}
 __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
   asm volatile(
       "{\n"
@@ -465,13 +462,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
       "@!P1 bra WAIT_%=;\n"
       "}\n" ::"r"(smem_u32(b)),
       "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(b))
       : "memory");
 }
 __device__ __forceinline__ void tma_box_g2s(void* dst, const CUtensorMap* map, int x, int y,
@@ -496,27 +486,23 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
   return p;
 }
-__device__ __forceinline__ uint64_t policy_evict_last() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
 __device__ __forceinline__ void consumers_sync() {  // warps 1..15 only
   asm volatile("bar.sync 1, %0;\n" ::"n"((kRingWarps - 1) * 32) : "memory");
 }
 
-// One CTA per SM, 16 warps. Warp 0: the pivot reduction. Warps 1..15:
-// the reflector; then the first `ncw` of them each stream their own share of the trailing
-// columns through a private ring of D shared-memory slots: lane 0 issues one cp.async.bulk per
-// column segment (rows j..l−1 = 16·(l−j) contiguous bytes, TMA engine, completion on the slot's
-// mbarrier) D − 1 columns ahead of the one being reduced (GEMV from shared memory, f_t, R(j, c),
-// the downdated norm). Columns are visited in alternating order from step to step, so the
-// segments read last in step j — still in the 126 MB L2 — are read first in step j + 1.
+// One CTA per SM, 8 warps (255 registers per thread). Warp 0: the pivot reduction. Warps 1..7:
+// the reflector (every CTA builds the same one); then up to `ncw` of them each stream batches of
+// 32 consecutive trailing columns as 16-row x 32-column boxes (2D TMA, 8 KB, completion on a
+// slot's mbarrier, D boxes in flight per warp) and reduce them: inside a box lane = (row, column
+// parity) with one register accumulator per column; at the end of a batch the partials are
+// transposed through the consumed slot and lane i finishes column i (f_t, R(j, c), the downdated
+// norm). Batches and rows are visited in alternating order from step to step (L2 reuse), and
+// boxes past the first l2_keep bytes of the trailing block carry an evict_first policy.
 template <int MAXQ>
 __global__ void __launch_bounds__(kRingThreads, 1)
     k_qrcp_ring(double2* __restrict__ Y, int64_t ldy, int l, int64_t n, int k, int j0, int jend,
-                double tol_rel, QrcpOut out, QrcpWork w, int ncw, int D, int per, int slot_elems,
-                int flags, double l2_keep, const __grid_constant__ CUtensorMap tmap) {
+                double tol_rel, QrcpOut out, QrcpWork w, int ncw, int D, int per,
+                double l2_keep, const __grid_constant__ CUtensorMap tmap) {
   constexpr int kCW = kRingWarps - 1;  // consumer warps in the reflector phase
   constexpr int kRQ = (MAXQ * 32 + kCW * 32 - 1) / (kCW * 32);
   extern __shared__ __align__(128) unsigned char ring_smem[];
@@ -591,7 +577,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
     const int t = j - j0;
     const int L = l - j;  // rows j..l-1
     if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 0] = globaltimer();
-    // ---- 1. global pivot (every CTA, identically); the owner drops it from its list ---------
+    // ---- 1. global pivot (every CTA, identically); the owner marks it chosen --------------
     if (warp == 0) {
       Top2 tt;
       top2_init(tt);
@@ -635,8 +621,8 @@ __global__ void __launch_bounds__(kRingThreads, 1)
       const int cw = warp - 1, idx = cw * 32 + lane;
       // the CTA's columns are cut into batches of 32 consecutive columns (lane i <-> column i of
       // the batch; chosen columns leave their lane idle); streaming warp cw takes batches cw,
-      // cw + ncw, ... and streams each batch's rows j..l-1 as 32-row x 32-column boxes (one 2D TMA
-      // copy of 16 KB per box, rows past l zero-filled) through its D ring slots
+      // cw + ncw, ... and streams each batch's rows j..l-1 as kCH-row x 32-column boxes (one 2D
+      // TMA copy of 8 KB per box, rows past l zero-filled) through its D ring slots
       const int nbat = (int)((c_hi - c_lo + 31) / 32);
       const int mybat = (cw < ncw && nbat > cw) ? (nbat - cw + ncw - 1) / ncw : 0;
       const int nch = (L + kCH - 1) / kCH;
@@ -670,8 +656,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
         if (++isl == D) isl = 0;
       };
       // ---- 2a. prologue: this warp's first D boxes start streaming now ---------------------
-      if (!(flags & 4))
-        for (; issued < nitems && issued < D; ++issued) issue_next();
+      for (; issued < nitems && issued < D; ++issued) issue_next();
       // ---- 2b. reflector H_j from x = y^(j0)_p[j:l] − Σ_{s<t} V[j:l, s] f_s(p) --------------
       // all loads of a round are issued before their fmas: the pivot column's rows, then the
       // pending reflectors V[j:l, s] (8 columns per round) and f_s(p) (a broadcast)
@@ -752,8 +737,6 @@ __global__ void __launch_bounds__(kRingThreads, 1)
       }
       consumers_sync();
       if (w.trace && b == 0 && idx == 0) w.trace[8 * j + 5] = globaltimer();
-      if (flags & 4)  // experiment: the prologue after the pivot column is built
-        for (; issued < nitems && issued < D; ++issued) issue_next();
       double xnorm2 = 0.0;
       for (int q = 0; q < kCW; ++q) xnorm2 = __dadd_rn(xnorm2, s_red[q]);  // fixed order
       const double ar = s_par[0], ai = s_par[1];
@@ -1045,7 +1028,6 @@ static cudaError_t launch_qrcp_blocked(double2* Y, int64_t ldy, int l, int64_t n
   if (blocks < 1) blocks = 1;
   const int per = (int)((n + blocks - 1) / blocks);
   blocks = (int)((n + per - 1) / per);
-  const int slot_elems = 0;  // (unused: slots are 32 lanes x kLS rows)
   const size_t fixed = (size_t)kMaxSlots * 8 + (size_t)(MAXQ * 32 + 32) * sizeof(double2) + 128;
   const size_t avail = (size_t)optin - fa.sharedSizeBytes - 1024;
   const size_t slot_bytes = (size_t)32 * kCH * sizeof(double2);
@@ -1097,12 +1079,11 @@ static cudaError_t launch_qrcp_blocked(double2* Y, int64_t ldy, int l, int64_t n
     if ((e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
     QrcpOut o = out;
     QrcpWork ww = w;
-    int j0v = j0, jendv = jend, ncwv = ncw, Dv = D, perv = per, sev = slot_elems;
-    int flags = getenv("RID_QRCP_FLAGS") ? atoi(getenv("RID_QRCP_FLAGS")) : 0;
+    int j0v = j0, jendv = jend, ncwv = ncw, Dv = D, perv = per;
     double l2_keep = 80.0 * (1 << 20);  // bytes of the trailing block kept in L2 (126 MB L2)
     if (const char* v = getenv("RID_QRCP_L2KEEP_MB")) l2_keep = atof(v) * (1 << 20);
-    void* args[] = {&Y, &ldy, &l, &n, &k, &j0v, &jendv, &tol_rel, &o, &ww, &ncwv, &Dv, &perv, &sev,
-                    &flags, &l2_keep, &tmap};
+    void* args[] = {&Y, &ldy, &l, &n, &k, &j0v, &jendv, &tol_rel, &o, &ww, &ncwv, &Dv, &perv,
+                    &l2_keep, &tmap};
     e = cudaLaunchCooperativeKernel((void*)kern, dim3(blocks), dim3(kRingThreads), args, smem, st);
     if (e != cudaSuccess) return e;
     *launches += 1;
