@@ -188,20 +188,31 @@ cudaError_t srft_sketch(uint64_t seed, bool retry, int64_t l, const double2* A, 
     dim3 g1((unsigned)((m1 + 127) / 128), (unsigned)nc);
     k_srft_pass1<<<g1, 128, 0, st>>>(A + c0 * lda, lda, m1, nc, d, Z);
     *launches += 1;
-    for (int r = 0; r < kSrftR; ++r) {
-      const int64_t lr = hoffs[r + 1] - hoffs[r];
-      if (lr == 0) continue;
-      const bool g3 = sketch_mults() == 3;  // Gauss's three products, as the Gaussian sketch
-      int S = g3 ? zgemm3m_ksplit(lr, m1, n / 8, num_sms) : zgemm_ksplit(lr, m1, n / 8, num_sms);
-      if ((size_t)S * lr * nc > splitk_elems) S = 1;
-      if (g3)
-        e = zgemm3m(Wg + hoffs[r], l, nullptr, 0, Z + (int64_t)r * m1 * nc, m1, Yg + hoffs[r], l,
-                    lr, nc, m1, st, S, splitk);
-      else
+    if (sketch_mults() == 3) {  // the 16 residue products in one batched launch (no K split)
+      Z3Batch bt{};
+      for (int r = 0; r < kSrftR; ++r) {
+        const int64_t lr = hoffs[r + 1] - hoffs[r];
+        if (lr == 0) continue;
+        bt.roff[bt.n] = hoffs[r];
+        bt.boff[bt.n] = (int64_t)r * m1 * nc;
+        bt.coff[bt.n] = hoffs[r];
+        bt.mout[bt.n] = lr;
+        ++bt.n;
+      }
+      e = zgemm3m_batched(Wg, l, Z, m1, Yg, l, bt, nc, m1, st);
+      if (e != cudaSuccess) return e;
+      *launches += 1;
+    } else {
+      for (int r = 0; r < kSrftR; ++r) {
+        const int64_t lr = hoffs[r + 1] - hoffs[r];
+        if (lr == 0) continue;
+        int S = zgemm_ksplit(lr, m1, n / 8, num_sms);
+        if ((size_t)S * lr * nc > splitk_elems) S = 1;
         e = zgemm_ordered(Wg + hoffs[r], l, Z + (int64_t)r * m1 * nc, m1, Yg + hoffs[r], l, lr,
                           nc, m1, 0, 0.0, 0, 0, st, S, splitk);
-      if (e != cudaSuccess) return e;
-      *launches += S > 1 ? 2 : 1;
+        if (e != cudaSuccess) return e;
+        *launches += S > 1 ? 2 : 1;
+      }
     }
     int64_t sb = (l * nc + 255) / 256;
     if (sb > 8192) sb = 8192;

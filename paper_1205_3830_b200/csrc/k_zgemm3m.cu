@@ -49,7 +49,8 @@ template <int FJ, int FR, int WJ, int WR, int BKC, int STAGES, int MINB, int RS,
 __global__ void __launch_bounds__(WJ* WR * 32, MINB)
     k_zgemm3m(const double2* __restrict__ Rm, int64_t ldr, const double* __restrict__ Rs,
               int64_t ldrs, const double2* __restrict__ Bm, int64_t ldb, double2* __restrict__ C,
-              int64_t ldc, int64_t Mout, int64_t N, int64_t K, int64_t kchunk, int64_t zstride) {
+              int64_t ldc, int64_t Mout, int64_t N, int64_t K, int64_t kchunk, int64_t zstride,
+              const Z3Batch bt) {
   using Cfg = Z3Cfg<FJ, FR, WJ, WR, BKC, STAGES, RS>;
   extern __shared__ __align__(16) double smem[];
   const int tid = threadIdx.x;
@@ -58,9 +59,19 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
   const int wj = warp % WJ, wr = warp / WJ;
   const int64_t r0 = (int64_t)blockIdx.x * Cfg::BR;
   const int64_t j0 = (int64_t)blockIdx.y * Cfg::BJ;
-  const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
-  K = (kbeg + kchunk < K) ? kbeg + kchunk : K;  // end of this K slice
-  C += (int64_t)blockIdx.z * zstride;
+  int64_t kbeg = 0;
+  if (bt.n > 0) {  // batched: blockIdx.z selects one of bt.n independent products (no K split)
+    const int z = blockIdx.z;
+    Rm += bt.roff[z];
+    Bm += bt.boff[z];
+    C += bt.coff[z];
+    Mout = bt.mout[z];
+    if (r0 >= Mout) return;
+  } else {
+    kbeg = (int64_t)blockIdx.z * kchunk;
+    K = (kbeg + kchunk < K) ? kbeg + kchunk : K;  // end of this K slice
+    C += (int64_t)blockIdx.z * zstride;
+  }
   const int64_t nk = (K - kbeg + BKC - 1) / BKC;
 
   // per-thread copy plan, fixed for the K loop (only the K offset moves from stage to stage)
@@ -262,13 +273,38 @@ static cudaError_t launch3(const double2* Rm, int64_t ldr, const double* Rs, int
   }
   if (tiles_r > 0x7FFFFFFF || tiles_j > 65535 || S > 65535) return cudaErrorInvalidConfiguration;
   dim3 grid((unsigned)tiles_r, (unsigned)tiles_j, (unsigned)S);
+  Z3Batch none{};
   kern<<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(Rm, ldr, Rs, ldrs, Bm, ldb, Cout, ldo, Mout, N, K,
-                                                kc, zs);
+                                                kc, zs, none);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess || S == 1) return e;
   int64_t blocks = (Mout * N + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   k_splitk_reduce3<<<(unsigned)blocks, 256, 0, st>>>(partial, S, Mout, N, C, ldc);
+  return cudaGetLastError();
+}
+
+template <int FJ, int FR, int WJ, int WR, int BKC, int STAGES, int MINB>
+static cudaError_t launch3_batched(const double2* Rm, int64_t ldr, const double2* Bm, int64_t ldb,
+                                   double2* C, int64_t ldc, const Z3Batch& bt, int64_t N, int64_t K,
+                                   cudaStream_t st) {
+  using Cfg = Z3Cfg<FJ, FR, WJ, WR, BKC, STAGES, 0>;
+  auto kern = k_zgemm3m<FJ, FR, WJ, WR, BKC, STAGES, MINB, 0, 0>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e =
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  int64_t mmax = 0;
+  for (int z = 0; z < bt.n; ++z) mmax = bt.mout[z] > mmax ? bt.mout[z] : mmax;
+  const int64_t tiles_r = (mmax + Cfg::BR - 1) / Cfg::BR;
+  const int64_t tiles_j = (N + Cfg::BJ - 1) / Cfg::BJ;
+  if (tiles_r < 1 || tiles_j > 65535) return cudaErrorInvalidConfiguration;
+  dim3 grid((unsigned)tiles_r, (unsigned)tiles_j, (unsigned)bt.n);
+  kern<<<grid, Cfg::kThreads, Cfg::kSmem, st>>>(Rm, ldr, nullptr, 0, Bm, ldb, C, ldc, mmax, N, K, K,
+                                                0, bt);
   return cudaGetLastError();
 }
 
@@ -372,6 +408,20 @@ cudaError_t zgemm3m(const double2* Rm, int64_t ldr, const double* Rs, int64_t ld
     default: return RID_L3(1, 3, 8, 1, 16, 3, 2, 1, 1);
   }
 #undef RID_L3
+}
+
+cudaError_t zgemm3m_batched(const double2* Rm, int64_t ldr, const double2* Bm, int64_t ldb,
+                            double2* C, int64_t ldc, const Z3Batch& bt, int64_t N, int64_t K,
+                            cudaStream_t st) {
+  if (bt.n <= 0 || N <= 0) return cudaSuccess;
+  if (bt.n > kZ3BatchMax) return cudaErrorInvalidValue;
+  int64_t mmax = 0;
+  for (int z = 0; z < bt.n; ++z) mmax = bt.mout[z] > mmax ? bt.mout[z] : mmax;
+  switch (pick3(mmax)) {
+    case 0: return launch3_batched<2, 3, 4, 2, 16, 3, 2>(Rm, ldr, Bm, ldb, C, ldc, bt, N, K, st);
+    case 1: return launch3_batched<1, 5, 8, 1, 16, 3, 2>(Rm, ldr, Bm, ldb, C, ldc, bt, N, K, st);
+    default: return launch3_batched<1, 3, 8, 1, 16, 3, 2>(Rm, ldr, Bm, ldb, C, ldc, bt, N, K, st);
+  }
 }
 
 int sketch_mults() {

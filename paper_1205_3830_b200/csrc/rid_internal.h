@@ -22,6 +22,16 @@ cudaError_t zgemm3m(const double2* Rm, int64_t ldr, const double* Rs, int64_t ld
                     const double2* Bm, int64_t ldb, double2* C, int64_t ldc, int64_t Mout,
                     int64_t N, int64_t K, cudaStream_t st, int ksplit, double2* partial);
 int zgemm3m_ksplit(int64_t Mout, int64_t K, int64_t n_ref, int num_sms);
+// Up to kZ3BatchMax independent products C_z (mout[z] x N) = Rm_z · Bm_z (K each) in one launch
+// (blockIdx.z = z; element offsets from the base pointers; the SRFT's residue GEMMs).
+constexpr int kZ3BatchMax = 16;
+struct Z3Batch {
+  int n;
+  int64_t roff[kZ3BatchMax], boff[kZ3BatchMax], coff[kZ3BatchMax], mout[kZ3BatchMax];
+};
+cudaError_t zgemm3m_batched(const double2* Rm, int64_t ldr, const double2* Bm, int64_t ldb,
+                            double2* C, int64_t ldc, const Z3Batch& bt, int64_t N, int64_t K,
+                            cudaStream_t st);
 inline int64_t rsum_ld(int64_t l) { return (l + 1) / 2 * 2; }
 cudaError_t rsum_fill(const double2* R, int64_t l, int64_t m, int64_t ldr, double* Rs,
                       int64_t ldrs, cudaStream_t st);
