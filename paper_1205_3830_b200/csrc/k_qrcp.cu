@@ -778,8 +778,6 @@ __global__ void __launch_bounds__(kRingThreads, 1)
           out.beta[j] = beta;
           out.R11[(int64_t)j * k + j] = make_double2(beta, 0.0);
         }
-        // rows 0..j-1 of the pivot column are final R entries
-        for (int r = idx; r < j; r += kCW * 32) out.R11[(int64_t)j * k + r] = Y[p * ldy + r];
       }
       consumers_sync();
       if (w.trace && b == 0 && idx == 0) w.trace[8 * j + 6] = globaltimer();
@@ -926,10 +924,16 @@ __global__ void __launch_bounds__(kRingThreads, 1)
       ubase += (unsigned)nitems;
       top2_warp(loc);
       if (lane == 0) sred[warp] = loc;
-    } else if (lane == 0) {
-      Top2 z;
-      top2_init(z);
-      sred[0] = z;
+    } else {
+      // warp 0 is idle while warps 1.. build the reflector and stream: CTA 0's copies rows
+      // 0..j-1 of the pivot column (final R entries) into the dense R11 off the critical path
+      if (b == 0)
+        for (int r = lane; r < j; r += 32) out.R11[(int64_t)j * k + r] = Y[p * ldy + r];
+      if (lane == 0) {
+        Top2 z;
+        top2_init(z);
+        sred[0] = z;
+      }
     }
     __syncthreads();
     if (threadIdx.x == 0) {
