@@ -406,6 +406,264 @@ __global__ void __launch_bounds__(kQrcpThreads, 2)
 }
 
 // =============================================================================================
+// Small sketches (C1–C3: 16·l·n well under the SMs' shared memory): the exact-recompute QR with
+// every CTA's columns resident in shared memory for all k steps. Per step the only global traffic
+// is the per-CTA candidate triple and one column: before each grid barrier every CTA writes its
+// local best column (rows j+1..l-1, double-buffered by step parity) to a slot, so after the
+// barrier every CTA builds the reflector from the winner's slot — the global pivot is always some
+// CTA's local best. The trailing update and the exact norms run from shared memory; the columns
+// go back to Y after the last step.
+// =============================================================================================
+template <int MAXQ>
+__global__ void __launch_bounds__(kQrcpThreads, 1)
+    k_qrcp_smem(double2* __restrict__ Y, int64_t ldy, int l, int64_t n, int k, double tol_rel,
+                QrcpOut out, QrcpWork w, int per) {
+  extern __shared__ __align__(16) unsigned char qs_raw[];
+  double2* sv = reinterpret_cast<double2*>(qs_raw);                   // MAXQ*32: v_j, rows j..
+  double* snu = reinterpret_cast<double*>(sv + MAXQ * 32);            // per (even): norms, -1 chosen
+  double2* sy = reinterpret_cast<double2*>(snu + ((per + 1) & ~1));   // per x l: the columns
+  __shared__ double s_tau[2];
+  __shared__ Top2 sred[kQrcpWarps];
+  __shared__ long long s_p;
+  __shared__ int s_stop, s_best;
+
+  // rows per lane in the column passes: up to QP (more columns per warp at once, shorter
+  // butterflies) — the column lives in shared memory, so only registers bound it
+  constexpr int QP = MAXQ < 12 ? 12 : MAXQ;
+  const int nb = gridDim.x, b = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c_lo = (int64_t)b * per;
+  const int ncol = (int)((c_lo + per < n) ? per : (n > c_lo ? n - c_lo : 0));
+  double nu0max = 0.0;
+  unsigned phase = 0;
+
+  // publish the CTA's (best, second, index) and copy its best column's rows r0..l-1 to the slot
+  auto publish = [&](Top2 loc, int parity, int r0) {
+    top2_warp(loc);
+    if (lane == 0) sred[warp] = loc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Top2 tt = sred[0];
+      for (int q = 1; q < kQrcpWarps; ++q) top2_merge(tt, sred[q]);
+      double* c = w.cand + ((size_t)parity * w.max_blocks + b) * 3;
+      c[0] = tt.b1;
+      c[1] = tt.b2;
+      c[2] = (double)tt.i1;
+      s_best = (tt.b1 >= 0.0) ? (int)(tt.i1 - c_lo) : -1;
+    }
+    __syncthreads();
+    const int bl = s_best;
+    if (bl >= 0) {
+      double2* slot = w.xslot + ((size_t)parity * w.max_blocks + b) * l;
+      for (int r = r0 + threadIdx.x; r < l; r += kQrcpThreads) slot[r] = sy[(int64_t)bl * l + r];
+    }
+  };
+
+  // ---- phase 0: load the CTA's columns, exact norms -------------------------------------------
+  for (int q = threadIdx.x; q < ncol * l; q += kQrcpThreads) {
+    const int cl = q / l, r = q - cl * l;
+    sy[q] = Y[(c_lo + cl) * ldy + r];
+  }
+  __syncthreads();
+  {
+    const int lpc = pick_lpc(l, QP);
+    const int cpw = 32 / lpc, sg = lane / lpc, sl = lane % lpc;
+    Top2 loc;
+    top2_init(loc);
+    for (int c0 = warp * cpw; c0 < ncol; c0 += kQrcpWarps * cpw) {
+      const int cl = c0 + sg;
+      const bool live = cl < ncol;
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < QP; ++q) {
+        const int r = sl + lpc * q;
+        if (live && r < l) {
+          const double2 y = sy[(int64_t)cl * l + r];
+          s = __fma_rn(y.x, y.x, s);
+          s = __fma_rn(y.y, y.y, s);
+        }
+      }
+      const double nu = __dsqrt_rn(group_sum(s, lpc));
+      if (live && sl == 0) {
+        snu[cl] = nu;
+        top2_push(loc, nu, c_lo + cl);
+      }
+    }
+    publish(loc, 0, 0);
+    grid_barrier(w.bar, (unsigned)nb * (++phase));
+  }
+
+  for (int j = 0; j < k; ++j) {
+    const int L = l - j;  // rows j..l-1
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 0] = globaltimer();
+    // ---- 1. global pivot (every CTA, identically) -----------------------------------------
+    if (warp == 0) {
+      Top2 tt;
+      top2_init(tt);
+      const double* cb = w.cand + (size_t)(j & 1) * w.max_blocks * 3;
+      for (int q = lane; q < nb; q += 32) {
+        Top2 o;
+        o.b1 = cb[q * 3 + 0];
+        o.b2 = cb[q * 3 + 1];
+        o.i1 = (long long)cb[q * 3 + 2];
+        top2_merge(tt, o);
+      }
+      top2_warp(tt);
+      if (j == 0) nu0max = tt.b1;
+      if (lane == 0) {
+        s_p = tt.i1;
+        s_stop = (!(tt.b1 >= tol_rel * nu0max) || tt.b1 <= 0.0) ? 1 : 0;
+        if (b == 0) {
+          out.resid[j] = tt.b1;
+          out.margin[j] = (tt.b2 < 0.0) ? DBL_MAX : (tt.b1 - tt.b2) / tt.b1;
+          if (!s_stop) out.J[j] = tt.i1;
+        }
+      }
+    }
+    __syncthreads();
+    if (s_stop) {
+      if (b == 0 && threadIdx.x == 0) {
+        out.info[0] = 2;
+        out.info[1] = j;
+      }
+      return;
+    }
+    const int64_t p = s_p;
+    const int bp = (int)(p / per);  // the winner CTA: p was its local best
+
+    // ---- 2. reflector H_j from the winner's slot (rows j..l-1 of column p) -------------------
+    if (warp == 0) {
+      const double2* xs = w.xslot + ((size_t)(j & 1) * w.max_blocks + bp) * l + j;
+      double2 x[MAXQ];
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int rr = lane + 32 * q;
+        x[q] = (rr < L) ? xs[rr] : make_double2(0.0, 0.0);
+      }
+      double s2 = 0.0;
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int rr = lane + 32 * q;
+        if (rr > 0 && rr < L) {
+          s2 = __fma_rn(x[q].x, x[q].x, s2);
+          s2 = __fma_rn(x[q].y, x[q].y, s2);
+        }
+      }
+      const double xnorm2 = group_sum(s2, 32);
+      const double ar = __shfl_sync(0xffffffffu, x[0].x, 0), ai = __shfl_sync(0xffffffffu, x[0].y, 0);
+      double tau_re, tau_im, beta, sc_re, sc_im;
+      if (xnorm2 == 0.0 && ai == 0.0) {
+        tau_re = 0.0;
+        tau_im = 0.0;
+        beta = ar;
+        sc_re = 0.0;
+        sc_im = 0.0;
+      } else {
+        const double nrm = __dsqrt_rn(__fma_rn(ar, ar, __fma_rn(ai, ai, xnorm2)));
+        beta = (ar >= 0.0) ? -nrm : nrm;
+        tau_re = __ddiv_rn(__dsub_rn(beta, ar), beta);
+        tau_im = __ddiv_rn(-ai, beta);
+        const double dr = __dsub_rn(ar, beta), di = ai;  // scal = 1 / (alpha - beta)
+        const double den = __fma_rn(dr, dr, __dmul_rn(di, di));
+        sc_re = __ddiv_rn(dr, den);
+        sc_im = __ddiv_rn(-di, den);
+      }
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int rr = lane + 32 * q;
+        if (rr < L) {
+          double2 v;
+          if (rr == 0) {
+            v = make_double2(1.0, 0.0);
+          } else {
+            v.x = __fma_rn(x[q].x, sc_re, -__dmul_rn(x[q].y, sc_im));
+            v.y = __fma_rn(x[q].x, sc_im, __dmul_rn(x[q].y, sc_re));
+          }
+          sv[rr] = v;
+        }
+      }
+      if (lane == 0) {
+        s_tau[0] = tau_re;
+        s_tau[1] = tau_im;
+        if (b == 0) {
+          out.beta[j] = beta;
+          out.R11[(int64_t)j * k + j] = make_double2(beta, 0.0);
+        }
+      }
+    } else if (warp == 1 && b == bp) {
+      // the owner: column p is chosen; rows 0..j-1 are final R entries
+      const int pl = (int)(p - c_lo);
+      if (lane == 0) snu[pl] = -1.0;
+      for (int r = lane; r < j; r += 32) out.R11[(int64_t)j * k + r] = sy[(int64_t)pl * l + r];
+    }
+    __syncthreads();
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 1] = globaltimer();
+
+    // ---- 3. every owned unchosen column in shared memory: apply H_j, exact norm --------------
+    const double tr = s_tau[0], ti = s_tau[1];
+    const int lpc = pick_lpc(L, QP);
+    const int cpw = 32 / lpc, sg = lane / lpc, sl = lane % lpc;
+    Top2 loc;
+    top2_init(loc);
+    for (int c0 = warp * cpw; c0 < ncol; c0 += kQrcpWarps * cpw) {
+      const int cl = c0 + sg;
+      const bool live = cl < ncol && snu[cl] >= 0.0;
+      double2* yc = sy + (int64_t)(cl < ncol ? cl : 0) * l + j;
+      double2 y[QP];
+      double wr = 0.0, wi = 0.0;
+#pragma unroll
+      for (int q = 0; q < QP; ++q) {
+        const int rr = sl + lpc * q;
+        y[q] = make_double2(0.0, 0.0);
+        if (live && rr < L) {
+          y[q] = yc[rr];
+          const double2 vv = sv[rr];
+          wr = __fma_rn(vv.x, y[q].x, __fma_rn(vv.y, y[q].y, wr));  // conj(v) y
+          wi = __fma_rn(vv.x, y[q].y, __fma_rn(-vv.y, y[q].x, wi));
+        }
+      }
+      wr = group_sum(wr, lpc);
+      wi = group_sum(wi, lpc);
+      const double s_re = __fma_rn(tr, wr, __dmul_rn(ti, wi));  // s = conj(tau) w
+      const double s_im = __fma_rn(tr, wi, -__dmul_rn(ti, wr));
+      double nn = 0.0;
+#pragma unroll
+      for (int q = 0; q < QP; ++q) {
+        const int rr = sl + lpc * q;
+        if (live && rr < L) {
+          const double2 vv = sv[rr];
+          y[q].x = __fma_rn(-s_re, vv.x, __fma_rn(s_im, vv.y, y[q].x));  // y -= s v
+          y[q].y = __fma_rn(-s_re, vv.y, __fma_rn(-s_im, vv.x, y[q].y));
+          yc[rr] = y[q];
+          if (rr > 0) {
+            nn = __fma_rn(y[q].x, y[q].x, nn);
+            nn = __fma_rn(y[q].y, y[q].y, nn);
+          }
+        }
+      }
+      const double nu = __dsqrt_rn(group_sum(nn, lpc));
+      if (live && sl == 0) {
+        snu[cl] = nu;
+        top2_push(loc, nu, c_lo + cl);
+      }
+    }
+    publish(loc, (j + 1) & 1, j + 1);
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 2] = globaltimer();
+    grid_barrier(w.bar, (unsigned)nb * (++phase));
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 3] = globaltimer();
+  }
+  // ---- the columns go back: rows 0..k-1 hold R (R12 for the solve), the rest the residual ----
+  for (int q = threadIdx.x; q < ncol * l; q += kQrcpThreads) {
+    const int cl = q / l, r = q - cl * l;
+    Y[(c_lo + cl) * ldy + r] = sy[q];
+  }
+  if (b == 0 && threadIdx.x == 0) {
+    out.info[0] = 0;
+    out.info[1] = k;
+  }
+}
+
+// =============================================================================================
 // Blocked variant (default): LAPACK zlaqps-style panels of nb <= kNB reflectors.
 //
 // The exact-recompute kernel above reads AND writes the whole trailing block every step (C4:
@@ -956,7 +1214,8 @@ __global__ void __launch_bounds__(kRingThreads, 1)
 
 size_t qrcp_work_bytes(int64_t n, int64_t l, int max_blocks) {
   return (size_t)2 * n * sizeof(double) + (size_t)2 * 3 * max_blocks * sizeof(double) +
-         (size_t)l * kNB * sizeof(double2) + (size_t)kNB * n * sizeof(double2) + 512;
+         (size_t)l * kNB * sizeof(double2) + (size_t)kNB * n * sizeof(double2) +
+         (size_t)2 * max_blocks * l * sizeof(double2) + 512;
 }
 
 QrcpWork qrcp_work_carve(void* buf, int64_t n, int64_t l, int max_blocks) {
@@ -967,6 +1226,8 @@ QrcpWork qrcp_work_carve(void* buf, int64_t n, int64_t l, int max_blocks) {
   p += (size_t)l * kNB * sizeof(double2);
   w.F = (double2*)p;
   p += (size_t)kNB * n * sizeof(double2);
+  w.xslot = (double2*)p;
+  p += (size_t)2 * max_blocks * l * sizeof(double2);
   w.nu = (double*)p;
   p += (size_t)n * sizeof(double);
   w.nuref = (double*)p;
@@ -1013,6 +1274,51 @@ static cudaError_t launch_qrcp(double2* Y, int64_t ldy, int l, int64_t n, int k,
   *launches += 1;
   return cudaLaunchCooperativeKernel((void*)k_qrcp<MAXQ>, dim3(blocks), dim3(kQrcpThreads), args,
                                      smem, st);
+}
+
+// The shared-memory-resident exact kernel, when the columns fit (2 CTAs per SM, else 1);
+// cudaErrorNotSupported when they do not (the caller falls back to k_qrcp).
+template <int MAXQ>
+static cudaError_t launch_qrcp_smem(double2* Y, int64_t ldy, int l, int64_t n, int k,
+                                    double tol_rel, const QrcpOut& out, const QrcpWork& w,
+                                    int num_sms, cudaStream_t st, int* launches) {
+  auto kern = k_qrcp_smem<MAXQ>;
+  cudaError_t e;
+  int dev = 0, optin = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
+    return e;
+  cudaFuncAttributes fa;
+  if ((e = cudaFuncGetAttributes(&fa, (const void*)kern)) != cudaSuccess) return e;
+  for (int per_sm = 2; per_sm >= 1; --per_sm) {
+    int blocks = num_sms * per_sm;
+    if (blocks > w.max_blocks) blocks = w.max_blocks;
+    if ((int64_t)blocks * 8 > n) blocks = (int)((n + 7) / 8);
+    if (blocks < 1) blocks = 1;
+    const int per = (int)((n + blocks - 1) / blocks);
+    blocks = (int)((n + per - 1) / per);
+    const size_t smem = (size_t)MAXQ * 32 * sizeof(double2) + (size_t)((per + 1) & ~1) * 8 +
+                        (size_t)per * l * sizeof(double2);
+    const size_t cap = (size_t)optin / per_sm - fa.sharedSizeBytes - 1024;
+    if (smem > cap) continue;
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+      return e;
+    int occ = 0;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kQrcpThreads, smem)) !=
+        cudaSuccess)
+      return e;
+    if (occ * num_sms < blocks) continue;  // a cooperative launch needs every CTA resident
+    if ((e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+    QrcpOut o = out;
+    QrcpWork ww = w;
+    int perv = per;
+    void* args[] = {&Y, &ldy, &l, &n, &k, &tol_rel, &o, &ww, &perv};
+    *launches += 1;
+    return cudaLaunchCooperativeKernel((void*)kern, dim3(blocks), dim3(kQrcpThreads), args, smem,
+                                       st);
+  }
+  return cudaErrorNotSupported;
 }
 
 // Panels of nb steps (k_qrcp_ring), each followed by the tensor-core trailing update
@@ -1124,11 +1430,17 @@ cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, doubl
   int dummy = 0;
   if (!launches) launches = &dummy;
 #define RID_Q(QV)                                                                              \
-  if (qneed <= QV)                                                                             \
-    return variant == 0                                                                        \
-               ? launch_qrcp<QV>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st, launches)    \
-               : launch_qrcp_blocked<QV>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st,      \
-                                         launches, nbw);
+  if (qneed <= QV) {                                                                           \
+    if (variant == 1)                                                                          \
+      return launch_qrcp_blocked<QV>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st,          \
+                                     launches, nbw);                                           \
+    if (variant == 0) {                                                                        \
+      const cudaError_t es =                                                                   \
+          launch_qrcp_smem<QV>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st, launches);     \
+      if (es != cudaErrorNotSupported) return es;                                              \
+    }                                                                                          \
+    return launch_qrcp<QV>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st, launches);         \
+  }
   RID_Q(1) RID_Q(2) RID_Q(3) RID_Q(4) RID_Q(5) RID_Q(6) RID_Q(8) RID_Q(9) RID_Q(12) RID_Q(17)
   RID_Q(24) RID_Q(32)
 #undef RID_Q

@@ -79,6 +79,8 @@ struct QrcpWork {
   double* scal = nullptr;   // 1: max_c ||Y[:, c]||
   double2* V = nullptr;     // l x kNB: the panel's reflectors (column-major, ld = l)
   double2* F = nullptr;     // kNB x n: f_s(c) (column-major, ld = kNB)
+  // shared-memory-resident exact kernel (k_qrcp_smem)
+  double2* xslot = nullptr; // 2 x max_blocks x l: each CTA's best column, by step parity
 };
 // one workspace buffer of qrcp_work_bytes(n, l, max_blocks) bytes, carved by qrcp_work_carve
 size_t qrcp_work_bytes(int64_t n, int64_t l, int max_blocks);

@@ -62,7 +62,7 @@ def oracle_dec(orc):
     return get
 
 
-@pytest.mark.parametrize("variant", ["0", "1"])
+@pytest.mark.parametrize("variant", ["0", "1", "2"])
 @pytest.mark.parametrize("name,seed,m,n,k,l,noise", CASES)
 def test_variant_parity(rid, oracle_dec, monkeypatch, variant, name, seed, m, n, k, l, noise):
     monkeypatch.setenv("RID_QRCP_VARIANT", variant)
