@@ -247,6 +247,14 @@ def test_bad_arguments(rid):
     assert e.value.status == rid.RID_EINVAL
     with pytest.raises(rid.RidError):
         rid.decompose(A, 4, 2000, 1)  # l > m
+    with pytest.raises(rid.RidError) as e:
+        rid.sketch(A, 1, 8, n=60, col0=20)  # columns [20, 70) outside n = 60
+    assert e.value.status == rid.RID_EINVAL
+    with pytest.raises(rid.RidError):
+        rid.sketch(A, 1, 8, n=50, col0=-1)
+    B = rid.generate(1, 3000, 40, 4, 0.0)
+    with pytest.raises(rid.RidError):
+        rid.decompose(B, 4, 2100, 1)  # l > 2048 (QR limit)
 
 
 # ------------------------------------------------------------------------------ estimator ----
