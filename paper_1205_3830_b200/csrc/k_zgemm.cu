@@ -342,6 +342,10 @@ cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int
                           int ksplit, double2* partial) {
   if (Mout <= 0 || N <= 0) return cudaSuccess;
   ZgemmEpilogue ep{mode, noise, seed, col0, K, 0, 0};
+  // QRCP trailing update (mode 2, K = nb <= 16): latency-bound read-modify-write of C, so small
+  // register-light CTAs, 2 stages, 3 per SM keep more tiles in flight (measured at C4: update total
+  // 2.95 -> 2.36 ms against the sketch tiles; 64-row/4-per-SM 2.55, 32x64/3-per-SM 2.76 ms)
+  if (mode == 2) return launch_cfg<1, 8, 8, 1, 16, 2, 3>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
   if (const char* v = getenv("RID_ZGEMM_VARIANT")) {  // tile experiments (tools/tune_*.py)
     const int id = atoi(v);
 #define RID_V(ID, ...) \
