@@ -76,7 +76,12 @@ class ClockSampler:
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
-    def stop(self):
+    def wait_first(self, timeout: float = 5.0):
+        t0 = time.time()
+        while self.proc and not self.lines and time.time() - t0 < timeout:
+            time.sleep(0.01)
+
+    def stop(self, first: int = 0):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -87,7 +92,7 @@ class ClockSampler:
         self.t.join(timeout=2)
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for ln in self.lines[first:]:
             f = [x.strip() for x in ln.split(",")]
             if len(f) < 7:
                 continue
@@ -214,16 +219,23 @@ def run_ours(args, cfg):
         # ---- timed region: K steps of rid_decompose on resident A -------------------------
         clocks = ClockSampler(local)
         clocks.start()
+        clocks.wait_first()  # nvidia-smi is up before the region starts
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         diags = []
+        n_before = len(clocks.lines)
         e0.record(stream)
         for _ in range(args.steps):
             r = rid.decompose(A, k, l, seed, n=n, col0=col0, J=J, P=P, ctx=ctx)
             diags.append(r.diag)
         e1.record(stream)
         barrier()
-        clk = clocks.stop()
+        # a region shorter than the 200 ms sampling period (C1-C2) may see no sample: keep the
+        # same load running, untimed, until one arrives, so the clocks line describes this load
+        t_extra = time.time()
+        while len(clocks.lines) == n_before and clocks.proc and time.time() - t_extra < 2.0:
+            rid.decompose(A, k, l, seed, n=n, col0=col0, J=J, P=P, ctx=ctx)
+        clk = clocks.stop(first=n_before)
         step_s = max_over_ranks(e0.elapsed_time(e1) * 1e-3 / args.steps)
         launches = sum(d["launches"] for d in diags)
 

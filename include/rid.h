@@ -64,6 +64,15 @@ typedef enum {
   RID_SKETCH_SRFT = 1      /* Y = S F D A (Eqs. 4–7); m a power of two >= 16     */
 } rid_sketch_kind;
 
+/* Pivoted QR of the sketch used by rid_decompose, rid_qrcp and rid_factor_solve (rid_set_qr).
+ * Both choose the same columns (the greedy largest-residual pivot of PAPER.md:82-86) and agree on
+ * R = Q^H Y to rounding. */
+typedef enum {
+  RID_QR_HOUSEHOLDER = 0, /* Householder QRCP (default; the cheaper choice PAPER.md:108 names)    */
+  RID_QR_CGS2 = 1         /* classical Gram-Schmidt with one reorthogonalisation, the paper's own
+                             QR ("CGS with iteration"); exact norms every step     */
+} rid_qr_kind;
+
 /* Per-call diagnostics (SPEC.md:298-302 IdDiagnostics); every field is written by the call that
  * receives it; times are device times from CUDA events on the context stream, in seconds. */
 typedef struct {
@@ -140,6 +149,10 @@ rid_status rid_sketch_srft(rid_ctx* ctx, uint64_t seed, int retry, int64_t l, co
                            int64_t ldy);
 /* Select the randomisation of subsequent rid_decompose calls on ctx (default GAUSSIAN). */
 rid_status rid_set_sketch(rid_ctx* ctx, int kind);
+/* Select the pivoted QR of subsequent rid_decompose / rid_qrcp / rid_factor_solve calls on ctx
+ * (default HOUSEHOLDER). RID_EINVAL for an unknown kind. CGS2 needs a workspace of
+ * 16 (2 l n + 2 l k + k n) + 8 l (k + 1) bytes beyond Householder's. */
+rid_status rid_set_qr(rid_ctx* ctx, int kind);
 /* Number of K slices S the sketch of an m-row, n-column matrix uses (1 = unsplit): chosen so that
  * the n/8-column shard of an 8-GPU run still fills the GPU, a function of (m, l, n) only. */
 int rid_sketch_splits(const rid_ctx* ctx, int64_t m, int64_t l, int64_t n);

@@ -59,8 +59,10 @@ EXPORTS = ["rid_create", "rid_destroy", "rid_last_error", "rid_version", "rid_co
            "rid_comm_get_id", "rid_comm_init", "rid_comm_info", "rid_generate", "rid_sketch",
            "rid_decompose", "rid_error_estimate", "rid_error_bound", "rid_normal_fill",
            "rid_qrcp", "rid_factor_solve", "rid_sketch_splits", "rid_sketch_srft",
-           "rid_set_sketch", "rid_sketch_mults", "rid_sketch_cols"]
+           "rid_set_sketch", "rid_sketch_mults", "rid_sketch_cols", "rid_set_qr"]
 SKETCH_GAUSSIAN, SKETCH_SRFT = 0, 1
+QR_HOUSEHOLDER, QR_CGS2 = 0, 1
+_QR_KINDS = {"householder": QR_HOUSEHOLDER, "cgs2": QR_CGS2}
 
 
 def lib():
@@ -90,6 +92,7 @@ def lib():
         "rid_sketch_cols": ([p, u64, u32, i64, p, i64, i64, i64, i64, i64, p, i64], ci),
         "rid_sketch_srft": ([p, u64, ci, i64, p, i64, i64, i64, i64, p, i64], ci),
         "rid_set_sketch": ([p, ci], ci),
+        "rid_set_qr": ([p, ci], ci),
         "rid_decompose": ([p, p, i64, i64, i64, i64, i64, i64, i64, u64, p, p, i64, p], ci),
         "rid_error_estimate": ([p, p, i64, i64, i64, i64, i64, p, i64, p, i64, ci, u64, p, p], ci),
         "rid_error_bound": ([i64, i64, i64, d, d], d),
@@ -309,13 +312,20 @@ class IdResult:
     diag: dict
 
 
+def _set_qr(ctx, qr: str):
+    ctx.check(lib().rid_set_qr(ctx.h, _QR_KINDS[qr]), "rid_set_qr")
+
+
 def decompose(A, k: int, l: int, seed: int, n: int | None = None, col0: int = 0, J=None, P=None,
-              ctx: Context | None = None, sketch: str = "gaussian") -> IdResult:
+              ctx: Context | None = None, sketch: str = "gaussian",
+              qr: str = "householder") -> IdResult:
     """The whole ID of the (shard of the) matrix A: J (k, global ids) and P_loc.
-    sketch: 'gaussian' (north star, default) or 'srft' (the paper's Y = S F D A)."""
+    sketch: 'gaussian' (north star, default) or 'srft' (the paper's Y = S F D A); qr:
+    'householder' (default) or 'cgs2' (the paper's CGS with iteration)."""
     ctx = ctx or default_context()
     kind = {"gaussian": SKETCH_GAUSSIAN, "srft": SKETCH_SRFT}[sketch]
     ctx.check(lib().rid_set_sketch(ctx.h, kind), "rid_set_sketch")
+    _set_qr(ctx, qr)
     m, n_loc = A.shape
     n = n_loc if n is None else n
     a = _Buf(A, m, n_loc, "A")
@@ -367,10 +377,12 @@ def normal_fill(seed: int, s: int, rows: int, cols: int, row0: int = 0, col0: in
     return out
 
 
-def qrcp(Y, k: int, ctx: Context | None = None, want_R: bool = True):
-    """Pivoted Householder QR of a full sketch: (J, R (k x n) or None, resid, margin, diag)."""
+def qrcp(Y, k: int, ctx: Context | None = None, want_R: bool = True, qr: str = "householder"):
+    """Pivoted QR of a full sketch: (J, R (k x n) or None, resid, margin, diag). qr:
+    'householder' (default) or 'cgs2' (PAPER.md:108)."""
     torch = _torch()
     ctx = ctx or default_context()
+    _set_qr(ctx, qr)
     l, n = Y.shape
     y = _Buf(Y, l, n, "Y")
     dev = Y.device
@@ -388,10 +400,12 @@ def qrcp(Y, k: int, ctx: Context | None = None, want_R: bool = True):
     return J, R, resid, margin, d.as_dict()
 
 
-def factor_solve(Y, k: int, col0: int, n_loc: int, ctx: Context | None = None):
+def factor_solve(Y, k: int, col0: int, n_loc: int, ctx: Context | None = None,
+                 qr: str = "householder"):
     """(J, P_loc) from a full sketch Y: factorisation + solve for one column shard."""
     torch = _torch()
     ctx = ctx or default_context()
+    _set_qr(ctx, qr)
     l, n = Y.shape
     y = _Buf(Y, l, n, "Y")
     J = torch.empty(k, dtype=torch.int64, device=Y.device)

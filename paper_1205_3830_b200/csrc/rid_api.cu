@@ -34,6 +34,7 @@ struct rid_ctx {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {}, ev_used[2] = {}, ev_copy0 = nullptr, ev_copy1 = nullptr;
   int sketch_kind = 0;  // RID_SKETCH_GAUSSIAN (north star) or RID_SKETCH_SRFT
+  int qr_kind = 0;      // RID_QR_HOUSEHOLDER (default) or RID_QR_CGS2
 };
 
 namespace {
@@ -190,8 +191,15 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
     w.trace = (unsigned long long*)pt;
   }
   RID_CUDA(c, cudaMemsetAsync(pR11, 0, sizeof(double2) * k * k, c->stream));
-  RID_CUDA(c, rid::qrcp(Yw, l, l, n, k, kRankTol, o, w, c->num_sms, c->stream,
-                        diag ? &diag->launches : nullptr));
+  if (c->qr_kind == RID_QR_CGS2) {  // the paper's own QR
+    void* pc;
+    RID_TRY(ws_get(c, "cgs2_work", rid::cgs2_work_bytes(l, n, k, c->num_sms), &pc));
+    RID_CUDA(c, rid::cgs2(Yw, l, l, n, k, kRankTol, o, pc, c->num_sms, c->stream,
+                          diag ? &diag->launches : nullptr, w.trace));
+  } else {
+    RID_CUDA(c, rid::qrcp(Yw, l, l, n, k, kRankTol, o, w, c->num_sms, c->stream,
+                          diag ? &diag->launches : nullptr));
+  }
   if (trace_path) {
     std::vector<unsigned long long> tr(8 * k);
     RID_CUDA(c, cudaMemcpyAsync(tr.data(), w.trace, sizeof(unsigned long long) * 8 * k,
@@ -474,6 +482,14 @@ rid_status rid_set_sketch(rid_ctx* c, int kind) {
   if (kind != RID_SKETCH_GAUSSIAN && kind != RID_SKETCH_SRFT)
     return fail(c, RID_EINVAL, "rid_set_sketch: unknown kind %d", kind);
   c->sketch_kind = kind;
+  return RID_OK;
+}
+
+rid_status rid_set_qr(rid_ctx* c, int kind) {
+  if (!c) return RID_EINVAL;
+  if (kind != RID_QR_HOUSEHOLDER && kind != RID_QR_CGS2)
+    return fail(c, RID_EINVAL, "rid_set_qr: unknown kind %d", kind);
+  c->qr_kind = kind;
   return RID_OK;
 }
 

@@ -91,6 +91,14 @@ cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, doubl
                  const QrcpOut& out, const QrcpWork& w, int num_sms, cudaStream_t st,
                  int* launches, int variant = -1);
 
+// The paper's QR: column-pivoted CGS with one reorthogonalisation (k_cgs2.cu).
+// Same outputs as qrcp (J, beta, resid, margin, info, R11) and the same contract on Y: on return
+// Y[0:k, c] = R[:, c] with R = Q^H Y (the rows below k are left as they were).
+size_t cgs2_work_bytes(int64_t l, int64_t n, int64_t k, int num_sms);
+cudaError_t cgs2(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, double tol_rel,
+                 const QrcpOut& out, void* work, int num_sms, cudaStream_t st, int* launches,
+                 unsigned long long* trace = nullptr);
+
 // Inverse of the pivoted triangle R11 (R11[t, s] = Y[t, J[s]] for t < s, beta[s] on the diagonal)
 cudaError_t tri_inverse(const double2* R11, int64_t k, double2* Rinv, cudaStream_t st);
 // P[:, J_t - col0] = e_t for pivots inside the shard (k_misc.cu)

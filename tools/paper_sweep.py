@@ -6,9 +6,11 @@ Gaussian sketch of the north star, timing the phases the paper tabulates — ran
 ("FFT", Table 2 in source order), the pivoted QR ("Gram-Schmidt"), the factorisation of R and P
 (the R11^-1 R12 solve) and the total — and estimating ||A - BP||_2 (q = 10, compensated).
 The paper's 4-processor XMT numbers are printed beside ours as context (different hardware).
-Writes one JSON line per (shape, randomisation).
+Each also runs with the paper's own QR (--qrs cgs2: classical Gram-Schmidt with one
+reorthogonalisation, k_cgs2.cu); srft + cgs2 is the paper's algorithm exactly.
+Writes one JSON line per (shape, randomisation, QR).
 
-    python tools/paper_sweep.py [--shapes 0,1,2] [--kinds srft,gaussian]
+    python tools/paper_sweep.py [--shapes 0,1,2] [--kinds srft,gaussian] [--qrs householder,cgs2]
 """
 import argparse
 import json
@@ -34,6 +36,7 @@ SHAPES = [
 ap = argparse.ArgumentParser()
 ap.add_argument("--shapes", default=",".join(str(i) for i in range(len(SHAPES))))
 ap.add_argument("--kinds", default="srft,gaussian")
+ap.add_argument("--qrs", default="householder")
 ap.add_argument("--q", type=int, default=10)
 args = ap.parse_args()
 for si in [int(x) for x in args.shapes.split(",")]:
@@ -46,14 +49,14 @@ for si in [int(x) for x in args.shapes.split(",")]:
     P0.zero_()
     normA = rid.error_estimate(A, J0, P0, args.q, 1)
     del P0
-    for kind in args.kinds.split(","):
-        rid.decompose(A, k, l, 1, sketch=kind)  # warm (workspace, plan)
+    for kind, qr in [(a, b) for a in args.kinds.split(",") for b in args.qrs.split(",")]:
+        rid.decompose(A, k, l, 1, sketch=kind, qr=qr)  # warm (workspace, plan)
         torch.cuda.synchronize()
-        r = rid.decompose(A, k, l, 1, sketch=kind)
+        r = rid.decompose(A, k, l, 1, sketch=kind, qr=qr)
         d = r.diag
         est = rid.error_estimate(A, r.J, r.P, args.q, 1)
         print(json.dumps({
-            "shape": f"k={k} m=2^{lm} n=2^{ln} l={l}", "randomisation": kind,
+            "shape": f"k={k} m=2^{lm} n=2^{ln} l={l}", "randomisation": kind, "qr": qr,
             "t_total_s": d["t_total"], "t_randomise_s": d["t_rgen"] + d["t_sketch"],
             "t_qr_s": d["t_qrcp"], "t_factor_s": d["t_solve"],
             "err_2norm_est": est, "norm_A_2_est": normA, "rel_err": est / normA,
