@@ -37,6 +37,7 @@
 
 #include "rid_device.cuh"
 #include "rid_internal.h"
+#include "rid_tma.cuh"
 
 namespace rid {
 
@@ -699,51 +700,6 @@ __device__ __forceinline__ void cmac_add(double& ar, double& ai, const double2 g
   ai = __fma_rn(g.x, f.y, __fma_rn(g.y, f.x, ai));
 }
 
-// ---- PTX helpers: mbarrier + bulk async copy (TMA engine, no tensor map) -------------------
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void tma_box_g2s(void* dst, const CUtensorMap* map, int x, int y,
-                                            uint64_t* b) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(b))
-      : "memory");
-}
-// the same with an L2 eviction-priority policy (createpolicy) for the box's lines
-__device__ __forceinline__ void tma_box_g2s_hint(void* dst, const CUtensorMap* map, int x, int y,
-                                                 uint64_t* b, uint64_t policy) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(
-          smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(b)), "l"(policy)
-      : "memory");
-}
-__device__ __forceinline__ uint64_t policy_evict_first() {
-  uint64_t p;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(p));
-  return p;
-}
 __device__ __forceinline__ void consumers_sync() {  // warps 1..15 only
   asm volatile("bar.sync 1, %0;\n" ::"n"((kRingWarps - 1) * 32) : "memory");
 }

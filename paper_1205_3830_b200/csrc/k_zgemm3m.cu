@@ -336,6 +336,7 @@ static int rows3(int id) {
   const int rows[3] = {48, 40, 24};
   return rows[id];
 }
+int zgemm3m_tile_rows(int64_t Mout) { return rows3(pick3(Mout)); }
 
 int zgemm3m_ksplit(int64_t Mout, int64_t K, int64_t n_ref, int num_sms) {
   if (const char* v = getenv("RID_SKETCH_SPLIT")) {
@@ -398,6 +399,8 @@ cudaError_t zgemm3m(const double2* Rm, int64_t ldr, const double* Rs, int64_t ld
       default: break;
     }
   }
+  if (zgemm3m_tma_enabled(Mout))
+    return zgemm3m_tma(Rm, ldr, Rs, ldrs, Bm, ldb, C, ldc, Mout, N, K, st, ksplit, partial);
   if (!Rs) {  // no Re R + Im R plane (e.g. the SRFT's row-grouped W): sums in registers
     switch (pick3(Mout)) {
       case 0: return RID_L3(2, 3, 4, 2, 16, 3, 2, 0, 0);

@@ -1,0 +1,86 @@
+"""The TMA-fed three-product sketch kernel (k_zgemm3m_tma.cu) against the cp.async kernel it
+replaces (k_zgemm3m.cu) and against the oracle, through the C ABI.
+
+Both kernels evaluate the same ascending fma chains per K slice (reading R31), only the
+operand staging differs (TMA boxes with a 128-byte swizzle and mbarrier hand-over vs cp.async and
+__syncthreads), so Y must be BITWISE equal (RID_Z3_TMA=0 selects the old kernel). The shapes put
+the 48-row tile (the one the TMA kernel covers) under every edge the TMA unit handles by
+zero-filling: rows past l (l = 47, 143), K past m (m not a multiple of 16), columns past n, K
+slices (split-K) and the wave-tail split; against the oracle Y holds the north-star bar (1e-12
+relative Frobenius; measured 1e-15 .. 1e-14).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint64)
+
+
+@pytest.fixture(scope="module")
+def rid():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1205_3830_b200 import build
+
+    build.build()
+    import paper_1205_3830_b200 as rid
+
+    return rid
+
+
+SHAPES = [  # (seed, m, n, k, l, noise)
+    (1, 2048, 2048, 512, 528, 1e-8),     # C4's k/l, reduced
+    (2, 4096, 1024, 128, 144, 1e-12),    # C3's k/l, reduced
+    (3, 1000, 777, 13, 47, 1e-8),        # ragged rows, K tail, ragged columns
+    (4, 4099, 300, 100, 143, 0.0),       # ragged everything, exact rank
+    (5, 65536, 64, 32, 144, 1e-12),      # narrow: K split into slices
+    (6, 64, 5, 3, 48, 0.0),              # four stages, one tile
+    (9, 2048, 1000, 64, 80, 1e-10),      # C2's k/l: the 40-row tile with the Re R + Im R plane
+    (10, 4096, 600, 256, 272, 1e-10),    # C5's k/l: 40-row tiles, rows past l in the last one
+    (11, 1003, 333, 20, 39, 1e-9),       # 40-row tile, ragged everything
+]
+
+
+@pytest.mark.parametrize("seed,m,n,k,l,noise", SHAPES)
+def test_tma_sketch_bitwise_vs_cpasync_and_oracle(rid, orc, monkeypatch, seed, m, n, k, l, noise):
+    A = rid.generate(seed, m, n, k, noise)
+    monkeypatch.setenv("RID_Z3_TMA", "0")
+    Y_old = rid.sketch(A, seed, l).cpu().numpy()
+    monkeypatch.setenv("RID_Z3_TMA", "1")
+    Y_tma = rid.sketch(A, seed, l).cpu().numpy()
+    torch.cuda.synchronize()
+    assert np.array_equal(bits(Y_tma), bits(Y_old))
+    if m * n * l <= 2048 * 2048 * 528:
+        Y_o = orc.sketch(orc.generate(seed, m, n, k, noise), seed, l)
+        rel = np.linalg.norm(Y_tma - Y_o) / np.linalg.norm(Y_o)
+        assert rel <= 1e-12, rel
+
+
+@pytest.mark.parametrize("variant,l", [("2", 96), ("4", 96), ("2", 80)])
+def test_tma_pipeline_depths_bitwise(rid, monkeypatch, variant, l):
+    """Two and four stages (RID_Z3T_VARIANT) give the same bits as the default three."""
+    A = rid.generate(7, 3000, 700, 40, 1e-9)
+    Y3 = rid.sketch(A, 7, l).cpu().numpy()
+    monkeypatch.setenv("RID_Z3T_VARIANT", variant)
+    Yv = rid.sketch(A, 7, l).cpu().numpy()
+    assert np.array_equal(bits(Yv), bits(Y3))
+
+
+def test_tma_wave_tail_and_shards_bitwise(rid, monkeypatch):
+    """Column blocks of a matrix sketched as shards (different tensor maps, base pointers and the
+    wave-tail split set) equal the whole-matrix sketch bit for bit, and equal the old kernel."""
+    seed, m, n, k, l = 8, 2048, 4096, 64, 96
+    A = rid.generate(seed, m, n, k, 1e-10)
+    Y = rid.sketch(A, seed, l).cpu().numpy()
+    for G in (2, 8):
+        w = n // G
+        for g in range(G):
+            Yg = rid.sketch(A[:, g * w:(g + 1) * w], seed, l, n=n, col0=g * w).cpu().numpy()
+            assert np.array_equal(bits(Yg), bits(Y[:, g * w:(g + 1) * w]))
+    monkeypatch.setenv("RID_Z3_TMA", "0")
+    Y_old = rid.sketch(A, seed, l).cpu().numpy()
+    assert np.array_equal(bits(Y), bits(Y_old))
