@@ -318,7 +318,7 @@ def run_ours(args, cfg):
                      "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": sketch_exec_tf / FP64_DMMA_PEAK_TFLOPS,
                      "traffic": prof.get("dram_bytes_per_launch"),
-                     "kernel": ("k_zgemm3m (sketch Y = R A, Gauss 3M, DMMA.8x8x4)" if mults == 3
+                     "kernel": ("k_zgemm3m_tma (sketch Y = R A, Gauss 3M, DMMA.8x8x4, TMA-fed)" if mults == 3
                                 else "k_zgemm_dmma (sketch Y = R A, real embedding, DMMA.8x8x4)"),
                      "algorithmic": (f"{2 * mults}*l*m*n_loc = {2.0 * mults * l * m * n_loc:.4g} "
                                      f"flop per launch ({mults} real products per complex "

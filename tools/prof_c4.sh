@@ -7,7 +7,7 @@ CMD="python bench.py --config $CFG --steps 1 --warmup 1 --q 1 --no-e2e --no-cpu-
 mkdir -p gpurun_out
 $CMD > gpurun_out/prof_plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$CFG.csv $CMD > gpurun_out/ncu_launch.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_zgemm3m -s 3 -c 1 -o gpurun_out/prof_sketch_$CFG -f $CMD > gpurun_out/ncu_sketch.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_zgemm3m_tma -s 3 -c 1 -o gpurun_out/prof_sketch_$CFG -f $CMD > gpurun_out/ncu_sketch.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_qrcp_ring -s 8 -c 1 -o gpurun_out/prof_qrcp_$CFG -f $CMD > gpurun_out/ncu_qrcp.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_zgemm_dmma -s 12 -c 1 -o gpurun_out/prof_update_$CFG -f $CMD > gpurun_out/ncu_update.log 2>&1
 echo "exit $?"
