@@ -12,8 +12,11 @@
 //   z  = A^H y − P^H sb  k_z    warp per column j (coalesced down A), rounds; + ||z||^2 partials
 // All merges of partial (s, c) accumulators happen in a fixed order, so the estimate is
 // deterministic for a given launch shape.
+#include <cstdlib>
+
 #include "rid_device.cuh"
 #include "rid_internal.h"
+#include "rid_tma.cuh"
 
 namespace rid {
 
@@ -120,16 +123,41 @@ __global__ void __launch_bounds__(256) k_merge_scalar(const double* __restrict__
 
 // x *= 1 / ||v|| where the norm^2 is the dd in nn[0..1] (x = v / ||v||, one division each)
 // Also writes est = sqrt(||v||) to est_out (when non-null) — the estimate after this iteration.
+// vmax (nullable): atomicMax of max_j |x_j.re| + |x_j.im| (non-negative doubles order like their
+// bit patterns), the bound the fixed-offset accumulation of k_ax_tma needs
+__device__ __forceinline__ void vmax_update(unsigned long long* vmax, double v) {
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0 && v > 0.0) atomicMax(vmax, (unsigned long long)__double_as_longlong(v));
+}
 __global__ void k_normalise(const double2* __restrict__ v, int64_t n_loc, const double* __restrict__ nn,
-                            double2* __restrict__ x, double* __restrict__ est_out) {
+                            double2* __restrict__ x, double* __restrict__ est_out,
+                            unsigned long long* __restrict__ vmax) {
   const double nv = __dsqrt_rn(__dadd_rn(nn[0], nn[1]));
   if (blockIdx.x == 0 && threadIdx.x == 0 && est_out) est_out[0] = __dsqrt_rn(nv);
   if (!(nv > 0.0)) return;
+  double mx = 0.0;
   for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n_loc;
        j += (int64_t)gridDim.x * blockDim.x) {
     const double2 a = v[j];
-    x[j] = make_double2(__ddiv_rn(a.x, nv), __ddiv_rn(a.y, nv));
+    const double2 r = make_double2(__ddiv_rn(a.x, nv), __ddiv_rn(a.y, nv));
+    x[j] = r;
+    mx = fmax(mx, fabs(r.x) + fabs(r.y));
   }
+  if (vmax) vmax_update(vmax, mx);
+}
+
+// amax = max_ij |A_ij.re| + |A_ij.im| (bits, atomicMax): one pass over A per estimate
+__global__ void __launch_bounds__(256) k_absmax(const double2* __restrict__ A, int64_t lda,
+                                                int64_t m, int64_t n_loc,
+                                                unsigned long long* __restrict__ amax) {
+  double mx = 0.0;
+  for (int64_t j = blockIdx.x; j < n_loc; j += gridDim.x)
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+      const double2 a = __ldcs(A + j * lda + i);
+      mx = fmax(mx, fabs(a.x) + fabs(a.y));
+    }
+  vmax_update(amax, mx);
 }
 
 // ---- u partials: part[chunk][t] = sum_{j in chunk} P[t, j] x[j] -------------------------------
@@ -154,6 +182,20 @@ __global__ void k_merge_vec(const double* __restrict__ part, int nparts, int64_t
     for (int q = 1; q < nparts; ++q) cdd_merge(a, cdd_load(part + ((size_t)q * len + i) * 4));
     cdd_store(out + (size_t)i * 4, a);
   }
+}
+
+// the same merge with a warp per output (short vectors, many parts: u = P x's partials): lane l
+// merges parts l, l + 32, ... in order, then a fixed-shape butterfly over the lanes
+__global__ void k_merge_vec_warp(const double* __restrict__ part, int nparts, int64_t len,
+                                 double* __restrict__ out) {
+  const int lane = threadIdx.x & 31;
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (i >= len) return;  // warp-uniform
+  cdd a;
+  cdd_zero(a);
+  for (int q = lane; q < nparts; q += 32) cdd_merge(a, cdd_load(part + ((size_t)q * len + i) * 4));
+  cdd_warp(a);
+  if (lane == 0) cdd_store(out + (size_t)i * 4, a);
 }
 
 // ---- w partials: part[split][i] = sum_{j in split} A[i, j] x[j] -------------------------------
@@ -181,22 +223,39 @@ __global__ void __launch_bounds__(256) k_ax(const double2* __restrict__ A, int64
 }
 
 // ---- y = round(w - B (u_s + u_c)); w_parts: nparts x m cdd, u: k cdd --------------------------
-__global__ void k_y(const double* __restrict__ wpart, int nparts, int64_t m,
-                    const double2* __restrict__ B, int64_t ldb, int64_t k,
-                    const double* __restrict__ u, double2* __restrict__ y) {
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    cdd a = cdd_load(wpart + (size_t)i * 4);
-    for (int q = 1; q < nparts; ++q) cdd_merge(a, cdd_load(wpart + ((size_t)q * m + i) * 4));
-    for (int64_t t = 0; t < k; ++t) {
+// CTA = 32 rows (lane = row) x 8 warps; warp w takes t = w, w + 8, ... (coalesced rows of B);
+// warp 0 merges the w partials and the eight B u chains in order (fixed shape: deterministic).
+__global__ void __launch_bounds__(256) k_y(const double* __restrict__ wpart, int nparts, int64_t m,
+                                           const double2* __restrict__ B, int64_t ldb, int64_t k,
+                                           const double* __restrict__ u, double2* __restrict__ y,
+                                           unsigned long long* __restrict__ vmax) {
+  __shared__ double4 sbu[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * 32 + lane;
+  cdd bu;
+  cdd_zero(bu);
+  if (i < m) {
+    for (int64_t t = warp; t < k; t += 8) {
       const double2 b = B[t * ldb + i];
       const double4 ut = reinterpret_cast<const double4*>(u)[t];
       const double2 nb = make_double2(-b.x, -b.y);
-      cdd_mac(a, nb, make_double2(ut.x, ut.z), false);  // exact part of B u_s
-      cdd_mac(a, nb, make_double2(ut.y, ut.w), false);  // B u_c
+      cdd_mac(bu, nb, make_double2(ut.x, ut.z), false);  // exact part of B u_s
+      cdd_mac(bu, nb, make_double2(ut.y, ut.w), false);  // B u_c
     }
-    y[i] = make_double2(dd_val(a.re), dd_val(a.im));
   }
+  sbu[warp][lane] = make_double4(bu.re.s, bu.re.c, bu.im.s, bu.im.c);
+  __syncthreads();
+  double mx = 0.0;
+  if (warp == 0 && i < m) {
+    cdd a = cdd_load(wpart + (size_t)i * 4);
+    for (int q = 1; q < nparts; ++q) cdd_merge(a, cdd_load(wpart + ((size_t)q * m + i) * 4));
+#pragma unroll
+    for (int w = 0; w < 8; ++w) cdd_merge(a, cdd_load(&sbu[w][lane].x));
+    const double2 yi = make_double2(dd_val(a.re), dd_val(a.im));
+    y[i] = yi;
+    mx = fabs(yi.x) + fabs(yi.y);
+  }
+  if (vmax && warp == 0) vmax_update(vmax, mx);
 }
 
 // ---- sb[t] = sum_i conj(B[i, t]) y[i]; one CTA per t -------------------------------------------
@@ -267,21 +326,301 @@ __global__ void __launch_bounds__(256) k_z(const double2* __restrict__ A, int64_
   }
 }
 
+// ---- TMA-fed streaming passes (default; RID_EST_TMA=0 selects k_ax / k_z above) ---------------
+// Both passes read A once as boxes of 128 rows x 8 columns (16 KB, cp.async.bulk.tensor, zero-fill
+// past m and n_loc) through an NS-stage ring (the x / y values ride along as a one-row box) handed over with mbarriers (one producing thread,
+// per-warp release), so the bytes in flight no longer cost registers and the Dot2 arithmetic
+// runs from shared memory. Persistent grids: CTA b takes work items b, b + gridDim.x, ... and
+// the ring runs on across item boundaries. Same partial layouts and fixed merge orders as above.
+// Fixed-offset compensated accumulation (the TMA passes): with B a bound on the sum of |terms|
+// an accumulator will ever see and C a power of two >= 4B, the running sum s starts at C and
+// stays in [C − B, C + B], so |s| >= 3B >= |p| for every product p and Dekker's Fast2Sum (3 FP64
+// operations) is error-free — against TwoSum's 6 in the Dot2 accumulator: 7 instead of 10 FP64
+// operations per real product, on the pipe these passes are bound by. The value is (s − C) + c
+// with s − C exact (Sterbenz: s ∈ [C/2, 2C]); the error is that of Dot2 scaled by C / Σ|terms|
+// (≤ 2^3 · amax·vmax·count / Σ|terms|), i.e. still O(u²)·Σ|terms| — far inside the 1e-10 parity
+// bar (reading R16; tested against the Dot2 passes, RID_EST_TMA=0).
+struct fdd {
+  double s, c;
+};
+__device__ __forceinline__ void fdd_add_prod(fdd& a, double x, double y) {
+  const double p = __dmul_rn(x, y);
+  const double pe = __fma_rn(x, y, -p);
+  const double t = __dadd_rn(a.s, p);
+  const double e = __dsub_rn(p, __dsub_rn(t, a.s));
+  a.s = t;
+  a.c = __dadd_rn(a.c, __dadd_rn(pe, e));
+}
+struct cfdd {
+  fdd re, im;
+};
+__device__ __forceinline__ void cfdd_init(cfdd& a, double C) { a.re = {C, 0.0}; a.im = {C, 0.0}; }
+__device__ __forceinline__ void cfdd_mac(cfdd& a, double2 x, double2 y, bool conj_x) {
+  const double xi = conj_x ? -x.y : x.y;
+  fdd_add_prod(a.re, x.x, y.x);
+  fdd_add_prod(a.re, -xi, y.y);
+  fdd_add_prod(a.im, x.x, y.y);
+  fdd_add_prod(a.im, xi, y.x);
+}
+// back to a Dot2 pair (s − C exact)
+__device__ __forceinline__ cdd cfdd_value(const cfdd& a, double C) {
+  cdd r;
+  r.re = {__dsub_rn(a.re.s, C), a.re.c};
+  r.im = {__dsub_rn(a.im.s, C), a.im.c};
+  return r;
+}
+// a power of two >= 4 B, B = 2 · count · amax · vmax (two products per element per accumulator,
+// |re·re'| + |im·im'| <= (|re| + |im|)(|re'| + |im'|))
+__device__ __forceinline__ double fdd_offset(const unsigned long long* bounds, int64_t count) {
+  const double B = 2.0 * (double)count * __longlong_as_double((long long)bounds[0]) *
+                   __longlong_as_double((long long)bounds[1]);
+  if (!(B > 0.0)) return 1.0;
+  return scalbn(1.0, ilogb(B) + 3);  // 2^(ilogb B + 1) > B
+}
+
+constexpr int kEstNS = 6;               // ring stages
+constexpr int kEstRows = 128;           // complex rows per box
+constexpr int kEstBoxA = kEstRows * 8 * 16;  // bytes of one A box (8 columns)
+
+
+// w partials: item = (row block rb, column split sp); 256 threads: row r = tid & 127, column half
+// h = tid >> 7 (columns 4h..4h+3 of every box); the halves merge in order h = 0, 1 at item end.
+// Stage = A box + the 8 x values of its columns (128 B, 1D box).
+__global__ void __launch_bounds__(256, 2)
+    k_ax_tma(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapX,
+             int64_t m, int rblocks, int nitems, int64_t split_cols, int64_t n_loc,
+             const unsigned long long* __restrict__ bounds, double* __restrict__ part) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t full[kEstNS], empty[kEstNS];
+  __shared__ double4 shalf[128][2];
+  constexpr int kStage = kEstBoxA + 128;
+  const int tid = threadIdx.x, lane = tid & 31, r = tid & 127, h = tid >> 7;
+  if (tid == 0) {
+    tma_prefetch_map(&mapA);
+    tma_prefetch_map(&mapX);
+    for (int s = 0; s < kEstNS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    mbar_init_fence();
+  }
+  __syncthreads();
+  const int my_items = blockIdx.x < nitems ? (nitems - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int nb = (int)((split_cols + 7) / 8);  // boxes per item
+  const int64_t nq = (int64_t)my_items * nb;
+  auto issue = [&](int64_t q) {
+    const int it = blockIdx.x + (int)(q / nb) * gridDim.x, b = (int)(q % nb);
+    const int rb = it % rblocks, sp = it / rblocks;
+    const int s = (int)(q % kEstNS);
+    unsigned char* st = smraw + (size_t)s * kStage;
+    const int64_t c0 = sp * split_cols + 8 * (int64_t)b;
+    mbar_expect_tx(&full[s], kStage);
+    tma_box_g2s(st, &mapA, 2 * rb * kEstRows, (int)c0, &full[s]);
+    tma_box_g2s(st + kEstBoxA, &mapX, (int)(2 * c0), 0, &full[s]);
+  };
+  if (tid == 0)
+    for (int64_t q = 0; q < kEstNS - 1 && q < nq; ++q) issue(q);
+  int64_t q = 0;
+  for (int ii = 0; ii < my_items; ++ii) {
+    const int it = blockIdx.x + ii * gridDim.x;
+    const int rb = it % rblocks, sp = it / rblocks;
+    const double C = fdd_offset(bounds, split_cols);  // same for every item of the launch
+    cfdd acc[4];  // one per column slot: four independent dependency chains
+#pragma unroll
+    for (int c = 0; c < 4; ++c) cfdd_init(acc[c], C);
+    for (int b = 0; b < nb; ++b, ++q) {
+      if (tid == 0 && q + kEstNS - 1 < nq) {
+        const int64_t qn = q + kEstNS - 1;
+        if (qn >= kEstNS) mbar_wait(&empty[qn % kEstNS], (unsigned)(((qn / kEstNS) - 1) & 1));
+        issue(qn);
+      }
+      const int s = (int)(q % kEstNS);
+      mbar_wait(&full[s], (unsigned)((q / kEstNS) & 1));
+      const unsigned char* st = smraw + (size_t)s * kStage;
+      // columns past the split (only in its last box, past n_loc) were zero-filled by the TMA
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const int cc = 4 * h + c;
+        const double2 av = *reinterpret_cast<const double2*>(st + (cc * kEstRows + r) * 16);
+        const double2 xv = *reinterpret_cast<const double2*>(st + kEstBoxA + cc * 16);
+        cfdd_mac(acc[c], av, xv, false);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    cdd a = cfdd_value(acc[0], C);
+#pragma unroll
+    for (int c = 1; c < 4; ++c) cdd_merge(a, cfdd_value(acc[c], C));
+    if (h == 1) shalf[r][0] = make_double4(a.re.s, a.re.c, a.im.s, a.im.c);
+    __syncthreads();
+    if (h == 0) {
+      const double4 o = shalf[r][0];
+      cdd b2;
+      b2.re = {o.x, o.y};
+      b2.im = {o.z, o.w};
+      cdd_merge(a, b2);
+      const int64_t i = (int64_t)rb * kEstRows + r;
+      if (i < m) cdd_store(part + ((size_t)sp * m + i) * 4, a);
+    }
+    __syncthreads();
+  }
+}
+
+// z = round(A^H y − P^H sb): item = 8 consecutive columns, warp w owns column 8 item + w; lane
+// holds rows lane + 32 u (u < 4) of every box. Stage = A box + the 128 y values of its rows (2 KB,
+// 1D box). One dd partial of ||z||^2 per item (npart[item]), as k_z writes per CTA of 8 columns.
+__global__ void __launch_bounds__(256, 2)
+    k_z_tma(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapY,
+            int64_t m, int64_t n_loc, int nitems, const double2* __restrict__ P, int64_t ldp,
+            int64_t k, const double* __restrict__ sb, double2* __restrict__ z,
+            const unsigned long long* __restrict__ bounds, double* __restrict__ npart) {
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t full[kEstNS], empty[kEstNS];
+  __shared__ dd sred[8];
+  constexpr int kStage = kEstBoxA + kEstRows * 16;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    tma_prefetch_map(&mapA);
+    tma_prefetch_map(&mapY);
+    for (int s = 0; s < kEstNS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    mbar_init_fence();
+  }
+  __syncthreads();
+  const int my_items = blockIdx.x < nitems ? (nitems - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int nb = (int)((m + kEstRows - 1) / kEstRows);
+  const int64_t nq = (int64_t)my_items * nb;
+  auto issue = [&](int64_t q) {
+    const int it = blockIdx.x + (int)(q / nb) * gridDim.x, b = (int)(q % nb);
+    const int s = (int)(q % kEstNS);
+    unsigned char* st = smraw + (size_t)s * kStage;
+    mbar_expect_tx(&full[s], kStage);
+    tma_box_g2s(st, &mapA, 2 * b * kEstRows, 8 * it, &full[s]);
+    tma_box_g2s(st + kEstBoxA, &mapY, 2 * b * kEstRows, 0, &full[s]);
+  };
+  if (tid == 0)
+    for (int64_t q = 0; q < kEstNS - 1 && q < nq; ++q) issue(q);
+  int64_t q = 0;
+  for (int ii = 0; ii < my_items; ++ii) {
+    const int it = blockIdx.x + ii * gridDim.x;
+    const int64_t j = 8 * (int64_t)it + warp;
+    const double C = fdd_offset(bounds, m);
+    cfdd acc[4];  // one per row slot u: four independent dependency chains
+#pragma unroll
+    for (int u = 0; u < 4; ++u) cfdd_init(acc[u], C);
+    for (int b = 0; b < nb; ++b, ++q) {
+      if (tid == 0 && q + kEstNS - 1 < nq) {
+        const int64_t qn = q + kEstNS - 1;
+        if (qn >= kEstNS) mbar_wait(&empty[qn % kEstNS], (unsigned)(((qn / kEstNS) - 1) & 1));
+        issue(qn);
+      }
+      const int s = (int)(q % kEstNS);
+      mbar_wait(&full[s], (unsigned)((q / kEstNS) & 1));
+      const unsigned char* st = smraw + (size_t)s * kStage;
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int rr = lane + 32 * u;
+        const double2 av = *reinterpret_cast<const double2*>(st + (warp * kEstRows + rr) * 16);
+        const double2 yv = *reinterpret_cast<const double2*>(st + kEstBoxA + rr * 16);
+        cfdd_mac(acc[u], av, yv, true);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    cdd a = cfdd_value(acc[0], C);
+#pragma unroll
+    for (int u = 1; u < 4; ++u) cdd_merge(a, cfdd_value(acc[u], C));
+    dd nz = {0.0, 0.0};
+    if (j < n_loc) {
+      for (int64_t t = lane; t < k; t += 32) {
+        const double2 p = P[j * ldp + t];
+        const double4 sv = reinterpret_cast<const double4*>(sb)[t];
+        const double2 np = make_double2(-p.x, p.y);  // -conj(p)
+        cdd_mac(a, np, make_double2(sv.x, sv.z), false);
+        cdd_mac(a, np, make_double2(sv.y, sv.w), false);
+      }
+    }
+    cdd_warp(a);
+    if (lane == 0 && j < n_loc) {
+      const double2 zj = make_double2(dd_val(a.re), dd_val(a.im));
+      z[j] = zj;
+      dd_add_prod(nz, zj.x, zj.x);
+      dd_add_prod(nz, zj.y, zj.y);
+    }
+    if (lane == 0) sred[warp] = nz;
+    __syncthreads();
+    if (tid == 0) {
+      dd t = sred[0];
+      for (int w = 1; w < 8; ++w) dd_merge(t, sred[w]);
+      npart[2 * it] = t.s;
+      npart[2 * it + 1] = t.c;
+    }
+    __syncthreads();
+  }
+}
+
+bool est_tma_enabled() {
+  const char* v = getenv("RID_EST_TMA");
+  return !(v && atoi(v) == 0);
+}
+
+static cudaError_t est_maps(const double2* A, int64_t lda, int64_t m, int64_t n_loc,
+                            const double2* v, int64_t vlen, int vbox, CUtensorMap* mapA,
+                            CUtensorMap* mapV) {
+  PFN_cuTensorMapEncodeTiled encode;
+  cudaError_t e = tensor_map_encoder(&encode);
+  if (e != cudaSuccess) return e;
+  const cuuint32_t estr[2] = {1u, 1u};
+  const cuuint64_t gdim[2] = {(cuuint64_t)(2 * m), (cuuint64_t)n_loc};
+  const cuuint64_t gstr[1] = {(cuuint64_t)lda * sizeof(double2)};
+  const cuuint32_t box[2] = {(cuuint32_t)(2 * kEstRows), 8u};
+  if (encode(mapA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)A, gdim, gstr, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  // the vector as a one-row 2D tensor (2 vlen doubles x 1)
+  const cuuint64_t vdim[2] = {(cuuint64_t)(2 * vlen), 1};
+  const cuuint64_t vstr[1] = {(cuuint64_t)((16 * vlen + 15) / 16 * 16)};
+  const cuuint32_t vb[2] = {(cuuint32_t)vbox, 1u};
+  if (encode(mapV, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)v, vdim, vstr, vb, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  return cudaSuccess;
+}
+
 // ------------------------------------------------------------------------------ launchers ------
 EstPlan est_plan(int64_t m, int64_t n_loc, int64_t k, int num_sms) {
   EstPlan p;
+  p.tma = est_tma_enabled();
   p.px_chunk = 64;
   p.px_parts = (int)((n_loc + p.px_chunk - 1) / p.px_chunk);
-  const int64_t row_blocks = (m + 255) / 256;
-  int64_t splits = (8 * num_sms + row_blocks - 1) / row_blocks;
-  if (splits < 1) splits = 1;
-  if (splits > n_loc) splits = n_loc;
-  if (splits > 1024) splits = 1024;
-  p.ax_split_cols = (n_loc + splits - 1) / splits;
-  p.ax_parts = (int)((n_loc + p.ax_split_cols - 1) / p.ax_split_cols);
+  if (p.tma) {
+    // work items (row block, column split): >= 12 per CTA slot (2 per SM) for balance
+    p.ax_rblocks = (int)((m + kEstRows - 1) / kEstRows);
+    int64_t splits = (12 * 2 * (int64_t)num_sms + p.ax_rblocks - 1) / p.ax_rblocks;
+    const int64_t cols8 = (n_loc + 7) / 8;
+    if (splits > cols8) splits = cols8;
+    if (splits > 256) splits = 256;
+    if (splits < 1) splits = 1;
+    p.ax_split_cols = ((n_loc + splits - 1) / splits + 7) / 8 * 8;
+    p.ax_parts = (int)((n_loc + p.ax_split_cols - 1) / p.ax_split_cols);
+  } else {
+    const int64_t row_blocks = (m + 255) / 256;
+    int64_t splits = (8 * num_sms + row_blocks - 1) / row_blocks;
+    if (splits < 1) splits = 1;
+    if (splits > n_loc) splits = n_loc;
+    if (splits > 1024) splits = 1024;
+    p.ax_split_cols = (n_loc + splits - 1) / splits;
+    p.ax_parts = (int)((n_loc + p.ax_split_cols - 1) / p.ax_split_cols);
+    p.ax_rblocks = 0;
+  }
   p.z_blocks = (int)((n_loc + 7) / 8);
   p.x0_blocks = (int)((n_loc + 255) / 256 < 4 * num_sms ? (n_loc + 255) / 256 : 4 * num_sms);
   if (p.x0_blocks < 1) p.x0_blocks = 1;
+  p.num_sms = num_sms;
   (void)k;
   return p;
 }
@@ -295,12 +634,24 @@ cudaError_t est_merge_scalar(const double* part, int nparts, double* out, cudaSt
   k_merge_scalar<<<1, 256, 0, st>>>(part, nparts, out);
   return cudaGetLastError();
 }
+cudaError_t est_absmax(const double2* A, int64_t lda, int64_t m, int64_t n_loc,
+                       unsigned long long* amax, const EstPlan& p, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(amax, 0, sizeof(unsigned long long), st);
+  if (e != cudaSuccess) return e;
+  const int64_t g = n_loc < 8 * (int64_t)p.num_sms ? n_loc : 8 * (int64_t)p.num_sms;
+  k_absmax<<<(unsigned)g, 256, 0, st>>>(A, lda, m, n_loc, amax);
+  return cudaGetLastError();
+}
 cudaError_t est_normalise(const double2* v, int64_t n_loc, const double* nn, double2* x,
-                          double* est_out, cudaStream_t st) {
+                          double* est_out, unsigned long long* vmax, cudaStream_t st) {
+  if (vmax) {
+    cudaError_t e = cudaMemsetAsync(vmax, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+  }
   int64_t b = (n_loc + 255) / 256;
   if (b > 4096) b = 4096;
   if (b < 1) b = 1;
-  k_normalise<<<(unsigned)b, 256, 0, st>>>(v, n_loc, nn, x, est_out);
+  k_normalise<<<(unsigned)b, 256, 0, st>>>(v, n_loc, nn, x, est_out, vmax);
   return cudaGetLastError();
 }
 cudaError_t est_px(const double2* P, int64_t ldp, int64_t k, int64_t n_loc, const double2* x,
@@ -308,7 +659,7 @@ cudaError_t est_px(const double2* P, int64_t ldp, int64_t k, int64_t n_loc, cons
   k_px<<<p.px_parts, 256, 0, st>>>(P, ldp, k, n_loc, x, p.px_chunk, part);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_merge_vec<<<(unsigned)((k + 127) / 128), 128, 0, st>>>(part, p.px_parts, k, u_out);
+  k_merge_vec_warp<<<(unsigned)((k + 7) / 8), 256, 0, st>>>(part, p.px_parts, k, u_out);
   return cudaGetLastError();
 }
 cudaError_t est_merge_vec(const double* part, int nparts, int64_t len, double* out, cudaStream_t st) {
@@ -318,16 +669,38 @@ cudaError_t est_merge_vec(const double* part, int nparts, int64_t len, double* o
   return cudaGetLastError();
 }
 cudaError_t est_ax(const double2* A, int64_t lda, int64_t m, int64_t n_loc, const double2* x,
-                   double* part, const EstPlan& p, cudaStream_t st) {
+                   const unsigned long long* bounds, double* part, const EstPlan& p,
+                   cudaStream_t st) {
+  if (p.tma) {
+    CUtensorMap mapA, mapX;
+    cudaError_t e = est_maps(A, lda, m, n_loc, x, n_loc, 16, &mapA, &mapX);
+    if (e != cudaSuccess) return e;
+    const size_t smem = (size_t)kEstNS * (kEstBoxA + 128);
+    static bool attr = false;
+    if (!attr) {
+      if ((e = cudaFuncSetAttribute(k_ax_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem)) != cudaSuccess)
+        return e;
+      attr = true;
+    }
+    const int nitems = p.ax_rblocks * p.ax_parts;
+    const int grid = nitems < 2 * p.num_sms ? nitems : 2 * p.num_sms;
+    k_ax_tma<<<grid, 256, smem, st>>>(mapA, mapX, m, p.ax_rblocks, nitems, p.ax_split_cols, n_loc,
+                                      bounds, part);
+    return cudaGetLastError();
+  }
   dim3 grid((unsigned)((m + 255) / 256), (unsigned)p.ax_parts);
   k_ax<<<grid, 256, 0, st>>>(A, lda, m, n_loc, x, p.ax_split_cols, part);
   return cudaGetLastError();
 }
 cudaError_t est_y(const double* wpart, int nparts, int64_t m, const double2* B, int64_t ldb,
-                  int64_t k, const double* u, double2* y, cudaStream_t st) {
-  int64_t b = (m + 255) / 256;
-  if (b > 4096) b = 4096;
-  k_y<<<(unsigned)b, 256, 0, st>>>(wpart, nparts, m, B, ldb, k, u, y);
+                  int64_t k, const double* u, double2* y, unsigned long long* vmax,
+                  cudaStream_t st) {
+  if (vmax) {
+    cudaError_t e = cudaMemsetAsync(vmax, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return e;
+  }
+  k_y<<<(unsigned)((m + 31) / 32), 256, 0, st>>>(wpart, nparts, m, B, ldb, k, u, y, vmax);
   return cudaGetLastError();
 }
 cudaError_t est_bhy(const double2* B, int64_t ldb, int64_t m, int64_t k, const double2* y,
@@ -337,7 +710,26 @@ cudaError_t est_bhy(const double2* B, int64_t ldb, int64_t m, int64_t k, const d
 }
 cudaError_t est_z(const double2* A, int64_t lda, int64_t m, int64_t n_loc, const double2* y,
                   const double2* P, int64_t ldp, int64_t k, const double* sb, double2* z,
-                  double* npart, const EstPlan& p, cudaStream_t st) {
+                  const unsigned long long* bounds, double* npart, const EstPlan& p,
+                  cudaStream_t st) {
+  if (p.tma) {
+    CUtensorMap mapA, mapY;
+    cudaError_t e = est_maps(A, lda, m, n_loc, y, m, 2 * kEstRows, &mapA, &mapY);
+    if (e != cudaSuccess) return e;
+    const size_t smem = (size_t)kEstNS * (kEstBoxA + kEstRows * 16);
+    static bool attr = false;
+    if (!attr) {
+      if ((e = cudaFuncSetAttribute(k_z_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem)) != cudaSuccess)
+        return e;
+      attr = true;
+    }
+    const int nitems = p.z_blocks;
+    const int grid = nitems < 2 * p.num_sms ? nitems : 2 * p.num_sms;
+    k_z_tma<<<grid, 256, smem, st>>>(mapA, mapY, m, n_loc, nitems, P, ldp, k, sb, z, bounds,
+                                     npart);
+    return cudaGetLastError();
+  }
   k_z<<<p.z_blocks, 256, 0, st>>>(A, lda, m, n_loc, y, P, ldp, k, sb, z, npart);
   return cudaGetLastError();
 }

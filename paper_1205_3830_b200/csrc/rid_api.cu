@@ -772,6 +772,11 @@ rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, 
   RID_TRY(ws_get(c, "estnp", sizeof(double) * 2 * nparts_max, &pnp));
   RID_TRY(ws_get(c, "estnn", sizeof(double) * 2 * (G + 1), &pnn));
   RID_TRY(ws_get(c, "estval", sizeof(double), &pest));
+  // bounds of the fixed-offset accumulation: [amax, xmax] for A x, [amax, ymax] for A^H y
+  void* pmax;
+  RID_TRY(ws_get(c, "estmax", sizeof(unsigned long long) * 4, &pmax));
+  unsigned long long* bax = (unsigned long long*)pmax;  // {amax, xmax}
+  unsigned long long* bz = bax + 2;                     // {amax, ymax}
   double2* B = (double2*)pB;
   double2 *x = (double2*)px, *z = (double2*)pz, *y = (double2*)py;
   double *u = (double*)pu, *nn = (double*)pnn;
@@ -794,7 +799,12 @@ rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, 
   const double* nn_final = nn + (coll ? 2 * G : 0);
   RID_CUDA(c, rid::est_x0(seed, col0, n_loc, x, (double*)pnp, pl, c->stream));
   RID_TRY(scalar_allreduce((const double*)pnp, pl.x0_blocks));
-  RID_CUDA(c, rid::est_normalise(x, n_loc, nn_final, x, nullptr, c->stream));
+  RID_CUDA(c, rid::est_normalise(x, n_loc, nn_final, x, nullptr, bax + 1, c->stream));
+  if (pl.tma) {
+    RID_CUDA(c, rid::est_absmax((const double2*)a.dev, lda, m, n_loc, bax, pl, c->stream));
+    RID_CUDA(c, cudaMemcpyAsync(bz, bax, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                                c->stream));
+  }
   RID_CUDA(c, cudaEventRecord(ev[1], c->stream));
   for (int it = 0; it < q; ++it) {
     // u = P x (replicated after the exchange)
@@ -806,21 +816,21 @@ rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, 
       RID_CUDA(c, cudaMemcpyAsync(u, psb, sizeof(double) * 4 * k, cudaMemcpyDeviceToDevice, c->stream));
     }
     // y = A x - B u (replicated)
-    RID_CUDA(c, rid::est_ax((const double2*)a.dev, lda, m, n_loc, x, (double*)pax, pl, c->stream));
+    RID_CUDA(c, rid::est_ax((const double2*)a.dev, lda, m, n_loc, x, bax, (double*)pax, pl, c->stream));
     if (coll) {
       double* w_loc = (double*)pwall + (size_t)4 * m * c->rank;
       RID_CUDA(c, rid::est_merge_vec((const double*)pax, pl.ax_parts, m, w_loc, c->stream));
       RID_NCCL(c, ncclAllGather(w_loc, pwall, (size_t)(4 * m), ncclDouble, c->comm, c->stream));
-      RID_CUDA(c, rid::est_y((const double*)pwall, G, m, B, m, k, u, y, c->stream));
+      RID_CUDA(c, rid::est_y((const double*)pwall, G, m, B, m, k, u, y, bz + 1, c->stream));
     } else {
-      RID_CUDA(c, rid::est_y((const double*)pax, pl.ax_parts, m, B, m, k, u, y, c->stream));
+      RID_CUDA(c, rid::est_y((const double*)pax, pl.ax_parts, m, B, m, k, u, y, bz + 1, c->stream));
     }
     // sb = B^H y ; z = A^H y - P^H sb ; x = z / ||z||
     RID_CUDA(c, rid::est_bhy(B, m, m, k, y, (double*)psb, c->stream));
     RID_CUDA(c, rid::est_z((const double2*)a.dev, lda, m, n_loc, y, (const double2*)p.dev, ldp, k,
-                           (const double*)psb, z, (double*)pnp, pl, c->stream));
+                           (const double*)psb, z, bz, (double*)pnp, pl, c->stream));
     RID_TRY(scalar_allreduce((const double*)pnp, pl.z_blocks));
-    RID_CUDA(c, rid::est_normalise(z, n_loc, nn_final, x, (double*)pest, c->stream));
+    RID_CUDA(c, rid::est_normalise(z, n_loc, nn_final, x, (double*)pest, bax + 1, c->stream));
   }
   RID_CUDA(c, cudaEventRecord(ev[2], c->stream));
   RID_CUDA(c, cudaMemcpyAsync(est, pest, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
@@ -829,7 +839,7 @@ rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, 
     rid_diag d{};
     d.t_total = ev_ms(ev[0], ev[2]) * 1e-3;
     d.t_h2d = ev_ms(ev[0], ev[1]) * 1e-3;
-    d.launches = 3 + 3 + q * (3 + 4 + (coll ? 2 : 1) + 1);
+    d.launches = 3 + 4 + q * (3 + 4 + (coll ? 2 : 1) + 1);
     *diag = d;
   }
   return RID_OK;

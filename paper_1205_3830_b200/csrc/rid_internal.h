@@ -118,32 +118,43 @@ cudaError_t gather_columns(const double2* A, int64_t lda, int64_t m, const int64
 // Compensated power-iteration pieces (k_estimate.cu). Vectors of "cdd" are 4 doubles per entry
 // (re.s, re.c, im.s, im.c): a Dot2 accumulator whose value is s + c.
 struct EstPlan {
+  bool tma;  // TMA-fed passes (k_ax_tma / k_z_tma; RID_EST_TMA=0 selects k_ax / k_z)
   int64_t px_chunk;
   int px_parts;
   int64_t ax_split_cols;
   int ax_parts;
+  int ax_rblocks;  // row blocks of 128 (TMA pass)
   int z_blocks;
   int x0_blocks;
+  int num_sms;
 };
 EstPlan est_plan(int64_t m, int64_t n_loc, int64_t k, int num_sms);
 cudaError_t est_x0(uint64_t seed, int64_t col0, int64_t n_loc, double2* x, double* part,
                    const EstPlan& p, cudaStream_t st);
 cudaError_t est_merge_scalar(const double* part, int nparts, double* out, cudaStream_t st);
+// vmax / amax: max |re| + |im| of the produced vector / of A (atomicMax on the bits; zeroed by
+// the launcher), the bounds of the fixed-offset accumulation in the TMA passes
+cudaError_t est_absmax(const double2* A, int64_t lda, int64_t m, int64_t n_loc,
+                       unsigned long long* amax, const EstPlan& p, cudaStream_t st);
 cudaError_t est_normalise(const double2* v, int64_t n_loc, const double* nn, double2* x,
-                          double* est_out, cudaStream_t st);
+                          double* est_out, unsigned long long* vmax, cudaStream_t st);
 cudaError_t est_px(const double2* P, int64_t ldp, int64_t k, int64_t n_loc, const double2* x,
                    double* part, double* u_out, const EstPlan& p, cudaStream_t st);
 cudaError_t est_merge_vec(const double* part, int nparts, int64_t len, double* out,
                           cudaStream_t st);
+// bounds = {amax, xmax} (est_ax) / {amax, ymax} (est_z), device
 cudaError_t est_ax(const double2* A, int64_t lda, int64_t m, int64_t n_loc, const double2* x,
-                   double* part, const EstPlan& p, cudaStream_t st);
+                   const unsigned long long* bounds, double* part, const EstPlan& p,
+                   cudaStream_t st);
 cudaError_t est_y(const double* wpart, int nparts, int64_t m, const double2* B, int64_t ldb,
-                  int64_t k, const double* u, double2* y, cudaStream_t st);
+                  int64_t k, const double* u, double2* y, unsigned long long* vmax,
+                  cudaStream_t st);
 cudaError_t est_bhy(const double2* B, int64_t ldb, int64_t m, int64_t k, const double2* y,
                     double* sb, cudaStream_t st);
 cudaError_t est_z(const double2* A, int64_t lda, int64_t m, int64_t n_loc, const double2* y,
                   const double2* P, int64_t ldp, int64_t k, const double* sb, double2* z,
-                  double* npart, const EstPlan& p, cudaStream_t st);
+                  const unsigned long long* bounds, double* npart, const EstPlan& p,
+                  cudaStream_t st);
 
 }  // namespace rid
 

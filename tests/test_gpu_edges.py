@@ -96,3 +96,22 @@ def test_host_outputs(rid, orc):
     ref = rid.decompose(A, k, l, 4)
     assert J.tolist() == np_(ref.J).tolist()
     assert np.array_equal(P, np_(ref.P))
+
+
+@pytest.mark.parametrize("seed,m,n,k,l,noise", [
+    (1, 2048, 2048, 64, 80, 1e-10),    # C2's k/l, reduced
+    (2, 1001, 777, 13, 29, 1e-8),      # m not /128, n not /8
+    (3, 1024, 512, 16, 24, 0.0),       # exact rank (C1): the residual is rounding only
+    (4, 130, 9, 3, 7, 1e-6),           # one row block plus two rows, two column groups
+])
+def test_estimator_tma_matches_register_passes(rid, monkeypatch, seed, m, n, k, l, noise):
+    """The TMA-fed estimator passes (k_ax_tma / k_z_tma, default) and the register-streaming ones
+    (RID_EST_TMA=0) sum in different orders, both compensated (Dot2): the estimates agree far
+    inside the 1e-10 parity bar (reading R16), relative to ||A||."""
+    A = rid.generate(seed, m, n, k, noise)
+    r = rid.decompose(A, k, l, seed)
+    e_t = rid.error_estimate(A, r.J, r.P, 6, seed)
+    monkeypatch.setenv("RID_EST_TMA", "0")
+    e_r = rid.error_estimate(A, r.J, r.P, 6, seed)
+    nA = rid.error_estimate(A, r.J, torch.zeros_like(r.P), 30, seed)  # ~||A||_2 (P = 0, B unused)
+    assert abs(e_t - e_r) <= 1e-13 * nA, (e_t, e_r, nA)
