@@ -14,6 +14,8 @@
 // Plan (docs/RNG.md §7): d_i = (cos, sin)(2 pi u1) of Philox (i, 0, s_phase, 0) via the spec'd
 // sincos, s_k = x0 & (m - 1) of Philox (k, 0, s_sample, 0); W entries from the same sincos on
 // u = ((s_k i1) mod m) / m. Agreement with the oracle's direct ascending sum is to rounding.
+#include <cstdlib>
+
 #include "rid_device.cuh"
 #include "rid_internal.h"
 
@@ -199,7 +201,10 @@ cudaError_t srft_sketch(uint64_t seed, bool retry, int64_t l, const double2* A, 
         bt.mout[bt.n] = lr;
         ++bt.n;
       }
-      e = zgemm3m_batched(Wg, l, Z, m1, Yg, l, bt, nc, m1, st);
+      const char* v = getenv("RID_Z3_TMA");
+      e = (v && atoi(v) == 0) ? zgemm3m_batched(Wg, l, Z, m1, Yg, l, bt, nc, m1, st)
+                              : zgemm3m_tma_batched(Wg, l, l, Z, m1, kSrftR * nc, Yg, l, bt, nc,
+                                                    m1, st);
       if (e != cudaSuccess) return e;
       *launches += 1;
     } else {

@@ -50,7 +50,7 @@ template <int FJ, int FR, int WJ, int WR, int STAGES, int MINB, int RS>
 __global__ void __launch_bounds__(WJ* WR * 32, MINB)
     k_zgemm3m_tma(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapR,
                   const __grid_constant__ CUtensorMap mapS, double2* __restrict__ C, int64_t ldc, int64_t Mout, int64_t N, int64_t K,
-                  int64_t kchunk, int64_t zstride) {
+                  int64_t kchunk, int64_t zstride, const Z3Batch bt) {
   using Cf = Z3T<FJ, FR, WJ, WR, STAGES, RS>;
   extern __shared__ __align__(1024) unsigned char smraw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
@@ -61,11 +61,22 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
   const int g = lane >> 2, t = lane & 3;
   const int pg = (g >> 1) + 4 * (g & 1);  // π(g)
   const int wj = warp % WJ, wr = warp / WJ;
-  const int r0 = (int)blockIdx.x * Cf::BR;
+  const int r0 = (int)blockIdx.x * Cf::BR;  // first output row of the tile
   const int64_t j0 = (int64_t)blockIdx.y * Cf::BJ;
-  const int64_t kbeg = (int64_t)blockIdx.z * kchunk;
-  const int64_t kend = (kbeg + kchunk < K) ? kbeg + kchunk : K;
-  C += (int64_t)blockIdx.z * zstride;
+  int rt0 = r0, jt0 = (int)j0;               // tile origin in the tensor maps
+  int64_t kbeg = 0, kend = K;
+  if (bt.n > 0) {  // batched (blockIdx.z = product): row / column offsets into shared maps
+    const int z = blockIdx.z;
+    Mout = bt.mout[z];
+    if (r0 >= Mout) return;
+    rt0 += (int)bt.roff[z];
+    jt0 += (int)bt.boff[z];
+    C += bt.coff[z];
+  } else {
+    kbeg = (int64_t)blockIdx.z * kchunk;
+    kend = (kbeg + kchunk < K) ? kbeg + kchunk : K;
+    C += (int64_t)blockIdx.z * zstride;
+  }
   const int nk = (int)((kend - kbeg + Cf::BKC - 1) / Cf::BKC);
 
   if (tid == 0) {
@@ -88,15 +99,15 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
     const int kc0 = (int)(kbeg + (int64_t)kt * Cf::BKC);
 #pragma unroll
     for (int b = 0; b < Cf::kNA; ++b)
-      tma_box_g2s(st + b * Cf::kABox, &mapA, 2 * kc0 + 16 * b, (int)j0, &full[s]);
+      tma_box_g2s(st + b * Cf::kABox, &mapA, 2 * kc0 + 16 * b, jt0, &full[s]);
 #pragma unroll
     for (int b = 0; b < Cf::kNR; ++b)
-      tma_box_g2s(st + Cf::kNA * Cf::kABox + b * Cf::kRBox, &mapR, 2 * (r0 + 8 * b), kc0, &full[s]);
+      tma_box_g2s(st + Cf::kNA * Cf::kABox + b * Cf::kRBox, &mapR, 2 * (rt0 + 8 * b), kc0, &full[s]);
     if (RS) {
 #pragma unroll
       for (int b = 0; b < Cf::kNR; ++b)
         tma_box_g2s(st + Cf::kNA * Cf::kABox + Cf::kNR * Cf::kRBox + b * Cf::kRsBox, &mapS,
-                    r0 + 8 * b, kc0, &full[s]);
+                    rt0 + 8 * b, kc0, &full[s]);
     }
   };
   if (tid == 0)
@@ -193,10 +204,14 @@ __global__ void k_splitk_reduce3t(const double2* __restrict__ part, int S, int64
   }
 }
 
+// bt (nullable): bt->n products in one launch, product z = rows [roff, roff + mout) of Rm (Rm
+// holding Mout rows in all) times columns [boff, boff + N) of Bm (Bm holding Nb columns in all),
+// written to C + coff; rows and columns a tile reads past its product are discarded.
 template <int FJ, int FR, int WJ, int WR, int STAGES, int MINB, int RS>
 static cudaError_t launch3t(const double2* Rm, int64_t ldr, const double* Rs, int64_t ldrs,
                             const double2* Bm, int64_t ldb, double2* C, int64_t ldc, int64_t Mout,
-                            int64_t N, int64_t K, cudaStream_t st, int S, double2* partial) {
+                            int64_t N, int64_t K, cudaStream_t st, int S, double2* partial,
+                            const Z3Batch* bt = nullptr, int64_t Nb = 0) {
   using Cf = Z3T<FJ, FR, WJ, WR, STAGES, RS>;
   auto kern = k_zgemm3m_tma<FJ, FR, WJ, WR, STAGES, MINB, RS>;
   static bool attr_set = false;
@@ -214,7 +229,7 @@ static cudaError_t launch3t(const double2* Rm, int64_t ldr, const double* Rs, in
   CUtensorMap mapA, mapR, mapS;
   const cuuint32_t estr[2] = {1u, 1u};
   {
-    const cuuint64_t gdim[2] = {(cuuint64_t)(2 * K), (cuuint64_t)N};
+    const cuuint64_t gdim[2] = {(cuuint64_t)(2 * K), (cuuint64_t)(bt ? Nb : N)};
     const cuuint64_t gstr[1] = {(cuuint64_t)ldb * sizeof(double2)};
     const cuuint32_t box[2] = {16u, (cuuint32_t)Cf::BJ};
     if (encode(&mapA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)Bm, gdim, gstr, box, estr,
@@ -242,6 +257,16 @@ static cudaError_t launch3t(const double2* Rm, int64_t ldr, const double* Rs, in
                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
+  if (bt) {
+    int64_t mmax = 0;
+    for (int z = 0; z < bt->n; ++z) mmax = bt->mout[z] > mmax ? bt->mout[z] : mmax;
+    const int64_t tr = (mmax + Cf::BR - 1) / Cf::BR, tj = (N + Cf::BJ - 1) / Cf::BJ;
+    if (tr < 1 || tj > 65535 || Mout > INT32_MAX / 2 || Nb > INT32_MAX)
+      return cudaErrorInvalidConfiguration;
+    dim3 grid((unsigned)tr, (unsigned)tj, (unsigned)bt->n);
+    kern<<<grid, Cf::kThreads, Cf::kSmem, st>>>(mapA, mapR, mapS, C, ldc, Mout, N, K, K, 0, *bt);
+    return cudaGetLastError();
+  }
   const int64_t tiles_r = (Mout + Cf::BR - 1) / Cf::BR;
   const int64_t tiles_j = (N + Cf::BJ - 1) / Cf::BJ;
   int64_t kc = K > 0 ? K : 1;
@@ -261,7 +286,8 @@ static cudaError_t launch3t(const double2* Rm, int64_t ldr, const double* Rs, in
   }
   if (tiles_r > 65535 || tiles_j > 65535 || S > 65535) return cudaErrorInvalidConfiguration;
   dim3 grid((unsigned)tiles_r, (unsigned)tiles_j, (unsigned)S);
-  kern<<<grid, Cf::kThreads, Cf::kSmem, st>>>(mapA, mapR, mapS, Cout, ldo, Mout, N, K, kc, zs);
+  Z3Batch none{};
+  kern<<<grid, Cf::kThreads, Cf::kSmem, st>>>(mapA, mapR, mapS, Cout, ldo, Mout, N, K, kc, zs, none);
   e = cudaGetLastError();
   if (e != cudaSuccess || S == 1) return e;
   int64_t blocks = (Mout * N + 255) / 256;
@@ -270,13 +296,11 @@ static cudaError_t launch3t(const double2* Rm, int64_t ldr, const double* Rs, in
   return cudaGetLastError();
 }
 
-// The TMA pipeline covers the 48-row tile (C3, C4) and the 40-row tile (C2, C5; with the
-// Re R + Im R plane when one is passed) unless RID_Z3_TMA=0.
+// The TMA pipeline covers all three tiles — 48 rows (C3, C4), 40 (C2, C5; with the Re R + Im R
+// plane when one is passed), 24 (C1) — unless RID_Z3_TMA=0.
 bool zgemm3m_tma_enabled(int64_t Mout) {
   const char* v = getenv("RID_Z3_TMA");
-  if (v && atoi(v) == 0) return false;
-  const int rows = zgemm3m_tile_rows(Mout);
-  return rows == 48 || rows == 40;
+  return !(v && atoi(v) == 0) && Mout > 0;
 }
 
 cudaError_t zgemm3m_tma(const double2* Rm, int64_t ldr, const double* Rs, int64_t ldrs,
@@ -291,12 +315,41 @@ cudaError_t zgemm3m_tma(const double2* Rm, int64_t ldr, const double* Rs, int64_
     if (!Rs) return RID_L3T(1, 5, 8, 1, 3, 2, 0);
     return var == 2 ? RID_L3T(1, 5, 8, 1, 2, 2, 1) : RID_L3T(1, 5, 8, 1, 3, 2, 1);
   }
+  if (zgemm3m_tile_rows(Mout) == 24)
+    return Rs ? RID_L3T(1, 3, 8, 1, 3, 2, 1) : RID_L3T(1, 3, 8, 1, 3, 2, 0);
   switch (var) {
     case 2: return RID_L3T(2, 3, 4, 2, 2, 2, 0);
     case 4: return RID_L3T(2, 3, 4, 2, 4, 2, 0);
     default: return RID_L3T(2, 3, 4, 2, 3, 2, 0);
   }
 #undef RID_L3T
+}
+
+// The SRFT's residue products (k_srft.cu): bt.roff = first row of product z in Rm (Mtot rows in
+// all), bt.boff = ELEMENT offset of its B block in Bm (a multiple of ldb: the block starts at
+// column boff / ldb of the Nb = nblk * N columns), bt.coff / bt.mout as for zgemm3m_batched.
+cudaError_t zgemm3m_tma_batched(const double2* Rm, int64_t ldr, int64_t Mtot, const double2* Bm,
+                                int64_t ldb, int64_t Nb, double2* C, int64_t ldc,
+                                const Z3Batch& bt, int64_t N, int64_t K, cudaStream_t st) {
+  if (bt.n <= 0 || N <= 0) return cudaSuccess;
+  Z3Batch b = bt;
+  for (int z = 0; z < b.n; ++z) {
+    if (b.boff[z] % ldb) return cudaErrorInvalidValue;
+    b.boff[z] /= ldb;
+  }
+  int64_t mmax = 0;
+  for (int z = 0; z < b.n; ++z) mmax = b.mout[z] > mmax ? b.mout[z] : mmax;
+  switch (zgemm3m_tile_rows(mmax)) {
+    case 48:
+      return launch3t<2, 3, 4, 2, 3, 2, 0>(Rm, ldr, nullptr, 0, Bm, ldb, C, ldc, Mtot, N, K, st, 1,
+                                           nullptr, &b, Nb);
+    case 40:
+      return launch3t<1, 5, 8, 1, 3, 2, 0>(Rm, ldr, nullptr, 0, Bm, ldb, C, ldc, Mtot, N, K, st, 1,
+                                           nullptr, &b, Nb);
+    default:  // 24 rows (the residues' l/16 rows at C2, C3)
+      return launch3t<1, 3, 8, 1, 3, 2, 0>(Rm, ldr, nullptr, 0, Bm, ldb, C, ldc, Mtot, N, K, st, 1,
+                                           nullptr, &b, Nb);
+  }
 }
 
 }  // namespace rid

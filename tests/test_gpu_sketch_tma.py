@@ -4,7 +4,7 @@ replaces (k_zgemm3m.cu) and against the oracle, through the C ABI.
 Both kernels evaluate the same ascending fma chains per K slice (reading R31), only the
 operand staging differs (TMA boxes with a 128-byte swizzle and mbarrier hand-over vs cp.async and
 __syncthreads), so Y must be BITWISE equal (RID_Z3_TMA=0 selects the old kernel). The shapes put
-the 48-row tile (the one the TMA kernel covers) under every edge the TMA unit handles by
+each tile height (48, 40 and 24 rows) under every edge the TMA unit handles by
 zero-filling: rows past l (l = 47, 143), K past m (m not a multiple of 16), columns past n, K
 slices (split-K) and the wave-tail split; against the oracle Y holds the north-star bar (1e-12
 relative Frobenius; measured 1e-15 .. 1e-14).
@@ -42,6 +42,8 @@ SHAPES = [  # (seed, m, n, k, l, noise)
     (9, 2048, 1000, 64, 80, 1e-10),      # C2's k/l: the 40-row tile with the Re R + Im R plane
     (10, 4096, 600, 256, 272, 1e-10),    # C5's k/l: 40-row tiles, rows past l in the last one
     (11, 1003, 333, 20, 39, 1e-9),       # 40-row tile, ragged everything
+    (12, 1024, 512, 16, 24, 0.0),        # C1: the 24-row tile
+    (13, 777, 100, 5, 21, 1e-9),         # 24-row tile, ragged
 ]
 
 
@@ -84,3 +86,14 @@ def test_tma_wave_tail_and_shards_bitwise(rid, monkeypatch):
     monkeypatch.setenv("RID_Z3_TMA", "0")
     Y_old = rid.sketch(A, seed, l).cpu().numpy()
     assert np.array_equal(bits(Y), bits(Y_old))
+
+
+@pytest.mark.parametrize("seed,m,n,l", [(1, 4096, 700, 80), (2, 2048, 333, 528), (3, 1024, 64, 47)])
+def test_srft_residue_products_tma_bitwise(rid, monkeypatch, seed, m, n, l):
+    """The SRFT's batched residue products on the TMA kernel equal the cp.async
+    kernel's bit for bit (rows / columns a tile reads past its residue are discarded)."""
+    A = rid.generate(seed, m, n, 8, 1e-9)
+    Y_t = rid.sketch_srft(A, seed, l).cpu().numpy()
+    monkeypatch.setenv("RID_Z3_TMA", "0")
+    Y_o = rid.sketch_srft(A, seed, l).cpu().numpy()
+    assert np.array_equal(bits(Y_t), bits(Y_o))
