@@ -165,6 +165,52 @@ def run_reference(args, cfg):
     return 0
 
 
+# ------------------------------------------------------------------------------ per-row rooflines -
+def row_rooflines(cfg, n_loc, world, gen_s, sketch_s, gather_s, qrcp_s, solve_s, est_s, q,
+                  sketch_exec_tf):
+    """Every SURVEY.md §8(a) row of the slowest rank against the roofline that bounds it
+    (DESIGN.md §5): algorithmic work per call ÷ the measured phase time ÷ the measured peak
+    (DMMA 37.11 TFLOP/s, profiles/r01_box_facts_fp64_microbench.txt; HBM copy from
+    MEASURED_PEAKS.json). Work counts only what the method must do, not what a kernel re-reads."""
+    m, n, k, l = cfg.m, cfg.n, cfg.k, cfg.l
+    hbm = measured_peaks().get("hbm_gbs", 6536.7)
+    P = FP64_DMMA_PEAK_TFLOPS
+
+    def tensor(flops, t, what):
+        a = flops / t / 1e12 if t else None
+        return {"bound": "tensor", "work": what, "seconds": t, "achieved": a, "unit": "TFLOP/s",
+                "peak": P, "frac": a / P if a else None}
+
+    def hbm_row(nbytes, t, what, bound="hbm"):
+        a = nbytes / t / 1e9 if t else None
+        return {"bound": bound, "work": what, "seconds": t, "achieved": a, "unit": "GB/s",
+                "peak": hbm, "frac": a / hbm if a else None}
+
+    rows = {
+        "a1_generate": tensor(8.0 * m * n_loc * k, gen_s,
+                              "8*m*n_loc*k flop (ordered 4-product chain, bit-exact)"),
+        "a2_sketch": {"bound": "tensor", "work": "6*l*m*n_loc flop executed (Gauss 3M)",
+                      "seconds": sketch_s, "achieved": sketch_exec_tf, "unit": "TFLOP/s",
+                      "peak": P, "frac": sketch_exec_tf / P},
+        "a5_solve": tensor(6.0 * k * k * n_loc, solve_s,
+                           "6*k^2*n_loc flop (T = R11^-1 R12, Gauss 3M)"),
+    }
+    if world > 1:
+        rows["a3_allgather"] = {"bound": "nvlink", "work": f"{16 * l * n * (world - 1) / world:.4g}"
+                                " B received per rank", "seconds": gather_s}
+    big = 16 * l * n >= 64 << 20  # the blocked, streaming QR (k_qrcp_ring); else shared-memory
+    qr_bytes = 16.0 * n * (k * l - k * (k - 1) / 2) if big else 32.0 * l * n
+    rows["a4_qrcp"] = hbm_row(qr_bytes, qrcp_s,
+                              "sum_j 16*(l-j)*n B (one read of the trailing block per step)" if big
+                              else "32*l*n B (Y in and out once; k grid-synchronised steps)",
+                              "hbm" if big else "latency")
+    if est_s:
+        rows["a6_estimate"] = hbm_row((2 * q + 1) * 16.0 * m * n_loc, est_s,
+                                      f"(2q+1)*16*m*n_loc B (two passes per iteration, q = {q}, "
+                                      "plus the amax pass)")
+    return rows
+
+
 # ------------------------------------------------------------------------------ our arm ----------
 def run_ours(args, cfg):
     import torch
@@ -327,6 +373,8 @@ def run_ours(args, cfg):
                                      f"flop per launch ({mults} real products per complex "
                                      f"multiply-add; the metric counts 8*l*m*n)"),
                      "peak_source": FP64_PEAK_SOURCE},
+        "rows": row_rooflines(cfg, n_loc, world, gen_s, sketch_s, gather_s, qrcp_s, solve_s,
+                              est_s, args.q, sketch_exec_tf),
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -46,7 +46,10 @@ struct Z3T {
 
 // RS = 1: Re R + Im R comes from a precomputed plane (k_rsum), boxes of 8 rows x BKC K without
 // swizzle (a lane's 8-byte load: rows t of 64 B, two wavefronts per warp, the minimum)
-template <int FJ, int FR, int WJ, int WR, int STAGES, int MINB, int RS>
+// ORD: DMMA issue order within a k-step — 0: (fa, fb, p) with volatile asm; 1: p outermost (the
+// products that need the Re + Im sums come last); 2: (fa, fb, p), non-volatile; 3: p outermost,
+// non-volatile.
+template <int FJ, int FR, int WJ, int WR, int STAGES, int MINB, int RS, int ORD = 0>
 __global__ void __launch_bounds__(WJ* WR * 32, MINB)
     k_zgemm3m_tma(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapR,
                   const __grid_constant__ CUtensorMap mapS, double2* __restrict__ C, int64_t ldc, int64_t Mout, int64_t N, int64_t K,
@@ -160,13 +163,27 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
         b[f][2] = RS ? *reinterpret_cast<const double*>(st + sRow + f * Cf::kRsBox + kk * 256)
                      : __dadd_rn(v.x, v.y);
       }
+      if (ORD == 0 || ORD == 2) {
 #pragma unroll
-      for (int fa = 0; fa < FJ; ++fa)
+        for (int fa = 0; fa < FJ; ++fa)
 #pragma unroll
-        for (int fb = 0; fb < FR; ++fb)
+          for (int fb = 0; fb < FR; ++fb)
 #pragma unroll
-          for (int p = 0; p < 3; ++p)
-            dmma8x8x4(acc[fa][fb][p][0], acc[fa][fb][p][1], a[fa][p], b[fb][p]);
+            for (int p = 0; p < 3; ++p) {
+              if (ORD == 0) dmma8x8x4(acc[fa][fb][p][0], acc[fa][fb][p][1], a[fa][p], b[fb][p]);
+              else dmma8x8x4_nv(acc[fa][fb][p][0], acc[fa][fb][p][1], a[fa][p], b[fb][p]);
+            }
+      } else {
+#pragma unroll
+        for (int p = 0; p < 3; ++p)
+#pragma unroll
+          for (int fa = 0; fa < FJ; ++fa)
+#pragma unroll
+            for (int fb = 0; fb < FR; ++fb) {
+              if (ORD == 1) dmma8x8x4(acc[fa][fb][p][0], acc[fa][fb][p][1], a[fa][p], b[fb][p]);
+              else dmma8x8x4_nv(acc[fa][fb][p][0], acc[fa][fb][p][1], a[fa][p], b[fb][p]);
+            }
+      }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -207,13 +224,13 @@ __global__ void k_splitk_reduce3t(const double2* __restrict__ part, int S, int64
 // bt (nullable): bt->n products in one launch, product z = rows [roff, roff + mout) of Rm (Rm
 // holding Mout rows in all) times columns [boff, boff + N) of Bm (Bm holding Nb columns in all),
 // written to C + coff; rows and columns a tile reads past its product are discarded.
-template <int FJ, int FR, int WJ, int WR, int STAGES, int MINB, int RS>
+template <int FJ, int FR, int WJ, int WR, int STAGES, int MINB, int RS, int ORD = 0>
 static cudaError_t launch3t(const double2* Rm, int64_t ldr, const double* Rs, int64_t ldrs,
                             const double2* Bm, int64_t ldb, double2* C, int64_t ldc, int64_t Mout,
                             int64_t N, int64_t K, cudaStream_t st, int S, double2* partial,
                             const Z3Batch* bt = nullptr, int64_t Nb = 0) {
   using Cf = Z3T<FJ, FR, WJ, WR, STAGES, RS>;
-  auto kern = k_zgemm3m_tma<FJ, FR, WJ, WR, STAGES, MINB, RS>;
+  auto kern = k_zgemm3m_tma<FJ, FR, WJ, WR, STAGES, MINB, RS, ORD>;
   static bool attr_set = false;
   cudaError_t e;
   if (!attr_set) {
@@ -313,13 +330,22 @@ cudaError_t zgemm3m_tma(const double2* Rm, int64_t ldr, const double* Rs, int64_
   if (const char* v = getenv("RID_Z3T_VARIANT")) var = atoi(v);  // pipeline-depth experiments
   if (zgemm3m_tile_rows(Mout) == 40) {
     if (!Rs) return RID_L3T(1, 5, 8, 1, 3, 2, 0);
-    return var == 2 ? RID_L3T(1, 5, 8, 1, 2, 2, 1) : RID_L3T(1, 5, 8, 1, 3, 2, 1);
+    switch (var) {
+      case 2: return RID_L3T(1, 5, 8, 1, 2, 2, 1);
+      case 11: return RID_L3T(1, 5, 8, 1, 3, 2, 1, 1);
+      case 12: return RID_L3T(1, 5, 8, 1, 3, 2, 1, 2);
+      case 13: return RID_L3T(1, 5, 8, 1, 3, 2, 1, 3);
+      default: return RID_L3T(1, 5, 8, 1, 3, 2, 1);
+    }
   }
   if (zgemm3m_tile_rows(Mout) == 24)
     return Rs ? RID_L3T(1, 3, 8, 1, 3, 2, 1) : RID_L3T(1, 3, 8, 1, 3, 2, 0);
   switch (var) {
     case 2: return RID_L3T(2, 3, 4, 2, 2, 2, 0);
     case 4: return RID_L3T(2, 3, 4, 2, 4, 2, 0);
+    case 11: return RID_L3T(2, 3, 4, 2, 3, 2, 0, 1);
+    case 12: return RID_L3T(2, 3, 4, 2, 3, 2, 0, 2);
+    case 13: return RID_L3T(2, 3, 4, 2, 3, 2, 0, 3);
     default: return RID_L3T(2, 3, 4, 2, 3, 2, 0);
   }
 #undef RID_L3T

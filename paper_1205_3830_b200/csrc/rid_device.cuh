@@ -123,6 +123,15 @@ __device__ __forceinline__ void dmma8x8x4(double& c0, double& c1, double a, doub
                : "d"(a), "d"(b));
 }
 
+// The same instruction without `volatile`: the compiler may schedule it against the fragment
+// loads and adds (each accumulator's chain order is fixed by its data dependence, so the results
+// are unchanged).
+__device__ __forceinline__ void dmma8x8x4_nv(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
 // ---------------------------------------------------------------- cp.async helpers -------------
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool pred) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
