@@ -345,7 +345,11 @@ cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int
   // QRCP trailing update (mode 2, K = nb <= 16): latency-bound read-modify-write of C, so small
   // register-light CTAs, 2 stages, 3 per SM keep more tiles in flight (measured at C4: update total
   // 2.95 -> 2.36 ms against the sketch tiles; 64-row/4-per-SM 2.55, 32x64/3-per-SM 2.76 ms)
-  if (mode == 2) return launch_cfg<1, 8, 8, 1, 16, 2, 3>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
+  if (mode == 2) {
+    if (zgemm_tma_enabled() && getenv("RID_ZGEMM_TMA_UPDATE"))
+      return zgemm_tma_ordered(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, mode, noise, seed, col0, st);
+    return launch_cfg<1, 8, 8, 1, 16, 2, 3>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
+  }
   if (const char* v = getenv("RID_ZGEMM_VARIANT")) {  // tile experiments (tools/tune_*.py)
     const int id = atoi(v);
 #define RID_V(ID, ...) \
@@ -368,8 +372,11 @@ cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int
                                                    ksplit, partial);
     }
   }
-  if (Mout >= 2048)
+  if (Mout >= 2048) {  // generation (and any tall product); RID_ZGEMM_TMA=1: the TMA-fed kernel
+    if (zgemm_tma_enabled())
+      return zgemm_tma_ordered(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, mode, noise, seed, col0, st);
     return launch_cfg<1, 8, 8, 1, 16, 3, 3>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
+  }
   switch (zgemm_pick_fr(Mout)) {
 #define RID_CASE_A(FRV)                                                                        \
   case FRV:                                                                                    \

@@ -15,6 +15,14 @@ cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int
                           double noise, uint64_t seed, int64_t col0, cudaStream_t st,
                           int ksplit = 1, double2* partial = nullptr);
 int zgemm_pick_fr(int64_t Mout);
+// The same ordered product with TMA-fed, mbarrier-pipelined stages (k_zgemm_tma.cu; bit-identical
+// chains), used by zgemm_ordered for tall products (Mout >= 2048: the generation) when
+// RID_ZGEMM_TMA=1 (measured no faster; see k_zgemm_tma.cu).
+bool zgemm_tma_enabled();
+cudaError_t zgemm_tma_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int64_t ldb,
+                              double2* C, int64_t ldc, int64_t Mout, int64_t N, int64_t K,
+                              int mode, double noise, uint64_t seed, int64_t col0,
+                              cudaStream_t st);
 // The sketch as three real products (Gauss), 6·l·m·n flops (k_zgemm3m.cu); split-K as above.
 // Rs = Re R + Im R (l x m doubles, leading dimension rsum_ld(l), pad rows zero) from rsum_fill;
 // Rs == nullptr selects tiles that form the sums in registers.

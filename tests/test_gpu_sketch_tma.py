@@ -97,3 +97,30 @@ def test_srft_residue_products_tma_bitwise(rid, monkeypatch, seed, m, n, l):
     monkeypatch.setenv("RID_Z3_TMA", "0")
     Y_o = rid.sketch_srft(A, seed, l).cpu().numpy()
     assert np.array_equal(bits(Y_t), bits(Y_o))
+
+
+@pytest.mark.parametrize("seed,m,n,k,noise", [(1, 2048, 300, 64, 1e-10), (2, 4099, 77, 13, 1e-8),
+                                               (3, 2500, 1000, 512, 0.0), (4, 8192, 64, 1, 1e-6)])
+def test_generation_tma_bitwise(rid, orc, monkeypatch, seed, m, n, k, noise):
+    """The TMA-fed ordered GEMM (k_zgemm_tma.cu, RID_ZGEMM_TMA=1) generates A = X·Y0 + ε·E bit for
+    bit like the cp.async kernel (the default) and the oracle's ascending fma chains (RNG.md §5)."""
+    monkeypatch.setenv("RID_ZGEMM_TMA", "1")
+    A_t = rid.generate(seed, m, n, k, noise).cpu().numpy()
+    monkeypatch.setenv("RID_ZGEMM_TMA", "0")
+    A_c = rid.generate(seed, m, n, k, noise).cpu().numpy()
+    assert np.array_equal(bits(A_t), bits(A_c))
+    if m * n <= 2048 * 300:
+        assert np.array_equal(bits(A_t), bits(orc.generate(seed, m, n, k, noise)))
+
+
+def test_qr_update_tma_bitwise(rid, monkeypatch):
+    """The QR's panel update on the TMA kernel (RID_ZGEMM_TMA_UPDATE=1) leaves J and P bitwise
+    unchanged (a C4-shaped sketch, reduced: the blocked QR path)."""
+    monkeypatch.setenv("RID_QRCP_VARIANT", "1")
+    A = rid.generate(5, 2048, 3000, 256, 1e-9)
+    r0 = rid.decompose(A, 256, 272, 5)
+    monkeypatch.setenv("RID_ZGEMM_TMA", "1")
+    monkeypatch.setenv("RID_ZGEMM_TMA_UPDATE", "1")
+    r1 = rid.decompose(A, 256, 272, 5)
+    assert torch.equal(r0.J, r1.J)
+    assert np.array_equal(bits(r0.P.cpu().numpy()), bits(r1.P.cpu().numpy()))
