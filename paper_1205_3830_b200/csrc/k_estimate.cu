@@ -445,6 +445,7 @@ __global__ void __launch_bounds__(256, 2)
         const double2 xv = *reinterpret_cast<const double2*>(st + kEstBoxA + cc * 16);
         cfdd_mac(acc[c], av, xv, false);
       }
+      fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
@@ -526,6 +527,7 @@ __global__ void __launch_bounds__(256, 2)
         const double2 yv = *reinterpret_cast<const double2*>(st + kEstBoxA + rr * 16);
         cfdd_mac(acc[u], av, yv, true);
       }
+      fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }

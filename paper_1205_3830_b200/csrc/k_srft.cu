@@ -202,11 +202,53 @@ cudaError_t srft_sketch(uint64_t seed, bool retry, int64_t l, const double2* A, 
         ++bt.n;
       }
       const char* v = getenv("RID_Z3_TMA");
-      e = (v && atoi(v) == 0) ? zgemm3m_batched(Wg, l, Z, m1, Yg, l, bt, nc, m1, st)
-                              : zgemm3m_tma_batched(Wg, l, l, Z, m1, kSrftR * nc, Yg, l, bt, nc,
-                                                    m1, st);
-      if (e != cudaSuccess) return e;
-      *launches += 1;
+      if (v && atoi(v) == 0) {
+        e = zgemm3m_batched(Wg, l, Z, m1, Yg, l, bt, nc, m1, st);
+        if (e != cudaSuccess) return e;
+        *launches += 1;
+      } else {
+        // each residue's l_r rows cut into 48-, 40- and 24-row tiles with the fewest padded rows
+        // (l_r ~ l/16 ± 25%: one fixed height pads 20-30% of the residue products), one batched
+        // launch per tile height
+        Z3Batch bh[3] = {};
+        const int hts[3] = {48, 40, 24};
+        for (int z = 0; z < bt.n; ++z) {
+          const int64_t lr = bt.mout[z];
+          int64_t best = INT64_MAX;
+          int cnt[3] = {0, 0, 0};
+          for (int a3 = 0; a3 <= (int)((lr + 47) / 48); ++a3)
+            for (int b3 = 0; b3 <= 2; ++b3)
+              for (int c3 = 0; c3 <= 2; ++c3) {
+                const int64_t cover = 48 * a3 + 40 * b3 + 24 * c3;
+                if (cover < lr) continue;
+                const int64_t cost = (cover - lr) * 16 + a3 + b3 + c3;  // padding, then tiles
+                if (cost < best) {
+                  best = cost;
+                  cnt[0] = a3;
+                  cnt[1] = b3;
+                  cnt[2] = c3;
+                }
+              }
+          int64_t row = 0;
+          for (int h = 0; h < 3 && row < lr; ++h) {
+            if (cnt[h] == 0) continue;
+            const int64_t rows = (lr - row < (int64_t)cnt[h] * hts[h]) ? lr - row : (int64_t)cnt[h] * hts[h];
+            Z3Batch& q = bh[h];
+            q.roff[q.n] = bt.roff[z] + row;
+            q.boff[q.n] = bt.boff[z];
+            q.coff[q.n] = bt.coff[z] + row;
+            q.mout[q.n] = rows;
+            ++q.n;
+            row += rows;
+          }
+        }
+        for (int h = 0; h < 3; ++h) {
+          if (bh[h].n == 0) continue;
+          e = zgemm3m_tma_batched_h(Wg, l, l, Z, m1, kSrftR * nc, Yg, l, bh[h], nc, m1, hts[h], st);
+          if (e != cudaSuccess) return e;
+          *launches += 1;
+        }
+      }
     } else {
       for (int r = 0; r < kSrftR; ++r) {
         const int64_t lr = hoffs[r + 1] - hoffs[r];

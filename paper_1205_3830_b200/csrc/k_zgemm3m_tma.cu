@@ -185,6 +185,7 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
             }
       }
     }
+    fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
@@ -357,6 +358,14 @@ cudaError_t zgemm3m_tma(const double2* Rm, int64_t ldr, const double* Rs, int64_
 cudaError_t zgemm3m_tma_batched(const double2* Rm, int64_t ldr, int64_t Mtot, const double2* Bm,
                                 int64_t ldb, int64_t Nb, double2* C, int64_t ldc,
                                 const Z3Batch& bt, int64_t N, int64_t K, cudaStream_t st) {
+  return zgemm3m_tma_batched_h(Rm, ldr, Mtot, Bm, ldb, Nb, C, ldc, bt, N, K, 0, st);
+}
+
+// rows = 48 / 40 / 24 forces the tile height; 0 picks it from the largest product
+cudaError_t zgemm3m_tma_batched_h(const double2* Rm, int64_t ldr, int64_t Mtot, const double2* Bm,
+                                  int64_t ldb, int64_t Nb, double2* C, int64_t ldc,
+                                  const Z3Batch& bt, int64_t N, int64_t K, int rows,
+                                  cudaStream_t st) {
   if (bt.n <= 0 || N <= 0) return cudaSuccess;
   Z3Batch b = bt;
   for (int z = 0; z < b.n; ++z) {
@@ -365,7 +374,7 @@ cudaError_t zgemm3m_tma_batched(const double2* Rm, int64_t ldr, int64_t Mtot, co
   }
   int64_t mmax = 0;
   for (int z = 0; z < b.n; ++z) mmax = b.mout[z] > mmax ? b.mout[z] : mmax;
-  switch (zgemm3m_tile_rows(mmax)) {
+  switch (rows ? rows : zgemm3m_tile_rows(mmax)) {
     case 48:
       return launch3t<2, 3, 4, 2, 3, 2, 0>(Rm, ldr, nullptr, 0, Bm, ldb, C, ldc, Mtot, N, K, st, 1,
                                            nullptr, &b, Nb);

@@ -139,6 +139,7 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
 #pragma unroll
         for (int fb = 0; fb < FR; ++fb) dmma8x8x4(acc[fa][fb][0], acc[fa][fb][1], a[fa], b[fb]);
     }
+    fence_proxy_async_smem();
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }

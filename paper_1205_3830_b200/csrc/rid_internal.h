@@ -51,6 +51,10 @@ cudaError_t zgemm3m_batched(const double2* Rm, int64_t ldr, const double2* Bm, i
 cudaError_t zgemm3m_tma_batched(const double2* Rm, int64_t ldr, int64_t Mtot, const double2* Bm,
                                 int64_t ldb, int64_t Nb, double2* C, int64_t ldc,
                                 const Z3Batch& bt, int64_t N, int64_t K, cudaStream_t st);
+cudaError_t zgemm3m_tma_batched_h(const double2* Rm, int64_t ldr, int64_t Mtot, const double2* Bm,
+                                  int64_t ldb, int64_t Nb, double2* C, int64_t ldc,
+                                  const Z3Batch& bt, int64_t N, int64_t K, int rows,
+                                  cudaStream_t st);
 inline int64_t rsum_ld(int64_t l) { return (l + 1) / 2 * 2; }
 cudaError_t rsum_fill(const double2* R, int64_t l, int64_t m, int64_t ldr, double* Rs,
                       int64_t ldrs, cudaStream_t st);

@@ -24,6 +24,13 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
                "r"(bytes)
                : "memory");
 }
+// Order this thread's generic-proxy accesses to shared memory (the LDS of a consumed stage)
+// before later async-proxy (TMA) writes to the same bytes: every consumer thread executes it
+// before its warp releases a ring slot (WAR across proxies; without it a refill was measured to
+// land under a lagging warp's reads, rarely: 1 in ~6 runs of one generation shape).
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(b)) : "memory");
 }
