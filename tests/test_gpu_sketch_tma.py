@@ -124,3 +124,16 @@ def test_qr_update_tma_bitwise(rid, monkeypatch):
     r1 = rid.decompose(A, 256, 272, 5)
     assert torch.equal(r0.J, r1.J)
     assert np.array_equal(bits(r0.P.cpu().numpy()), bits(r1.P.cpu().numpy()))
+
+
+def test_tma_rings_repeatable(rid, monkeypatch):
+    """Run-to-run bitwise repeatability of the TMA rings (a slot refilled under a lagging warp's
+    reads would show as a changed block in some run): sketch and, opt-in, the ordered GEMM."""
+    A = rid.generate(3, 2500, 1000, 64, 1e-9)
+    Y0 = bits(rid.sketch(A, 3, 528).cpu().numpy())
+    for _ in range(8):
+        assert np.array_equal(bits(rid.sketch(A, 3, 528).cpu().numpy()), Y0)
+    monkeypatch.setenv("RID_ZGEMM_TMA", "1")
+    G0 = bits(rid.generate(3, 2500, 1000, 512, 0.0).cpu().numpy())
+    for _ in range(8):
+        assert np.array_equal(bits(rid.generate(3, 2500, 1000, 512, 0.0).cpu().numpy()), G0)
