@@ -16,6 +16,7 @@ VARIANTS = [("cp.async", {"RID_Z3_TMA": "0"}), ("tma3", {"RID_Z3_TMA": "1"}),
 if os.environ.get("ORDER_VARIANTS"):
     VARIANTS = [("tma3", {"RID_Z3_TMA": "1"})] + [
         (f"ord{v}", {"RID_Z3_TMA": "1", "RID_Z3T_VARIANT": str(v)}) for v in (11, 12, 13)]
+
 names = sys.argv[1:] or ["C4"]
 for name in names:
     c = CONFIGS[name]
