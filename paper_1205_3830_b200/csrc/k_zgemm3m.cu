@@ -320,6 +320,10 @@ static cudaError_t launch3_batched(const double2* Rm, int64_t ldr, const double2
 //   id 2: 24 rows (1 x 3) x 64 columns, as id 1                          C1 (24)
 static int pick3(int64_t Mout) {
   const int rows[3] = {48, 40, 24};
+  if (const char* v = getenv("RID_Z3_ROWS")) {  // tile-height experiments (tools/tma_sketch_time.py)
+    for (int i = 0; i < 3; ++i)
+      if (atoi(v) == rows[i]) return i;
+  }
   int best = 0;
   int64_t bw = INT64_MAX, br = 0;
   for (int i = 0; i < 3; ++i) {

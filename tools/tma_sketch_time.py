@@ -17,6 +17,9 @@ if os.environ.get("ORDER_VARIANTS"):
     VARIANTS = [("tma3", {"RID_Z3_TMA": "1"})] + [
         (f"ord{v}", {"RID_Z3_TMA": "1", "RID_Z3T_VARIANT": str(v)}) for v in (11, 12, 13)]
 
+if os.environ.get("ROWS_VARIANTS"):
+    VARIANTS = [("rows40", {"RID_Z3_TMA": "1", "RID_Z3_ROWS": "40"}),
+                ("rows48", {"RID_Z3_TMA": "1", "RID_Z3_ROWS": "48"})]
 names = sys.argv[1:] or ["C4"]
 for name in names:
     c = CONFIGS[name]
@@ -24,7 +27,7 @@ for name in names:
     Y = rid.colmajor_empty(c.l, c.n, device="cuda")
     reps = 5 if c.m * c.n >= 1 << 28 else 20
     for label, env in VARIANTS:
-        for key in ("RID_Z3_TMA", "RID_Z3T_VARIANT"):
+        for key in ("RID_Z3_TMA", "RID_Z3T_VARIANT", "RID_Z3_ROWS"):
             os.environ.pop(key, None)
         os.environ.update(env)
         for _ in range(2):
