@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(256, 2)
              const unsigned long long* __restrict__ bounds, double* __restrict__ part) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t full[kEstNS], empty[kEstNS];
-  __shared__ double4 shalf[128][2];
+  __shared__ double4 shalf[128];  // the h = 1 half's accumulators, merged by h = 0
   constexpr int kStage = kEstBoxA + 128;
   const int tid = threadIdx.x, lane = tid & 31, r = tid & 127, h = tid >> 7;
   if (tid == 0) {
@@ -452,10 +452,10 @@ __global__ void __launch_bounds__(256, 2)
     cdd a = cfdd_value(acc[0], C);
 #pragma unroll
     for (int c = 1; c < 4; ++c) cdd_merge(a, cfdd_value(acc[c], C));
-    if (h == 1) shalf[r][0] = make_double4(a.re.s, a.re.c, a.im.s, a.im.c);
+    if (h == 1) shalf[r] = make_double4(a.re.s, a.re.c, a.im.s, a.im.c);
     __syncthreads();
     if (h == 0) {
-      const double4 o = shalf[r][0];
+      const double4 o = shalf[r];
       cdd b2;
       b2.re = {o.x, o.y};
       b2.im = {o.z, o.w};

@@ -1438,8 +1438,89 @@ __global__ void k_tri_inverse(const double2* __restrict__ R11, int k, double2* _
     Rinv[(int64_t)c * k + i] = (i <= c) ? bvec[i] : make_double2(0.0, 0.0);
 }
 
+// The same back-substitutions with one WARP per column of R11^{-1} and the right-hand side in
+// registers (lane L holds rows L, L + 32, ...): no CTA barrier per step, and the next step's column
+// of R11 is loaded into registers while the current step computes, so a step costs a division, a
+// shuffle and the fmas instead of two __syncthreads and an exposed L2 load. Every element sees the
+// same fma sequence in the same order as k_tri_inverse: bit-identical (tested).
+template <int NSLOT>
+__global__ void __launch_bounds__(256) k_tri_inverse_warp(const double2* __restrict__ R11, int k,
+                                                          double2* __restrict__ Rinv) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (c >= k) return;  // warp-uniform
+  double2 b[NSLOT], rcur[NSLOT], rnext[NSLOT];
+#pragma unroll
+  for (int q = 0; q < NSLOT; ++q) {
+    b[q] = make_double2((32 * q + lane == c) ? 1.0 : 0.0, 0.0);
+    rcur[q] = make_double2(0.0, 0.0);
+    rnext[q] = make_double2(0.0, 0.0);
+  }
+  // column c of R11 (rows above the diagonal) and its diagonal: the first step's operands
+  double dcur = __ldg(&R11[(int64_t)c * k + c].x);
+#pragma unroll
+  for (int q = 0; q < NSLOT; ++q) {
+    const int i = 32 * q + lane;
+    if (i < c) rcur[q] = __ldg(R11 + (int64_t)c * k + i);
+  }
+#pragma unroll
+  for (int q = NSLOT - 1; q >= 0; --q) {
+    if (32 * q > c) continue;
+    for (int p = (c - 32 * q < 31 ? c - 32 * q : 31); p >= 0; --p) {
+      const int s = 32 * q + p;
+      // prefetch column s - 1 (rows < s - 1) and its diagonal
+      double dnext = 1.0;
+      if (s > 0) {
+        dnext = __ldg(&R11[(int64_t)(s - 1) * k + (s - 1)].x);
+#pragma unroll
+        for (int qq = 0; qq <= q; ++qq) {
+          const int i = 32 * qq + lane;
+          rnext[qq] = (i < s - 1) ? __ldg(R11 + (int64_t)(s - 1) * k + i) : make_double2(0.0, 0.0);
+        }
+      }
+      const double2 bs = make_double2(__shfl_sync(0xffffffffu, b[q].x, p),
+                                       __shfl_sync(0xffffffffu, b[q].y, p));
+      const double2 xs = make_double2(__ddiv_rn(bs.x, dcur), __ddiv_rn(bs.y, dcur));
+#pragma unroll
+      for (int qq = 0; qq < q; ++qq) {
+        const double2 r = rcur[qq];
+        double2 bi = b[qq];
+        bi.x = __fma_rn(-r.x, xs.x, __fma_rn(r.y, xs.y, bi.x));
+        bi.y = __fma_rn(-r.x, xs.y, __fma_rn(-r.y, xs.x, bi.y));
+        b[qq] = bi;
+      }
+      if (lane < p) {
+        const double2 r = rcur[q];
+        double2 bi = b[q];
+        bi.x = __fma_rn(-r.x, xs.x, __fma_rn(r.y, xs.y, bi.x));
+        bi.y = __fma_rn(-r.x, xs.y, __fma_rn(-r.y, xs.x, bi.y));
+        b[q] = bi;
+      } else if (lane == p) {
+        b[q] = xs;
+      }
+#pragma unroll
+      for (int qq = 0; qq <= q; ++qq) rcur[qq] = rnext[qq];
+      dcur = dnext;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < NSLOT; ++q) {
+    const int i = 32 * q + lane;
+    if (i < k) Rinv[(int64_t)c * k + i] = (i <= c) ? b[q] : make_double2(0.0, 0.0);
+  }
+}
+
 cudaError_t tri_inverse(const double2* R11, int64_t k, double2* Rinv, cudaStream_t st) {
   if (k <= 0) return cudaSuccess;
+  const char* old = getenv("RID_TRI_OLD");
+  if (!(old && atoi(old) != 0) && k <= 512) {  // k > 512: 32+ slots per lane would spill
+    const unsigned g = (unsigned)((k + 7) / 8);
+    if (k <= 64) k_tri_inverse_warp<2><<<g, 256, 0, st>>>(R11, (int)k, Rinv);
+    else if (k <= 128) k_tri_inverse_warp<4><<<g, 256, 0, st>>>(R11, (int)k, Rinv);
+    else if (k <= 256) k_tri_inverse_warp<8><<<g, 256, 0, st>>>(R11, (int)k, Rinv);
+    else k_tri_inverse_warp<16><<<g, 256, 0, st>>>(R11, (int)k, Rinv);
+    return cudaGetLastError();
+  }
   const size_t sm = (size_t)k * sizeof(double2);
   if (sm > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_tri_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -115,3 +115,18 @@ def test_estimator_tma_matches_register_passes(rid, monkeypatch, seed, m, n, k, 
     e_r = rid.error_estimate(A, r.J, r.P, 6, seed)
     nA = rid.error_estimate(A, r.J, torch.zeros_like(r.P), 30, seed)  # ~||A||_2 (P = 0, B unused)
     assert abs(e_t - e_r) <= 1e-13 * nA, (e_t, e_r, nA)
+
+
+@pytest.mark.parametrize("seed,m,n,k,l", [(1, 1024, 512, 16, 24), (2, 2048, 700, 100, 116),
+                                          (3, 1500, 900, 256, 272), (4, 2048, 1200, 512, 528),
+                                          (5, 1300, 800, 600, 616)])
+def test_tri_inverse_warp_kernel_bitwise(rid, monkeypatch, seed, m, n, k, l):
+    """R11^-1 by one warp per column (registers, prefetched columns) gives the same bits as the
+    CTA-per-column back-substitution (RID_TRI_OLD=1): P is bitwise equal (k > 512 uses the latter)."""
+    A = rid.generate(seed, m, n, k, 1e-9)
+    r_new = rid.decompose(A, k, l, seed)
+    monkeypatch.setenv("RID_TRI_OLD", "1")
+    r_old = rid.decompose(A, k, l, seed)
+    assert torch.equal(r_new.J, r_old.J)
+    assert np.array_equal(np.ascontiguousarray(r_new.P.cpu().numpy()).view(np.uint64),
+                          np.ascontiguousarray(r_old.P.cpu().numpy()).view(np.uint64))
