@@ -327,7 +327,7 @@ cudaError_t zgemm3m_tma(const double2* Rm, int64_t ldr, const double* Rs, int64_
   if (Mout <= 0 || N <= 0) return cudaSuccess;
 #define RID_L3T(...) \
   launch3t<__VA_ARGS__>(Rm, ldr, Rs, ldrs, Bm, ldb, C, ldc, Mout, N, K, st, ksplit, partial)
-  int var = 3;
+  int var = 0;
   if (const char* v = getenv("RID_Z3T_VARIANT")) var = atoi(v);  // pipeline-depth experiments
   if (zgemm3m_tile_rows(Mout) == 40) {
     if (!Rs) return RID_L3T(1, 5, 8, 1, 3, 2, 0);
@@ -341,14 +341,19 @@ cudaError_t zgemm3m_tma(const double2* Rm, int64_t ldr, const double* Rs, int64_
   }
   if (zgemm3m_tile_rows(Mout) == 24)
     return Rs ? RID_L3T(1, 3, 8, 1, 3, 2, 1) : RID_L3T(1, 3, 8, 1, 3, 2, 0);
+  // 48 rows: with the Re R + Im R plane (3 of the 5 adds per k-step gone from the FP64 pipe the
+  // DMMAs share) and 2 stages: C4 103.0 -> 100.5 ms (3 stages 101.3); sums in registers otherwise
   switch (var) {
     case 2: return RID_L3T(2, 3, 4, 2, 2, 2, 0);
+    case 3: return RID_L3T(2, 3, 4, 2, 3, 2, 0);
     case 4: return RID_L3T(2, 3, 4, 2, 4, 2, 0);
+    case 30: if (Rs) return RID_L3T(2, 3, 4, 2, 3, 2, 1); break;
     case 11: return RID_L3T(2, 3, 4, 2, 3, 2, 0, 1);
     case 12: return RID_L3T(2, 3, 4, 2, 3, 2, 0, 2);
     case 13: return RID_L3T(2, 3, 4, 2, 3, 2, 0, 3);
-    default: return RID_L3T(2, 3, 4, 2, 3, 2, 0);
+    default: break;
   }
+  return Rs ? RID_L3T(2, 3, 4, 2, 2, 2, 1) : RID_L3T(2, 3, 4, 2, 3, 2, 0);
 #undef RID_L3T
 }
 

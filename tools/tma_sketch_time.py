@@ -17,6 +17,10 @@ if os.environ.get("ORDER_VARIANTS"):
     VARIANTS = [("tma3", {"RID_Z3_TMA": "1"})] + [
         (f"ord{v}", {"RID_Z3_TMA": "1", "RID_Z3T_VARIANT": str(v)}) for v in (11, 12, 13)]
 
+if os.environ.get("RS_VARIANTS"):  # 48-row tiles: sums in registers (3 stages) vs the Rs plane
+    VARIANTS = [("regs3", {"RID_Z3_TMA": "1", "RID_Z3T_VARIANT": "3"}),
+                ("rs3", {"RID_Z3_TMA": "1", "RID_Z3T_VARIANT": "30"}),
+                ("rs2", {"RID_Z3_TMA": "1"})]
 if os.environ.get("ROWS_VARIANTS"):
     VARIANTS = [("rows40", {"RID_Z3_TMA": "1", "RID_Z3_ROWS": "40"}),
                 ("rows48", {"RID_Z3_TMA": "1", "RID_Z3_ROWS": "48"})]
