@@ -70,6 +70,34 @@ __global__ void k_srft_wgen(const int64_t* __restrict__ samples, const int* __re
   }
 }
 
+// Ws(prow(k'), i1) = Re Wg(k', i1) + Im Wg(k', i1) with each residue group starting on an even
+// row (ps[r] = sum of the earlier groups' sizes rounded up to even; pad rows zero): the 3M
+// kernel's non-swizzled TMA boxes of the plane must start on a 16-byte boundary.
+__global__ void k_srft_wsum(const double2* __restrict__ Wg, int64_t l, int64_t m1,
+                            const int* __restrict__ offs, double* __restrict__ Ws, int64_t ldws) {
+  __shared__ int so[kSrftR + 1], sp[kSrftR + 1];
+  if (threadIdx.x == 0) {
+    sp[0] = 0;
+    for (int r = 0; r <= kSrftR; ++r) so[r] = offs[r];
+    for (int r = 0; r < kSrftR; ++r) sp[r + 1] = sp[r] + ((so[r + 1] - so[r] + 1) & ~1);
+  }
+  __syncthreads();
+  const int64_t total = ldws * m1;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i1 = q / ldws, pr = q % ldws;
+    int r = 0;
+    while (r < kSrftR - 1 && pr >= sp[r + 1]) ++r;
+    const int64_t kk = so[r] + (pr - sp[r]);
+    double v = 0.0;
+    if (pr < sp[kSrftR] && kk < so[r + 1]) {
+      const double2 w = Wg[i1 * l + kk];
+      v = __dadd_rn(w.x, w.y);
+    }
+    Ws[q] = v;
+  }
+}
+
 // complex helpers
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(__fma_rn(a.x, b.x, -__dmul_rn(a.y, b.y)), __fma_rn(a.x, b.y, __dmul_rn(a.y, b.x)));
@@ -146,7 +174,8 @@ size_t srft_work_bytes(int64_t m, int64_t l, int64_t n_loc) {
   const int64_t m1 = m / kSrftR, ch = srft_chunk_cols(m, n_loc);
   return sizeof(double2) * ((size_t)m + (size_t)l * m1 + (size_t)kSrftR * m1 * ch +
                             (size_t)l * ch) +
-         sizeof(int64_t) * (size_t)l + sizeof(int) * ((size_t)l + kSrftR + 1) + 2048;
+         sizeof(double) * (size_t)(rsum_ld(l) + kSrftR) * m1 +  // Re Wg + Im Wg, padded
+         sizeof(int64_t) * (size_t)l + sizeof(int) * ((size_t)l + kSrftR + 1) + 2304;
 }
 
 cudaError_t srft_sketch(uint64_t seed, bool retry, int64_t l, const double2* A, int64_t m,
@@ -164,6 +193,8 @@ cudaError_t srft_sketch(uint64_t seed, bool retry, int64_t l, const double2* A, 
   };
   double2* d = (double2*)take(sizeof(double2) * m);
   double2* Wg = (double2*)take(sizeof(double2) * l * m1);
+  const int64_t ldws = rsum_ld(l) + kSrftR;  // >= every padded group layout, even
+  double* Wgs = (double*)take(sizeof(double) * ldws * m1);  // Re Wg + Im Wg (3M sums)
   double2* Z = (double2*)take(sizeof(double2) * kSrftR * m1 * ch);
   double2* Yg = (double2*)take(sizeof(double2) * l * ch);
   int64_t* samples = (int64_t*)take(sizeof(int64_t) * l);
@@ -177,6 +208,11 @@ cudaError_t srft_sketch(uint64_t seed, bool retry, int64_t l, const double2* A, 
   int64_t wb = (l * m1 + 255) / 256;
   if (wb > 8192) wb = 8192;
   k_srft_wgen<<<(unsigned)wb, 256, 0, st>>>(samples, order, l, m, m1, Wg);
+  {
+    int64_t sb = (ldws * m1 + 255) / 256;
+    if (sb > 8192) sb = 8192;
+    k_srft_wsum<<<(unsigned)sb, 256, 0, st>>>(Wg, l, m1, offs, Wgs, ldws);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   int hoffs[kSrftR + 1];
@@ -184,7 +220,7 @@ cudaError_t srft_sketch(uint64_t seed, bool retry, int64_t l, const double2* A, 
   if (e != cudaSuccess) return e;
   e = cudaStreamSynchronize(st);
   if (e != cudaSuccess) return e;
-  *launches += 3;
+  *launches += 4;
   for (int64_t c0 = 0; c0 < n_loc; c0 += ch) {
     const int64_t nc = (c0 + ch <= n_loc) ? ch : n_loc - c0;
     dim3 g1((unsigned)((m1 + 127) / 128), (unsigned)nc);
@@ -212,6 +248,12 @@ cudaError_t srft_sketch(uint64_t seed, bool retry, int64_t l, const double2* A, 
         // launch per tile height
         Z3Batch bh[3] = {};
         const int hts[3] = {48, 40, 24};
+        int64_t ps[kSrftR + 1];  // even-padded group starts in Wgs (k_srft_wsum)
+        ps[0] = 0;
+        for (int r = 0; r < kSrftR; ++r) ps[r + 1] = ps[r] + ((hoffs[r + 1] - hoffs[r] + 1) & ~1);
+        int zr[kZ3BatchMax];  // residue of item z of bt
+        for (int r = 0, z = 0; r < kSrftR; ++r)
+          if (hoffs[r + 1] > hoffs[r]) zr[z++] = r;
         for (int z = 0; z < bt.n; ++z) {
           const int64_t lr = bt.mout[z];
           int64_t best = INT64_MAX;
@@ -235,6 +277,7 @@ cudaError_t srft_sketch(uint64_t seed, bool retry, int64_t l, const double2* A, 
             const int64_t rows = (lr - row < (int64_t)cnt[h] * hts[h]) ? lr - row : (int64_t)cnt[h] * hts[h];
             Z3Batch& q = bh[h];
             q.roff[q.n] = bt.roff[z] + row;
+            q.soff[q.n] = ps[zr[z]] + row;  // row is a multiple of 48 / 40 / 24: even
             q.boff[q.n] = bt.boff[z];
             q.coff[q.n] = bt.coff[z] + row;
             q.mout[q.n] = rows;
@@ -244,7 +287,8 @@ cudaError_t srft_sketch(uint64_t seed, bool retry, int64_t l, const double2* A, 
         }
         for (int h = 0; h < 3; ++h) {
           if (bh[h].n == 0) continue;
-          e = zgemm3m_tma_batched_h(Wg, l, l, Z, m1, kSrftR * nc, Yg, l, bh[h], nc, m1, hts[h], st);
+          e = zgemm3m_tma_batched_h(Wg, l, l, Z, m1, kSrftR * nc, Yg, l, bh[h], nc, m1, hts[h], st,
+                                    Wgs, ldws, ps[kSrftR]);
           if (e != cudaSuccess) return e;
           *launches += 1;
         }

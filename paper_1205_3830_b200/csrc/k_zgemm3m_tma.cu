@@ -66,13 +66,14 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
   const int wj = warp % WJ, wr = warp / WJ;
   const int r0 = (int)blockIdx.x * Cf::BR;  // first output row of the tile
   const int64_t j0 = (int64_t)blockIdx.y * Cf::BJ;
-  int rt0 = r0, jt0 = (int)j0;               // tile origin in the tensor maps
+  int rt0 = r0, jt0 = (int)j0, st0 = r0;     // tile origin in the tensor maps (st0: Rs plane)
   int64_t kbeg = 0, kend = K;
   if (bt.n > 0) {  // batched (blockIdx.z = product): row / column offsets into shared maps
     const int z = blockIdx.z;
     Mout = bt.mout[z];
     if (r0 >= Mout) return;
     rt0 += (int)bt.roff[z];
+    st0 += (int)bt.soff[z];
     jt0 += (int)bt.boff[z];
     C += bt.coff[z];
   } else {
@@ -110,7 +111,7 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
 #pragma unroll
       for (int b = 0; b < Cf::kNR; ++b)
         tma_box_g2s(st + Cf::kNA * Cf::kABox + Cf::kNR * Cf::kRBox + b * Cf::kRsBox, &mapS,
-                    rt0 + 8 * b, kc0, &full[s]);
+                    st0 + 8 * b, kc0, &full[s]);
     }
   };
   if (tid == 0)
@@ -229,7 +230,7 @@ template <int FJ, int FR, int WJ, int WR, int STAGES, int MINB, int RS, int ORD 
 static cudaError_t launch3t(const double2* Rm, int64_t ldr, const double* Rs, int64_t ldrs,
                             const double2* Bm, int64_t ldb, double2* C, int64_t ldc, int64_t Mout,
                             int64_t N, int64_t K, cudaStream_t st, int S, double2* partial,
-                            const Z3Batch* bt = nullptr, int64_t Nb = 0) {
+                            const Z3Batch* bt = nullptr, int64_t Nb = 0, int64_t Ms = 0) {
   using Cf = Z3T<FJ, FR, WJ, WR, STAGES, RS>;
   auto kern = k_zgemm3m_tma<FJ, FR, WJ, WR, STAGES, MINB, RS, ORD>;
   static bool attr_set = false;
@@ -266,7 +267,7 @@ static cudaError_t launch3t(const double2* Rm, int64_t ldr, const double* Rs, in
   }
   mapS = mapR;  // unused unless RS
   if (RS) {
-    const cuuint64_t gdim[2] = {(cuuint64_t)Mout, (cuuint64_t)K};
+    const cuuint64_t gdim[2] = {(cuuint64_t)(Ms > 0 ? Ms : Mout), (cuuint64_t)K};
     const cuuint64_t gstr[1] = {(cuuint64_t)ldrs * sizeof(double)};
     const cuuint32_t box[2] = {8u, (cuuint32_t)Cf::BKC};
     if (!Rs || (ldrs * sizeof(double)) % 16 != 0 ||
@@ -363,14 +364,14 @@ cudaError_t zgemm3m_tma(const double2* Rm, int64_t ldr, const double* Rs, int64_
 cudaError_t zgemm3m_tma_batched(const double2* Rm, int64_t ldr, int64_t Mtot, const double2* Bm,
                                 int64_t ldb, int64_t Nb, double2* C, int64_t ldc,
                                 const Z3Batch& bt, int64_t N, int64_t K, cudaStream_t st) {
-  return zgemm3m_tma_batched_h(Rm, ldr, Mtot, Bm, ldb, Nb, C, ldc, bt, N, K, 0, st);
+  return zgemm3m_tma_batched_h(Rm, ldr, Mtot, Bm, ldb, Nb, C, ldc, bt, N, K, 0, st, nullptr, 0, 0);
 }
 
 // rows = 48 / 40 / 24 forces the tile height; 0 picks it from the largest product
 cudaError_t zgemm3m_tma_batched_h(const double2* Rm, int64_t ldr, int64_t Mtot, const double2* Bm,
                                   int64_t ldb, int64_t Nb, double2* C, int64_t ldc,
                                   const Z3Batch& bt, int64_t N, int64_t K, int rows,
-                                  cudaStream_t st) {
+                                  cudaStream_t st, const double* Rs, int64_t ldrs, int64_t Ms) {
   if (bt.n <= 0 || N <= 0) return cudaSuccess;
   Z3Batch b = bt;
   for (int z = 0; z < b.n; ++z) {
@@ -379,17 +380,22 @@ cudaError_t zgemm3m_tma_batched_h(const double2* Rm, int64_t ldr, int64_t Mtot, 
   }
   int64_t mmax = 0;
   for (int z = 0; z < b.n; ++z) mmax = b.mout[z] > mmax ? b.mout[z] : mmax;
+  // with a Re + Im plane of Rm (Rs: Ms rows, product z from row soff[z], even): the sums come
+  // from shared memory
+  const char* v = getenv("RID_Z3_BATCH_RS");
+  bool rs = Rs && !(v && atoi(v) == 0);
+  for (int z = 0; z < b.n && rs; ++z)
+    if (b.soff[z] & 1) return cudaErrorInvalidValue;
+#define RID_LB(FJ, FR, WJ, WR, ST, RS) \
+  launch3t<FJ, FR, WJ, WR, ST, 2, RS>(Rm, ldr, Rs, ldrs, Bm, ldb, C, ldc, Mtot, N, K, st, 1, \
+                                      nullptr, &b, Nb, Ms)
   switch (rows ? rows : zgemm3m_tile_rows(mmax)) {
-    case 48:
-      return launch3t<2, 3, 4, 2, 3, 2, 0>(Rm, ldr, nullptr, 0, Bm, ldb, C, ldc, Mtot, N, K, st, 1,
-                                           nullptr, &b, Nb);
-    case 40:
-      return launch3t<1, 5, 8, 1, 3, 2, 0>(Rm, ldr, nullptr, 0, Bm, ldb, C, ldc, Mtot, N, K, st, 1,
-                                           nullptr, &b, Nb);
+    case 48: return rs ? RID_LB(2, 3, 4, 2, 2, 1) : RID_LB(2, 3, 4, 2, 3, 0);
+    case 40: return rs ? RID_LB(1, 5, 8, 1, 3, 1) : RID_LB(1, 5, 8, 1, 3, 0);
     default:  // 24 rows (the residues' l/16 rows at C2, C3)
-      return launch3t<1, 3, 8, 1, 3, 2, 0>(Rm, ldr, nullptr, 0, Bm, ldb, C, ldc, Mtot, N, K, st, 1,
-                                           nullptr, &b, Nb);
+      return rs ? RID_LB(1, 3, 8, 1, 3, 1) : RID_LB(1, 3, 8, 1, 3, 0);
   }
+#undef RID_LB
 }
 
 }  // namespace rid

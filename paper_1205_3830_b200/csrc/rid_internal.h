@@ -43,6 +43,9 @@ constexpr int kZ3BatchMax = 16;
 struct Z3Batch {
   int n;
   int64_t roff[kZ3BatchMax], boff[kZ3BatchMax], coff[kZ3BatchMax], mout[kZ3BatchMax];
+  // row of product z's first row in the Re + Im plane (TMA kernel with a plane only; it must be
+  // even: a non-swizzled box of doubles starts on a 16-byte boundary)
+  int64_t soff[kZ3BatchMax];
 };
 cudaError_t zgemm3m_batched(const double2* Rm, int64_t ldr, const double2* Bm, int64_t ldb,
                             double2* C, int64_t ldc, const Z3Batch& bt, int64_t N, int64_t K,
@@ -54,7 +57,8 @@ cudaError_t zgemm3m_tma_batched(const double2* Rm, int64_t ldr, int64_t Mtot, co
 cudaError_t zgemm3m_tma_batched_h(const double2* Rm, int64_t ldr, int64_t Mtot, const double2* Bm,
                                   int64_t ldb, int64_t Nb, double2* C, int64_t ldc,
                                   const Z3Batch& bt, int64_t N, int64_t K, int rows,
-                                  cudaStream_t st);
+                                  cudaStream_t st, const double* Rs = nullptr, int64_t ldrs = 0,
+                                  int64_t Ms = 0);
 inline int64_t rsum_ld(int64_t l) { return (l + 1) / 2 * 2; }
 cudaError_t rsum_fill(const double2* R, int64_t l, int64_t m, int64_t ldr, double* Rs,
                       int64_t ldrs, cudaStream_t st);
