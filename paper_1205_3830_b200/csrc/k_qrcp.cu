@@ -1240,12 +1240,20 @@ static cudaError_t launch_qrcp_smem(double2* Y, int64_t ldy, int l, int64_t n, i
                                     int num_sms, cudaStream_t st, int* launches) {
   auto kern = k_qrcp_smem<MAXQ>;
   cudaError_t e;
-  int dev = 0, optin = 0;
-  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-  if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
-    return e;
-  cudaFuncAttributes fa;
-  if ((e = cudaFuncGetAttributes(&fa, (const void*)kern)) != cudaSuccess) return e;
+  // device and function attributes and the occupancy of the last shared-memory size: queried once
+  // (host API calls on every decompose cost ~10 us, a visible share of the small configs' step)
+  static int optin = -1;
+  static cudaFuncAttributes fa;
+  static size_t last_smem = 0;
+  static int last_occ = 0;
+  if (optin < 0) {
+    int dev = 0, o = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&o, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
+      return e;
+    if ((e = cudaFuncGetAttributes(&fa, (const void*)kern)) != cudaSuccess) return e;
+    optin = o;
+  }
   for (int per_sm = 2; per_sm >= 1; --per_sm) {
     int blocks = num_sms * per_sm;
     if (blocks > w.max_blocks) blocks = w.max_blocks;
@@ -1257,13 +1265,19 @@ static cudaError_t launch_qrcp_smem(double2* Y, int64_t ldy, int l, int64_t n, i
                         (size_t)per * l * sizeof(double2);
     const size_t cap = (size_t)optin / per_sm - fa.sharedSizeBytes - 1024;
     if (smem > cap) continue;
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
-        cudaSuccess)
-      return e;
     int occ = 0;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kQrcpThreads, smem)) !=
-        cudaSuccess)
-      return e;
+    if (smem == last_smem) {
+      occ = last_occ;
+    } else {
+      if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+          cudaSuccess)
+        return e;
+      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kQrcpThreads, smem)) !=
+          cudaSuccess)
+        return e;
+      last_smem = smem;
+      last_occ = occ;
+    }
     if (occ * num_sms < blocks) continue;  // a cooperative launch needs every CTA resident
     if ((e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
     QrcpOut o = out;
@@ -1285,12 +1299,16 @@ static cudaError_t launch_qrcp_blocked(double2* Y, int64_t ldy, int l, int64_t n
                                        int num_sms, cudaStream_t st, int* launches, int nbw) {
   auto kern = k_qrcp_ring<MAXQ>;
   cudaError_t e;
-  int dev = 0, optin = 0;
-  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-  if ((e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
-    return e;
-  cudaFuncAttributes fa;
-  if ((e = cudaFuncGetAttributes(&fa, (const void*)kern)) != cudaSuccess) return e;
+  static int optin = -1;  // queried once (see launch_qrcp_smem)
+  static cudaFuncAttributes fa;
+  if (optin < 0) {
+    int dev = 0, o = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    if ((e = cudaDeviceGetAttribute(&o, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
+      return e;
+    if ((e = cudaFuncGetAttributes(&fa, (const void*)kern)) != cudaSuccess) return e;
+    optin = o;
+  }
   int blocks = num_sms;
   if ((int64_t)blocks * 8 > n) blocks = (int)((n + 7) / 8);
   if (blocks > w.max_blocks) blocks = w.max_blocks;
@@ -1321,8 +1339,13 @@ static cudaError_t launch_qrcp_blocked(double2* Y, int64_t ldy, int l, int64_t n
     if (x >= 2 && x * ncw <= slots) D = x;
   }
   const size_t smem = fixed + (size_t)ncw * D * slot_bytes;
-  if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
-    return e;
+  static size_t smem_set = 0;
+  if (smem != smem_set) {
+    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+        cudaSuccess)
+      return e;
+    smem_set = smem;
+  }
   // 2D tensor map of Y as a (2l doubles) x n matrix, boxes of kCH complex rows x 32 columns
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {

@@ -35,6 +35,9 @@ struct rid_ctx {
   cudaEvent_t ev_copied[2] = {}, ev_used[2] = {}, ev_copy0 = nullptr, ev_copy1 = nullptr;
   int sketch_kind = 0;  // RID_SKETCH_GAUSSIAN (north star) or RID_SKETCH_SRFT
   int qr_kind = 0;      // RID_QR_HOUSEHOLDER (default) or RID_QR_CGS2
+  // pinned host mirror of the QR's status block (info, beta, resid, margin): one copy, one sync
+  void* host_qr = nullptr;
+  size_t host_qr_bytes = 0;
 };
 
 namespace {
@@ -170,12 +173,16 @@ rid_status solve_T(rid_ctx* c, const double2* Rinv, int64_t k, const double2* Y,
 rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64_t k, int64_t col0,
                             int64_t n_loc, double2* Pdev, int64_t ldp, int64_t** Jdev_out,
                             int* info_host, rid_diag* diag, bool solve, double** beta_out) {
-  void *pJ, *pbeta, *presid, *pmargin, *pinfo, *pwork;
+  void *pJ, *pbeta, *presid, *pmargin, *pinfo, *pwork, *pstat;
   RID_TRY(ws_get(c, "J", sizeof(int64_t) * k, &pJ));
-  RID_TRY(ws_get(c, "beta", sizeof(double) * k, &pbeta));
-  RID_TRY(ws_get(c, "resid", sizeof(double) * k, &presid));
-  RID_TRY(ws_get(c, "margin", sizeof(double) * k, &pmargin));
-  RID_TRY(ws_get(c, "info", sizeof(int) * 2, &pinfo));
+  // the QR's status block, contiguous so the host reads it with one copy: info (2 ints, 16 B),
+  // then beta, resid, margin (k doubles each)
+  const size_t stat_bytes = 16 + 3 * sizeof(double) * (size_t)k;
+  RID_TRY(ws_get(c, "qr_status", stat_bytes, &pstat));
+  pinfo = pstat;
+  pbeta = (char*)pstat + 16;
+  presid = (double*)pbeta + k;
+  pmargin = (double*)presid + k;
   const int max_blocks = 4 * c->num_sms;
   RID_TRY(ws_get(c, "qrcp_work", rid::qrcp_work_bytes(n, l, max_blocks), &pwork));
   void* pR11;
@@ -214,13 +221,23 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
       fclose(f);
     }
   }
-  // one synchronisation: rank status, R11 diagonal (singularity), diagnostics
-  std::vector<double> hb(k), hr(k), hm(k);
-  RID_CUDA(c, cudaMemcpyAsync(info_host, pinfo, sizeof(int) * 2, cudaMemcpyDeviceToHost, c->stream));
-  RID_CUDA(c, cudaMemcpyAsync(hb.data(), pbeta, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
-  RID_CUDA(c, cudaMemcpyAsync(hr.data(), presid, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
-  RID_CUDA(c, cudaMemcpyAsync(hm.data(), pmargin, sizeof(double) * k, cudaMemcpyDeviceToHost, c->stream));
+  // one synchronisation: rank status, R11 diagonal (singularity), diagnostics — the status block
+  // in one copy into the context's pinned mirror (pageable copies cost a round trip each)
+  if (c->host_qr_bytes < stat_bytes) {
+    if (c->host_qr) cudaFreeHost(c->host_qr);
+    c->host_qr = nullptr;
+    c->host_qr_bytes = 0;
+    RID_CUDA(c, cudaMallocHost(&c->host_qr, stat_bytes));
+    c->host_qr_bytes = stat_bytes;
+  }
+  RID_CUDA(c, cudaMemcpyAsync(c->host_qr, pstat, stat_bytes, cudaMemcpyDeviceToHost, c->stream));
   RID_CUDA(c, cudaStreamSynchronize(c->stream));
+  const int* hinfo = (const int*)c->host_qr;
+  info_host[0] = hinfo[0];
+  info_host[1] = hinfo[1];
+  const double* hb = (const double*)((const char*)c->host_qr + 16);
+  const double* hr = hb + k;
+  const double* hm = hr + k;
   *Jdev_out = (int64_t*)pJ;
   if (beta_out) *beta_out = (double*)pbeta;
   if (diag) {
@@ -383,6 +400,7 @@ void rid_destroy(rid_ctx* c) {
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->host_qr) cudaFreeHost(c->host_qr);
   if (c->copy_stream) {
     cudaStreamSynchronize(c->copy_stream);
     cudaStreamDestroy(c->copy_stream);
@@ -698,9 +716,10 @@ rid_status rid_qrcp(rid_ctx* c, const rid_z* Y, int64_t l, int64_t n, int64_t ld
     RID_CUDA(c, cudaGetLastError());
     RID_TRY(stage_out(c, r, R, k, n, ldr, sizeof(rid_z)));
   }
-  void *presid, *pmargin;
-  RID_TRY(ws_get(c, "resid", sizeof(double) * k, &presid));
-  RID_TRY(ws_get(c, "margin", sizeof(double) * k, &pmargin));
+  void* pstat;  // the status block factor_and_solve filled: info | beta | resid | margin
+  RID_TRY(ws_get(c, "qr_status", 16 + 3 * sizeof(double) * (size_t)k, &pstat));
+  const double* presid = (const double*)((const char*)pstat + 16) + k;
+  const double* pmargin = presid + k;
   if (resid)
     RID_CUDA(c, cudaMemcpyAsync(resid, presid, sizeof(double) * k, cudaMemcpyDefault, c->stream));
   if (margin)
