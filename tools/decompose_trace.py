@@ -15,7 +15,7 @@ A = rid.generate(1, c.m, c.n, c.k, c.noise)
 for _ in range(3):
     rid.decompose(A, c.k, c.l, 1)
 torch.cuda.synchronize()
-with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
+with profile(activities=[ProfilerActivity.CUDA]) as prof:
     r = rid.decompose(A, c.k, c.l, 1)
     torch.cuda.synchronize()
 ev = sorted([e for e in prof.events() if e.device_type.name == "CUDA"],
