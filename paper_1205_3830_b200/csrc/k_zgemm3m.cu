@@ -478,7 +478,7 @@ int64_t sketch_partial_elems(int64_t l, int64_t m, int64_t n, int64_t ncols, int
 cudaError_t sketch_gemm(const double2* R, int64_t ldr, const double* Rs, const double2* A,
                         int64_t lda, double2* Y, int64_t ldy, int64_t l, int64_t ncols, int64_t m,
                         cudaStream_t st, int ksplit, double2* partial, int64_t col0, int64_t n,
-                        int num_sms, int* launches) {
+                        int num_sms, int* launches, const SketchAux* aux) {
   int dummy = 0;
   if (!launches) launches = &dummy;
   if (sketch_mults() == 4) {
@@ -490,6 +490,13 @@ cudaError_t sketch_gemm(const double2* R, int64_t ldr, const double* Rs, const d
   int64_t nmain = ncols;
   if (t.cols > 0 && col0 + ncols > tail0) nmain = tail0 > col0 ? tail0 - col0 : 0;
   cudaError_t e = cudaSuccess;
+  // the K-split tail set runs on the aux stream (when given), launched after the main product so
+  // its CTAs take the SMs the main launch's last wave leaves idle; disjoint columns of Y
+  const bool fork = aux && aux->stream && nmain > 0 && nmain < ncols;
+  if (fork) {
+    if ((e = cudaEventRecord(aux->fork, st)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(aux->stream, aux->fork, 0)) != cudaSuccess) return e;
+  }
   if (nmain > 0) {
     e = zgemm3m(R, ldr, Rs, rsum_ld(l), A, lda, Y, ldy, l, nmain, m, st, ksplit, partial);
     *launches += ksplit > 1 ? 2 : 1;
@@ -497,8 +504,13 @@ cudaError_t sketch_gemm(const double2* R, int64_t ldr, const double* Rs, const d
   }
   if (nmain < ncols) {
     e = zgemm3m(R, ldr, Rs, rsum_ld(l), A + nmain * lda, lda, Y + nmain * ldy, ldy, l,
-                ncols - nmain, m, st, t.S, partial);
+                ncols - nmain, m, fork ? aux->stream : st, t.S, partial);
     *launches += 2;
+    if (e != cudaSuccess) return e;
+    if (fork) {
+      if ((e = cudaEventRecord(aux->join, aux->stream)) != cudaSuccess) return e;
+      if ((e = cudaStreamWaitEvent(st, aux->join, 0)) != cudaSuccess) return e;
+    }
   }
   return e;
 }

@@ -38,6 +38,9 @@ struct rid_ctx {
   // pinned host mirror of the QR's status block (info, beta, resid, margin): one copy, one sync
   void* host_qr = nullptr;
   size_t host_qr_bytes = 0;
+  // aux stream for the sketch's K-split tail set (rid::SketchAux), created on first use
+  cudaStream_t aux_stream = nullptr;
+  cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
 };
 
 namespace {
@@ -401,6 +404,12 @@ void rid_destroy(rid_ctx* c) {
     if (ev) cudaEventDestroy(ev);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->host_qr) cudaFreeHost(c->host_qr);
+  if (c->aux_stream) {
+    cudaStreamSynchronize(c->aux_stream);
+    cudaStreamDestroy(c->aux_stream);
+    cudaEventDestroy(c->aux_fork);
+    cudaEventDestroy(c->aux_join);
+  }
   if (c->copy_stream) {
     cudaStreamSynchronize(c->copy_stream);
     cudaStreamDestroy(c->copy_stream);
@@ -623,9 +632,16 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
       RID_TRY(sketch_streamed(c, Rg, Rsg, A, m, n, col0, n_loc, lda, l, Yw + col0 * l,
                               &d.launches, nullptr, S, (double2*)pS));
     } else {
+      if (!c->aux_stream && !getenv("RID_SKETCH_NOAUX")) {
+        RID_CUDA(c, cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+        RID_CUDA(c, cudaEventCreateWithFlags(&c->aux_fork, cudaEventDisableTiming));
+        RID_CUDA(c, cudaEventCreateWithFlags(&c->aux_join, cudaEventDisableTiming));
+      }
+      const rid::SketchAux aux{c->aux_stream, c->aux_fork, c->aux_join};
       RID_CUDA(c, rid::sketch_gemm(Rg, l, Rsg, (const double2*)a.dev, lda, Yw + col0 * l, l, l,
                                    n_loc, m, c->stream, S, (double2*)pS, col0, n, c->num_sms,
-                                   &d.launches));
+                                   &d.launches, (c->aux_stream && !getenv("RID_SKETCH_NOAUX"))
+                                                    ? &aux : nullptr));
     }
     }
     RID_CUDA(c, cudaEventRecord(ev[4], c->stream));

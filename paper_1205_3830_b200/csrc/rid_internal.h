@@ -75,10 +75,15 @@ struct SketchTail {
 };
 SketchTail sketch_tail(int64_t l, int64_t m, int64_t n, int num_sms);
 int64_t sketch_partial_elems(int64_t l, int64_t m, int64_t n, int64_t ncols, int num_sms);
+// aux (nullable): a second stream and two events for running the tail set concurrently
+struct SketchAux {
+  cudaStream_t stream;
+  cudaEvent_t fork, join;
+};
 cudaError_t sketch_gemm(const double2* R, int64_t ldr, const double* Rs, const double2* A,
                         int64_t lda, double2* Y, int64_t ldy, int64_t l, int64_t ncols, int64_t m,
                         cudaStream_t st, int ksplit, double2* partial, int64_t col0, int64_t n,
-                        int num_sms, int* launches);
+                        int num_sms, int* launches, const SketchAux* aux = nullptr);
 // K slices for a sketch of Mout rows, K = m, chosen from n_ref = n_global / 8 only (G-invariant)
 int zgemm_ksplit(int64_t Mout, int64_t K, int64_t n_ref, int num_sms);
 
