@@ -173,9 +173,14 @@ rid_status solve_T(rid_ctx* c, const double2* Rinv, int64_t k, const double2* Y,
 
 // Factor the full sketch in workspace "Y" and solve for the local shard columns.
 // On entry Yw holds the full l x n sketch (ld = l). Writes J (device ws), P_loc (device).
+rid_status qr_check(rid_ctx* c, int64_t k, int* info_host, rid_diag* diag);
+
+// defer = true (rid_decompose): enqueue the QR and the copy of its status block, return without
+// synchronising; the caller synchronises once at its end and calls qr_check.
 rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64_t k, int64_t col0,
                             int64_t n_loc, double2* Pdev, int64_t ldp, int64_t** Jdev_out,
-                            int* info_host, rid_diag* diag, bool solve, double** beta_out) {
+                            int* info_host, rid_diag* diag, bool solve, double** beta_out,
+                            bool defer = false) {
   void *pJ, *pbeta, *presid, *pmargin, *pinfo, *pwork, *pstat;
   RID_TRY(ws_get(c, "J", sizeof(int64_t) * k, &pJ));
   // the QR's status block, contiguous so the host reads it with one copy: info (2 ints, 16 B),
@@ -234,15 +239,29 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
     c->host_qr_bytes = stat_bytes;
   }
   RID_CUDA(c, cudaMemcpyAsync(c->host_qr, pstat, stat_bytes, cudaMemcpyDeviceToHost, c->stream));
+  *Jdev_out = (int64_t*)pJ;
+  if (beta_out) *beta_out = (double*)pbeta;
+  if (defer) return RID_OK;
   RID_CUDA(c, cudaStreamSynchronize(c->stream));
+  RID_TRY(qr_check(c, k, info_host, diag));
+  if (!solve) return RID_OK;
+  void* pRinv;
+  RID_TRY(ws_get(c, "Rinv", sizeof(double2) * k * k, &pRinv));
+  RID_CUDA(c, rid::tri_inverse((const double2*)pR11, k, (double2*)pRinv, c->stream));
+  RID_TRY(solve_T(c, (const double2*)pRinv, k, Yw + col0 * l, l, Pdev, ldp, n_loc));
+  RID_CUDA(c, rid::assemble_identity((const int64_t*)pJ, k, col0, n_loc, Pdev, ldp, c->stream));
+  return RID_OK;
+}
+
+// Reads the QR's status block from the pinned mirror (after the caller's synchronisation): rank
+// status, R11 diagonal (singularity), diagnostics.
+rid_status qr_check(rid_ctx* c, int64_t k, int* info_host, rid_diag* diag) {
   const int* hinfo = (const int*)c->host_qr;
   info_host[0] = hinfo[0];
   info_host[1] = hinfo[1];
   const double* hb = (const double*)((const char*)c->host_qr + 16);
   const double* hr = hb + k;
   const double* hm = hr + k;
-  *Jdev_out = (int64_t*)pJ;
-  if (beta_out) *beta_out = (double*)pbeta;
   if (diag) {
     const int kk = info_host[0] == 0 ? (int)k : info_host[1];
     double mm = INFINITY;
@@ -258,12 +277,6 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
     if (std::fabs(hb[t]) < kSingTol * dmax)
       return fail(c, RID_ESINGULAR, "R11[%lld,%lld] = %g below 1e-13 * %g", (long long)t,
                   (long long)t, hb[t], dmax);
-  if (!solve) return RID_OK;
-  void* pRinv;
-  RID_TRY(ws_get(c, "Rinv", sizeof(double2) * k * k, &pRinv));
-  RID_CUDA(c, rid::tri_inverse((const double2*)pR11, k, (double2*)pRinv, c->stream));
-  RID_TRY(solve_T(c, (const double2*)pRinv, k, Yw + col0 * l, l, Pdev, ldp, n_loc));
-  RID_CUDA(c, rid::assemble_identity((const int64_t*)pJ, k, col0, n_loc, Pdev, ldp, c->stream));
   return RID_OK;
 }
 
@@ -650,9 +663,29 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
                                 c->stream));
     }
     RID_CUDA(c, cudaEventRecord(ev[5], c->stream));
-    st = factor_and_solve(c, Yw, l, n, k, col0, n_loc, (double2*)p.dev, ldp, &Jdev, info, &d,
-                          false, nullptr);
+    // the QR, its status copy and the solve are enqueued together; the status is checked after
+    // the one synchronisation at the end (a failed attempt's solve output is discarded)
+    RID_TRY(factor_and_solve(c, Yw, l, n, k, col0, n_loc, (double2*)p.dev, ldp, &Jdev, info, &d,
+                             false, nullptr, /*defer=*/true));
     RID_CUDA(c, cudaEventRecord(ev[6], c->stream));
+    {  // solve
+      void *pR11, *pRinv;
+      RID_TRY(ws_get(c, "R11", sizeof(double2) * k * k, &pR11));
+      RID_TRY(ws_get(c, "Rinv", sizeof(double2) * k * k, &pRinv));
+      RID_CUDA(c, rid::tri_inverse((const double2*)pR11, k, (double2*)pRinv, c->stream));
+      RID_TRY(solve_T(c, (const double2*)pRinv, k, Yw + col0 * l, l, (double2*)p.dev, ldp, n_loc));
+      RID_CUDA(c, rid::assemble_identity(Jdev, k, col0, n_loc, (double2*)p.dev, ldp, c->stream));
+      d.launches += rid::sketch_mults() == 3 ? 4 : 3;  // R11^-1, (sum plane), T GEMM, identity
+    }
+    RID_CUDA(c, cudaEventRecord(ev[7], c->stream));
+    RID_TRY(stage_out(c, p, P, k, n_loc, ldp, sizeof(rid_z)));
+    if (is_device_ptr(J))
+      RID_CUDA(c, cudaMemcpyAsync(J, Jdev, sizeof(int64_t) * k, cudaMemcpyDeviceToDevice, c->stream));
+    else
+      RID_CUDA(c, cudaMemcpyAsync(J, Jdev, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, c->stream));
+    RID_CUDA(c, cudaEventRecord(ev[8], c->stream));
+    RID_CUDA(c, cudaEventSynchronize(ev[8]));
+    st = qr_check(c, k, info, &d);
     if (st == RID_ERANK && attempt == 0) {
       d.retries = 1;
       continue;  // repeat with a different instance of the random matrix
@@ -665,23 +698,6 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
                 (long long)k);
   }
   if (st != RID_OK) return st;
-  {  // solve
-    void *pR11, *pRinv;
-    RID_TRY(ws_get(c, "R11", sizeof(double2) * k * k, &pR11));
-    RID_TRY(ws_get(c, "Rinv", sizeof(double2) * k * k, &pRinv));
-    RID_CUDA(c, rid::tri_inverse((const double2*)pR11, k, (double2*)pRinv, c->stream));
-    RID_TRY(solve_T(c, (const double2*)pRinv, k, Yw + col0 * l, l, (double2*)p.dev, ldp, n_loc));
-    RID_CUDA(c, rid::assemble_identity(Jdev, k, col0, n_loc, (double2*)p.dev, ldp, c->stream));
-    d.launches += rid::sketch_mults() == 3 ? 4 : 3;  // R11^-1, (sum plane), T GEMM, identity
-  }
-  RID_CUDA(c, cudaEventRecord(ev[7], c->stream));
-  RID_TRY(stage_out(c, p, P, k, n_loc, ldp, sizeof(rid_z)));
-  if (is_device_ptr(J))
-    RID_CUDA(c, cudaMemcpyAsync(J, Jdev, sizeof(int64_t) * k, cudaMemcpyDeviceToDevice, c->stream));
-  else
-    RID_CUDA(c, cudaMemcpyAsync(J, Jdev, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, c->stream));
-  RID_CUDA(c, cudaEventRecord(ev[8], c->stream));
-  RID_CUDA(c, cudaEventSynchronize(ev[8]));
   if (diag) {
     // host A: the streamed copies overlap the sketch (t_sketch then includes copy stalls)
     d.t_h2d = a_host ? ev_ms(c->ev_copy0, c->ev_copy1) * 1e-3 : ev_ms(ev[0], ev[1]) * 1e-3;
