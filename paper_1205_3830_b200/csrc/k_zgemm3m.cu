@@ -350,7 +350,9 @@ int zgemm3m_ksplit(int64_t Mout, int64_t K, int64_t n_ref, int num_sms) {
   if (n_ref <= 0 || K <= 0) return 1;
   const int64_t tiles = ((n_ref + 63) / 64) * ((Mout + rows3(pick3(Mout)) - 1) / rows3(pick3(Mout)));
   int64_t s = (2 * (int64_t)num_sms + tiles - 1) / tiles;
-  const int64_t smax = K / 512 > 1 ? K / 512 : 1;
+  // slices of at least 128 complex K (8 stages): binds only when the tiles are very few (C1:
+  // 8 slices, sketch 30 -> ~8 us); the larger configs' slice counts come from the tile count
+  const int64_t smax = K / 128 > 1 ? K / 128 : 1;
   if (s > smax) s = smax;
   if (s > 64) s = 64;
   return s < 1 ? 1 : (int)s;

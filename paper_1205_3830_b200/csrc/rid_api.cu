@@ -13,6 +13,8 @@
 #include <string>
 #include <vector>
 
+extern char** environ;  // POSIX: the RID_* knobs are part of the graph key
+
 #include "../../include/rid.h"
 #include "rid_internal.h"
 
@@ -41,6 +43,15 @@ struct rid_ctx {
   // aux stream for the sketch's K-split tail set (rid::SketchAux), created on first use
   cudaStream_t aux_stream = nullptr;
   cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
+  // CUDA graph of rid_decompose's device work (repeated calls with identical arguments): the
+  // key of the last call seen, the captured executable and its key; ws_epoch counts workspace
+  // reallocations (a graph holds workspace pointers)
+  unsigned long long ws_epoch = 0;
+  std::string g_seen, g_key, g_bad;
+  cudaGraphExec_t g_exec = nullptr;
+  int g_launches = 0;
+  cudaStream_t cap_stream = nullptr;
+  cudaEvent_t g_in = nullptr, g_out = nullptr;
 };
 
 namespace {
@@ -79,6 +90,7 @@ rid_status fail(rid_ctx* c, rid_status st, const char* fmt, ...) {
 rid_status ws_get(rid_ctx* c, const char* name, size_t bytes, void** out) {
   auto& b = c->ws[name];
   if (b.bytes < bytes) {
+    ++c->ws_epoch;
     if (b.p) {
       RID_CUDA(c, cudaStreamSynchronize(c->stream));
       RID_CUDA(c, cudaFree(b.p));
@@ -232,6 +244,7 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
   // one synchronisation: rank status, R11 diagonal (singularity), diagnostics — the status block
   // in one copy into the context's pinned mirror (pageable copies cost a round trip each)
   if (c->host_qr_bytes < stat_bytes) {
+    ++c->ws_epoch;
     if (c->host_qr) cudaFreeHost(c->host_qr);
     c->host_qr = nullptr;
     c->host_qr_bytes = 0;
@@ -422,6 +435,13 @@ void rid_destroy(rid_ctx* c) {
     cudaStreamDestroy(c->aux_stream);
     cudaEventDestroy(c->aux_fork);
     cudaEventDestroy(c->aux_join);
+  }
+  if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
+  if (c->cap_stream) {
+    cudaStreamSynchronize(c->cap_stream);
+    cudaStreamDestroy(c->cap_stream);
+    cudaEventDestroy(c->g_in);
+    cudaEventDestroy(c->g_out);
   }
   if (c->copy_stream) {
     cudaStreamSynchronize(c->copy_stream);
@@ -629,18 +649,28 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
   int64_t* Jdev = nullptr;
   rid_status st = RID_OK;
   int info[2] = {0, 0};
-  for (int attempt = 0; attempt < 2; ++attempt) {
+  const bool j_dev = is_device_ptr(J);
+  // the device work of one attempt (events ev[2]..ev[8], R, sketch, all-gather, QR, its status
+  // copy, solve, J): enqueue only, no synchronisation
+  // ev[2..8]: while capturing, recorded as external events, so inside the graph they stay real
+  // event records the host can synchronise on and time (the flag is refused outside capture)
+  bool capturing = false;
+  auto rec = [&](cudaEvent_t e) {
+    return capturing ? cudaEventRecordWithFlags(e, c->stream, cudaEventRecordExternal)
+                     : cudaEventRecord(e, c->stream);
+  };
+  auto enqueue = [&](int attempt) -> rid_status {
     const uint32_t sR = attempt == 0 ? kStreamR : kStreamRRetry;
-    RID_CUDA(c, cudaEventRecord(ev[2], c->stream));
+    RID_CUDA(c, rec(ev[2]));
     if (c->sketch_kind == RID_SKETCH_SRFT) {  // the paper's own randomisation
-      RID_CUDA(c, cudaEventRecord(ev[3], c->stream));
+      RID_CUDA(c, rec(ev[3]));
       RID_TRY(srft_into(c, seed, attempt == 1, l, A, a_host ? nullptr : a.dev, m, n, n_loc, lda,
                         Yw + col0 * l, l, &d.launches));
     } else {
     double2* Rg;
     double* Rsg;
     RID_TRY(fill_R(c, seed, sR, l, m, &Rg, &Rsg, &d.launches));
-    RID_CUDA(c, cudaEventRecord(ev[3], c->stream));
+    RID_CUDA(c, rec(ev[3]));
     if (a_host) {
       RID_TRY(sketch_streamed(c, Rg, Rsg, A, m, n, col0, n_loc, lda, l, Yw + col0 * l,
                               &d.launches, nullptr, S, (double2*)pS));
@@ -657,17 +687,17 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
                                                     ? &aux : nullptr));
     }
     }
-    RID_CUDA(c, cudaEventRecord(ev[4], c->stream));
+    RID_CUDA(c, rec(ev[4]));
     if (c->comm) {
       RID_NCCL(c, ncclAllGather(Yw + col0 * l, Yw, (size_t)(2 * l * n_loc), ncclDouble, c->comm,
                                 c->stream));
     }
-    RID_CUDA(c, cudaEventRecord(ev[5], c->stream));
+    RID_CUDA(c, rec(ev[5]));
     // the QR, its status copy and the solve are enqueued together; the status is checked after
     // the one synchronisation at the end (a failed attempt's solve output is discarded)
     RID_TRY(factor_and_solve(c, Yw, l, n, k, col0, n_loc, (double2*)p.dev, ldp, &Jdev, info, &d,
                              false, nullptr, /*defer=*/true));
-    RID_CUDA(c, cudaEventRecord(ev[6], c->stream));
+    RID_CUDA(c, rec(ev[6]));
     {  // solve
       void *pR11, *pRinv;
       RID_TRY(ws_get(c, "R11", sizeof(double2) * k * k, &pR11));
@@ -677,13 +707,87 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
       RID_CUDA(c, rid::assemble_identity(Jdev, k, col0, n_loc, (double2*)p.dev, ldp, c->stream));
       d.launches += rid::sketch_mults() == 3 ? 4 : 3;  // R11^-1, (sum plane), T GEMM, identity
     }
-    RID_CUDA(c, cudaEventRecord(ev[7], c->stream));
+    RID_CUDA(c, rec(ev[7]));
     RID_TRY(stage_out(c, p, P, k, n_loc, ldp, sizeof(rid_z)));
-    if (is_device_ptr(J))
+    if (j_dev)
       RID_CUDA(c, cudaMemcpyAsync(J, Jdev, sizeof(int64_t) * k, cudaMemcpyDeviceToDevice, c->stream));
     else
       RID_CUDA(c, cudaMemcpyAsync(J, Jdev, sizeof(int64_t) * k, cudaMemcpyDeviceToHost, c->stream));
-    RID_CUDA(c, cudaEventRecord(ev[8], c->stream));
+    RID_CUDA(c, rec(ev[8]));
+    return RID_OK;
+  };
+  // repeated calls with identical arguments replay a CUDA graph of that work (one launch instead
+  // of ~30 API calls: the small configs are launch-bound); captured on the second such call,
+  // device A / J / P and no communicator only, RID_GRAPH=0 disables; any capture failure falls
+  // back to the eager path
+  const bool graphable = !a_host && !p.host && j_dev && !c->comm &&
+                         c->sketch_kind != RID_SKETCH_SRFT &&
+                         !(getenv("RID_GRAPH") && atoi(getenv("RID_GRAPH")) == 0);
+  std::string gkey;
+  if (graphable) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "%p %lld %lld %lld %lld %lld %lld %lld %llu %p %p %lld %d %llu %p",
+             (const void*)A, (long long)m, (long long)n, (long long)col0, (long long)n_loc,
+             (long long)lda, (long long)k, (long long)l, (unsigned long long)seed, (void*)J,
+             (void*)p.dev, (long long)ldp, c->qr_kind, c->ws_epoch, c->host_qr);
+    gkey = buf;
+    for (char** e = environ; *e; ++e)  // every RID_* knob selects kernels: part of the key
+      if (strncmp(*e, "RID_", 4) == 0) {
+        gkey += ' ';
+        gkey += *e;
+      }
+  }
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    bool replayed = false;
+    if (attempt == 0 && graphable) {
+      if (!c->cap_stream) {
+        RID_CUDA(c, cudaStreamCreateWithFlags(&c->cap_stream, cudaStreamNonBlocking));
+        RID_CUDA(c, cudaEventCreateWithFlags(&c->g_in, cudaEventDisableTiming));
+        RID_CUDA(c, cudaEventCreateWithFlags(&c->g_out, cudaEventDisableTiming));
+      }
+      if (!(c->g_exec && c->g_key == gkey) && c->g_seen == gkey && c->g_bad != gkey) {  // capture
+        cudaStream_t orig = c->stream;
+        c->stream = c->cap_stream;
+        const int l0 = d.launches;
+        cudaGraph_t g = nullptr;
+        rid_status es = RID_ECUDA;
+        if (cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+          capturing = true;
+          es = enqueue(0);
+          capturing = false;
+          if (cudaStreamEndCapture(c->cap_stream, &g) != cudaSuccess) es = RID_ECUDA;
+        }
+        c->stream = orig;
+        cudaGraphExec_t ex = nullptr;
+        if (es == RID_OK && g && cudaGraphInstantiate(&ex, g, 0) == cudaSuccess) {
+          if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
+          c->g_exec = ex;
+          c->g_key = gkey;
+          c->g_launches = d.launches - l0;
+        } else {
+          c->g_bad = gkey;  // not capturable: stay eager for these arguments
+        }
+        if (getenv("RID_GRAPH_DEBUG"))
+          fprintf(stderr, "rid_decompose: graph capture %s (%s; %s)\n",
+                  c->g_key == gkey ? "ok" : "FAILED", es == RID_OK ? "enqueue ok" : c->err.c_str(),
+                  cudaGetErrorString(cudaGetLastError()));
+        if (g) cudaGraphDestroy(g);
+        cudaGetLastError();  // a failed capture leaves no sticky error: the eager path follows
+        d.launches = l0;
+        c->err.clear();
+      }
+      if (c->g_exec && c->g_key == gkey) {
+        RID_CUDA(c, cudaEventRecord(c->g_in, c->stream));
+        RID_CUDA(c, cudaStreamWaitEvent(c->cap_stream, c->g_in, 0));
+        RID_CUDA(c, cudaGraphLaunch(c->g_exec, c->cap_stream));
+        RID_CUDA(c, cudaEventRecord(c->g_out, c->cap_stream));
+        RID_CUDA(c, cudaStreamWaitEvent(c->stream, c->g_out, 0));
+        d.launches += c->g_launches;
+        replayed = true;
+      }
+      c->g_seen = gkey;
+    }
+    if (!replayed) RID_TRY(enqueue(attempt));
     RID_CUDA(c, cudaEventSynchronize(ev[8]));
     st = qr_check(c, k, info, &d);
     if (st == RID_ERANK && attempt == 0) {

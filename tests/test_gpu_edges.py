@@ -130,3 +130,24 @@ def test_tri_inverse_warp_kernel_bitwise(rid, monkeypatch, seed, m, n, k, l):
     assert torch.equal(r_new.J, r_old.J)
     assert np.array_equal(np.ascontiguousarray(r_new.P.cpu().numpy()).view(np.uint64),
                           np.ascontiguousarray(r_old.P.cpu().numpy()).view(np.uint64))
+
+
+@pytest.mark.parametrize("seed,m,n,k,l", [(1, 1024, 512, 16, 24), (2, 2048, 3000, 256, 272)])
+def test_decompose_graph_replay(rid, monkeypatch, seed, m, n, k, l):
+    """Repeated rid_decompose calls with identical arguments replay a captured CUDA graph (from
+    the second call on); J and P stay bitwise equal to the eager path (RID_GRAPH=0) and the
+    diagnostics stay meaningful."""
+    A = rid.generate(seed, m, n, k, 1e-9)
+    J = torch.empty(k, dtype=torch.int64, device="cuda")
+    P = rid.colmajor_empty(k, n, device="cuda")
+    outs = []
+    for _ in range(4):
+        r = rid.decompose(A, k, l, seed, J=J, P=P)
+        outs.append((J.clone(), P.clone(), r.diag))
+    monkeypatch.setenv("RID_GRAPH", "0")
+    r0 = rid.decompose(A, k, l, seed)
+    for Jg, Pg, dg in outs:
+        assert torch.equal(Jg, r0.J)
+        assert np.array_equal(np.ascontiguousarray(Pg.cpu().numpy()).view(np.uint64),
+                              np.ascontiguousarray(r0.P.cpu().numpy()).view(np.uint64))
+        assert dg["t_total"] > 0 and dg["t_qrcp"] > 0 and dg["launches"] > 0
