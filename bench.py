@@ -205,9 +205,8 @@ def row_rooflines(cfg, n_loc, world, gen_s, sketch_s, gather_s, qrcp_s, solve_s,
                               else "32*l*n B (Y in and out once; k grid-synchronised steps)",
                               "hbm" if big else "latency")
     if est_s:
-        rows["a6_estimate"] = hbm_row((2 * q + 1) * 16.0 * m * n_loc, est_s,
-                                      f"(2q+1)*16*m*n_loc B (two passes per iteration, q = {q}, "
-                                      "plus the amax pass)")
+        rows["a6_estimate"] = hbm_row(2 * q * 16.0 * m * n_loc, est_s,
+                                      f"2q*16*m*n_loc B (two passes over A per iteration, q = {q})")
     return rows
 
 

@@ -147,18 +147,6 @@ __global__ void k_normalise(const double2* __restrict__ v, int64_t n_loc, const 
   if (vmax) vmax_update(vmax, mx);
 }
 
-// amax = max_ij |A_ij.re| + |A_ij.im| (bits, atomicMax): one pass over A per estimate
-__global__ void __launch_bounds__(256) k_absmax(const double2* __restrict__ A, int64_t lda,
-                                                int64_t m, int64_t n_loc,
-                                                unsigned long long* __restrict__ amax) {
-  double mx = 0.0;
-  for (int64_t j = blockIdx.x; j < n_loc; j += gridDim.x)
-    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
-      const double2 a = __ldcs(A + j * lda + i);
-      mx = fmax(mx, fabs(a.x) + fabs(a.y));
-    }
-  vmax_update(amax, mx);
-}
 
 // ---- u partials: part[chunk][t] = sum_{j in chunk} P[t, j] x[j] -------------------------------
 __global__ void k_px(const double2* __restrict__ P, int64_t ldp, int64_t k, int64_t n_loc,
@@ -386,10 +374,14 @@ constexpr int kEstBoxA = kEstRows * 8 * 16;  // bytes of one A box (8 columns)
 // w partials: item = (row block rb, column split sp); 256 threads: row r = tid & 127, column half
 // h = tid >> 7 (columns 4h..4h+3 of every box); the halves merge in order h = 0, 1 at item end.
 // Stage = A box + the 8 x values of its columns (128 B, 1D box).
+// FIRST (the first iteration): Dot2 accumulators, which need no bound, and the pass records
+// amax = max |Re A| + |Im A| into amax_out on the way (no separate pass over A for the bound)
+template <bool FIRST>
 __global__ void __launch_bounds__(256, 2)
     k_ax_tma(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapX,
              int64_t m, int rblocks, int nitems, int64_t split_cols, int64_t n_loc,
-             const unsigned long long* __restrict__ bounds, double* __restrict__ part) {
+             const unsigned long long* __restrict__ bounds, double* __restrict__ part,
+             unsigned long long* __restrict__ amax_out) {
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t full[kEstNS], empty[kEstNS];
   __shared__ double4 shalf[128];  // the h = 1 half's accumulators, merged by h = 0
@@ -421,13 +413,18 @@ __global__ void __launch_bounds__(256, 2)
   if (tid == 0)
     for (int64_t q = 0; q < kEstNS - 1 && q < nq; ++q) issue(q);
   int64_t q = 0;
+  double amx = 0.0;
   for (int ii = 0; ii < my_items; ++ii) {
     const int it = blockIdx.x + ii * gridDim.x;
     const int rb = it % rblocks, sp = it / rblocks;
-    const double C = fdd_offset(bounds, split_cols);  // same for every item of the launch
+    const double C = FIRST ? 0.0 : fdd_offset(bounds, split_cols);  // same for every item
     cfdd acc[4];  // one per column slot: four independent dependency chains
+    cdd acc1[4];  // FIRST: Dot2
 #pragma unroll
-    for (int c = 0; c < 4; ++c) cfdd_init(acc[c], C);
+    for (int c = 0; c < 4; ++c) {
+      cfdd_init(acc[c], C);
+      cdd_zero(acc1[c]);
+    }
     for (int b = 0; b < nb; ++b, ++q) {
       if (tid == 0 && q + kEstNS - 1 < nq) {
         const int64_t qn = q + kEstNS - 1;
@@ -443,15 +440,20 @@ __global__ void __launch_bounds__(256, 2)
         const int cc = 4 * h + c;
         const double2 av = *reinterpret_cast<const double2*>(st + (cc * kEstRows + r) * 16);
         const double2 xv = *reinterpret_cast<const double2*>(st + kEstBoxA + cc * 16);
-        cfdd_mac(acc[c], av, xv, false);
+        if (FIRST) {
+          cdd_mac(acc1[c], av, xv, false);
+          amx = fmax(amx, fabs(av.x) + fabs(av.y));
+        } else {
+          cfdd_mac(acc[c], av, xv, false);
+        }
       }
       fence_proxy_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    cdd a = cfdd_value(acc[0], C);
+    cdd a = FIRST ? acc1[0] : cfdd_value(acc[0], C);
 #pragma unroll
-    for (int c = 1; c < 4; ++c) cdd_merge(a, cfdd_value(acc[c], C));
+    for (int c = 1; c < 4; ++c) cdd_merge(a, FIRST ? acc1[c] : cfdd_value(acc[c], C));
     if (h == 1) shalf[r] = make_double4(a.re.s, a.re.c, a.im.s, a.im.c);
     __syncthreads();
     if (h == 0) {
@@ -465,6 +467,7 @@ __global__ void __launch_bounds__(256, 2)
     }
     __syncthreads();
   }
+  if (FIRST) vmax_update(amax_out, amx);
 }
 
 // z = round(A^H y − P^H sb): item = 8 consecutive columns, warp w owns column 8 item + w; lane
@@ -636,14 +639,6 @@ cudaError_t est_merge_scalar(const double* part, int nparts, double* out, cudaSt
   k_merge_scalar<<<1, 256, 0, st>>>(part, nparts, out);
   return cudaGetLastError();
 }
-cudaError_t est_absmax(const double2* A, int64_t lda, int64_t m, int64_t n_loc,
-                       unsigned long long* amax, const EstPlan& p, cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(amax, 0, sizeof(unsigned long long), st);
-  if (e != cudaSuccess) return e;
-  const int64_t g = n_loc < 8 * (int64_t)p.num_sms ? n_loc : 8 * (int64_t)p.num_sms;
-  k_absmax<<<(unsigned)g, 256, 0, st>>>(A, lda, m, n_loc, amax);
-  return cudaGetLastError();
-}
 cudaError_t est_normalise(const double2* v, int64_t n_loc, const double* nn, double2* x,
                           double* est_out, unsigned long long* vmax, cudaStream_t st) {
   if (vmax) {
@@ -671,8 +666,8 @@ cudaError_t est_merge_vec(const double* part, int nparts, int64_t len, double* o
   return cudaGetLastError();
 }
 cudaError_t est_ax(const double2* A, int64_t lda, int64_t m, int64_t n_loc, const double2* x,
-                   const unsigned long long* bounds, double* part, const EstPlan& p,
-                   cudaStream_t st) {
+                   unsigned long long* bounds, double* part, const EstPlan& p, cudaStream_t st,
+                   bool first) {
   if (p.tma) {
     CUtensorMap mapA, mapX;
     cudaError_t e = est_maps(A, lda, m, n_loc, x, n_loc, 16, &mapA, &mapX);
@@ -680,15 +675,23 @@ cudaError_t est_ax(const double2* A, int64_t lda, int64_t m, int64_t n_loc, cons
     const size_t smem = (size_t)kEstNS * (kEstBoxA + 128);
     static bool attr = false;
     if (!attr) {
-      if ((e = cudaFuncSetAttribute(k_ax_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      if ((e = cudaFuncSetAttribute(k_ax_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem)) != cudaSuccess ||
+          (e = cudaFuncSetAttribute(k_ax_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     (int)smem)) != cudaSuccess)
         return e;
       attr = true;
     }
     const int nitems = p.ax_rblocks * p.ax_parts;
     const int grid = nitems < 2 * p.num_sms ? nitems : 2 * p.num_sms;
-    k_ax_tma<<<grid, 256, smem, st>>>(mapA, mapX, m, p.ax_rblocks, nitems, p.ax_split_cols, n_loc,
-                                      bounds, part);
+    if (first) {  // amax (bounds[0]) is recorded by this pass
+      if ((e = cudaMemsetAsync(bounds, 0, sizeof(unsigned long long), st)) != cudaSuccess) return e;
+      k_ax_tma<true><<<grid, 256, smem, st>>>(mapA, mapX, m, p.ax_rblocks, nitems,
+                                              p.ax_split_cols, n_loc, bounds, part, bounds);
+    } else {
+      k_ax_tma<false><<<grid, 256, smem, st>>>(mapA, mapX, m, p.ax_rblocks, nitems,
+                                               p.ax_split_cols, n_loc, bounds, part, nullptr);
+    }
     return cudaGetLastError();
   }
   dim3 grid((unsigned)((m + 255) / 256), (unsigned)p.ax_parts);

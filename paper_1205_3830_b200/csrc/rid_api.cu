@@ -955,11 +955,7 @@ rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, 
   RID_CUDA(c, rid::est_x0(seed, col0, n_loc, x, (double*)pnp, pl, c->stream));
   RID_TRY(scalar_allreduce((const double*)pnp, pl.x0_blocks));
   RID_CUDA(c, rid::est_normalise(x, n_loc, nn_final, x, nullptr, bax + 1, c->stream));
-  if (pl.tma) {
-    RID_CUDA(c, rid::est_absmax((const double2*)a.dev, lda, m, n_loc, bax, pl, c->stream));
-    RID_CUDA(c, cudaMemcpyAsync(bz, bax, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
-                                c->stream));
-  }
+  // amax (the fixed-offset bound) comes from the first iteration's A x pass (Dot2 there)
   RID_CUDA(c, cudaEventRecord(ev[1], c->stream));
   for (int it = 0; it < q; ++it) {
     // u = P x (replicated after the exchange)
@@ -971,7 +967,11 @@ rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, 
       RID_CUDA(c, cudaMemcpyAsync(u, psb, sizeof(double) * 4 * k, cudaMemcpyDeviceToDevice, c->stream));
     }
     // y = A x - B u (replicated)
-    RID_CUDA(c, rid::est_ax((const double2*)a.dev, lda, m, n_loc, x, bax, (double*)pax, pl, c->stream));
+    RID_CUDA(c, rid::est_ax((const double2*)a.dev, lda, m, n_loc, x, bax, (double*)pax, pl, c->stream,
+                            it == 0));
+    if (pl.tma && it == 0)
+      RID_CUDA(c, cudaMemcpyAsync(bz, bax, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                                  c->stream));
     if (coll) {
       double* w_loc = (double*)pwall + (size_t)4 * m * c->rank;
       RID_CUDA(c, rid::est_merge_vec((const double*)pax, pl.ax_parts, m, w_loc, c->stream));
@@ -994,7 +994,7 @@ rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, 
     rid_diag d{};
     d.t_total = ev_ms(ev[0], ev[2]) * 1e-3;
     d.t_h2d = ev_ms(ev[0], ev[1]) * 1e-3;
-    d.launches = 3 + 4 + q * (3 + 4 + (coll ? 2 : 1) + 1);
+    d.launches = 3 + 3 + q * (3 + 4 + (coll ? 2 : 1) + 1);
     *diag = d;
   }
   return RID_OK;

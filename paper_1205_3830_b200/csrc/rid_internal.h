@@ -157,10 +157,8 @@ EstPlan est_plan(int64_t m, int64_t n_loc, int64_t k, int num_sms);
 cudaError_t est_x0(uint64_t seed, int64_t col0, int64_t n_loc, double2* x, double* part,
                    const EstPlan& p, cudaStream_t st);
 cudaError_t est_merge_scalar(const double* part, int nparts, double* out, cudaStream_t st);
-// vmax / amax: max |re| + |im| of the produced vector / of A (atomicMax on the bits; zeroed by
-// the launcher), the bounds of the fixed-offset accumulation in the TMA passes
-cudaError_t est_absmax(const double2* A, int64_t lda, int64_t m, int64_t n_loc,
-                       unsigned long long* amax, const EstPlan& p, cudaStream_t st);
+// vmax: max |re| + |im| of the produced vector (atomicMax on the bits; zeroed by the launcher),
+// with amax (from the first A x pass) the bounds of the fixed-offset accumulation
 cudaError_t est_normalise(const double2* v, int64_t n_loc, const double* nn, double2* x,
                           double* est_out, unsigned long long* vmax, cudaStream_t st);
 cudaError_t est_px(const double2* P, int64_t ldp, int64_t k, int64_t n_loc, const double2* x,
@@ -168,9 +166,10 @@ cudaError_t est_px(const double2* P, int64_t ldp, int64_t k, int64_t n_loc, cons
 cudaError_t est_merge_vec(const double* part, int nparts, int64_t len, double* out,
                           cudaStream_t st);
 // bounds = {amax, xmax} (est_ax) / {amax, ymax} (est_z), device
+// first = true: the first iteration's pass, Dot2 and recording amax into bounds[0]
 cudaError_t est_ax(const double2* A, int64_t lda, int64_t m, int64_t n_loc, const double2* x,
-                   const unsigned long long* bounds, double* part, const EstPlan& p,
-                   cudaStream_t st);
+                   unsigned long long* bounds, double* part, const EstPlan& p, cudaStream_t st,
+                   bool first = false);
 cudaError_t est_y(const double* wpart, int nparts, int64_t m, const double2* B, int64_t ldb,
                   int64_t k, const double* u, double2* y, unsigned long long* vmax,
                   cudaStream_t st);
