@@ -175,7 +175,8 @@ rid_status rid_decompose(rid_ctx* ctx, const rid_z* A, int64_t m, int64_t n, int
  * normalised, q fixed iterations of y = A x - B (P x), z = A^H y - P^H (B^H y), est = sqrt(||z||),
  * x = z / ||z||, with compensated accumulation in every dot product: TwoProd + TwoSum (Dot2), and
  * in the two streaming passes over A TwoProd + Fast2Sum against a power-of-two offset above a
- * bound from max|A| (one extra pass) and max|x| / max|y| (error-free as well; R16').
+ * bound from max|A| (recorded by the first iteration's pass, which runs Dot2) and max|x| / max|y|
+ * (error-free as well; R16').
  * J are global column ids (as returned by rid_decompose), P the local k x n_loc block.
  * *est is written on the host. Preconditions: q >= 1, shapes as above. */
 rid_status rid_error_estimate(rid_ctx* ctx, const rid_z* A, int64_t m, int64_t n, int64_t col0,
