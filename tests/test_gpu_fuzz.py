@@ -2,7 +2,9 @@
 (m, n, k, l, noise) pick every sketch tile height (24 / 40 / 48 rows), ragged K and column tails,
 split-K, the small and the blocked QR and both R11^-1 kernels. Bars as everywhere: generated A
 bitwise, Y <= 1e-12 relative (reading R31), J equal (R18), P <= 1e-10 (R17).
-tools/fuzz_parity.py runs the same sweep at larger counts (60 of 60 on B200 at the round's end)."""
+tools/fuzz_parity.py runs the same sweep at larger counts, also for the SRFT and the CGS2 QR (at
+the round's end on B200: 150/150 Gaussian + Householder, 60/60 SRFT + Householder, 60/60 SRFT +
+CGS2 — the paper's own algorithm — and 60/60 Gaussian + CGS2)."""
 import numpy as np
 import pytest
 
@@ -49,3 +51,33 @@ def test_random_shape_parity(rid, orc, seed, m, n, k, l, noise):
     assert r.J.cpu().numpy().tolist() == list(d.J)
     P = r.P.cpu().numpy()
     assert np.linalg.norm(P - d.P) <= 1e-10 * np.linalg.norm(d.P)
+
+
+def _srft_shapes(count, seed):
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(count):
+        m = int(2 ** rng.integers(5, 12))
+        n = int(rng.integers(1, 1000))
+        k = int(rng.integers(1, min(m, n, 150) + 1))
+        l = int(min(m, k + rng.integers(0, 40)))
+        out.append((int(rng.integers(1, 1 << 30)), m, n, k, l,
+                    float(rng.choice([0.0, 1e-12, 1e-9]))))
+    return out
+
+
+@pytest.mark.parametrize("seed,m,n,k,l,noise", _srft_shapes(6, 77))
+def test_random_shape_parity_srft_cgs2(rid, orc, seed, m, n, k, l, noise):
+    """The paper's own algorithm end to end (SRFT randomisation, Gram-Schmidt QR) on random
+    shapes against the oracle's SRFT + CGS2."""
+    A = rid.generate(seed, m, n, k, noise)
+    A_o = orc.generate(seed, m, n, k, noise)
+    Y = rid.sketch_srft(A, seed, l).cpu().numpy()
+    Y_o = orc.srft_sketch(A_o, seed, l)
+    assert np.linalg.norm(Y - Y_o) <= 1e-12 * np.linalg.norm(Y_o)
+    r = rid.decompose(A, k, l, seed, sketch="srft", qr="cgs2")
+    d = orc.decompose(A_o, k, l, seed, sketch_kind="srft")
+    assert r.J.cpu().numpy().tolist() == list(d.J)
+    P = r.P.cpu().numpy()
+    assert np.linalg.norm(P - d.P) <= 1e-10 * np.linalg.norm(d.P)
+

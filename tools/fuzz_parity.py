@@ -1,7 +1,8 @@
 """Randomised parity sweep of the whole CUDA path against the oracle on small random shapes
 (every kernel variant the shapes select: 24/40/48-row sketch tiles, K tails, split-K, the
 small and blocked QR, both solves), seeded and reproducible.
-    python tools/fuzz_parity.py [count] [seed]"""
+    python tools/fuzz_parity.py [count] [seed] [gaussian|srft] [householder|cgs2]
+(srft: m is drawn as a power of two, the paper's randomisation Y = S F D A)"""
 import os
 import sys
 
@@ -13,10 +14,12 @@ import paper_1205_3830_b200 as rid  # noqa: E402
 
 count = int(sys.argv[1]) if len(sys.argv) > 1 else 40
 rng = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 12345)
+kind = sys.argv[3] if len(sys.argv) > 3 else "gaussian"
+qr = sys.argv[4] if len(sys.argv) > 4 else "householder"
 oracle.build()
 bad = 0
 for it in range(count):
-    m = int(rng.integers(16, 3000))
+    m = int(2 ** rng.integers(5, 12)) if kind == "srft" else int(rng.integers(16, 3000))
     n = int(rng.integers(1, 1500))
     k = int(rng.integers(1, min(m, n, 300) + 1))
     l = int(min(m, k + rng.integers(0, 40)))
@@ -26,13 +29,17 @@ for it in range(count):
     A_o = oracle.generate(seed, m, n, k, noise)
     ok_a = np.array_equal(np.ascontiguousarray(A.cpu().numpy()).view(np.uint64),
                           np.ascontiguousarray(A_o).view(np.uint64))
-    Y = rid.sketch(A, seed, l).cpu().numpy()
-    Y_o = oracle.sketch(A_o, seed, l)
+    if kind == "srft":
+        Y = rid.sketch_srft(A, seed, l).cpu().numpy()
+        Y_o = oracle.srft_sketch(A_o, seed, l)
+    else:
+        Y = rid.sketch(A, seed, l).cpu().numpy()
+        Y_o = oracle.sketch(A_o, seed, l)
     ry = np.linalg.norm(Y - Y_o) / max(np.linalg.norm(Y_o), 1e-300)
     msg = ""
     try:
-        r = rid.decompose(A, k, l, seed)
-        d = oracle.decompose(A_o, k, l, seed)
+        r = rid.decompose(A, k, l, seed, sketch=kind, qr=qr)
+        d = oracle.decompose(A_o, k, l, seed, sketch_kind=kind)
         J, P = r.J.cpu().numpy(), r.P.cpu().numpy()
         same_j = J.tolist() == list(d.J)
         rp = np.linalg.norm(P - d.P) / max(np.linalg.norm(d.P), 1e-300) if same_j else float("nan")
