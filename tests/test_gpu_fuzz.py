@@ -75,8 +75,16 @@ def test_random_shape_parity_srft_cgs2(rid, orc, seed, m, n, k, l, noise):
     Y = rid.sketch_srft(A, seed, l).cpu().numpy()
     Y_o = orc.srft_sketch(A_o, seed, l)
     assert np.linalg.norm(Y - Y_o) <= 1e-12 * np.linalg.norm(Y_o)
+    # sampling rows with replacement can leave l <= m sampled rows rank-deficient
+    # (duplicates): then both sides must report the rank failure after the one retry
+    try:
+        d = orc.decompose(A_o, k, l, seed, sketch_kind="srft")
+    except orc.OracleError as e:
+        assert e.status == orc.RID_ERANK
+        with pytest.raises(rid.RidError, match="RANK"):
+            rid.decompose(A, k, l, seed, sketch="srft", qr="cgs2")
+        return
     r = rid.decompose(A, k, l, seed, sketch="srft", qr="cgs2")
-    d = orc.decompose(A_o, k, l, seed, sketch_kind="srft")
     assert r.J.cpu().numpy().tolist() == list(d.J)
     P = r.P.cpu().numpy()
     assert np.linalg.norm(P - d.P) <= 1e-10 * np.linalg.norm(d.P)

@@ -38,8 +38,15 @@ for it in range(count):
     ry = np.linalg.norm(Y - Y_o) / max(np.linalg.norm(Y_o), 1e-300)
     msg = ""
     try:
+        try:
+            d = oracle.decompose(A_o, k, l, seed, sketch_kind=kind)
+        except oracle.OracleError as oe:  # rank-deficient sketch: the GPU must say so as well
+            try:
+                rid.decompose(A, k, l, seed, sketch=kind, qr=qr)
+                raise RuntimeError(f"oracle failed ({oe}) but the GPU path did not")
+            except rid.RidError as ge:
+                raise ge from None
         r = rid.decompose(A, k, l, seed, sketch=kind, qr=qr)
-        d = oracle.decompose(A_o, k, l, seed, sketch_kind=kind)
         J, P = r.J.cpu().numpy(), r.P.cpu().numpy()
         same_j = J.tolist() == list(d.J)
         rp = np.linalg.norm(P - d.P) / max(np.linalg.norm(d.P), 1e-300) if same_j else float("nan")
