@@ -492,27 +492,51 @@ cudaError_t sketch_gemm(const double2* R, int64_t ldr, const double* Rs, const d
   int64_t nmain = ncols;
   if (t.cols > 0 && col0 + ncols > tail0) nmain = tail0 > col0 ? tail0 - col0 : 0;
   cudaError_t e = cudaSuccess;
-  // the K-split tail set runs on the aux stream (when given), launched after the main product so
-  // its CTAs take the SMs the main launch's last wave leaves idle; disjoint columns of Y
-  const bool fork = aux && aux->stream && nmain > 0 && nmain < ncols;
+  // row split: when the 48-row tile (the most efficient) does not divide l but l = 48 a + r with
+  // r a tile height of its own (24 / 32 / 40, e.g. C5: 272 = 5 x 48 + 32), rows [0, 48 a) run on
+  // 48-row tiles and the last r rows on r-row tiles (aux stream) instead of padding l to a single
+  // height (C5: 40-row tiles, 280 rows). Each element's chain is the same: Y is bitwise unchanged.
+  int rsplit = 0;
+  if (zgemm3m_tma_enabled(l) && Rs && l > 48 && !getenv("RID_SKETCH_NOROWSPLIT")) {
+    const int64_t r = l % 48;
+    if (r == 24 || r == 32 || r == 40) rsplit = (int)r;
+  }
+  const bool use_aux = aux && aux->stream;
+  // the K-split tail set (and the r-row part) run on the aux stream, launched after the main
+  // product so their CTAs take the SMs the main launch's last wave leaves idle
+  const bool fork = use_aux && nmain > 0 && (nmain < ncols || rsplit);
   if (fork) {
     if ((e = cudaEventRecord(aux->fork, st)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(aux->stream, aux->fork, 0)) != cudaSuccess) return e;
   }
-  if (nmain > 0) {
+  if (nmain > 0 && rsplit) {
+    const int64_t l48 = l - rsplit;
+    e = zgemm3m_tma_rows(R, ldr, Rs, rsum_ld(l), A, lda, Y, ldy, l48, nmain, m, st, ksplit,
+                         partial, 48);
+    *launches += ksplit > 1 ? 2 : 1;
+    if (e != cudaSuccess) return e;
+    e = zgemm3m_tma_rows(R + l48, ldr, Rs + l48, rsum_ld(l), A, lda, Y + l48, ldy, rsplit, nmain,
+                         m, fork ? aux->stream : st, ksplit,
+                         partial ? partial + (int64_t)ksplit * l48 * nmain : nullptr, rsplit);
+    *launches += ksplit > 1 ? 2 : 1;
+    if (e != cudaSuccess) return e;
+  } else if (nmain > 0) {
     e = zgemm3m(R, ldr, Rs, rsum_ld(l), A, lda, Y, ldy, l, nmain, m, st, ksplit, partial);
     *launches += ksplit > 1 ? 2 : 1;
     if (e != cudaSuccess) return e;
   }
   if (nmain < ncols) {
+    // (the tail's partials may not overlap the r-row part's, which runs concurrently)
+    double2* tpart = partial;
+    if (fork && rsplit && ksplit > 1) tpart = nullptr;  // not reached: the tail set needs S = 1
     e = zgemm3m(R, ldr, Rs, rsum_ld(l), A + nmain * lda, lda, Y + nmain * ldy, ldy, l,
-                ncols - nmain, m, fork ? aux->stream : st, t.S, partial);
+                ncols - nmain, m, fork ? aux->stream : st, t.S, tpart);
     *launches += 2;
     if (e != cudaSuccess) return e;
-    if (fork) {
-      if ((e = cudaEventRecord(aux->join, aux->stream)) != cudaSuccess) return e;
-      if ((e = cudaStreamWaitEvent(st, aux->join, 0)) != cudaSuccess) return e;
-    }
+  }
+  if (fork) {
+    if ((e = cudaEventRecord(aux->join, aux->stream)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(st, aux->join, 0)) != cudaSuccess) return e;
   }
   return e;
 }

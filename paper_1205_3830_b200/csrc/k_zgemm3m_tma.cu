@@ -358,6 +358,25 @@ cudaError_t zgemm3m_tma(const double2* Rm, int64_t ldr, const double* Rs, int64_
 #undef RID_L3T
 }
 
+// One tile height forced (48 / 40 / 32 / 24 rows), with the Re R + Im R plane when given: the two
+// parts of a row-split sketch (sketch_gemm)
+cudaError_t zgemm3m_tma_rows(const double2* Rm, int64_t ldr, const double* Rs, int64_t ldrs,
+                             const double2* Bm, int64_t ldb, double2* C, int64_t ldc, int64_t Mout,
+                             int64_t N, int64_t K, cudaStream_t st, int ksplit, double2* partial,
+                             int rows) {
+  if (Mout <= 0 || N <= 0) return cudaSuccess;
+#define RID_L3T(...) \
+  launch3t<__VA_ARGS__>(Rm, ldr, Rs, ldrs, Bm, ldb, C, ldc, Mout, N, K, st, ksplit, partial)
+  switch (rows) {
+    case 48: return Rs ? RID_L3T(2, 3, 4, 2, 2, 2, 1) : RID_L3T(2, 3, 4, 2, 3, 2, 0);
+    case 40: return Rs ? RID_L3T(1, 5, 8, 1, 3, 2, 1) : RID_L3T(1, 5, 8, 1, 3, 2, 0);
+    case 32: return Rs ? RID_L3T(2, 2, 4, 2, 2, 2, 1) : RID_L3T(2, 2, 4, 2, 3, 2, 0);
+    case 24: return Rs ? RID_L3T(1, 3, 8, 1, 3, 2, 1) : RID_L3T(1, 3, 8, 1, 3, 2, 0);
+    default: return cudaErrorInvalidValue;
+  }
+#undef RID_L3T
+}
+
 // The SRFT's residue products (k_srft.cu): bt.roff = first row of product z in Rm (Mtot rows in
 // all), bt.boff = ELEMENT offset of its B block in Bm (a multiple of ldb: the block starts at
 // column boff / ldb of the Nb = nblk * N columns), bt.coff / bt.mout as for zgemm3m_batched.

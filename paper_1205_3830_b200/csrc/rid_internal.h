@@ -34,6 +34,10 @@ int zgemm3m_ksplit(int64_t Mout, int64_t K, int64_t n_ref, int num_sms);
 // for the tile sizes it covers (zgemm3m_tma_enabled) unless RID_Z3_TMA=0. Bit-identical results.
 int zgemm3m_tile_rows(int64_t Mout);
 bool zgemm3m_tma_enabled(int64_t Mout);
+cudaError_t zgemm3m_tma_rows(const double2* Rm, int64_t ldr, const double* Rs, int64_t ldrs,
+                             const double2* Bm, int64_t ldb, double2* C, int64_t ldc, int64_t Mout,
+                             int64_t N, int64_t K, cudaStream_t st, int ksplit, double2* partial,
+                             int rows);
 cudaError_t zgemm3m_tma(const double2* Rm, int64_t ldr, const double* Rs, int64_t ldrs,
                         const double2* Bm, int64_t ldb, double2* C, int64_t ldc, int64_t Mout,
                         int64_t N, int64_t K, cudaStream_t st, int ksplit, double2* partial);

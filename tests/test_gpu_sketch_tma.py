@@ -137,3 +137,16 @@ def test_tma_rings_repeatable(rid, monkeypatch):
     G0 = bits(rid.generate(3, 2500, 1000, 512, 0.0).cpu().numpy())
     for _ in range(8):
         assert np.array_equal(bits(rid.generate(3, 2500, 1000, 512, 0.0).cpu().numpy()), G0)
+
+
+@pytest.mark.parametrize("seed,m,n,l", [(1, 4096, 2048, 272), (2, 2048, 3000, 80), (3, 1500, 700, 88),
+                                        (4, 1024, 333, 72), (5, 65536, 128, 272)])
+def test_row_split_sketch_bitwise(rid, monkeypatch, seed, m, n, l):
+    """l = 48 a + r with r in {24, 32, 40} runs as 48-row tiles plus r-row tiles (sketch_gemm's
+    row split); every element is the same chain: Y equals the single-height plan bit for bit,
+    with and without split-K, and the decomposition is unchanged."""
+    A = rid.generate(seed, m, n, 16, 1e-9)
+    Y_s = rid.sketch(A, seed, l).cpu().numpy()
+    monkeypatch.setenv("RID_SKETCH_NOROWSPLIT", "1")
+    Y_1 = rid.sketch(A, seed, l).cpu().numpy()
+    assert np.array_equal(bits(Y_s), bits(Y_1))
