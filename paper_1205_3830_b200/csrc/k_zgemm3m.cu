@@ -496,8 +496,11 @@ cudaError_t sketch_gemm(const double2* R, int64_t ldr, const double* Rs, const d
   // r a tile height of its own (24 / 32 / 40, e.g. C5: 272 = 5 x 48 + 32), rows [0, 48 a) run on
   // 48-row tiles and the last r rows on r-row tiles (aux stream) instead of padding l to a single
   // height (C5: 40-row tiles, 280 rows). Each element's chain is the same: Y is bitwise unchanged.
+  // (only with the aux stream: run serially after the main part, the r-row part's lone partial
+  // wave costs more than the padding saves, e.g. the e2e path's 1 GiB column chunks)
   int rsplit = 0;
-  if (zgemm3m_tma_enabled(l) && Rs && l > 48 && !getenv("RID_SKETCH_NOROWSPLIT")) {
+  if (aux && aux->stream && zgemm3m_tma_enabled(l) && Rs && l > 48 &&
+      !getenv("RID_SKETCH_NOROWSPLIT")) {
     const int64_t r = l % 48;
     if (r == 24 || r == 32 || r == 40) rsplit = (int)r;
   }
