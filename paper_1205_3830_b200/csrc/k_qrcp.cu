@@ -98,13 +98,15 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   return v;
 }
 
+// Grid barrier: the CTA's writes are ordered before thread 0's arrival by bar.sync, the arrival is
+// a gpu-scope release reduction, the wait a gpu-scope acquire load (no full fences; the polling
+// is unslept: one thread per CTA on one L2 line)
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1u);
-    while (ld_acquire(bar) < target) __nanosleep(20);
-    __threadfence();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
+    while (ld_acquire(bar) < target) {
+    }
   }
   __syncthreads();
 }
