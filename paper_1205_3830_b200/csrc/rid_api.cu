@@ -169,16 +169,30 @@ constexpr uint32_t kStreamR = 4, kStreamRRetry = 20;
 
 // T = R11^-1 R12 for the shard's columns (reading R29), on the same complex-product kernel as
 // the sketch (Gauss's three products by default, R31), written straight into P_loc.
+// With the context's aux stream (created by the sketch) the product goes through sketch_gemm, so
+// k = 48 a + r (r = 24/32/40; C3 128, C4 512) runs its last r rows of T on r-row tiles beside the
+// 48-row launch (bitwise the same T). Adds its kernel launches to *launches.
 rid_status solve_T(rid_ctx* c, const double2* Rinv, int64_t k, const double2* Y, int64_t ldy,
-                   double2* P, int64_t ldp, int64_t n_loc) {
+                   double2* P, int64_t ldp, int64_t n_loc, int* launches = nullptr) {
+  int dummy = 0;
+  if (!launches) launches = &dummy;
   if (rid::sketch_mults() == 3) {
     void* ps;
     RID_TRY(ws_get(c, "Rinvs", sizeof(double) * rid::rsum_ld(k) * k, &ps));
     RID_CUDA(c, rid::rsum_fill(Rinv, k, k, k, (double*)ps, rid::rsum_ld(k), c->stream));
-    RID_CUDA(c, rid::zgemm3m(Rinv, k, (const double*)ps, rid::rsum_ld(k), Y, ldy, P, ldp, k, n_loc,
-                             k, c->stream, 1, nullptr));
+    *launches += 1;
+    if (c->aux_stream && !getenv("RID_SOLVE_NOAUX")) {
+      const rid::SketchAux aux{c->aux_stream, c->aux_fork, c->aux_join};
+      RID_CUDA(c, rid::sketch_gemm(Rinv, k, (const double*)ps, Y, ldy, P, ldp, k, n_loc, k,
+                                   c->stream, 1, nullptr, 0, n_loc, c->num_sms, launches, &aux));
+    } else {
+      RID_CUDA(c, rid::zgemm3m(Rinv, k, (const double*)ps, rid::rsum_ld(k), Y, ldy, P, ldp, k,
+                               n_loc, k, c->stream, 1, nullptr));
+      *launches += 1;
+    }
   } else {
     RID_CUDA(c, rid::zgemm_ordered(Rinv, k, Y, ldy, P, ldp, k, n_loc, k, 0, 0.0, 0, 0, c->stream));
+    *launches += 1;
   }
   return RID_OK;
 }
@@ -703,9 +717,10 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
       RID_TRY(ws_get(c, "R11", sizeof(double2) * k * k, &pR11));
       RID_TRY(ws_get(c, "Rinv", sizeof(double2) * k * k, &pRinv));
       RID_CUDA(c, rid::tri_inverse((const double2*)pR11, k, (double2*)pRinv, c->stream));
-      RID_TRY(solve_T(c, (const double2*)pRinv, k, Yw + col0 * l, l, (double2*)p.dev, ldp, n_loc));
+      RID_TRY(solve_T(c, (const double2*)pRinv, k, Yw + col0 * l, l, (double2*)p.dev, ldp, n_loc,
+                      &d.launches));
       RID_CUDA(c, rid::assemble_identity(Jdev, k, col0, n_loc, (double2*)p.dev, ldp, c->stream));
-      d.launches += rid::sketch_mults() == 3 ? 4 : 3;  // R11^-1, (sum plane), T GEMM, identity
+      d.launches += 2;  // R11^-1, identity (solve_T counts the sum plane and the T GEMM)
     }
     RID_CUDA(c, rec(ev[7]));
     RID_TRY(stage_out(c, p, P, k, n_loc, ldp, sizeof(rid_z)));

@@ -150,3 +150,18 @@ def test_row_split_sketch_bitwise(rid, monkeypatch, seed, m, n, l):
     monkeypatch.setenv("RID_SKETCH_NOROWSPLIT", "1")
     Y_1 = rid.sketch(A, seed, l).cpu().numpy()
     assert np.array_equal(bits(Y_s), bits(Y_1))
+
+
+@pytest.mark.parametrize("seed,m,n,k,l", [(6, 3000, 2500, 80, 96), (7, 2048, 4000, 128, 144),
+                                          (8, 1200, 1500, 72, 88)])
+def test_row_split_solve_bitwise(rid, monkeypatch, seed, m, n, k, l):
+    """T = R11^-1 R12 with k = 48 a + r (r in {24, 32, 40}) runs its last r rows on r-row tiles
+    beside the 48-row launch (solve_T through sketch_gemm on the aux stream): J and P equal the
+    single-launch solve bit for bit."""
+    A = rid.generate(seed, m, n, k, 1e-10)
+    r_s = rid.decompose(A, k, l, seed)
+    J_s, P_s = r_s.J.cpu().numpy(), r_s.P.cpu().numpy()
+    monkeypatch.setenv("RID_SOLVE_NOAUX", "1")
+    r_1 = rid.decompose(A, k, l, seed)
+    assert np.array_equal(r_1.J.cpu().numpy(), J_s)
+    assert np.array_equal(bits(r_1.P.cpu().numpy()), bits(P_s))
