@@ -33,11 +33,28 @@ from paper_1205_3830_b200.configs import CONFIGS, HEADLINE_SEED  # noqa: E402
 
 METRIC = "ID sketch FP64-complex TFLOP/s & end-to-end ID s at 1/2/4/8 B200 vs roofline"
 UNIT = "TFLOP/s"
-# FP64 tensor-pipe (DMMA.8x8x4) peak measured on this pool's B200 with tools/microbench_fp64.cu:
-# 37.11 TFLOP/s sustained (400 launches, ~2 s) and 37.10 burst; clocks stayed at 1965 MHz
-# (profiles/r01_box_facts_fp64_microbench.txt). MEASURED_PEAKS.json has no FP64 entry.
-FP64_DMMA_PEAK_TFLOPS = 37.11
-FP64_PEAK_SOURCE = "measured DMMA m8n8k4 microbenchmark, profiles/r01_box_facts_fp64_microbench.txt"
+# FP64 tensor-pipe (DMMA.8x8x4) peak: measured on this pool's B200 by tools/fp64_peaks.py (the
+# microbenchmark under an nvidia-smi sampler) into profiles/fp64_peaks.json; MEASURED_PEAKS.json
+# (driver-written) has HBM and bf16 only. The sketch runs inside a long step, so the SUSTAINED
+# figure is its denominator (B200_PROFILING.md); burst and sustained agree for FP64 (no power cap).
+
+
+def fp64_peak():
+    """(peak TFLOP/s, source string) from profiles/fp64_peaks.json; the round-1 measurement
+    (37.11, profiles/r01_box_facts_fp64_microbench.txt, no clock record) if the file is absent."""
+    path = os.path.join(ROOT, "profiles", "fp64_peaks.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        if d.get("valid", True) and d.get("dmma_tflops_sustained"):
+            c = d.get("clocks", {})
+            return (float(d["dmma_tflops_sustained"]),
+                    f"profiles/fp64_peaks.json: DMMA sustained {d['dmma_tflops_sustained']:.2f} "
+                    f"(burst {d.get('dmma_tflops_burst', 0):.2f}) TFLOP/s at SM "
+                    f"{c.get('sm_mhz')} / {c.get('sm_max_mhz')} MHz, {d.get('when')}")
+    except (OSError, ValueError, KeyError):
+        pass
+    return 37.11, "profiles/r01_box_facts_fp64_microbench.txt (round 1, DMMA sustained)"
 
 
 def measured_peaks():
@@ -109,60 +126,120 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------------------ oracle arm -------
-def oracle_sample(cfg, seed: int, target_s: float = 15.0):
-    """The CPU oracle (as it stands) on a bounded sample of the workload: the sketch of n_s
-    columns of A (R regenerated inside, as the GPU step does). Returns (TFLOP/s, seconds, n_s,
-    threads)."""
+def cpu_model():
+    """The host CPU (lscpu's model name, sockets, logical CPUs) for the cpu_baseline record."""
+    info = {"model": None, "sockets": None, "cpus": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            k, _, v = ln.partition(":")
+            if k.strip() == "Model name":
+                info["model"] = v.strip()
+            elif k.strip() == "Socket(s)":
+                info["sockets"] = int(v.strip())
+    except (OSError, ValueError, subprocess.TimeoutExpired):
+        pass
+    return info
+
+
+def oracle_calibrate(cfg, seed: int, target_s: float):
+    """n_s: the number of columns whose oracle generation + sketch take about target_s on all host
+    cores (two-point calibration: fixed cost, e.g. regenerating R, + per-column cost)."""
     import oracle
 
     threads = oracle.set_threads(os.cpu_count() or 1)
 
     def timed(ncols):
-        A = oracle.generate(seed, cfg.m, cfg.n, cfg.k, cfg.noise, 0, ncols)
         t0 = time.perf_counter()
+        A = oracle.generate(seed, cfg.m, cfg.n, cfg.k, cfg.noise, 0, ncols)
         oracle.sketch(A, seed, cfg.l)
         return time.perf_counter() - t0
 
-    # two-point calibration: fixed cost (R regeneration) + per-column cost
     n1, n2 = threads, 4 * threads
     t1, t2 = timed(n1), timed(n2)
     per_col = max((t2 - t1) / (n2 - n1), 1e-9)
     fixed = max(t1 - n1 * per_col, 0.0)
     n_s = int((target_s - fixed) / per_col)
     n_s = max(threads, min(cfg.n, (n_s // threads) * threads))
-    A = oracle.generate(seed, cfg.m, cfg.n, cfg.k, cfg.noise, 0, n_s)
+    n_s = max(n_s, min(cfg.n, cfg.k + 8))  # the QR of the sample needs n_s > k columns
+    return n_s, threads
+
+
+def oracle_phases(cfg, seed: int, n_s: int, q: int = 1):
+    """Every §8(a) row of the CPU oracle (as it stands) on the first n_s columns of the workload:
+    generation, sketch (R regenerated inside), pivoted CGS2 of the l x n_s sample sketch,
+    back-substitution, and q iterations of the compensated estimator on the sample. Each phase's
+    work is linear in n at fixed (m, k, l), so `projected_full_s` scales it by n / n_s."""
+    import oracle
+
+    ph = {}
     t0 = time.perf_counter()
-    oracle.sketch(A, seed, cfg.l)
-    dt = time.perf_counter() - t0
-    return 8.0 * cfg.l * cfg.m * n_s / dt / 1e12, dt, n_s, threads
+    A = oracle.generate(seed, cfg.m, cfg.n, cfg.k, cfg.noise, 0, n_s)
+    ph["generate_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    Y = oracle.sketch(A, seed, cfg.l)
+    ph["sketch_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    qr = oracle.pivoted_qr(Y, cfg.k)
+    ph["qr_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    P = oracle.backsolve(qr.R, qr.J, cfg.k)
+    ph["solve_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    oracle.error_estimate(A, qr.J, P, q, seed)
+    ph["estimate_s"] = time.perf_counter() - t0
+    ph["estimate_q"] = q
+    ph["id_s"] = ph["sketch_s"] + ph["qr_s"] + ph["solve_s"]
+    f = cfg.n / n_s
+    ph["projected_full_s"] = {k: v * f for k, v in ph.items() if k.endswith("_s")}
+    return ph
+
+
+def oracle_record(cfg, seed: int, n_s: int, threads: int, ph: dict):
+    """cpu_baseline object: value = the metric (8 l m n_s / the oracle's ID seconds on the sample,
+    sketch + QR + solve, the rows the GPU step times)."""
+    tf = 8.0 * cfg.l * cfg.m * n_s / ph["id_s"] / 1e12
+    return {"value": tf, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": (f"oracle/rid_oracle.c on the first {n_s} of {cfg.n} columns of {cfg.name}: "
+                       f"sketch (naive ascending fused loops, R regenerated) + pivoted CGS2 of the "
+                       f"{cfg.l} x {n_s} sample sketch + back-substitution; value = 8*l*m*n_sample "
+                       f"/ those seconds ({threads} OpenMP threads)"),
+            "phases": ph, "cpu": cpu_model()}
 
 
 def run_reference(args, cfg):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return 0
-    steps = []
-    info = None
+    # each step one bounded sample, sized so warm-up + steps end within a few minutes
+    per_step = min(args.ref_seconds, 150.0 / max(1, args.steps + args.warmup))
+    n_s, threads = oracle_calibrate(cfg, args.seed, 0.8 * per_step)
+    recs = []
     for i in range(args.warmup + args.steps):
-        tf, dt, n_s, threads = oracle_sample(cfg, args.seed, target_s=args.ref_seconds)
+        ph = oracle_phases(cfg, args.seed, n_s, q=1)
         if i >= args.warmup:
-            steps.append((tf, dt))
-        info = (n_s, threads)
-    tf = statistics.median(s[0] for s in steps)
-    ms = statistics.median(s[1] for s in steps) * 1e3
-    sample = (f"oracle/rid_oracle.c sketch (naive ascending fused loops, R regenerated) of "
-              f"{info[0]} of {cfg.n} columns of {cfg.name}; TFLOP/s at 8*l*m*n_sample")
+            recs.append(ph)
+    ids = [r["id_s"] for r in recs]
+    id_s = statistics.median(ids)
+    tf = 8.0 * cfg.l * cfg.m * n_s / id_s / 1e12
+    rec = oracle_record(cfg, args.seed, n_s, threads, recs[len(recs) // 2])
+    rec["value"] = tf
     line = {"impl": "reference", "metric": METRIC, "value": tf, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": id_s * 1e3,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": cfg.name, "m": cfg.m, "n": cfg.n,
-                                            "k": cfg.k, "l": cfg.l, "noise": cfg.noise,
-                                            "seed": args.seed},
-            "cpu_baseline": {"value": tf, "unit": UNIT, "cores": info[1], "kind": "oracle",
-                             "sample": sample},
+            "data": "synthetic", "config": bench_config(cfg, args.seed),
+            "cpu_baseline": rec,
             "e2e": {"value": tf, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
+
+
+def bench_config(cfg, seed: int):
+    """The `config` object of both arms (identical keys: the driver compares them)."""
+    return {"workload": cfg.name, "m": cfg.m, "n": cfg.n, "k": cfg.k, "l": cfg.l,
+            "noise": cfg.noise, "seed": seed,
+            "l2": f"inputs larger than L2 (A = {16 * cfg.m * cfg.n / 2**30:.2f} GiB vs 126 MB)"
+            if 16 * cfg.m * cfg.n > 126 << 20 else "A fits in L2 (C1): not flushed"}
 
 
 # ------------------------------------------------------------------------------ per-row rooflines -
@@ -170,11 +247,10 @@ def row_rooflines(cfg, n_loc, world, gen_s, sketch_s, gather_s, qrcp_s, solve_s,
                   sketch_exec_tf):
     """Every SURVEY.md §8(a) row of the slowest rank against the roofline that bounds it
     (DESIGN.md §5): algorithmic work per call ÷ the measured phase time ÷ the measured peak
-    (DMMA 37.11 TFLOP/s, profiles/r01_box_facts_fp64_microbench.txt; HBM copy from
-    MEASURED_PEAKS.json). Work counts only what the method must do, not what a kernel re-reads."""
+    (DMMA: fp64_peak(), profiles/fp64_peaks.json; HBM copy from MEASURED_PEAKS.json). Work counts only what the method must do, not what a kernel re-reads."""
     m, n, k, l = cfg.m, cfg.n, cfg.k, cfg.l
     hbm = measured_peaks().get("hbm_gbs", 6536.7)
-    P = FP64_DMMA_PEAK_TFLOPS
+    P = fp64_peak()[0]
 
     def tensor(flops, t, what):
         a = flops / t / 1e12 if t else None
@@ -327,12 +403,11 @@ def run_ours(args, cfg):
     sketch_tf_rank = 8.0 * l * m * n_loc / sketch_s / 1e12  # slowest rank's kernel (8lmn)
     mults = rid.sketch_mults()  # 3: Gauss's three real products (6lmn executed), 4: real embedding
     sketch_exec_tf = sketch_tf_rank * mults / 4.0
+    peak, peak_src = fp64_peak()
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        tf, dt, n_s, threads = oracle_sample(cfg, seed, target_s=args.ref_seconds)
-        cpu = {"value": tf, "unit": UNIT, "cores": threads, "kind": "oracle",
-               "sample": f"oracle sketch of {n_s}/{cfg.n} columns of {cfg.name} "
-                         f"({dt:.1f} s, R regenerated, {threads} OpenMP threads)"}
+        n_s, threads = oracle_calibrate(cfg, seed, args.ref_seconds)
+        cpu = oracle_record(cfg, seed, n_s, threads, oracle_phases(cfg, seed, n_s, q=1))
     if rank != 0:
         return 0
     prof = {}
@@ -346,9 +421,8 @@ def run_ours(args, cfg):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
-        "config": {"workload": cfg.name, "m": m, "n": n, "k": k, "l": l, "noise": cfg.noise,
-                   "seed": seed, "parallelism": f"column-shard x{world}",
-                   "l2": f"inputs larger than L2 (A = {16 * m * n / 2**30:.2f} GiB vs 126 MB)"},
+        "config": bench_config(cfg, seed),
+        "parallelism": f"column-shard x{world}",
         "id_seconds": step_s,
         # every §8(a) row once (a1 generate + a2-a5 the ID + a6 the q-iteration estimate); the
         # headline value times the ID itself (a2-a5), the metric's "end-to-end ID"
@@ -363,15 +437,18 @@ def run_ours(args, cfg):
         if cfg.noise else None,
         "tie_margin_min": diags[-1]["tie_margin_min"],
         "roofline": {"bound": "tensor", "achieved": sketch_exec_tf,
-                     "peak": FP64_DMMA_PEAK_TFLOPS, "unit": "TFLOP/s",
-                     "frac": sketch_exec_tf / FP64_DMMA_PEAK_TFLOPS,
+                     "peak": peak, "unit": "TFLOP/s",
+                     "frac": sketch_exec_tf / peak,
+                     # the same launch in the metric's 8*l*m*n convention (Gauss 3M executes 3/4
+                     # of those products, so this can exceed 1)
+                     "achieved_8lmn": sketch_tf_rank, "frac_8lmn": sketch_tf_rank / peak,
                      "traffic": prof.get("dram_bytes_per_launch"),
                      "kernel": ("k_zgemm3m_tma (sketch Y = R A, Gauss 3M, DMMA.8x8x4, TMA-fed)" if mults == 3
                                 else "k_zgemm_dmma (sketch Y = R A, real embedding, DMMA.8x8x4)"),
                      "algorithmic": (f"{2 * mults}*l*m*n_loc = {2.0 * mults * l * m * n_loc:.4g} "
                                      f"flop per launch ({mults} real products per complex "
                                      f"multiply-add; the metric counts 8*l*m*n)"),
-                     "peak_source": FP64_PEAK_SOURCE},
+                     "peak_source": peak_src},
         "rows": row_rooflines(cfg, n_loc, world, gen_s, sketch_s, gather_s, qrcp_s, solve_s,
                               est_s, args.q, sketch_exec_tf),
         "cpu_baseline": cpu,
@@ -394,7 +471,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--seed", type=int, default=HEADLINE_SEED)
     ap.add_argument("--q", type=int, default=20, help="estimator iterations (0 = skip)")
-    ap.add_argument("--ref-seconds", type=float, default=15.0)
+    ap.add_argument("--ref-seconds", type=float, default=15.0,
+                    help="CPU seconds of each oracle sample (generation + sketch)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

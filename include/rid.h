@@ -95,6 +95,11 @@ typedef struct {
  * cudaStream_t owned by the caller; NULL = the legacy default stream, as everywhere in CUDA). */
 rid_status rid_create(rid_ctx** ctx, int device, void* cuda_stream);
 void rid_destroy(rid_ctx* ctx);
+/* Re-bind the context to `cuda_stream` (same meaning as in rid_create): subsequent calls are
+ * ordered on it. Work already enqueued stays ordered on the previous stream; the caller orders the
+ * two streams if the next call depends on it (the Python binding passes torch's current stream on
+ * every call of a default context, so both orders are torch's). */
+rid_status rid_set_stream(rid_ctx* ctx, void* cuda_stream);
 /* Last error message of this context ("" when none). Valid until the next call on ctx. */
 const char* rid_last_error(const rid_ctx* ctx);
 /* Library version string and the compiled GPU architecture ("sm_100a"). */
@@ -108,6 +113,17 @@ size_t rid_comm_id_bytes(void);
 rid_status rid_comm_get_id(void* id);
 /* Every rank: join the communicator of `nranks` ranks as `rank` (collective, blocking). */
 rid_status rid_comm_init(rid_ctx* ctx, const void* id, int rank, int nranks);
+/* In-process communicator over the `nranks` contexts ctxs[0..nranks-1] (one process, ONE device;
+ * context r becomes rank r). The collectives of rid_decompose / rid_error_estimate then run as
+ * device copies between the contexts' workspaces ordered by CUDA events, with a host rendezvous
+ * of the calling threads at each collective: every rank's calls must be made concurrently from
+ * its own host thread (exactly as with NCCL, one thread per rank). This is how the G > 1 data
+ * path runs on a machine with fewer GPUs than ranks (tests/test_gpu_multirank.py); results are
+ * the same bits as with NCCL (the all-gathers are copies; the one all-reduce, of B = A[:, J],
+ * adds one nonzero per element). RID_EINVAL: nranks outside [1, 64], repeated contexts, or
+ * contexts on different devices. A rank that does not reach a collective within 300 s makes
+ * every rank's call fail with RID_ENCCL. */
+rid_status rid_comm_init_local(rid_ctx** ctxs, int nranks);
 /* Query: rank and nranks (1, 0 when no communicator). */
 rid_status rid_comm_info(const rid_ctx* ctx, int* rank, int* nranks);
 

@@ -14,6 +14,7 @@ from __future__ import annotations
 
 import ctypes
 import os
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -59,7 +60,8 @@ EXPORTS = ["rid_create", "rid_destroy", "rid_last_error", "rid_version", "rid_co
            "rid_comm_get_id", "rid_comm_init", "rid_comm_info", "rid_generate", "rid_sketch",
            "rid_decompose", "rid_error_estimate", "rid_error_bound", "rid_normal_fill",
            "rid_qrcp", "rid_factor_solve", "rid_sketch_splits", "rid_sketch_srft",
-           "rid_set_sketch", "rid_sketch_mults", "rid_sketch_cols", "rid_set_qr"]
+           "rid_set_sketch", "rid_sketch_mults", "rid_sketch_cols", "rid_set_qr",
+           "rid_set_stream", "rid_comm_init_local"]
 SKETCH_GAUSSIAN, SKETCH_SRFT = 0, 1
 QR_HOUSEHOLDER, QR_CGS2 = 0, 1
 _QR_KINDS = {"householder": QR_HOUSEHOLDER, "cgs2": QR_CGS2}
@@ -79,6 +81,8 @@ def lib():
     sig = {
         "rid_create": ([ctypes.POINTER(p), ci, p], ci),
         "rid_destroy": ([p], None),
+        "rid_set_stream": ([p, p], ci),
+        "rid_comm_init_local": ([ctypes.POINTER(p), ci], ci),
         "rid_last_error": ([p], ctypes.c_char_p),
         "rid_version": ([], ctypes.c_char_p),
         "rid_comm_id_bytes": ([], ctypes.c_size_t),
@@ -127,9 +131,13 @@ def colmajor_empty(rows: int, cols: int, device="cuda", dtype=None, pin_memory=F
 
 
 class _Buf:
-    """(pointer, leading dimension, keep-alive) for a complex128 column-major matrix."""
+    """(pointer, leading dimension, keep-alive) for a complex128 column-major matrix.
 
-    def __init__(self, a, rows: int, cols: int, name: str):
+    Rejects (ValueError) any layout librid cannot address as (pointer, ld >= rows): a column stride
+    below the row count (broadcast / overlapping views), a stride that is not a whole number of
+    elements, and a CUDA tensor on another device than the context's."""
+
+    def __init__(self, a, rows: int, cols: int, name: str, ctx: "Context | None" = None):
         self.obj = a
         if isinstance(a, np.ndarray):
             if a.dtype != np.complex128:
@@ -140,6 +148,9 @@ class _Buf:
                 raise ValueError(f"{name}: shape {a.shape} != {(rows, cols)}")
             if cols > 1 and not a.flags.f_contiguous and a.strides[0] != 16:
                 raise ValueError(f"{name}: numpy array must be column-major (Fortran order)")
+            if cols > 1 and (a.strides[1] % 16 != 0 or a.strides[1] // 16 < rows):
+                raise ValueError(f"{name}: column stride {a.strides[1]} B is not a leading "
+                                 f"dimension >= {rows} complex128 elements")
             self.ptr = a.ctypes.data
             self.ld = a.strides[1] // 16 if cols > 1 else rows
             self.obj = a
@@ -153,6 +164,11 @@ class _Buf:
                 raise ValueError(f"{name}: shape {tuple(a.shape)} != {(rows, cols)}")
             if a.stride(0) != 1 and rows > 1:
                 raise ValueError(f"{name}: tensor must be column-major (stride(0) == 1)")
+            if cols > 1 and a.stride(1) < rows:
+                raise ValueError(f"{name}: column stride {a.stride(1)} < {rows} rows "
+                                 "(broadcast or overlapping view)")
+            if ctx is not None and a.is_cuda and a.device.index != ctx.device:
+                raise ValueError(f"{name}: tensor on {a.device}, context on cuda:{ctx.device}")
             self.ptr = a.data_ptr()
             self.ld = a.stride(1) if cols > 1 else max(rows, 1)
             self.obj = a
@@ -186,6 +202,14 @@ class Context:
         if st != RID_OK:
             raise RidError(st, f"rid_create(device={device}) failed (is a B200 visible?)")
         self.h = h
+        self._stream = sp.value if sp is not None else None
+
+    def set_stream(self, stream):
+        """Order subsequent calls on `stream` (a torch.cuda.Stream or a raw cudaStream_t)."""
+        s = stream if isinstance(stream, int) or stream is None else stream.cuda_stream
+        if s != self._stream:
+            self.check(self._L.rid_set_stream(self.h, ctypes.c_void_p(s)), "rid_set_stream")
+            self._stream = s
 
     def close(self):
         if getattr(self, "h", None):
@@ -214,6 +238,18 @@ class Context:
         return r.value, n.value
 
 
+def comm_init_local(ctxs) -> None:
+    """Join the contexts `ctxs` (one process, one device) into an in-process communicator, context
+    r as rank r (rid_comm_init_local). Each rank's calls must then run concurrently on its own
+    thread (tests/test_gpu_multirank.py): the G > 1 data path on one GPU."""
+    L = lib()
+    arr = (ctypes.c_void_p * len(ctxs))(*[c.h.value for c in ctxs])
+    st = L.rid_comm_init_local(arr, len(ctxs))
+    if st != RID_OK:
+        raise RidError(st, "rid_comm_init_local: " +
+                       L.rid_last_error(ctxs[0].h).decode(errors="replace"))
+
+
 def comm_get_id() -> bytes:
     L = lib()
     nb = L.rid_comm_id_bytes()
@@ -228,11 +264,15 @@ _default = {}
 
 
 def default_context(device=None) -> Context:
+    """The per-device context of calls made without ctx=, ordered on torch's CURRENT stream of
+    that device at each call (re-bound with rid_set_stream whenever it changes)."""
     torch = _torch()
     dev = torch.cuda.current_device() if device is None else device
     if dev not in _default:
         _default[dev] = Context(dev, torch.cuda.current_stream(dev))
-    return _default[dev]
+    ctx = _default[dev]
+    ctx.set_stream(torch.cuda.current_stream(dev))
+    return ctx
 
 
 def shard_range(n: int, rank: int, world: int):
@@ -253,7 +293,7 @@ def generate(seed: int, m: int, n: int, k: int, noise: float, col0: int = 0, n_l
     n_loc = n - col0 if n_loc is None else n_loc
     if out is None:
         out = colmajor_empty(m, n_loc, device=device)
-    b = _Buf(out, m, n_loc, "A")
+    b = _Buf(out, m, n_loc, "A", ctx)
     ctx.check(lib().rid_generate(ctx.h, seed, m, n, k, float(noise), col0, n_loc, b.ptr, b.ld),
               "rid_generate")
     return out
@@ -267,11 +307,11 @@ def sketch(A, seed: int, l: int, stream: int = STREAM_R, out=None, n: int | None
     ctx = ctx or default_context()
     m, n_loc = A.shape
     n = n_loc if n is None else n
-    a = _Buf(A, m, n_loc, "A")
+    a = _Buf(A, m, n_loc, "A", ctx)
     if out is None:
         out = colmajor_empty(l, n_loc, device=A.device if hasattr(A, "device") else "cpu") \
             if not isinstance(A, np.ndarray) else np.zeros((l, n_loc), np.complex128, order="F")
-    y = _Buf(out, l, n_loc, "Y")
+    y = _Buf(out, l, n_loc, "Y", ctx)
     ctx.check(lib().rid_sketch_cols(ctx.h, seed, stream, l, a.ptr, m, n, col0, n_loc, a.ld, y.ptr,
                                     y.ld), "rid_sketch")
     return out
@@ -283,11 +323,11 @@ def sketch_srft(A, seed: int, l: int, retry: bool = False, out=None, n: int | No
     ctx = ctx or default_context()
     m, n_loc = A.shape
     n = n_loc if n is None else n
-    a = _Buf(A, m, n_loc, "A")
+    a = _Buf(A, m, n_loc, "A", ctx)
     if out is None:
         out = colmajor_empty(l, n_loc, device=A.device if hasattr(A, "device") else "cpu") \
             if not isinstance(A, np.ndarray) else np.zeros((l, n_loc), np.complex128, order="F")
-    y = _Buf(out, l, n_loc, "Y")
+    y = _Buf(out, l, n_loc, "Y", ctx)
     ctx.check(lib().rid_sketch_srft(ctx.h, seed, int(retry), l, a.ptr, m, n, n_loc, a.ld, y.ptr,
                                     y.ld), "rid_sketch_srft")
     return out
@@ -328,7 +368,7 @@ def decompose(A, k: int, l: int, seed: int, n: int | None = None, col0: int = 0,
     _set_qr(ctx, qr)
     m, n_loc = A.shape
     n = n_loc if n is None else n
-    a = _Buf(A, m, n_loc, "A")
+    a = _Buf(A, m, n_loc, "A", ctx)
     host = isinstance(A, np.ndarray) or (hasattr(A, "device") and A.device.type == "cpu")
     if J is None:
         J = np.zeros(k, np.int64) if isinstance(A, np.ndarray) else _torch().empty(
@@ -337,10 +377,16 @@ def decompose(A, k: int, l: int, seed: int, n: int | None = None, col0: int = 0,
         P = np.zeros((k, n_loc), np.complex128, order="F") if isinstance(A, np.ndarray) else \
             colmajor_empty(k, n_loc, device="cpu" if host else A.device,
                            pin_memory=host and _torch().cuda.is_available())
-    p = _Buf(P, k, n_loc, "P")
+    p = _Buf(P, k, n_loc, "P", ctx)
     d = Diag()
     ctx.check(lib().rid_decompose(ctx.h, a.ptr, m, n, col0, n_loc, a.ld, k, l, seed, _ptr_i64(J),
                                   p.ptr, p.ld, ctypes.byref(d)), "rid_decompose")
+    if k > 1 and d.tie_margin_min < 1e-9:
+        # reading R18: below ~1e-9 the pivot choice is decided by rounding; the blocked QR's
+        # downdated norms (R11') may then pick another (equally valid) column than the
+        # exact-norm kernels or the oracle
+        warnings.warn(f"rid.decompose: near-tie pivot step (top-2 margin {d.tie_margin_min:.3g} "
+                      "< 1e-9); J is not uniquely determined at this precision", RuntimeWarning)
     return IdResult(J, P, d.as_dict())
 
 
@@ -351,8 +397,8 @@ def error_estimate(A, J, P, q: int, seed: int, n: int | None = None, col0: int =
     m, n_loc = A.shape
     k = P.shape[0]
     n = n_loc if n is None else n
-    a = _Buf(A, m, n_loc, "A")
-    p = _Buf(P, k, n_loc, "P")
+    a = _Buf(A, m, n_loc, "A", ctx)
+    p = _Buf(P, k, n_loc, "P", ctx)
     est = ctypes.c_double()
     d = Diag()
     ctx.check(lib().rid_error_estimate(ctx.h, a.ptr, m, n, col0, n_loc, a.ld, _ptr_i64(J), k, p.ptr,
@@ -371,7 +417,7 @@ def normal_fill(seed: int, s: int, rows: int, cols: int, row0: int = 0, col0: in
     ctx = ctx or default_context()
     if out is None:
         out = colmajor_empty(rows, cols, device=device)
-    b = _Buf(out, rows, cols, "out")
+    b = _Buf(out, rows, cols, "out", ctx)
     ctx.check(lib().rid_normal_fill(ctx.h, seed, s, rows, cols, row0, col0, b.ptr, b.ld),
               "rid_normal_fill")
     return out
@@ -384,7 +430,7 @@ def qrcp(Y, k: int, ctx: Context | None = None, want_R: bool = True, qr: str = "
     ctx = ctx or default_context()
     _set_qr(ctx, qr)
     l, n = Y.shape
-    y = _Buf(Y, l, n, "Y")
+    y = _Buf(Y, l, n, "Y", ctx)
     dev = Y.device
     J = torch.empty(k, dtype=torch.int64, device=dev)
     R = colmajor_empty(k, n, device=dev) if want_R else None
@@ -407,10 +453,10 @@ def factor_solve(Y, k: int, col0: int, n_loc: int, ctx: Context | None = None,
     ctx = ctx or default_context()
     _set_qr(ctx, qr)
     l, n = Y.shape
-    y = _Buf(Y, l, n, "Y")
+    y = _Buf(Y, l, n, "Y", ctx)
     J = torch.empty(k, dtype=torch.int64, device=Y.device)
     P = colmajor_empty(k, n_loc, device=Y.device)
-    p = _Buf(P, k, n_loc, "P")
+    p = _Buf(P, k, n_loc, "P", ctx)
     d = Diag()
     ctx.check(lib().rid_factor_solve(ctx.h, y.ptr, l, n, y.ld, k, col0, n_loc, J.data_ptr(), p.ptr,
                                      p.ld, ctypes.byref(d)), "rid_factor_solve")

@@ -1,8 +1,11 @@
 """Build librid.so (the C-ABI library of include/rid.h) in-tree for sm_100a with nvcc.
 
-    python -m paper_1205_3830_b200.build [--force]
+    python -m paper_1205_3830_b200.build [--force] [--experiments]
 
 The .so lands next to this file so it travels with the repo snapshot to the GPU box.
+--experiments (or RID_BUILD_EXPERIMENTS=1) compiles with -DRID_EXPERIMENTS, which makes the
+tuning knobs of the tools/ scripts (tile shapes, ring depths, ...; rid_host.h experiment_env)
+effective; the product build ignores them.
 """
 from __future__ import annotations
 
@@ -35,15 +38,32 @@ def headers():
                   [os.path.join(ROOT, "include", "rid.h")])
 
 
-def up_to_date() -> bool:
+STAMP = os.path.join(ROOT, "build", "rid_obj", "flags.txt")
+
+
+def _flags(experiments: bool):
+    return ["-DRID_EXPERIMENTS"] if experiments else []
+
+
+def up_to_date(experiments: bool = False) -> bool:
     if not os.path.exists(LIB):
         return False
+    try:
+        with open(STAMP) as f:
+            if f.read() != " ".join(_flags(experiments)):
+                return False
+    except OSError:
+        # no stamp (a fresh snapshot): the shipped .so is a product build
+        if experiments:
+            return False
     t = os.path.getmtime(LIB)
     return all(os.path.getmtime(f) <= t for f in sources() + headers() + [__file__])
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, experiments: bool | None = None) -> str:
+    if experiments is None:
+        experiments = os.environ.get("RID_BUILD_EXPERIMENTS", "0") not in ("", "0")
+    if not force and up_to_date(experiments):
         return LIB
     inc, libdir = _nccl_dirs()
     objdir = os.path.join(ROOT, "build", "rid_obj")
@@ -53,7 +73,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
-               "-Xptxas", "-v" if verbose else "-O3", "--expt-relaxed-constexpr",
+               "-Xptxas", "-v" if verbose else "-O3", "--expt-relaxed-constexpr", *_flags(experiments),
                "-I", inc, "-I", os.path.join(ROOT, "include"), "-c", src, "-o", obj]
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT,
                                             text=True)))
@@ -71,9 +91,12 @@ def build(force: bool = False, verbose: bool = False) -> str:
             f"-Xlinker=-rpath={libdir}", "-lcudart"]
     subprocess.check_call(link)
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as f:
+        f.write(" ".join(_flags(experiments)))
     return LIB
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv)
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+          experiments=True if "--experiments" in sys.argv else None)
     print(LIB)

@@ -650,19 +650,15 @@ cudaError_t cgs2(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, doubl
   const unsigned G = (unsigned)std::min<int64_t>(G0, (n + 7) / 8);
   const size_t sm_q = sizeof(double2) * (size_t)l;
   const size_t sm_c = sizeof(double2) * (size_t)k;
-  if (sm_q > 48 * 1024 &&
-      (e = cudaFuncSetAttribute(k_cgs_project, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sm_q)) != cudaSuccess)
+  if (sm_q > 48 * 1024 && (e = ensure_dyn_smem((const void*)k_cgs_project, sm_q)) != cudaSuccess)
     return e;
-  if (sm_c > 48 * 1024 &&
-      (e = cudaFuncSetAttribute(k_cgs_update, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)sm_c)) != cudaSuccess)
+  if (sm_c > 48 * 1024 && (e = ensure_dyn_smem((const void*)k_cgs_update, sm_c)) != cudaSuccess)
     return e;
   int nl = 0;
-  const char* ev = getenv("RID_CGS2_FUSED");  // 0: the multi-launch path (tests, measurements)
+  const char* ev = select_env("RID_CGS2_FUSED");  // 0: the multi-launch path (tests, measurements)
   bool fused = !(ev && ev[0] == '0');
   if (fused) {
-    const char* eo = getenv("RID_CGS2_OPT");
+    const char* eo = experiment_env("RID_CGS2_OPT");
     const int opt = eo ? atoi(eo) : 1;
     Cgs2Args a{W, l, n, k, Q, Qh, qbuf, coef, cand, chosen, &st->count, tol_rel, out, opt, trace};
     e = cgs2_fused(a, num_sms, stream);

@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(256, 2)
 }
 
 bool est_tma_enabled() {
-  const char* v = getenv("RID_EST_TMA");
+  const char* v = select_env("RID_EST_TMA");
   return !(v && atoi(v) == 0);
 }
 
@@ -673,15 +673,9 @@ cudaError_t est_ax(const double2* A, int64_t lda, int64_t m, int64_t n_loc, cons
     cudaError_t e = est_maps(A, lda, m, n_loc, x, n_loc, 16, &mapA, &mapX);
     if (e != cudaSuccess) return e;
     const size_t smem = (size_t)kEstNS * (kEstBoxA + 128);
-    static bool attr = false;
-    if (!attr) {
-      if ((e = cudaFuncSetAttribute(k_ax_tma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem)) != cudaSuccess ||
-          (e = cudaFuncSetAttribute(k_ax_tma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem)) != cudaSuccess)
-        return e;
-      attr = true;
-    }
+    if ((e = ensure_dyn_smem((const void*)k_ax_tma<true>, smem)) != cudaSuccess ||
+        (e = ensure_dyn_smem((const void*)k_ax_tma<false>, smem)) != cudaSuccess)
+      return e;
     const int nitems = p.ax_rblocks * p.ax_parts;
     const int grid = nitems < 2 * p.num_sms ? nitems : 2 * p.num_sms;
     if (first) {  // amax (bounds[0]) is recorded by this pass
@@ -722,13 +716,7 @@ cudaError_t est_z(const double2* A, int64_t lda, int64_t m, int64_t n_loc, const
     cudaError_t e = est_maps(A, lda, m, n_loc, y, m, 2 * kEstRows, &mapA, &mapY);
     if (e != cudaSuccess) return e;
     const size_t smem = (size_t)kEstNS * (kEstBoxA + kEstRows * 16);
-    static bool attr = false;
-    if (!attr) {
-      if ((e = cudaFuncSetAttribute(k_z_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    (int)smem)) != cudaSuccess)
-        return e;
-      attr = true;
-    }
+    if ((e = ensure_dyn_smem((const void*)k_z_tma, smem)) != cudaSuccess) return e;
     const int nitems = p.z_blocks;
     const int grid = nitems < 2 * p.num_sms ? nitems : 2 * p.num_sms;
     k_z_tma<<<grid, 256, smem, st>>>(mapA, mapY, m, n_loc, nitems, P, ldp, k, sb, z, bounds,

@@ -6,8 +6,15 @@
 // weighted vectors" (§2, Eqs. 8–9); the authors note Householder "should result
 // in similar stability with only half the runtime" of their CGS (§3.2).
 // Readings: R8 greedy max residual 2-norm pivot, ties -> lowest column index;
-// R11 the residual norms are recomputed exactly from the updated column every step (no
-// downdating); R13 rank failure when nu_p < 1e-13 * max_c ||Y[:, c]||.
+// R13 rank failure when nu_p < 1e-13 * max_c ||Y[:, c]||. Residual norms (R11 / R11'):
+//   * k_qrcp and k_qrcp_smem (the default for sketches under 64 MB: C1-C3) recompute every nu
+//     exactly from the updated column each step (no downdating), like the oracle;
+//   * k_qrcp_ring (the blocked default for larger sketches: C4, C5) DOWNDATES,
+//     nu_c^2 <- nu_c^2 - |R(j, c)|^2, and recomputes nu_c exactly only when it has cancelled below
+//     kRecompTol = 1e-4 of its last exact value (LAPACK zlaqps's safeguard, stricter). The
+//     downdate's relative error is <= j u / 1e-4 (~6e-10 at j = 512), far below the top-2 pivot
+//     gaps of the configs (>= 1.8e-6), so J is unchanged there; on inputs whose top-2 gap falls
+//     below ~1e-9 (rid_diag.tie_margin_min) J may differ from the exact kernels and the oracle.
 //
 // Deferred write-back (the kernel is HBM-bound: one step touches the whole trailing block):
 // steps are grouped in blocks of QB. Y is materialised only at block boundaries; inside a block,
@@ -1219,8 +1226,7 @@ static cudaError_t launch_qrcp(double2* Y, int64_t ldy, int l, int64_t n, int k,
                                const QrcpOut& out, const QrcpWork& w, int num_sms,
                                cudaStream_t st, int* launches) {
   const size_t smem = sizeof(double2) * kQB * MAXQ * 32;
-  cudaError_t e = cudaFuncSetAttribute(k_qrcp<MAXQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  cudaError_t e = ensure_dyn_smem((const void*)k_qrcp<MAXQ>, smem);
   if (e != cudaSuccess) return e;
   const int blocks = qrcp_blocks((const void*)k_qrcp<MAXQ>, smem, num_sms, w.max_blocks, n, &e);
   if (e != cudaSuccess) return e;
@@ -1242,20 +1248,12 @@ static cudaError_t launch_qrcp_smem(double2* Y, int64_t ldy, int l, int64_t n, i
                                     int num_sms, cudaStream_t st, int* launches) {
   auto kern = k_qrcp_smem<MAXQ>;
   cudaError_t e;
-  // device and function attributes and the occupancy of the last shared-memory size: queried once
-  // (host API calls on every decompose cost ~10 us, a visible share of the small configs' step)
-  static int optin = -1;
-  static cudaFuncAttributes fa;
-  static size_t last_smem = 0;
-  static int last_occ = 0;
-  if (optin < 0) {
-    int dev = 0, o = 0;
-    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-    if ((e = cudaDeviceGetAttribute(&o, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
-      return e;
-    if ((e = cudaFuncGetAttributes(&fa, (const void*)kern)) != cudaSuccess) return e;
-    optin = o;
-  }
+  // device and function attributes and occupancies: cached per device (rid_host.h; host API
+  // calls on every decompose cost ~10 us, a visible share of the small configs' step)
+  int optin = 0;
+  size_t fstatic = 0;
+  if ((e = optin_smem(&optin)) != cudaSuccess) return e;
+  if ((e = static_smem((const void*)kern, &fstatic)) != cudaSuccess) return e;
   for (int per_sm = 2; per_sm >= 1; --per_sm) {
     int blocks = num_sms * per_sm;
     if (blocks > w.max_blocks) blocks = w.max_blocks;
@@ -1265,21 +1263,10 @@ static cudaError_t launch_qrcp_smem(double2* Y, int64_t ldy, int l, int64_t n, i
     blocks = (int)((n + per - 1) / per);
     const size_t smem = (size_t)MAXQ * 32 * sizeof(double2) + (size_t)((per + 1) & ~1) * 8 +
                         (size_t)per * l * sizeof(double2);
-    const size_t cap = (size_t)optin / per_sm - fa.sharedSizeBytes - 1024;
+    const size_t cap = (size_t)optin / per_sm - fstatic - 1024;
     if (smem > cap) continue;
     int occ = 0;
-    if (smem == last_smem) {
-      occ = last_occ;
-    } else {
-      if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
-          cudaSuccess)
-        return e;
-      if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kQrcpThreads, smem)) !=
-          cudaSuccess)
-        return e;
-      last_smem = smem;
-      last_occ = occ;
-    }
+    if ((e = occupancy((const void*)kern, kQrcpThreads, smem, &occ)) != cudaSuccess) return e;
     if (occ * num_sms < blocks) continue;  // a cooperative launch needs every CTA resident
     if ((e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
     QrcpOut o = out;
@@ -1301,16 +1288,10 @@ static cudaError_t launch_qrcp_blocked(double2* Y, int64_t ldy, int l, int64_t n
                                        int num_sms, cudaStream_t st, int* launches, int nbw) {
   auto kern = k_qrcp_ring<MAXQ>;
   cudaError_t e;
-  static int optin = -1;  // queried once (see launch_qrcp_smem)
-  static cudaFuncAttributes fa;
-  if (optin < 0) {
-    int dev = 0, o = 0;
-    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
-    if ((e = cudaDeviceGetAttribute(&o, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
-      return e;
-    if ((e = cudaFuncGetAttributes(&fa, (const void*)kern)) != cudaSuccess) return e;
-    optin = o;
-  }
+  int optin = 0;  // cached per device (see launch_qrcp_smem)
+  size_t fstatic = 0;
+  if ((e = optin_smem(&optin)) != cudaSuccess) return e;
+  if ((e = static_smem((const void*)kern, &fstatic)) != cudaSuccess) return e;
   int blocks = num_sms;
   if ((int64_t)blocks * 8 > n) blocks = (int)((n + 7) / 8);
   if (blocks > w.max_blocks) blocks = w.max_blocks;
@@ -1318,7 +1299,7 @@ static cudaError_t launch_qrcp_blocked(double2* Y, int64_t ldy, int l, int64_t n
   const int per = (int)((n + blocks - 1) / blocks);
   blocks = (int)((n + per - 1) / per);
   const size_t fixed = (size_t)kMaxSlots * 8 + (size_t)(MAXQ * 32 + 32) * sizeof(double2) + 128;
-  const size_t avail = (size_t)optin - fa.sharedSizeBytes - 1024;
+  const size_t avail = (size_t)optin - fstatic - 1024;
   const size_t slot_bytes = (size_t)32 * kCH * sizeof(double2);
   if (avail < fixed + 2 * slot_bytes) return cudaErrorInvalidConfiguration;
   int slots = (int)((avail - fixed) / slot_bytes);
@@ -1330,24 +1311,18 @@ static cudaError_t launch_qrcp_blocked(double2* Y, int64_t ldy, int l, int64_t n
   int ncw = kRingWarps - 1;
   if (ncw > nbat) ncw = nbat;
   if (ncw > slots / 2) ncw = slots / 2;
-  if (const char* v = getenv("RID_QRCP_NCW")) {  // experiments
+  if (const char* v = experiment_env("RID_QRCP_NCW")) {  // experiments
     const int x = atoi(v);
     if (x >= 1 && x <= slots / 2) ncw = x;
   }
   int D = slots / ncw;
   if (D > 4) D = 4;
-  if (const char* v = getenv("RID_QRCP_D")) {  // ring-depth experiments
+  if (const char* v = experiment_env("RID_QRCP_D")) {  // ring-depth experiments
     const int x = atoi(v);
     if (x >= 2 && x * ncw <= slots) D = x;
   }
   const size_t smem = fixed + (size_t)ncw * D * slot_bytes;
-  static size_t smem_set = 0;
-  if (smem != smem_set) {
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
-        cudaSuccess)
-      return e;
-    smem_set = smem;
-  }
+  if ((e = ensure_dyn_smem((const void*)kern, smem)) != cudaSuccess) return e;
   // 2D tensor map of Y as a (2l doubles) x n matrix, boxes of kCH complex rows x 32 columns
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
@@ -1375,7 +1350,7 @@ static cudaError_t launch_qrcp_blocked(double2* Y, int64_t ldy, int l, int64_t n
     QrcpWork ww = w;
     int j0v = j0, jendv = jend, ncwv = ncw, Dv = D, perv = per;
     double l2_keep = 80.0 * (1 << 20);  // bytes of the trailing block kept in L2 (126 MB L2)
-    if (const char* v = getenv("RID_QRCP_L2KEEP_MB")) l2_keep = atof(v) * (1 << 20);
+    if (const char* v = experiment_env("RID_QRCP_L2KEEP_MB")) l2_keep = atof(v) * (1 << 20);
     void* args[] = {&Y, &ldy, &l, &n, &k, &j0v, &jendv, &tol_rel, &o, &ww, &ncwv, &Dv, &perv,
                     &l2_keep, &tmap};
     e = cudaLaunchCooperativeKernel((void*)kern, dim3(blocks), dim3(kRingThreads), args, smem, st);
@@ -1403,10 +1378,10 @@ cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, doubl
   // is faster there (C2: 0.68 vs 1.04 ms). Measured on B200, tools/trace_qrcp.py.
   if (variant < 0) {
     variant = (16.0 * (double)l * (double)n >= 64.0 * (1 << 20)) ? 1 : 0;
-    if (const char* v = getenv("RID_QRCP_VARIANT")) variant = atoi(v);
+    if (const char* v = select_env("RID_QRCP_VARIANT")) variant = atoi(v);
   }
   int nbw = kNBDefault;
-  if (const char* v = getenv("RID_QRCP_NB")) nbw = atoi(v);  // panel-width experiments
+  if (const char* v = select_env("RID_QRCP_NB")) nbw = atoi(v);  // panel-width experiments
   if (nbw < 1 || nbw > kNB) nbw = kNBDefault;
   int dummy = 0;
   if (!launches) launches = &dummy;
@@ -1537,7 +1512,7 @@ __global__ void __launch_bounds__(256) k_tri_inverse_warp(const double2* __restr
 
 cudaError_t tri_inverse(const double2* R11, int64_t k, double2* Rinv, cudaStream_t st) {
   if (k <= 0) return cudaSuccess;
-  const char* old = getenv("RID_TRI_OLD");
+  const char* old = select_env("RID_TRI_OLD");
   if (!(old && atoi(old) != 0) && k <= 512) {  // k > 512: 32+ slots per lane would spill
     const unsigned g = (unsigned)((k + 7) / 8);
     if (k <= 64) k_tri_inverse_warp<2><<<g, 256, 0, st>>>(R11, (int)k, Rinv);
@@ -1548,8 +1523,7 @@ cudaError_t tri_inverse(const double2* R11, int64_t k, double2* Rinv, cudaStream
   }
   const size_t sm = (size_t)k * sizeof(double2);
   if (sm > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_tri_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)sm);
+    cudaError_t e = ensure_dyn_smem((const void*)k_tri_inverse, sm);
     if (e != cudaSuccess) return e;
   }
   k_tri_inverse<<<(unsigned)k, 256, sm, st>>>(R11, (int)k, Rinv);

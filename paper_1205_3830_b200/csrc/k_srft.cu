@@ -237,7 +237,7 @@ cudaError_t srft_sketch(uint64_t seed, bool retry, int64_t l, const double2* A, 
         bt.mout[bt.n] = lr;
         ++bt.n;
       }
-      const char* v = getenv("RID_Z3_TMA");
+      const char* v = select_env("RID_Z3_TMA");
       if (v && atoi(v) == 0) {
         e = zgemm3m_batched(Wg, l, Z, m1, Yg, l, bt, nc, m1, st);
         if (e != cudaSuccess) return e;

@@ -239,12 +239,9 @@ static cudaError_t launch_cfg(const double2* Rm, int64_t ldr, const double2* Bm,
                               double2* partial = nullptr) {
   using Cfg = ZgemmCfg<FJ, FR, WARPS_J, WARPS_R, BK, STAGES>;
   auto kern = k_zgemm_dmma<FJ, FR, WARPS_J, WARPS_R, BK, STAGES, MINB, REGEN>;
-  static bool attr_set = false;  // per-instantiation, set once per process
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)Cfg::kSmem);
+  {
+    const cudaError_t e = ensure_dyn_smem((const void*)kern, Cfg::kSmem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const int64_t tiles_r = (Mout + Cfg::BRC - 1) / Cfg::BRC;
   const int64_t tiles_j = (N + Cfg::BJ - 1) / Cfg::BJ;
@@ -317,7 +314,7 @@ int zgemm_pick_fr(int64_t Mout) {
 // C4 (n_ref = 4096 -> 384 tiles) keeps S = 1 and with it the bit-identity to the oracle's single
 // ascending chain; C2, C3, C5 split (their Y then agrees with the oracle to rounding, ~1e-16).
 int zgemm_ksplit(int64_t Mout, int64_t K, int64_t n_ref, int num_sms) {
-  if (const char* v = getenv("RID_SKETCH_SPLIT")) {  // tests: force a slice count (1 = unsplit)
+  if (const char* v = select_env("RID_SKETCH_SPLIT")) {  // tests: force a slice count (1 = unsplit)
     const int s = atoi(v);
     if (s >= 1) return s;
   }
@@ -346,11 +343,11 @@ cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int
   // register-light CTAs, 2 stages, 3 per SM keep more tiles in flight (measured at C4: update total
   // 2.95 -> 2.36 ms against the sketch tiles; 64-row/4-per-SM 2.55, 32x64/3-per-SM 2.76 ms)
   if (mode == 2) {
-    if (zgemm_tma_enabled() && getenv("RID_ZGEMM_TMA_UPDATE"))
+    if (zgemm_tma_enabled() && select_env("RID_ZGEMM_TMA_UPDATE"))
       return zgemm_tma_ordered(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, mode, noise, seed, col0, st);
     return launch_cfg<1, 8, 8, 1, 16, 2, 3>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
   }
-  if (const char* v = getenv("RID_ZGEMM_VARIANT")) {  // tile experiments (tools/tune_*.py)
+  if (const char* v = experiment_env("RID_ZGEMM_VARIANT")) {  // tile experiments (tools/tune_*.py)
     const int id = atoi(v);
 #define RID_V(ID, ...) \
   if (id == ID)        \
@@ -361,10 +358,13 @@ cudaError_t zgemm_ordered(const double2* Rm, int64_t ldr, const double2* Bm, int
     RID_V(4, 1, 3, 8, 1, 16, 3, 4)
     RID_V(5, 4, 8, 4, 2, 16, 4, 1)    // round-1 first generation tile
 #undef RID_V
-    // in-kernel Philox regeneration of R (REGEN): ep.seed / regen_stream from RID_REGEN_STREAM
+    // in-kernel Philox regeneration of R (REGEN): the key of the R that fill_R generated for this
+    // sketch (sketch_key; round 1 passed the product's seed argument, 0 for a sketch, so the
+    // regenerated R was another matrix and the results differed — the REGEN runs of
+    // profiles/r01_tune_regen_vs_pregen.log)
     if (id >= 10 && id <= 11) {
-      ep.seed = seed;
-      ep.regen_stream = getenv("RID_REGEN_STREAM") ? atoi(getenv("RID_REGEN_STREAM")) : 4;
+      ep.seed = sketch_key().seed;
+      ep.regen_stream = (int)sketch_key().stream;
       if (id == 10)
         return launch_cfg<2, 11, 4, 2, 16, 3, 2, 1>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st,
                                                      ksplit, partial);

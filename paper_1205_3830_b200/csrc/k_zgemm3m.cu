@@ -45,8 +45,7 @@ struct Z3Cfg {
 // RS = 1: Re R + Im R comes from a precomputed plane (no add per R fragment, 6 KB more shared
 // memory per stage); RS = 0: it is formed in registers like the A side. DBUF = 1: the fragments
 // of k-step kk + 1 are loaded while the DMMAs of kk issue.
-template <int FJ, int FR, int WJ, int WR, int BKC, int STAGES, int MINB, int RS, int DBUF,
-          int NOLOAD = 0>
+template <int FJ, int FR, int WJ, int WR, int BKC, int STAGES, int MINB, int RS, int DBUF>
 __global__ void __launch_bounds__(WJ* WR * 32, MINB)
     k_zgemm3m(const double2* __restrict__ Rm, int64_t ldr, const double* __restrict__ Rs,
               int64_t ldrs, const double2* __restrict__ Bm, int64_t ldb, double2* __restrict__ C,
@@ -163,7 +162,7 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
     cp_async_commit();
   }
   for (int64_t kt = 0; kt < nk; ++kt) {
-    if (!NOLOAD) {  // (NOLOAD: a measurement of the inner loop alone, results are garbage)
+    {
       cp_async_wait<STAGES - 2>();
       __syncthreads();
       const int64_t kn = kt + STAGES - 1;
@@ -242,19 +241,15 @@ __global__ void k_splitk_reduce3(const double2* __restrict__ part, int S, int64_
   }
 }
 
-template <int FJ, int FR, int WJ, int WR, int BKC, int STAGES, int MINB, int RS, int DBUF,
-          int NOLOAD = 0>
+template <int FJ, int FR, int WJ, int WR, int BKC, int STAGES, int MINB, int RS, int DBUF>
 static cudaError_t launch3(const double2* Rm, int64_t ldr, const double* Rs, int64_t ldrs,
                            const double2* Bm, int64_t ldb, double2* C, int64_t ldc, int64_t Mout,
                            int64_t N, int64_t K, cudaStream_t st, int S, double2* partial) {
   using Cfg = Z3Cfg<FJ, FR, WJ, WR, BKC, STAGES, RS>;
-  auto kern = k_zgemm3m<FJ, FR, WJ, WR, BKC, STAGES, MINB, RS, DBUF, NOLOAD>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
+  auto kern = k_zgemm3m<FJ, FR, WJ, WR, BKC, STAGES, MINB, RS, DBUF>;
+  {
+    const cudaError_t e = ensure_dyn_smem((const void*)kern, Cfg::kSmem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   const int64_t tiles_r = (Mout + Cfg::BR - 1) / Cfg::BR;
   const int64_t tiles_j = (N + Cfg::BJ - 1) / Cfg::BJ;
@@ -292,12 +287,9 @@ static cudaError_t launch3_batched(const double2* Rm, int64_t ldr, const double2
                                    cudaStream_t st) {
   using Cfg = Z3Cfg<FJ, FR, WJ, WR, BKC, STAGES, 0>;
   auto kern = k_zgemm3m<FJ, FR, WJ, WR, BKC, STAGES, MINB, 0, 0>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e =
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem);
+  {
+    const cudaError_t e = ensure_dyn_smem((const void*)kern, Cfg::kSmem);
     if (e != cudaSuccess) return e;
-    attr_set = true;
   }
   int64_t mmax = 0;
   for (int z = 0; z < bt.n; ++z) mmax = bt.mout[z] > mmax ? bt.mout[z] : mmax;
@@ -320,7 +312,7 @@ static cudaError_t launch3_batched(const double2* Rm, int64_t ldr, const double2
 //   id 2: 24 rows (1 x 3) x 64 columns, as id 1                          C1 (24)
 static int pick3(int64_t Mout) {
   const int rows[3] = {48, 40, 24};
-  if (const char* v = getenv("RID_Z3_ROWS")) {  // tile-height experiments (tools/tma_sketch_time.py)
+  if (const char* v = experiment_env("RID_Z3_ROWS")) {  // tile-height experiments (tools/tma_sketch_time.py)
     for (int i = 0; i < 3; ++i)
       if (atoi(v) == rows[i]) return i;
   }
@@ -343,7 +335,7 @@ static int rows3(int id) {
 int zgemm3m_tile_rows(int64_t Mout) { return rows3(pick3(Mout)); }
 
 int zgemm3m_ksplit(int64_t Mout, int64_t K, int64_t n_ref, int num_sms) {
-  if (const char* v = getenv("RID_SKETCH_SPLIT")) {
+  if (const char* v = select_env("RID_SKETCH_SPLIT")) {
     const int s = atoi(v);
     if (s >= 1) return s;
   }
@@ -388,7 +380,7 @@ cudaError_t zgemm3m(const double2* Rm, int64_t ldr, const double* Rs, int64_t ld
                     int64_t N, int64_t K, cudaStream_t st, int ksplit, double2* partial) {
   if (Mout <= 0 || N <= 0) return cudaSuccess;
 #define RID_L3(...) launch3<__VA_ARGS__>(Rm, ldr, Rs, ldrs, Bm, ldb, C, ldc, Mout, N, K, st, ksplit, partial)
-  if (const char* v = getenv("RID_Z3_VARIANT")) {  // tile experiments (tools/sketch3m_check.py)
+  if (const char* v = experiment_env("RID_Z3_VARIANT")) {  // tile experiments (tools/sketch3m_check.py)
     switch (atoi(v)) {
       case 1: return RID_L3(2, 3, 4, 2, 16, 3, 2, 0, 0);
       case 2: return RID_L3(2, 3, 4, 2, 16, 3, 2, 0, 1);
@@ -401,7 +393,6 @@ cudaError_t zgemm3m(const double2* Rm, int64_t ldr, const double* Rs, int64_t ld
       case 9: return RID_L3(1, 6, 8, 1, 16, 3, 2, 1, 1);
       case 10: return RID_L3(2, 3, 4, 2, 8, 4, 2, 0, 0);
       case 11: return RID_L3(1, 3, 8, 1, 16, 3, 2, 1, 1);
-      case 90: return RID_L3(2, 3, 4, 2, 16, 3, 2, 0, 0, 1);  // inner loop only (garbage)
       default: break;
     }
   }
@@ -437,7 +428,7 @@ cudaError_t zgemm3m_batched(const double2* Rm, int64_t ldr, const double2* Bm, i
 }
 
 int sketch_mults() {
-  const char* v = getenv("RID_SKETCH_4M");
+  const char* v = select_env("RID_SKETCH_4M");
   return (v && atoi(v) != 0) ? 4 : 3;
 }
 int sketch_ksplit(int64_t l, int64_t m, int64_t n_ref, int num_sms) {
@@ -451,7 +442,7 @@ int sketch_ksplit(int64_t l, int64_t m, int64_t n_ref, int num_sms) {
 // every column of Y is still bitwise independent of the sharding.
 SketchTail sketch_tail(int64_t l, int64_t m, int64_t n, int num_sms) {
   SketchTail t{0, 1};
-  if (sketch_mults() != 3 || getenv("RID_SKETCH_SPLIT") || getenv("RID_SKETCH_NOTAIL")) return t;
+  if (sketch_mults() != 3 || select_env("RID_SKETCH_SPLIT") || select_env("RID_SKETCH_NOTAIL")) return t;
   if (zgemm3m_ksplit(l, m, n / 8, num_sms) != 1) return t;  // already split everywhere
   const int64_t rt = (l + rows3(pick3(l)) - 1) / rows3(pick3(l));
   const int64_t T = (n + 63) / 64, slots = 2 * (int64_t)num_sms, total = rt * T;
@@ -500,7 +491,7 @@ cudaError_t sketch_gemm(const double2* R, int64_t ldr, const double* Rs, const d
   // wave costs more than the padding saves, e.g. the e2e path's 1 GiB column chunks)
   int rsplit = 0;
   if (aux && aux->stream && zgemm3m_tma_enabled(l) && Rs && l > 48 &&
-      !getenv("RID_SKETCH_NOROWSPLIT")) {
+      !select_env("RID_SKETCH_NOROWSPLIT")) {
     const int64_t r = l % 48;
     if (r == 24 || r == 32 || r == 40) rsplit = (int)r;
   }

@@ -233,14 +233,8 @@ static cudaError_t launch3t(const double2* Rm, int64_t ldr, const double* Rs, in
                             const Z3Batch* bt = nullptr, int64_t Nb = 0, int64_t Ms = 0) {
   using Cf = Z3T<FJ, FR, WJ, WR, STAGES, RS>;
   auto kern = k_zgemm3m_tma<FJ, FR, WJ, WR, STAGES, MINB, RS, ORD>;
-  static bool attr_set = false;
   cudaError_t e;
-  if (!attr_set) {
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)Cf::kSmem)) != cudaSuccess)
-      return e;
-    attr_set = true;
-  }
+  if ((e = ensure_dyn_smem((const void*)kern, Cf::kSmem)) != cudaSuccess) return e;
   PFN_cuTensorMapEncodeTiled encode;
   if ((e = tensor_map_encoder(&encode)) != cudaSuccess) return e;
   // A as a (2K doubles) x N matrix, boxes of 16 doubles x BJ columns; R as (2 Mout) x K, boxes
@@ -318,7 +312,7 @@ static cudaError_t launch3t(const double2* Rm, int64_t ldr, const double* Rs, in
 // The TMA pipeline covers all three tiles — 48 rows (C3, C4), 40 (C2, C5; with the Re R + Im R
 // plane when one is passed), 24 (C1) — unless RID_Z3_TMA=0.
 bool zgemm3m_tma_enabled(int64_t Mout) {
-  const char* v = getenv("RID_Z3_TMA");
+  const char* v = select_env("RID_Z3_TMA");
   return !(v && atoi(v) == 0) && Mout > 0;
 }
 
@@ -329,7 +323,7 @@ cudaError_t zgemm3m_tma(const double2* Rm, int64_t ldr, const double* Rs, int64_
 #define RID_L3T(...) \
   launch3t<__VA_ARGS__>(Rm, ldr, Rs, ldrs, Bm, ldb, C, ldc, Mout, N, K, st, ksplit, partial)
   int var = 0;
-  if (const char* v = getenv("RID_Z3T_VARIANT")) var = atoi(v);  // pipeline-depth experiments
+  if (const char* v = select_env("RID_Z3T_VARIANT")) var = atoi(v);  // pipeline-depth experiments
   if (zgemm3m_tile_rows(Mout) == 40) {
     if (!Rs) return RID_L3T(1, 5, 8, 1, 3, 2, 0);
     switch (var) {
@@ -401,7 +395,7 @@ cudaError_t zgemm3m_tma_batched_h(const double2* Rm, int64_t ldr, int64_t Mtot, 
   for (int z = 0; z < b.n; ++z) mmax = b.mout[z] > mmax ? b.mout[z] : mmax;
   // with a Re + Im plane of Rm (Rs: Ms rows, product z from row soff[z], even): the sums come
   // from shared memory
-  const char* v = getenv("RID_Z3_BATCH_RS");
+  const char* v = select_env("RID_Z3_BATCH_RS");
   bool rs = Rs && !(v && atoi(v) == 0);
   for (int z = 0; z < b.n && rs; ++z)
     if (b.soff[z] & 1) return cudaErrorInvalidValue;

@@ -186,14 +186,8 @@ static cudaError_t launch_zt(const double2* Rm, int64_t ldr, const double2* Bm, 
                              const ZtmaEpilogue& ep, cudaStream_t st) {
   using Cf = ZTCfg<FJ, FR, WJ, WR, STAGES>;
   auto kern = k_zgemm_tma<FJ, FR, WJ, WR, STAGES, MINB>;
-  static bool attr_set = false;
   cudaError_t e;
-  if (!attr_set) {
-    if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)Cf::kSmem)) != cudaSuccess)
-      return e;
-    attr_set = true;
-  }
+  if ((e = ensure_dyn_smem((const void*)kern, Cf::kSmem)) != cudaSuccess) return e;
   PFN_cuTensorMapEncodeTiled encode;
   if ((e = tensor_map_encoder(&encode)) != cudaSuccess) return e;
   CUtensorMap mapB, mapR;
@@ -231,7 +225,7 @@ static cudaError_t launch_zt(const double2* Rm, int64_t ldr, const double2* Bm, 
 // its DMMA loop is bound by the 4-product fragment loads (9 LDS per 8 DMMA). Kept, tested
 // bitwise, as the measured alternative.
 bool zgemm_tma_enabled() {
-  const char* v = getenv("RID_ZGEMM_TMA");
+  const char* v = select_env("RID_ZGEMM_TMA");
   return v && atoi(v) != 0;
 }
 
@@ -244,7 +238,7 @@ cudaError_t zgemm_tma_ordered(const double2* Rm, int64_t ldr, const double2* Bm,
   if (Mout <= 0 || N <= 0) return cudaSuccess;
   const ZtmaEpilogue ep{mode, noise, seed, col0};
   int stages = 6;
-  if (const char* v = getenv("RID_ZGEMM_TMA_STAGES")) stages = atoi(v);
+  if (const char* v = experiment_env("RID_ZGEMM_TMA_STAGES")) stages = atoi(v);
   if (mode == 2) return launch_zt<1, 8, 8, 1, 2, 3>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);
   switch (stages) {
     case 4: return launch_zt<1, 8, 8, 1, 4, 3>(Rm, ldr, Bm, ldb, C, ldc, Mout, N, K, ep, st);

@@ -4,12 +4,16 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -17,6 +21,20 @@ extern char** environ;  // POSIX: the RID_* knobs are part of the graph key
 
 #include "../../include/rid.h"
 #include "rid_internal.h"
+
+// The data plane of a G-rank communicator: the two collectives the path needs.
+// Counts are in doubles; every call is collective (all ranks, same count) and ordered on the
+// calling context's stream. Implementations: NCCL (rid_comm_init, one process per GPU) and the
+// in-process plane of rid_comm_init_local (G contexts in one process, device copies ordered by
+// events; how the tests run the G > 1 path on one GPU).
+struct RidComm {
+  int rank = 0, nranks = 1;
+  virtual ~RidComm() = default;
+  // in place: buf holds nranks blocks of `count` doubles, block r is rank r's contribution
+  virtual rid_status allgather(rid_ctx* c, double* buf, size_t count) = 0;
+  // in place: buf = sum over ranks (bitwise the same on every rank)
+  virtual rid_status allreduce_sum(rid_ctx* c, double* buf, size_t count) = 0;
+};
 
 struct rid_ctx {
   int device = 0;
@@ -29,7 +47,7 @@ struct rid_ctx {
     size_t bytes = 0;
   };
   std::map<std::string, Buf> ws;
-  ncclComm_t comm = nullptr;
+  std::unique_ptr<RidComm> comm;  // null: G = 1
   int rank = 0, nranks = 1;
   cudaEvent_t ev[12] = {};
   // host-A streaming (e2e path): a copy stream and double-buffer events, created on first use
@@ -109,6 +127,95 @@ rid_status ws_get(rid_ctx* c, const char* name, size_t bytes, void** out) {
   return RID_OK;
 }
 
+// ---- NCCL data plane (one process per GPU) ----------------------------------------------------
+struct NcclComm final : RidComm {
+  ncclComm_t comm = nullptr;
+  ~NcclComm() override {
+    if (comm) ncclCommDestroy(comm);
+  }
+  rid_status allgather(rid_ctx* c, double* buf, size_t count) override {
+    RID_NCCL(c, ncclAllGather(buf + (size_t)rank * count, buf, count, ncclDouble, comm, c->stream));
+    return RID_OK;
+  }
+  rid_status allreduce_sum(rid_ctx* c, double* buf, size_t count) override {
+    RID_NCCL(c, ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, comm, c->stream));
+    return RID_OK;
+  }
+};
+
+// ---- in-process data plane (rid_comm_init_local) -----------------------------------------------
+// G contexts of one process and one device. A collective is two host rendezvous of the G calling
+// threads (like NCCL, every rank must call it) around stream-ordered device work:
+//   1. each rank publishes its buffer and records `ready` on its stream; rendezvous;
+//   2. each rank's stream waits for every peer's `ready`, then copies / reduces from the peers'
+//      buffers (plain device copies, a rank-ordered sum kernel); records `done`; rendezvous;
+//   3. each rank's stream waits for every peer's `done` before anything after the collective can
+//      overwrite the buffer the peers read.
+// No kernel waits on another: the only cross-rank dependencies are stream waits on events
+// recorded before the rendezvous, so the G streams may run in any order on the one GPU.
+struct LocalGroup {
+  int G = 0;
+  int device = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long phase = 0;
+  bool broken = false;
+  std::vector<double*> buf;
+  std::vector<cudaEvent_t> ready, done;
+  ~LocalGroup() {
+    cudaSetDevice(device);
+    for (auto e : ready) cudaEventDestroy(e);
+    for (auto e : done) cudaEventDestroy(e);
+  }
+};
+
+struct LocalComm final : RidComm {
+  std::shared_ptr<LocalGroup> g;
+  rid_status rendezvous(rid_ctx* c) {
+    std::unique_lock<std::mutex> lk(g->mu);
+    if (g->broken) return fail(c, RID_ENCCL, "local communicator: a rank failed or timed out");
+    const unsigned long long ph = g->phase;
+    if (++g->arrived == g->G) {
+      g->arrived = 0;
+      ++g->phase;
+      g->cv.notify_all();
+      return RID_OK;
+    }
+    const bool ok = g->cv.wait_for(lk, std::chrono::seconds(300),
+                                   [&] { return g->phase != ph || g->broken; });
+    if (!ok || g->broken) {
+      g->broken = true;
+      g->cv.notify_all();
+      return fail(c, RID_ENCCL, "local communicator: rank %d timed out at a collective", rank);
+    }
+    return RID_OK;
+  }
+  rid_status publish(rid_ctx* c, double* buf) {
+    g->buf[rank] = buf;
+    RID_CUDA(c, cudaEventRecord(g->ready[rank], c->stream));
+    return rendezvous(c);
+  }
+  rid_status finish(rid_ctx* c) {
+    RID_CUDA(c, cudaEventRecord(g->done[rank], c->stream));
+    RID_TRY(rendezvous(c));
+    for (int h = 0; h < g->G; ++h)
+      if (h != rank) RID_CUDA(c, cudaStreamWaitEvent(c->stream, g->done[h], 0));
+    return RID_OK;
+  }
+  rid_status allgather(rid_ctx* c, double* buf, size_t count) override {
+    RID_TRY(publish(c, buf));
+    for (int h = 0; h < g->G; ++h) {
+      if (h == rank) continue;
+      RID_CUDA(c, cudaStreamWaitEvent(c->stream, g->ready[h], 0));
+      RID_CUDA(c, cudaMemcpyAsync(buf + (size_t)h * count, g->buf[h] + (size_t)h * count,
+                                  count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+    }
+    return finish(c);
+  }
+  rid_status allreduce_sum(rid_ctx* c, double* buf, size_t count);
+};
+
 bool is_device_ptr(const void* p) {
   if (!p) return false;
   cudaPointerAttributes at;
@@ -181,7 +288,7 @@ rid_status solve_T(rid_ctx* c, const double2* Rinv, int64_t k, const double2* Y,
     RID_TRY(ws_get(c, "Rinvs", sizeof(double) * rid::rsum_ld(k) * k, &ps));
     RID_CUDA(c, rid::rsum_fill(Rinv, k, k, k, (double*)ps, rid::rsum_ld(k), c->stream));
     *launches += 1;
-    if (c->aux_stream && !getenv("RID_SOLVE_NOAUX")) {
+    if (c->aux_stream && !rid::select_env("RID_SOLVE_NOAUX")) {
       const rid::SketchAux aux{c->aux_stream, c->aux_fork, c->aux_join};
       RID_CUDA(c, rid::sketch_gemm(Rinv, k, (const double*)ps, Y, ldy, P, ldp, k, n_loc, k,
                                    c->stream, 1, nullptr, 0, n_loc, c->num_sms, launches, &aux));
@@ -224,7 +331,7 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
   rid::QrcpOut o{(int64_t*)pJ, (double*)pbeta, (double*)presid, (double*)pmargin, (int*)pinfo,
                  (double2*)pR11};
   rid::QrcpWork w = rid::qrcp_work_carve(pwork, n, l, max_blocks);
-  const char* trace_path = getenv("RID_QRCP_TRACE");  // per-step timing of k_qrcp (tools)
+  const char* trace_path = rid::select_env("RID_QRCP_TRACE");  // per-step timing of k_qrcp (tools)
   if (trace_path) {
     void* pt;
     RID_TRY(ws_get(c, "qrcp_trace", sizeof(unsigned long long) * 8 * k, &pt));
@@ -312,6 +419,7 @@ rid_status fill_R(rid_ctx* c, uint64_t seed, uint32_t s, int64_t l, int64_t m, d
                   double** Rs, int* launches) {
   void *pR, *pRs = nullptr;
   RID_TRY(ws_get(c, "R", sizeof(double2) * l * m, &pR));
+  rid::sketch_key() = rid::SketchKey{seed, s};
   RID_CUDA(c, rid::normal_fill(seed, s, l, m, 0, 0, (double2*)pR, l, c->stream));
   *launches += 1;
   if (rid::sketch_mults() == 3) {
@@ -394,6 +502,21 @@ rid_status srft_into(rid_ctx* c, uint64_t seed, bool retry, int64_t l, const rid
   return RID_OK;
 }
 
+rid_status LocalComm::allreduce_sum(rid_ctx* c, double* buf, size_t count) {
+  void* tmp;
+  RID_TRY(ws_get(c, "comm_sum", count * sizeof(double), &tmp));
+  RID_TRY(publish(c, buf));
+  rid::RankPtrs src{};
+  for (int h = 0; h < g->G; ++h) {
+    if (h != rank) RID_CUDA(c, cudaStreamWaitEvent(c->stream, g->ready[h], 0));
+    src.p[h] = g->buf[h];
+  }
+  RID_CUDA(c, rid::sum_ranks(src, g->G, (double*)tmp, (int64_t)count, c->stream));
+  RID_TRY(finish(c));  // every peer has read buf: it may be overwritten
+  RID_CUDA(c, cudaMemcpyAsync(buf, tmp, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  return RID_OK;
+}
+
 __global__ void k_extract_R(const double2* __restrict__ Y, int64_t ldy, const int64_t* __restrict__ J,
                             const double2* __restrict__ R11, int64_t k, int64_t n,
                             double2* __restrict__ R, int64_t ldr) {
@@ -434,6 +557,17 @@ rid_status rid_create(rid_ctx** out, int device, void* cuda_stream) {
   return RID_OK;
 }
 
+rid_status rid_set_stream(rid_ctx* c, void* cuda_stream) {
+  RID_TRY(check_ctx(c));
+  if (c->owns_stream && c->stream != (cudaStream_t)cuda_stream) {
+    RID_CUDA(c, cudaStreamSynchronize(c->stream));
+    RID_CUDA(c, cudaStreamDestroy(c->stream));
+    c->owns_stream = false;
+  }
+  c->stream = (cudaStream_t)cuda_stream;
+  return RID_OK;
+}
+
 void rid_destroy(rid_ctx* c) {
   if (!c) return;
   cudaSetDevice(c->device);
@@ -442,7 +576,7 @@ void rid_destroy(rid_ctx* c) {
     if (kv.second.p) cudaFree(kv.second.p);
   for (auto& ev : c->ev)
     if (ev) cudaEventDestroy(ev);
-  if (c->comm) ncclCommDestroy(c->comm);
+  c->comm.reset();
   if (c->host_qr) cudaFreeHost(c->host_qr);
   if (c->aux_stream) {
     cudaStreamSynchronize(c->aux_stream);
@@ -487,19 +621,55 @@ rid_status rid_comm_init(rid_ctx* c, const void* id, int rank, int nranks) {
   RID_TRY(check_ctx(c));
   if (!id || nranks < 1 || rank < 0 || rank >= nranks)
     return fail(c, RID_EINVAL, "rid_comm_init: bad rank %d / nranks %d", rank, nranks);
-  if (c->comm) {
-    ncclCommDestroy(c->comm);
-    c->comm = nullptr;
-  }
+  c->comm.reset();
+  c->rank = 0;
+  c->nranks = 1;
   // a 1-rank communicator is created only on request (RID_FORCE_NCCL=1): it routes a single
   // GPU through the collective code path (tests/test_gpu_collective.py)
-  if (nranks > 1 || getenv("RID_FORCE_NCCL")) {
+  if (nranks > 1 || rid::select_env("RID_FORCE_NCCL")) {
     ncclUniqueId u;
     std::memcpy(&u, id, sizeof u);
-    RID_NCCL(c, ncclCommInitRank(&c->comm, nranks, u, rank));
+    auto nc = std::make_unique<NcclComm>();
+    RID_NCCL(c, ncclCommInitRank(&nc->comm, nranks, u, rank));
+    nc->rank = rank;
+    nc->nranks = nranks;
+    c->comm = std::move(nc);
   }
   c->rank = rank;
   c->nranks = nranks;
+  return RID_OK;
+}
+
+rid_status rid_comm_init_local(rid_ctx** ctxs, int nranks) {
+  if (!ctxs || nranks < 1 || nranks > rid::kMaxLocalRanks) return RID_EINVAL;
+  for (int r = 0; r < nranks; ++r) {
+    if (!ctxs[r]) return RID_EINVAL;
+    for (int h = 0; h < r; ++h)
+      if (ctxs[h] == ctxs[r]) return fail(ctxs[r], RID_EINVAL, "rid_comm_init_local: context repeated");
+    if (ctxs[r]->device != ctxs[0]->device)
+      return fail(ctxs[r], RID_EINVAL, "rid_comm_init_local: all contexts must be on one device");
+  }
+  rid_ctx* c = ctxs[0];
+  RID_TRY(check_ctx(c));
+  auto g = std::make_shared<LocalGroup>();
+  g->G = nranks;
+  g->device = c->device;
+  g->buf.assign(nranks, nullptr);
+  g->ready.assign(nranks, nullptr);
+  g->done.assign(nranks, nullptr);
+  for (int r = 0; r < nranks; ++r) {
+    RID_CUDA(c, cudaEventCreateWithFlags(&g->ready[r], cudaEventDisableTiming));
+    RID_CUDA(c, cudaEventCreateWithFlags(&g->done[r], cudaEventDisableTiming));
+  }
+  for (int r = 0; r < nranks; ++r) {
+    auto lc = std::make_unique<LocalComm>();
+    lc->g = g;
+    lc->rank = r;
+    lc->nranks = nranks;
+    ctxs[r]->comm = std::move(lc);
+    ctxs[r]->rank = r;
+    ctxs[r]->nranks = nranks;
+  }
   return RID_OK;
 }
 
@@ -689,7 +859,7 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
       RID_TRY(sketch_streamed(c, Rg, Rsg, A, m, n, col0, n_loc, lda, l, Yw + col0 * l,
                               &d.launches, nullptr, S, (double2*)pS));
     } else {
-      if (!c->aux_stream && !getenv("RID_SKETCH_NOAUX")) {
+      if (!c->aux_stream && !rid::select_env("RID_SKETCH_NOAUX")) {
         RID_CUDA(c, cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
         RID_CUDA(c, cudaEventCreateWithFlags(&c->aux_fork, cudaEventDisableTiming));
         RID_CUDA(c, cudaEventCreateWithFlags(&c->aux_join, cudaEventDisableTiming));
@@ -697,15 +867,12 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
       const rid::SketchAux aux{c->aux_stream, c->aux_fork, c->aux_join};
       RID_CUDA(c, rid::sketch_gemm(Rg, l, Rsg, (const double2*)a.dev, lda, Yw + col0 * l, l, l,
                                    n_loc, m, c->stream, S, (double2*)pS, col0, n, c->num_sms,
-                                   &d.launches, (c->aux_stream && !getenv("RID_SKETCH_NOAUX"))
+                                   &d.launches, (c->aux_stream && !rid::select_env("RID_SKETCH_NOAUX"))
                                                     ? &aux : nullptr));
     }
     }
     RID_CUDA(c, rec(ev[4]));
-    if (c->comm) {
-      RID_NCCL(c, ncclAllGather(Yw + col0 * l, Yw, (size_t)(2 * l * n_loc), ncclDouble, c->comm,
-                                c->stream));
-    }
+    if (c->comm) RID_TRY(c->comm->allgather(c, (double*)Yw, (size_t)(2 * l * n_loc)));
     RID_CUDA(c, rec(ev[5]));
     // the QR, its status copy and the solve are enqueued together; the status is checked after
     // the one synchronisation at the end (a failed attempt's solve output is discarded)
@@ -737,7 +904,7 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
   // back to the eager path
   const bool graphable = !a_host && !p.host && j_dev && !c->comm &&
                          c->sketch_kind != RID_SKETCH_SRFT &&
-                         !(getenv("RID_GRAPH") && atoi(getenv("RID_GRAPH")) == 0);
+                         !(rid::select_env("RID_GRAPH") && atoi(rid::select_env("RID_GRAPH")) == 0);
   std::string gkey;
   if (graphable) {
     char buf[512];
@@ -782,7 +949,7 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
         } else {
           c->g_bad = gkey;  // not capturable: stay eager for these arguments
         }
-        if (getenv("RID_GRAPH_DEBUG"))
+        if (rid::select_env("RID_GRAPH_DEBUG"))
           fprintf(stderr, "rid_decompose: graph capture %s (%s; %s)\n",
                   c->g_key == gkey ? "ok" : "FAILED", es == RID_OK ? "enqueue ok" : c->err.c_str(),
                   cudaGetErrorString(cudaGetLastError()));
@@ -950,18 +1117,21 @@ rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, 
   double2* B = (double2*)pB;
   double2 *x = (double2*)px, *z = (double2*)pz, *y = (double2*)py;
   double *u = (double*)pu, *nn = (double*)pnn;
-  // B = A[:, J], replicated on every rank (owners contribute their columns, the rest are 0)
-  if (coll) RID_CUDA(c, cudaMemsetAsync(B, 0, sizeof(double2) * m * k, c->stream));
+  // B = A[:, J], replicated on every rank (owners contribute their columns, the rest are 0);
+  // a pivot outside [0, n) raises the flag read after the final synchronisation (RID_EINVAL)
+  void* pbad;
+  RID_TRY(ws_get(c, "estbad", sizeof(int), &pbad));
+  RID_CUDA(c, cudaMemsetAsync(pbad, 0, sizeof(int), c->stream));
+  RID_CUDA(c, cudaMemsetAsync(B, 0, sizeof(double2) * m * k, c->stream));
   RID_CUDA(c, rid::gather_columns((const double2*)a.dev, lda, m, (const int64_t*)pJ, k, col0, n_loc,
-                                  B, m, c->stream));
-  if (coll)
-    RID_NCCL(c, ncclAllReduce(B, B, (size_t)(2 * m * k), ncclDouble, ncclSum, c->comm, c->stream));
+                                  n, B, m, (int*)pbad, c->stream));
+  if (coll) RID_TRY(c->comm->allreduce_sum(c, (double*)B, (size_t)(2 * m * k)));
   // reduce a dd scalar over ranks: local parts -> nn[2*rank], allgather, merge -> nn[2*G]
   auto scalar_allreduce = [&](const double* parts, int nparts) -> rid_status {
     double* slot = nn + 2 * (coll ? c->rank : 0);
     RID_CUDA(c, rid::est_merge_scalar(parts, nparts, slot, c->stream));
     if (coll) {
-      RID_NCCL(c, ncclAllGather(slot, nn, 2, ncclDouble, c->comm, c->stream));
+      RID_TRY(c->comm->allgather(c, nn, 2));
       RID_CUDA(c, rid::est_merge_scalar(nn, G, nn + 2 * G, c->stream));
     }
     return RID_OK;
@@ -977,7 +1147,7 @@ rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, 
     double* u_loc = u + (size_t)4 * k * (coll ? c->rank : 0);
     RID_CUDA(c, rid::est_px((const double2*)p.dev, ldp, k, n_loc, x, (double*)ppx, u_loc, pl, c->stream));
     if (coll) {
-      RID_NCCL(c, ncclAllGather(u_loc, u, (size_t)(4 * k), ncclDouble, c->comm, c->stream));
+      RID_TRY(c->comm->allgather(c, u, (size_t)(4 * k)));
       RID_CUDA(c, rid::est_merge_vec(u, G, k, (double*)psb, c->stream));  // sb as scratch
       RID_CUDA(c, cudaMemcpyAsync(u, psb, sizeof(double) * 4 * k, cudaMemcpyDeviceToDevice, c->stream));
     }
@@ -990,7 +1160,7 @@ rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, 
     if (coll) {
       double* w_loc = (double*)pwall + (size_t)4 * m * c->rank;
       RID_CUDA(c, rid::est_merge_vec((const double*)pax, pl.ax_parts, m, w_loc, c->stream));
-      RID_NCCL(c, ncclAllGather(w_loc, pwall, (size_t)(4 * m), ncclDouble, c->comm, c->stream));
+      RID_TRY(c->comm->allgather(c, (double*)pwall, (size_t)(4 * m)));
       RID_CUDA(c, rid::est_y((const double*)pwall, G, m, B, m, k, u, y, bz + 1, c->stream));
     } else {
       RID_CUDA(c, rid::est_y((const double*)pax, pl.ax_parts, m, B, m, k, u, y, bz + 1, c->stream));
@@ -1003,8 +1173,11 @@ rid_status rid_error_estimate(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, 
     RID_CUDA(c, rid::est_normalise(z, n_loc, nn_final, x, (double*)pest, bax + 1, c->stream));
   }
   RID_CUDA(c, cudaEventRecord(ev[2], c->stream));
+  int bad = 0;
   RID_CUDA(c, cudaMemcpyAsync(est, pest, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  RID_CUDA(c, cudaMemcpyAsync(&bad, pbad, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
   RID_CUDA(c, cudaStreamSynchronize(c->stream));
+  if (bad) return fail(c, RID_EINVAL, "rid_error_estimate: a pivot index lies outside [0, n)");
   if (diag) {
     rid_diag d{};
     d.t_total = ev_ms(ev[0], ev[2]) * 1e-3;

@@ -3,8 +3,8 @@
 // Philox4x32-10 and the RID normal transform, written from the text of docs/RNG.md (§1–§4) with
 // explicit IEEE intrinsics (__fma_rn, __dmul_rn, __dadd_rn, __ddiv_rn, __dsqrt_rn) so nvcc can
 // neither contract nor reassociate: the result is bit-identical to any other implementation of
-// that text (tests/test_gpu_gen.py checks it against the CPU oracle). No code is shared with
-// oracle/.
+// that text (tests/test_gpu_parity.py::test_normal_fill_bitexact checks it against the CPU
+// oracle). No code is shared with oracle/.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>

@@ -4,6 +4,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "rid_host.h"
+
 namespace rid {
 
 // Ordered complex GEMM C = Rm · Bm on DMMA (k_zgemm.cu). mode 1 adds noise·E(r, col0 + j) with
@@ -91,6 +93,17 @@ cudaError_t sketch_gemm(const double2* R, int64_t ldr, const double* Rs, const d
 // K slices for a sketch of Mout rows, K = m, chosen from n_ref = n_global / 8 only (G-invariant)
 int zgemm_ksplit(int64_t Mout, int64_t K, int64_t n_ref, int num_sms);
 
+// The Philox key (seed, stream) of the sketch matrix R most recently generated on this thread
+// (rid_api.cu fill_R): read only by the in-kernel regeneration experiment (RID_ZGEMM_VARIANT=10/11).
+struct SketchKey {
+  uint64_t seed = 0;
+  uint32_t stream = 4;
+};
+inline SketchKey& sketch_key() {
+  static thread_local SketchKey k;
+  return k;
+}
+
 // out(i, j) = N(seed, s, row0 + i, col0 + j), column-major with leading dimension ld (k_misc.cu)
 cudaError_t normal_fill(uint64_t seed, uint32_t s, int64_t rows, int64_t cols, int64_t row0,
                         int64_t col0, double2* out, int64_t ld, cudaStream_t st);
@@ -140,9 +153,17 @@ cudaError_t tri_inverse(const double2* R11, int64_t k, double2* Rinv, cudaStream
 // P[:, J_t - col0] = e_t for pivots inside the shard (k_misc.cu)
 cudaError_t assemble_identity(const int64_t* J, int64_t k, int64_t col0, int64_t n_loc, double2* P,
                               int64_t ldp, cudaStream_t st);
-// B(:, t) = A(:, J_t - col0) for pivots inside the shard (k_misc.cu)
+// B(:, t) = A(:, J_t - col0) for pivots inside the shard (k_misc.cu); a J_t outside [0, n) sets
+// *bad (device int) and leaves column t untouched
 cudaError_t gather_columns(const double2* A, int64_t lda, int64_t m, const int64_t* J, int64_t k,
-                           int64_t col0, int64_t n_loc, double2* B, int64_t ldb, cudaStream_t st);
+                           int64_t col0, int64_t n_loc, int64_t n, double2* B, int64_t ldb,
+                           int* bad, cudaStream_t st);
+// dst = sum over g < G of src.p[g], elementwise, added in rank order (k_misc.cu)
+constexpr int kMaxLocalRanks = 64;
+struct RankPtrs {
+  const double* p[kMaxLocalRanks];
+};
+cudaError_t sum_ranks(const RankPtrs& src, int G, double* dst, int64_t count, cudaStream_t st);
 
 // Compensated power-iteration pieces (k_estimate.cu). Vectors of "cdd" are 4 doubles per entry
 // (re.s, re.c, im.s, im.c): a Dot2 accumulator whose value is s + c.

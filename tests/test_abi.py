@@ -124,3 +124,18 @@ def test_id_exchange_gloo_world2(rid, tmp_path):
              for r in range(2)]
     outs = [p.communicate(timeout=120)[0] for p in procs]
     assert all(p.returncode == 0 for p in procs), outs
+
+
+def test_buffer_layouts_rejected_on_host(rid):
+    """_Buf refuses layouts librid cannot address as (pointer, ld >= rows) — before any call."""
+    import torch
+
+    col = np.zeros((64, 1), np.complex128, order="F")
+    with pytest.raises(ValueError):
+        rid._Buf(np.broadcast_to(col, (64, 8)), 64, 8, "A")  # column stride 0
+    with pytest.raises(ValueError):
+        rid._Buf(torch.zeros(64, 1, dtype=torch.complex128).expand(64, 8), 64, 8, "A")
+    ok = rid._Buf(np.zeros((64, 8), np.complex128, order="F"), 64, 8, "A")
+    assert ok.ld == 64
+    sub = np.zeros((80, 8), np.complex128, order="F")[:64]  # ld 80 > rows: fine
+    assert rid._Buf(sub, 64, 8, "A").ld == 80

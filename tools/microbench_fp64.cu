@@ -83,7 +83,42 @@ __global__ void k_dmma_round(const double* A, const double* B, const double* C, 
 
 static double now_ms(cudaEvent_t a, cudaEvent_t b) { float ms; cudaEventElapsedTime(&ms, a, b); return ms; }
 
-int main() {
+// `mb peaks`: the two roofline denominators bench.py uses, as one JSON line — DMMA burst (best of
+// 10 single launches of ~10 ms) and sustained (back to back for ~4 s), the kernel and shape of the
+// sweep's best row (2 CTAs x 256 threads per SM, 8 independent accumulators). tools/fp64_peaks.py
+// runs it under an nvidia-smi sampler and writes profiles/fp64_peaks.json.
+static int peaks_main() {
+  int dev = 0; cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, dev));
+  double* out; CK(cudaMalloc(&out, 4096 * sizeof(double)));
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  const int grid = p.multiProcessorCount * 2, thr = 256, iters = 40000;
+  const double flops = (double)grid * (thr / 32) * iters * 8 * 512.0;
+  k_dmma<8><<<grid, thr>>>(out, 100, 1.0); CK(cudaDeviceSynchronize());
+  double best = 1e30;
+  for (int r = 0; r < 10; ++r) {
+    cudaEventRecord(e0);
+    k_dmma<8><<<grid, thr>>>(out, iters, 1.0);
+    cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+    const double ms = now_ms(e0, e1);
+    if (ms < best) best = ms;
+  }
+  int reps = 0;
+  cudaEventRecord(e0);
+  double ms = 0;
+  while (ms < 4000.0) {
+    for (int i = 0; i < 40; ++i, ++reps) k_dmma<8><<<grid, thr>>>(out, iters, 1.0);
+    cudaEventRecord(e1); CK(cudaEventSynchronize(e1));
+    ms = now_ms(e0, e1);
+  }
+  printf("{\"dmma_tflops_burst\": %.4f, \"dmma_tflops_sustained\": %.4f, \"burst_ms\": %.4f, "
+         "\"sustained_ms\": %.1f, \"sustained_launches\": %d, \"grid\": %d, \"threads\": %d, "
+         "\"kernel\": \"mma.sync.m8n8k4.f64 (DMMA.8x8x4), 8 accumulators per warp\"}\n",
+         flops / best / 1e9, flops * reps / ms / 1e9, best, ms, reps, grid, thr);
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1 && argv[1][0] == 'p') return peaks_main();
   int dev = 0; cudaDeviceProp p; CK(cudaGetDeviceProperties(&p, dev));
   int clk = 0; cudaDeviceGetAttribute(&clk, cudaDevAttrClockRate, dev);
   printf("device %s SMs %d L2 %d B smem/SM %zu clock(kHz) %d\n", p.name, p.multiProcessorCount, p.l2CacheSize,
