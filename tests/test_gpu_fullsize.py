@@ -117,3 +117,43 @@ def test_fullsize_c1_exact_rank(rid, orc):
     est = rid.error_estimate(A, r.J, r.P, 20, 1)
     nA = np.linalg.svd(A_o, compute_uv=False)[0]
     assert est / nA <= 1e-13
+
+
+@pytest.mark.parametrize("name", ["C2", "C3"])
+def test_fullsize_live_oracle(rid, orc, name):
+    """C2 and C3 at full size against the oracle run LIVE on the box's host (no stored values):
+    A bitwise, every element of P within 1e-10 relative (reading R17) and J equal, the estimator
+    on the oracle's (A, J, P) within 1e-10 of the oracle's Dot2 estimator (R16 (i), q = 3), and
+    each side's own P within 1e-10 in rho = est / ||A||_2 (R16 (ii); ||A||_2 from the oracle's
+    power iteration with P = 0, q = 5: a lower bound of ||A||_2, so the check is conservative)."""
+    from paper_1205_3830_b200.configs import CONFIGS
+
+    c = CONFIGS[name]
+    seed, q = 1, 3
+    free = torch.cuda.mem_get_info()[0]
+    if free < 1.5 * c.a_bytes + (2 << 30):
+        pytest.skip(f"{name}: needs {c.a_bytes / 2**30:.0f} GiB of free HBM")
+    A_o = orc.generate(seed, c.m, c.n, c.k, c.noise)
+    d = orc.decompose(A_o, c.k, c.l, seed)
+    assert d.tie_margins[:-1].min() > 1e-10
+    A = rid.generate(seed, c.m, c.n, c.k, c.noise)
+    assert np.array_equal(bits(A.cpu().numpy()), bits(A_o)), "A"
+    r = rid.decompose(A, c.k, c.l, seed)
+    assert r.J.cpu().numpy().tolist() == d.J.tolist()
+    P = r.P.cpu().numpy()
+    assert np.array_equal(bits(P[:, d.J]), bits(np.eye(c.k)))
+    assert np.linalg.norm(P - d.P) <= 1e-10 * np.linalg.norm(d.P)
+    # per column as well: no column of P may hide behind the Frobenius norm
+    colerr = np.linalg.norm(P - d.P, axis=0) / np.maximum(np.linalg.norm(d.P, axis=0), 1.0)
+    assert colerr.max() <= 1e-10, (int(colerr.argmax()), float(colerr.max()))
+    # (i) estimator parity on the same (A, J, P)
+    e_o = orc.error_estimate(A_o, d.J, d.P, q, seed)
+    Jt = torch.from_numpy(d.J.copy()).cuda()
+    Pt = torch.from_numpy(d.P.T.copy()).T.cuda()
+    e_g = rid.error_estimate(A, Jt, Pt, q, seed)
+    assert abs(e_g - e_o) <= 1e-10 * e_o, (e_g, e_o)
+    # (ii) each side's own P, relative to ||A||_2
+    e_g2 = rid.error_estimate(A, r.J, r.P, q, seed)
+    nA = orc.error_estimate(A_o, np.zeros(1, np.int64), np.zeros((1, c.n), np.complex128,
+                                                                   order="F"), 5, seed)
+    assert abs(e_g2 - e_o) / nA <= 1e-10
