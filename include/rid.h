@@ -73,6 +73,18 @@ typedef enum {
                              QR ("CGS with iteration"); exact norms every step     */
 } rid_qr_kind;
 
+/* How rid_decompose factors the sketch when a communicator of G > 1 ranks is set
+ * (rid_set_qr_dist). Both give the same J and P bits as one rank. */
+typedef enum {
+  RID_QR_REPLICATED = 0, /* all-gather Y (16 l n bytes), then every rank factors the whole l x n
+                            sketch (default)                                     */
+  RID_QR_SHARDED = 1     /* no all-gather: rank g keeps its l x n/G block and the ranks factor the
+                            sketch together, exchanging per pivot step only the pivot candidates
+                            and the pivot column. Householder QR, G <= 8;
+                            built on the in-process data plane of rid_comm_init_local (one GPU);
+                            an NCCL communicator refuses it (RID_EINVAL from rid_decompose).     */
+} rid_qr_dist;
+
 /* Per-call diagnostics (SPEC.md:298-302 IdDiagnostics); every field is written by the call that
  * receives it; times are device times from CUDA events on the context stream, in seconds. */
 typedef struct {
@@ -169,6 +181,10 @@ rid_status rid_set_sketch(rid_ctx* ctx, int kind);
  * (default HOUSEHOLDER). RID_EINVAL for an unknown kind. CGS2 needs a workspace of
  * 16 (2 l n + 2 l k + k n) + 8 l (k + 1) bytes beyond Householder's. */
 rid_status rid_set_qr(rid_ctx* ctx, int kind);
+/* Select how subsequent rid_decompose calls on ctx factor a sharded sketch (rid_qr_dist; default
+ * RID_QR_REPLICATED). Every rank of a communicator must select the same mode. RID_EINVAL for an
+ * unknown mode. */
+rid_status rid_set_qr_dist(rid_ctx* ctx, int mode);
 /* Number of K slices S the sketch of an m-row, n-column matrix uses (1 = unsplit): chosen so that
  * the n/8-column shard of an 8-GPU run still fills the GPU, a function of (m, l, n) only. */
 int rid_sketch_splits(const rid_ctx* ctx, int64_t m, int64_t l, int64_t n);

@@ -61,9 +61,11 @@ EXPORTS = ["rid_create", "rid_destroy", "rid_last_error", "rid_version", "rid_co
            "rid_decompose", "rid_error_estimate", "rid_error_bound", "rid_normal_fill",
            "rid_qrcp", "rid_factor_solve", "rid_sketch_splits", "rid_sketch_srft",
            "rid_set_sketch", "rid_sketch_mults", "rid_sketch_cols", "rid_set_qr",
-           "rid_set_stream", "rid_comm_init_local"]
+           "rid_set_stream", "rid_comm_init_local", "rid_set_qr_dist"]
 SKETCH_GAUSSIAN, SKETCH_SRFT = 0, 1
 QR_HOUSEHOLDER, QR_CGS2 = 0, 1
+QR_REPLICATED, QR_SHARDED = 0, 1
+_QR_DIST = {"replicated": QR_REPLICATED, "sharded": QR_SHARDED}
 _QR_KINDS = {"householder": QR_HOUSEHOLDER, "cgs2": QR_CGS2}
 
 
@@ -97,6 +99,7 @@ def lib():
         "rid_sketch_srft": ([p, u64, ci, i64, p, i64, i64, i64, i64, p, i64], ci),
         "rid_set_sketch": ([p, ci], ci),
         "rid_set_qr": ([p, ci], ci),
+        "rid_set_qr_dist": ([p, ci], ci),
         "rid_decompose": ([p, p, i64, i64, i64, i64, i64, i64, i64, u64, p, p, i64, p], ci),
         "rid_error_estimate": ([p, p, i64, i64, i64, i64, i64, p, i64, p, i64, ci, u64, p, p], ci),
         "rid_error_bound": ([i64, i64, i64, d, d], d),
@@ -231,6 +234,11 @@ class Context:
     def comm_init(self, id_bytes: bytes, rank: int, nranks: int):
         buf = ctypes.create_string_buffer(id_bytes, len(id_bytes))
         self.check(self._L.rid_comm_init(self.h, buf, rank, nranks), "rid_comm_init")
+
+    def set_qr_dist(self, mode: str):
+        """'replicated' (all-gather Y, whole-sketch QR on every rank; default) or 'sharded'
+        (NEXT-3: the ranks factor their blocks together; in-process communicator only)."""
+        self.check(self._L.rid_set_qr_dist(self.h, _QR_DIST[mode]), "rid_set_qr_dist")
 
     def comm_info(self):
         r, n = ctypes.c_int(), ctypes.c_int()

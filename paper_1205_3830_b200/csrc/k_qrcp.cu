@@ -721,11 +721,21 @@ __device__ __forceinline__ void consumers_sync() {  // warps 1..15 only
 // transposed through the consumed slot and lane i finishes column i (f_t, R(j, c), the downdated
 // norm). Batches and rows are visited in alternating order from step to step (L2 reuse), and
 // boxes past the first l2_keep bytes of the trailing block carry an evict_first policy.
+//
+// Sharding (NEXT-3): the grid is G rank groups of cpr CTAs; rank g's CTAs own rank g's columns
+// (sh.Y[g], sh.w[g]) and nothing else of that rank is read by another rank except the pivot
+// column of a step (from its owner's block, by every CTA, as the one-rank kernel reads it). The
+// per-CTA candidates carry GLOBAL column ids, so the argmax (ties -> lowest global index) and
+// every column's arithmetic are those of the one-rank kernel: any G gives the same bits.
+struct RingMaps {
+  CUtensorMap m[kQrMaxRanks];  // rank g's Y block as a (2l doubles) x n_loc matrix
+};
+
 template <int MAXQ>
 __global__ void __launch_bounds__(kRingThreads, 1)
-    k_qrcp_ring(double2* __restrict__ Y, int64_t ldy, int l, int64_t n, int k, int j0, int jend,
-                double tol_rel, QrcpOut out, QrcpWork w, int ncw, int D, int per,
-                double l2_keep, const __grid_constant__ CUtensorMap tmap) {
+    k_qrcp_ring(const __grid_constant__ QrShards sh, int64_t ldy, int l, int k, int j0, int jend,
+                double tol_rel, int ncw, int D, int per, int cpr, double l2_keep,
+                const __grid_constant__ RingMaps tm) {
   constexpr int kCW = kRingWarps - 1;  // consumer warps in the reflector phase
   constexpr int kRQ = (MAXQ * 32 + kCW * 32 - 1) / (kCW * 32);
   extern __shared__ __align__(128) unsigned char ring_smem[];
@@ -740,10 +750,21 @@ __global__ void __launch_bounds__(kRingThreads, 1)
   __shared__ long long s_p;
   __shared__ int s_stop;
 
-  if (out.info[0] == 2) return;  // an earlier panel stopped on rank failure (uniform)
   const int nbk = gridDim.x, b = blockIdx.x;
+  const int g = b / cpr, bl = b - g * cpr;  // rank group and block within it
+  double2* __restrict__ Y = sh.Y[g];
+  const QrcpOut& out = sh.out[g];
+  const QrcpWork& w = sh.w[g];
+  const CUtensorMap& tmap = tm.m[g];
+  double* const cand = sh.w[0].cand;  // the exchange: every CTA's candidates, all ranks
+  unsigned* const bar = sh.w[0].bar;
+  const int max_blocks = sh.w[0].max_blocks;
+  const int64_t n = sh.n_loc;                    // this rank's columns (local ids 0..n-1)
+  const int64_t gbase = (int64_t)g * sh.n_loc;   // global id of local column 0
+  const int64_t nglob = (int64_t)sh.G * sh.n_loc;
+  if (out.info[0] == 2) return;  // an earlier panel stopped on rank failure (uniform)
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t c_lo = (int64_t)b * per;
+  const int64_t c_lo = (int64_t)bl * per;
   const int64_t c_hi = (c_lo + per < n) ? c_lo + per : n;
   const int64_t ldv = l;
   double nu0max = (j0 > 0) ? w.scal[0] : 0.0;
@@ -778,7 +799,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
       if (live && sl == 0) {
         w.nu[c] = nu;
         w.nuref[c] = nu;
-        top2_push(loc, nu, c);
+        top2_push(loc, nu, gbase + c);
       }
     }
     top2_warp(loc);
@@ -787,12 +808,12 @@ __global__ void __launch_bounds__(kRingThreads, 1)
     if (threadIdx.x == 0) {
       Top2 tt = sred[0];
       for (int q = 1; q < kRingWarps; ++q) top2_merge(tt, sred[q]);
-      double* c = w.cand + (size_t)b * 3;  // parity 0
+      double* c = cand + (size_t)b * 3;  // parity 0
       c[0] = tt.b1;
       c[1] = tt.b2;
       c[2] = (double)tt.i1;
     }
-    grid_barrier(w.bar, (unsigned)nbk * (++phase));
+    grid_barrier(bar, (unsigned)nbk * (++phase));
   }
 
   unsigned ubase = 0;  // items this warp streamed in earlier steps of this launch (ring parity)
@@ -804,7 +825,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
     if (warp == 0) {
       Top2 tt;
       top2_init(tt);
-      const double* cb = w.cand + (size_t)(j & 1) * w.max_blocks * 3;
+      const double* cb = cand + (size_t)(j & 1) * max_blocks * 3;
       for (int q = lane; q < nbk; q += 32) {
         Top2 o;
         o.b1 = cb[q * 3 + 0];
@@ -814,29 +835,36 @@ __global__ void __launch_bounds__(kRingThreads, 1)
       }
       top2_warp(tt);
       if (j == 0) nu0max = tt.b1;  // max_c ||Y[:, c]||
-      const bool stop = !(tt.b1 >= tol_rel * nu0max) || tt.b1 <= 0.0 || tt.i1 < 0 || tt.i1 >= n;
-      const int64_t p = tt.i1;
+      const bool stop =
+          !(tt.b1 >= tol_rel * nu0max) || tt.b1 <= 0.0 || tt.i1 < 0 || tt.i1 >= nglob;
+      const int64_t p = tt.i1;  // global id
       if (lane == 0) {
         s_p = p;
         s_stop = stop ? 1 : 0;
-        if (b == 0) {
+        if (bl == 0) {  // every rank's replicated outputs
           if (j == 0) w.scal[0] = nu0max;
           out.resid[j] = tt.b1;
           out.margin[j] = (tt.b2 < 0.0) ? DBL_MAX : (tt.b1 - tt.b2) / tt.b1;
           if (!stop) out.J[j] = p;
         }
       }
-      if (!stop && p >= c_lo && p < c_hi && lane == 0) w.nu[p] = -1.0;  // the owner: chosen
+      if (!stop && p >= gbase + c_lo && p < gbase + c_hi && lane == 0)
+        w.nu[p - gbase] = -1.0;  // the owner: chosen
     }
     __syncthreads();
     if (s_stop) {
-      if (b == 0 && threadIdx.x == 0) {
+      if (bl == 0 && threadIdx.x == 0) {
         out.info[0] = 2;
         out.info[1] = j;
       }
       return;  // no copy is in flight: every item of the previous step was consumed
     }
+    // the pivot column lives in its owner's block: rows of y^(j0)_p and its f_s(p)
     const int64_t p = s_p;
+    const int go = (int)(p / sh.n_loc);
+    const int64_t pl = p - (int64_t)go * sh.n_loc;
+    const double2* __restrict__ Yp = sh.Y[go] + pl * ldy;
+    const double2* __restrict__ Fp = sh.w[go].F + pl * kNB;
     if (w.trace && b == 0 && threadIdx.x == 32) w.trace[8 * j + 4] = globaltimer();
     const bool rev = (j & 1) != 0;  // alternate the batch and row order (L2 reuse across steps)
 
@@ -852,7 +880,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
       const int nitems = mybat * nch;
       // L2 residency: the first nkeep batches of every CTA (≈ l2_keep bytes of the trailing
       // block over the whole grid) are re-read from L2 at every step
-      const double blk = 16.0 * (double)L * (double)n;
+      const double blk = 16.0 * (double)L * (double)nglob;  // all ranks' blocks share one L2
       const int nkeep = blk <= l2_keep ? nbat : (int)((double)nbat * l2_keep / blk);
       const uint64_t pol_first = policy_evict_first();
       // boxes are issued in consumption order, D ahead: (iq, ich) = batch and chunk of the next
@@ -890,7 +918,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
 #pragma unroll
       for (int q = 0; q < kRQ; ++q) {
         const int rr = idx + kCW * 32 * q;
-        x[q] = rr < L ? Y[p * ldy + j + rr] : make_double2(0.0, 0.0);
+        x[q] = rr < L ? Yp[j + rr] : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int s0 = 0; s0 < kNB; s0 += 8) {
@@ -898,7 +926,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
           double2 vv[kRQ][8], fp[8];
 #pragma unroll
           for (int s = 0; s < 8; ++s) {
-            fp[s] = s0 + s < t ? w.F[p * kNB + s0 + s] : make_double2(0.0, 0.0);
+            fp[s] = s0 + s < t ? Fp[s0 + s] : make_double2(0.0, 0.0);
 #pragma unroll
             for (int q = 0; q < kRQ; ++q) {
               const int rr = idx + kCW * 32 * q;
@@ -923,12 +951,12 @@ __global__ void __launch_bounds__(kRingThreads, 1)
 #pragma unroll
         for (int q = 0; q < kRQ; ++q) {
           const int rr = idx + kCW * 32 * q;
-          x[q] = rr < L ? Y[p * ldy + j + rr] : make_double2(0.0, 0.0);
+          x[q] = rr < L ? Yp[j + rr] : make_double2(0.0, 0.0);
           for (int s0 = 0; s0 < t; s0 += 8) {
             double2 vv[8], fp[8];
 #pragma unroll
             for (int s = 0; s < 8; ++s) {
-              fp[s] = s0 + s < t ? w.F[p * kNB + s0 + s] : make_double2(0.0, 0.0);
+              fp[s] = s0 + s < t ? Fp[s0 + s] : make_double2(0.0, 0.0);
               vv[s] = (s0 + s < t && rr < L) ? w.V[(int64_t)(s0 + s) * ldv + j + rr]
                                              : make_double2(0.0, 0.0);
             }
@@ -995,11 +1023,11 @@ __global__ void __launch_bounds__(kRingThreads, 1)
             v.y = __fma_rn(x[q].x, sc_im, __dmul_rn(x[q].y, sc_re));
           }
           sv[rr] = v;
-          if (b == 0) w.V[(int64_t)t * ldv + j + rr] = v;
+          if (bl == 0) w.V[(int64_t)t * ldv + j + rr] = v;  // each rank's copy of V
         }
       }
       if (idx < 32) sv[L + idx] = make_double2(0.0, 0.0);  // the last box reads up to L + 31
-      if (b == 0) {
+      if (bl == 0) {
         if (idx == 0) {
           out.beta[j] = beta;
           out.R11[(int64_t)j * k + j] = make_double2(beta, 0.0);
@@ -1136,7 +1164,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
           Y[c * ldy + j] = Rj;
           w.nu[c] = nu_new;
           if (need) w.nuref[c] = nu_new;
-          top2_push(loc, nu_new, c);
+          top2_push(loc, nu_new, gbase + c);
         }
         if (++cch == nch) {
           cch = 0;
@@ -1153,8 +1181,8 @@ __global__ void __launch_bounds__(kRingThreads, 1)
     } else {
       // warp 0 is idle while warps 1.. build the reflector and stream: CTA 0's copies rows
       // 0..j-1 of the pivot column (final R entries) into the dense R11 off the critical path
-      if (b == 0)
-        for (int r = lane; r < j; r += 32) out.R11[(int64_t)j * k + r] = Y[p * ldy + r];
+      if (bl == 0)  // every rank's copy, from the owner's block
+        for (int r = lane; r < j; r += 32) out.R11[(int64_t)j * k + r] = Yp[r];
       if (lane == 0) {
         Top2 z;
         top2_init(z);
@@ -1165,16 +1193,16 @@ __global__ void __launch_bounds__(kRingThreads, 1)
     if (threadIdx.x == 0) {
       Top2 tt = sred[0];
       for (int q = 1; q < kRingWarps; ++q) top2_merge(tt, sred[q]);
-      double* cc = w.cand + ((size_t)((j + 1) & 1) * w.max_blocks + b) * 3;
+      double* cc = cand + ((size_t)((j + 1) & 1) * max_blocks + b) * 3;
       cc[0] = tt.b1;
       cc[1] = tt.b2;
       cc[2] = (double)tt.i1;
     }
     if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 2] = globaltimer();
-    if (j + 1 < jend) grid_barrier(w.bar, (unsigned)nbk * (++phase));
+    if (j + 1 < jend) grid_barrier(bar, (unsigned)nbk * (++phase));
     if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 3] = globaltimer();
   }
-  if (b == 0 && threadIdx.x == 0) out.info[1] = jend;
+  if (bl == 0 && threadIdx.x == 0) out.info[1] = jend;
 }
 
 size_t qrcp_work_bytes(int64_t n, int64_t l, int max_blocks) {
@@ -1281,23 +1309,33 @@ static cudaError_t launch_qrcp_smem(double2* Y, int64_t ldy, int l, int64_t n, i
 }
 
 // Panels of nb steps (k_qrcp_ring), each followed by the tensor-core trailing update
-// Y[jend:l, :] -= V[jend:l, 0:nb] · F[0:nb, :] (k_zgemm.cu mode 2).
+// Y[jend:l, :] -= V[jend:l, 0:nb] · F[0:nb, :] (k_zgemm.cu mode 2) of every rank's block.
+// The grid is G rank groups of cpr CTAs (G = 1: the whole-sketch QR).
 template <int MAXQ>
-static cudaError_t launch_qrcp_blocked(double2* Y, int64_t ldy, int l, int64_t n, int k,
-                                       double tol_rel, const QrcpOut& out, const QrcpWork& w,
-                                       int num_sms, cudaStream_t st, int* launches, int nbw) {
+static cudaError_t launch_qrcp_blocked(const QrShards& sh, int64_t ldy, int l, int k,
+                                       double tol_rel, int num_sms, cudaStream_t st,
+                                       int* launches, int nbw) {
   auto kern = k_qrcp_ring<MAXQ>;
   cudaError_t e;
+  const int G = sh.G;
+  const int64_t n = sh.n_loc;
+  if (G < 1 || G > kQrMaxRanks || n < 1) return cudaErrorInvalidValue;
   int optin = 0;  // cached per device (see launch_qrcp_smem)
   size_t fstatic = 0;
   if ((e = optin_smem(&optin)) != cudaSuccess) return e;
   if ((e = static_smem((const void*)kern, &fstatic)) != cudaSuccess) return e;
-  int blocks = num_sms;
-  if ((int64_t)blocks * 8 > n) blocks = (int)((n + 7) / 8);
-  if (blocks > w.max_blocks) blocks = w.max_blocks;
-  if (blocks < 1) blocks = 1;
-  const int per = (int)((n + blocks - 1) / blocks);
-  blocks = (int)((n + per - 1) / per);
+  // CTAs per rank: the SMs split evenly over the ranks (one CTA per SM, cooperative)
+  int cpr = num_sms / G;
+  if ((int64_t)cpr * 8 > n) cpr = (int)((n + 7) / 8);
+  if (cpr * G > sh.w[0].max_blocks) cpr = sh.w[0].max_blocks / G;
+  if (cpr < 1) cpr = 1;
+  // columns per CTA: a multiple of 32, so a column's lane in its batch (which rotates the order
+  // of its 16 row-partial sums, bank-conflict avoidance) is its global index mod 32 whenever
+  // n_loc is a multiple of 32: the same bits for every G
+  int per = (int)((n + cpr - 1) / cpr);
+  per = (per + 31) / 32 * 32;
+  cpr = (int)((n + per - 1) / per);
+  const int blocks = cpr * G;
   const size_t fixed = (size_t)kMaxSlots * 8 + (size_t)(MAXQ * 32 + 32) * sizeof(double2) + 128;
   const size_t avail = (size_t)optin - fstatic - 1024;
   const size_t slot_bytes = (size_t)32 * kCH * sizeof(double2);
@@ -1323,7 +1361,8 @@ static cudaError_t launch_qrcp_blocked(double2* Y, int64_t ldy, int l, int64_t n
   }
   const size_t smem = fixed + (size_t)ncw * D * slot_bytes;
   if ((e = ensure_dyn_smem((const void*)kern, smem)) != cudaSuccess) return e;
-  // 2D tensor map of Y as a (2l doubles) x n matrix, boxes of kCH complex rows x 32 columns
+  // 2D tensor map of each rank's block as a (2l doubles) x n_loc matrix, boxes of kCH complex
+  // rows x 32 columns
   static PFN_cuTensorMapEncodeTiled encode = nullptr;
   if (!encode) {
     cudaDriverEntryPointQueryResult qr;
@@ -1332,40 +1371,83 @@ static cudaError_t launch_qrcp_blocked(double2* Y, int64_t ldy, int l, int64_t n
       return e;
     if (qr != cudaDriverEntryPointSuccess || !encode) return cudaErrorSymbolNotFound;
   }
-  CUtensorMap tmap;
-  const cuuint64_t gdim[2] = {(cuuint64_t)(2 * l), (cuuint64_t)n};
-  const cuuint64_t gstride[1] = {(cuuint64_t)ldy * sizeof(double2)};
-  const cuuint32_t box[2] = {(cuuint32_t)(2 * kCH), 32u};
-  const cuuint32_t estr[2] = {1u, 1u};
-  if (encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)Y, gdim, gstride, box, estr,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-    return cudaErrorInvalidValue;
-  if ((e = cudaMemsetAsync(out.info, 0, 2 * sizeof(int), st)) != cudaSuccess) return e;
-  if ((e = cudaMemsetAsync(w.F, 0, (size_t)kNB * n * sizeof(double2), st)) != cudaSuccess) return e;
+  RingMaps tm;
+  for (int g = 0; g < G; ++g) {
+    const cuuint64_t gdim[2] = {(cuuint64_t)(2 * l), (cuuint64_t)n};
+    const cuuint64_t gstride[1] = {(cuuint64_t)ldy * sizeof(double2)};
+    const cuuint32_t box[2] = {(cuuint32_t)(2 * kCH), 32u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    if (encode(&tm.m[g], CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)sh.Y[g], gdim, gstride, box,
+               estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  for (int g = 0; g < G; ++g) {
+    if ((e = cudaMemsetAsync(sh.out[g].info, 0, 2 * sizeof(int), st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(sh.w[g].F, 0, (size_t)kNB * n * sizeof(double2), st)) != cudaSuccess)
+      return e;
+  }
   for (int j0 = 0; j0 < k; j0 += nbw) {
     const int jend = (j0 + nbw < k) ? j0 + nbw : k;
-    if ((e = cudaMemsetAsync(w.bar, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
-    QrcpOut o = out;
-    QrcpWork ww = w;
-    int j0v = j0, jendv = jend, ncwv = ncw, Dv = D, perv = per;
+    if ((e = cudaMemsetAsync(sh.w[0].bar, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+    QrShards shv = sh;
+    int64_t ldyv = ldy;
+    int lv = l, kv = k, j0v = j0, jendv = jend, ncwv = ncw, Dv = D, perv = per, cprv = cpr;
+    double tolv = tol_rel;
     double l2_keep = 80.0 * (1 << 20);  // bytes of the trailing block kept in L2 (126 MB L2)
     if (const char* v = experiment_env("RID_QRCP_L2KEEP_MB")) l2_keep = atof(v) * (1 << 20);
-    void* args[] = {&Y, &ldy, &l, &n, &k, &j0v, &jendv, &tol_rel, &o, &ww, &ncwv, &Dv, &perv,
-                    &l2_keep, &tmap};
+    void* args[] = {&shv, &ldyv, &lv, &kv, &j0v, &jendv, &tolv, &ncwv, &Dv, &perv, &cprv,
+                    &l2_keep, &tm};
     e = cudaLaunchCooperativeKernel((void*)kern, dim3(blocks), dim3(kRingThreads), args, smem, st);
     if (e != cudaSuccess) return e;
     *launches += 1;
-    if (jend < k) {  // trailing rows jend..l-1 of every column
+    if (jend < k) {  // trailing rows jend..l-1 of every column of every rank
       // (a CUDA-core version holding V in registers was measured no faster: 2.97 vs 2.94 ms of
       // updates at C4, both ≈3 TB/s — the update has 4 flop/B against a 5.7 flop/B FP64 ridge)
-      e = zgemm_ordered(w.V + jend, l, w.F, kNB, Y + jend, ldy, l - jend, n, jend - j0, 2, 0.0, 0,
-                        0, st);
-      if (e != cudaSuccess) return e;
-      *launches += 1;
+      for (int g = 0; g < G; ++g) {
+        e = zgemm_ordered(sh.w[g].V + jend, l, sh.w[g].F, kNB, sh.Y[g] + jend, ldy, l - jend, n,
+                          jend - j0, 2, 0.0, 0, 0, st);
+        if (e != cudaSuccess) return e;
+        *launches += 1;
+      }
     }
   }
   return cudaSuccess;
+}
+
+static int blocked_panel_width() {
+  int nbw = kNBDefault;
+  if (const char* v = select_env("RID_QRCP_NB")) nbw = atoi(v);  // tested: J, P independent of nb
+  if (nbw < 1 || nbw > kNB) nbw = kNBDefault;
+  return nbw;
+}
+
+static QrShards one_shard(double2* Y, int64_t n, const QrcpOut& out, const QrcpWork& w) {
+  QrShards sh;
+  sh.G = 1;
+  sh.n_loc = n;
+  sh.Y[0] = Y;
+  sh.out[0] = out;
+  sh.w[0] = w;
+  return sh;
+}
+
+cudaError_t qrcp_sharded(const QrShards& sh, int64_t ldy, int64_t l, int64_t k, double tol_rel,
+                         int num_sms, cudaStream_t st, int* launches) {
+  int dummy = 0;
+  if (!launches) launches = &dummy;
+  if (sh.G < 1 || sh.G > kQrMaxRanks || sh.n_loc < 1 || k < 1 || k > l ||
+      k > (int64_t)sh.G * sh.n_loc)
+    return cudaErrorInvalidValue;
+  const int li = (int)l, ki = (int)k, nbw = blocked_panel_width();
+  const int qneed = (li + 31) / 32;
+#define RID_QS(QV) \
+  if (qneed <= QV) return launch_qrcp_blocked<QV>(sh, ldy, li, ki, tol_rel, num_sms, st, launches, nbw);
+  RID_QS(1) RID_QS(2) RID_QS(3) RID_QS(4) RID_QS(5) RID_QS(6) RID_QS(8) RID_QS(9) RID_QS(12)
+  RID_QS(17) RID_QS(24) RID_QS(32) RID_QS(48) RID_QS(64)
+#undef RID_QS
+  return cudaErrorInvalidValue;  // l > 2048 unsupported
 }
 
 cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, double tol_rel,
@@ -1380,16 +1462,14 @@ cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, doubl
     variant = (16.0 * (double)l * (double)n >= 64.0 * (1 << 20)) ? 1 : 0;
     if (const char* v = select_env("RID_QRCP_VARIANT")) variant = atoi(v);
   }
-  int nbw = kNBDefault;
-  if (const char* v = select_env("RID_QRCP_NB")) nbw = atoi(v);  // panel-width experiments
-  if (nbw < 1 || nbw > kNB) nbw = kNBDefault;
+  const int nbw = blocked_panel_width();
   int dummy = 0;
   if (!launches) launches = &dummy;
 #define RID_Q(QV)                                                                              \
   if (qneed <= QV) {                                                                           \
     if (variant == 1)                                                                          \
-      return launch_qrcp_blocked<QV>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st,          \
-                                     launches, nbw);                                           \
+      return launch_qrcp_blocked<QV>(one_shard(Y, n, out, w), ldy, li, ki, tol_rel, num_sms,   \
+                                     st, launches, nbw);                                       \
     if (variant == 0) {                                                                        \
       const cudaError_t es =                                                                   \
           launch_qrcp_smem<QV>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st, launches);     \
@@ -1403,9 +1483,11 @@ cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, doubl
   // l up to 2048 (the paper's l = 2k with k = 1000): blocked panels only (the exact kernel holds
   // a column segment in registers)
   if (qneed <= 48)
-    return launch_qrcp_blocked<48>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st, launches, nbw);
+    return launch_qrcp_blocked<48>(one_shard(Y, n, out, w), ldy, li, ki, tol_rel, num_sms, st,
+                                   launches, nbw);
   if (qneed <= 64)
-    return launch_qrcp_blocked<64>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st, launches, nbw);
+    return launch_qrcp_blocked<64>(one_shard(Y, n, out, w), ldy, li, ki, tol_rel, num_sms, st,
+                                   launches, nbw);
   return cudaErrorInvalidValue;  // l > 2048 unsupported
 }
 

@@ -27,6 +27,15 @@ extern char** environ;  // POSIX: the RID_* knobs are part of the graph key
 // calling context's stream. Implementations: NCCL (rid_comm_init, one process per GPU) and the
 // in-process plane of rid_comm_init_local (G contexts in one process, device copies ordered by
 // events; how the tests run the G > 1 path on one GPU).
+// This rank's part of a sharded QR (NEXT-3): its sketch block and its QR workspace / outputs.
+struct ShardQrPart {
+  double2* Y;
+  int64_t ldy, l, n_loc, k;
+  double tol;
+  rid::QrcpOut out;
+  rid::QrcpWork w;
+};
+
 struct RidComm {
   int rank = 0, nranks = 1;
   virtual ~RidComm() = default;
@@ -34,6 +43,10 @@ struct RidComm {
   virtual rid_status allgather(rid_ctx* c, double* buf, size_t count) = 0;
   // in place: buf = sum over ranks (bitwise the same on every rank)
   virtual rid_status allreduce_sum(rid_ctx* c, double* buf, size_t count) = 0;
+  // the pivoted QR of the G sketch blocks in place (every rank's outputs written, identical);
+  // false: this data plane has no sharded QR (the caller all-gathers Y and factors it whole)
+  virtual bool has_sharded_qr() const { return false; }
+  virtual rid_status qr_sharded(rid_ctx*, const ShardQrPart&, int*) { return RID_EINVAL; }
 };
 
 struct rid_ctx {
@@ -55,6 +68,7 @@ struct rid_ctx {
   cudaEvent_t ev_copied[2] = {}, ev_used[2] = {}, ev_copy0 = nullptr, ev_copy1 = nullptr;
   int sketch_kind = 0;  // RID_SKETCH_GAUSSIAN (north star) or RID_SKETCH_SRFT
   int qr_kind = 0;      // RID_QR_HOUSEHOLDER (default) or RID_QR_CGS2
+  int qr_dist = 0;      // RID_QR_REPLICATED (default) or RID_QR_SHARDED (NEXT-3)
   // pinned host mirror of the QR's status block (info, beta, resid, margin): one copy, one sync
   void* host_qr = nullptr;
   size_t host_qr_bytes = 0;
@@ -162,6 +176,9 @@ struct LocalGroup {
   unsigned long long phase = 0;
   bool broken = false;
   std::vector<double*> buf;
+  std::vector<ShardQrPart> qr;  // the sharded QR's per-rank parts
+  rid_status qr_status = RID_OK;
+  std::string qr_err;
   std::vector<cudaEvent_t> ready, done;
   ~LocalGroup() {
     cudaSetDevice(device);
@@ -214,6 +231,8 @@ struct LocalComm final : RidComm {
     return finish(c);
   }
   rid_status allreduce_sum(rid_ctx* c, double* buf, size_t count);
+  bool has_sharded_qr() const override { return g->G <= rid::kQrMaxRanks; }
+  rid_status qr_sharded(rid_ctx* c, const ShardQrPart& part, int* launches) override;
 };
 
 bool is_device_ptr(const void* p) {
@@ -310,10 +329,12 @@ rid_status qr_check(rid_ctx* c, int64_t k, int* info_host, rid_diag* diag);
 
 // defer = true (rid_decompose): enqueue the QR and the copy of its status block, return without
 // synchronising; the caller synchronises once at its end and calls qr_check.
+// sharded = true (rid_decompose with RID_QR_SHARDED): Yw is this rank's l x n block (n = n_loc)
+// and the QR is the communicator's collective sharded QR (NEXT-3).
 rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64_t k, int64_t col0,
                             int64_t n_loc, double2* Pdev, int64_t ldp, int64_t** Jdev_out,
                             int* info_host, rid_diag* diag, bool solve, double** beta_out,
-                            bool defer = false) {
+                            bool defer = false, bool sharded = false) {
   void *pJ, *pbeta, *presid, *pmargin, *pinfo, *pwork, *pstat;
   RID_TRY(ws_get(c, "J", sizeof(int64_t) * k, &pJ));
   // the QR's status block, contiguous so the host reads it with one copy: info (2 ints, 16 B),
@@ -339,7 +360,10 @@ rid_status factor_and_solve(rid_ctx* c, double2* Yw, int64_t l, int64_t n, int64
     w.trace = (unsigned long long*)pt;
   }
   RID_CUDA(c, cudaMemsetAsync(pR11, 0, sizeof(double2) * k * k, c->stream));
-  if (c->qr_kind == RID_QR_CGS2) {  // the paper's own QR
+  if (sharded) {
+    const ShardQrPart part{Yw, l, l, n, k, kRankTol, o, w};
+    RID_TRY(c->comm->qr_sharded(c, part, diag ? &diag->launches : nullptr));
+  } else if (c->qr_kind == RID_QR_CGS2) {  // the paper's own QR
     void* pc;
     RID_TRY(ws_get(c, "cgs2_work", rid::cgs2_work_bytes(l, n, k, c->num_sms), &pc));
     RID_CUDA(c, rid::cgs2(Yw, l, l, n, k, kRankTol, o, pc, c->num_sms, c->stream,
@@ -514,6 +538,51 @@ rid_status LocalComm::allreduce_sum(rid_ctx* c, double* buf, size_t count) {
   RID_CUDA(c, rid::sum_ranks(src, g->G, (double*)tmp, (int64_t)count, c->stream));
   RID_TRY(finish(c));  // every peer has read buf: it may be overwritten
   RID_CUDA(c, cudaMemcpyAsync(buf, tmp, count * sizeof(double), cudaMemcpyDeviceToDevice, c->stream));
+  return RID_OK;
+}
+
+// The sharded QR on one device: every rank publishes its part; rank 0 launches the one kernel
+// over all G blocks (rid::qrcp_sharded: G rank groups of CTAs in one cooperative grid, the form
+// the profiling rules prescribe for more ranks than GPUs) on its stream after every rank's
+// `ready`; every rank's stream then waits for rank 0's `done`.
+rid_status LocalComm::qr_sharded(rid_ctx* c, const ShardQrPart& part, int* launches) {
+  g->qr.resize(g->G);
+  g->qr[rank] = part;
+  RID_CUDA(c, cudaEventRecord(g->ready[rank], c->stream));
+  RID_TRY(rendezvous(c));
+  if (rank == 0) {
+    rid::QrShards sh;
+    sh.G = g->G;
+    sh.n_loc = part.n_loc;
+    rid_status st = RID_OK;
+    for (int h = 0; h < g->G; ++h) {
+      const ShardQrPart& q = g->qr[h];
+      if (q.n_loc != part.n_loc || q.l != part.l || q.k != part.k || q.ldy != part.ldy)
+        st = RID_EINVAL;
+      sh.Y[h] = q.Y;
+      sh.out[h] = q.out;
+      sh.w[h] = q.w;
+      if (h != rank) {
+        cudaError_t e = cudaStreamWaitEvent(c->stream, g->ready[h], 0);
+        if (e != cudaSuccess) st = RID_ECUDA;
+      }
+    }
+    g->qr_err.clear();
+    if (st == RID_OK) {
+      const cudaError_t e = rid::qrcp_sharded(sh, part.ldy, part.l, part.k, part.tol, c->num_sms,
+                                              c->stream, launches);
+      if (e != cudaSuccess) {
+        st = RID_ECUDA;
+        g->qr_err = cudaGetErrorString(e);
+      }
+    } else if (g->qr_err.empty()) {
+      g->qr_err = "ranks disagree on (l, k, n_loc, ldy)";
+    }
+    g->qr_status = st;
+  }
+  RID_TRY(finish(c));  // every rank's stream now waits for rank 0's done (after the kernel)
+  if (g->qr_status != RID_OK)
+    return fail(c, g->qr_status, "sharded QR (rank 0): %s", g->qr_err.c_str());
   return RID_OK;
 }
 
@@ -729,6 +798,14 @@ rid_status rid_set_sketch(rid_ctx* c, int kind) {
   return RID_OK;
 }
 
+rid_status rid_set_qr_dist(rid_ctx* c, int mode) {
+  if (!c) return RID_EINVAL;
+  if (mode != RID_QR_REPLICATED && mode != RID_QR_SHARDED)
+    return fail(c, RID_EINVAL, "rid_set_qr_dist: unknown mode %d", mode);
+  c->qr_dist = mode;
+  return RID_OK;
+}
+
 rid_status rid_set_qr(rid_ctx* c, int kind) {
   if (!c) return RID_EINVAL;
   if (kind != RID_QR_HOUSEHOLDER && kind != RID_QR_CGS2)
@@ -809,6 +886,13 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
                 (long long)col0, (long long)n_loc, c->rank, c->nranks, (long long)n);
   if (c->nranks == 1 && (col0 != 0 || n_loc != n))
     return fail(c, RID_EINVAL, "rid_decompose: without a communicator the shard must be all of A");
+  // sharded QR (NEXT-3): Householder only, on a data plane that has it, equal shards
+  const bool sharded = c->comm && c->qr_dist == RID_QR_SHARDED && c->comm->has_sharded_qr() &&
+                       c->qr_kind == RID_QR_HOUSEHOLDER;
+  if (c->comm && c->qr_dist == RID_QR_SHARDED && !sharded)
+    return fail(c, RID_EINVAL, "rid_decompose: RID_QR_SHARDED needs the Householder QR and a "
+                               "communicator with a sharded QR (rid_comm_init_local, <= %d ranks)",
+                rid::kQrMaxRanks);
   rid_diag d{};
   cudaEvent_t* ev = c->ev;
   RID_CUDA(c, cudaEventRecord(ev[0], c->stream));
@@ -872,12 +956,17 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
     }
     }
     RID_CUDA(c, rec(ev[4]));
-    if (c->comm) RID_TRY(c->comm->allgather(c, (double*)Yw, (size_t)(2 * l * n_loc)));
+    if (c->comm && !sharded) RID_TRY(c->comm->allgather(c, (double*)Yw, (size_t)(2 * l * n_loc)));
     RID_CUDA(c, rec(ev[5]));
     // the QR, its status copy and the solve are enqueued together; the status is checked after
-    // the one synchronisation at the end (a failed attempt's solve output is discarded)
-    RID_TRY(factor_and_solve(c, Yw, l, n, k, col0, n_loc, (double2*)p.dev, ldp, &Jdev, info, &d,
-                             false, nullptr, /*defer=*/true));
+    // the one synchronisation at the end (a failed attempt's solve output is discarded).
+    // Sharded (NEXT-3): no all-gather; this rank's block is factored with the others' in place.
+    if (sharded)
+      RID_TRY(factor_and_solve(c, Yw + col0 * l, l, n_loc, k, 0, n_loc, (double2*)p.dev, ldp,
+                               &Jdev, info, &d, false, nullptr, /*defer=*/true, /*sharded=*/true));
+    else
+      RID_TRY(factor_and_solve(c, Yw, l, n, k, col0, n_loc, (double2*)p.dev, ldp, &Jdev, info, &d,
+                               false, nullptr, /*defer=*/true));
     RID_CUDA(c, rec(ev[6]));
     {  // solve
       void *pR11, *pRinv;

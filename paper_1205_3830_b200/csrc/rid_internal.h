@@ -140,6 +140,28 @@ cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, doubl
                  const QrcpOut& out, const QrcpWork& w, int num_sms, cudaStream_t st,
                  int* launches, int variant = -1);
 
+// The sharded QR: the sketch of an n-column matrix held as G column
+// blocks, rank g's block (global columns [g n_loc, (g + 1) n_loc)) in its own buffer Y[g] with its
+// own workspace w[g] (nu, nuref, F sized n_loc; V; scal), factored by the blocked kernel with the
+// CTAs split into G rank groups: rank g's CTAs touch only rank g's columns, and across ranks only
+// the per-CTA pivot candidates (w[0].cand, one grid barrier per step) and, per step, the pivot
+// column (rows j..l-1 plus its k_NB pending-reflector coefficients, read from the owner's block)
+// move. Every rank's outputs out[g] (J in GLOBAL ids, beta, resid, margin, info, R11) are written
+// and identical. G = 1 is qrcp()'s blocked path: the same kernel, bitwise the same results for any
+// G (every column's arithmetic and the pivot reduction are independent of the sharding).
+constexpr int kQrMaxRanks = 8;
+struct QrShards {
+  int G = 1;
+  int64_t n_loc = 0;
+  double2* Y[kQrMaxRanks] = {};
+  QrcpOut out[kQrMaxRanks] = {};
+  QrcpWork w[kQrMaxRanks] = {};
+};
+// one cooperative launch per panel over all G blocks (the one-GPU form; the real multi-GPU
+// transport is not built: DESIGN.md §8.2), plus G tensor-core trailing updates per panel
+cudaError_t qrcp_sharded(const QrShards& sh, int64_t ldy, int64_t l, int64_t k, double tol_rel,
+                         int num_sms, cudaStream_t st, int* launches);
+
 // The paper's QR: column-pivoted CGS with one reorthogonalisation (k_cgs2.cu).
 // Same outputs as qrcp (J, beta, resid, margin, info, R11) and the same contract on Y: on return
 // Y[0:k, c] = R[:, c] with R = Q^H Y (the rows below k are left as they were).

@@ -147,6 +147,56 @@ def test_multirank_decompose_and_estimate(rid, orc, name, seed, m, n, k, l, nois
             c.close()
 
 
+@pytest.mark.parametrize("name,seed,m,n,k,l,noise", CASES)
+def test_multirank_sharded_qr(rid, orc, name, seed, m, n, k, l, noise, monkeypatch):
+    """NEXT-3: no all-gather of Y; the G ranks factor their sketch blocks
+    together (one pivot-candidate exchange and one pivot-column read from its owner per step).
+    J equal to the oracle's, P within 1e-10 of it and bitwise equal to the one-rank call of the
+    same (blocked) kernel; every rank's outputs identical."""
+    d, _ = oracle_case(orc, seed, m, n, k, l, noise, 6)
+    A = rid.generate(seed, m, n, k, noise)
+    monkeypatch.setenv("RID_QRCP_VARIANT", "1")  # the blocked kernel the sharded QR runs
+    ref = rid.decompose(A, k, l, seed)
+    monkeypatch.delenv("RID_QRCP_VARIANT")
+    assert np_(ref.J).tolist() == d.J.tolist()
+    assert relf(np_(ref.P), d.P) <= 1e-10
+    for G in (1, 2, 4, 8):
+        ctxs, _ = make_ranks(rid, G)
+        for c in ctxs:
+            c.set_qr_dist("sharded")
+        shards = [rid.shard_range(n, g, G) for g in range(G)]
+        A_loc = [A[:, c0:c0 + nl] for c0, nl in shards]
+        J_out = [torch.empty(k, dtype=torch.int64, device="cuda") for _ in range(G)]
+        P_out = [rid.colmajor_empty(k, nl) for _, nl in shards]
+        torch.cuda.synchronize()
+
+        def dec(g):
+            c0, nl = shards[g]
+            r = rid.decompose(A_loc[g], k, l, seed, n=n, col0=c0, J=J_out[g], P=P_out[g],
+                              ctx=ctxs[g])
+            return r.diag
+
+        diags = run_ranks(G, dec)
+        for g in range(G):
+            assert np_(J_out[g]).tolist() == d.J.tolist(), (name, G, g)
+            assert abs(diags[g]["tie_margin_min"] - diags[0]["tie_margin_min"]) == 0.0
+        P_cat = np.concatenate([np_(p) for p in P_out], axis=1)
+        assert bits_equal(P_cat, np_(ref.P)), (name, G)
+        for c in ctxs:
+            c.close()
+
+
+def test_sharded_qr_refused_without_local_comm(rid):
+    ctx = rid.Context(0, torch.cuda.current_stream())
+    ctx.set_qr_dist("sharded")  # no communicator: the one-rank QR (G = 1), nothing to shard
+    A = rid.generate(1, 300, 64, 4, 1e-9)
+    r = rid.decompose(A, 4, 8, 1, ctx=ctx)
+    assert r.J.numel() == 4
+    with pytest.raises(KeyError):
+        ctx.set_qr_dist("bogus")
+    ctx.close()
+
+
 def test_multirank_host_buffers(rid, orc):
     """The e2e path (host A streamed in chunks, host P) under a 2-rank communicator."""
     seed, m, n, k, l, noise = 5, 1500, 600, 24, 40, 1e-9
