@@ -61,7 +61,7 @@ EXPORTS = ["rid_create", "rid_destroy", "rid_last_error", "rid_version", "rid_co
            "rid_decompose", "rid_error_estimate", "rid_error_bound", "rid_normal_fill",
            "rid_qrcp", "rid_factor_solve", "rid_sketch_splits", "rid_sketch_srft",
            "rid_set_sketch", "rid_sketch_mults", "rid_sketch_cols", "rid_set_qr",
-           "rid_set_stream", "rid_comm_init_local", "rid_set_qr_dist"]
+           "rid_set_stream", "rid_comm_init_local", "rid_set_qr_dist", "rid_sketch_strassen"]
 SKETCH_GAUSSIAN, SKETCH_SRFT = 0, 1
 QR_HOUSEHOLDER, QR_CGS2 = 0, 1
 QR_REPLICATED, QR_SHARDED = 0, 1
@@ -95,6 +95,7 @@ def lib():
         "rid_sketch": ([p, u64, u32, i64, p, i64, i64, i64, i64, p, i64], ci),
         "rid_sketch_splits": ([p, i64, i64, i64], ci),
         "rid_sketch_mults": ([], ci),
+        "rid_sketch_strassen": ([p, i64, i64, i64], ci),
         "rid_sketch_cols": ([p, u64, u32, i64, p, i64, i64, i64, i64, i64, p, i64], ci),
         "rid_sketch_srft": ([p, u64, ci, i64, p, i64, i64, i64, i64, p, i64], ci),
         "rid_set_sketch": ([p, ci], ci),
@@ -345,6 +346,13 @@ def sketch_splits(m: int, l: int, n: int, ctx: Context | None = None) -> int:
     """K slices of the sketch of an m x n matrix."""
     ctx = ctx or default_context()
     return lib().rid_sketch_splits(ctx.h, m, l, n)
+
+
+def sketch_strassen(m: int, l: int, n: int, ctx: Context | None = None) -> bool:
+    """True when the sketch of an m x n matrix runs one Strassen level over Gauss's three products
+    (then column blocks must be 64-aligned)."""
+    ctx = ctx or default_context()
+    return bool(lib().rid_sketch_strassen(ctx.h, m, l, n))
 
 
 def sketch_mults() -> int:

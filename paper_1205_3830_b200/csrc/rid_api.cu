@@ -438,22 +438,84 @@ rid_status qr_check(rid_ctx* c, int64_t k, int* info_host, rid_diag* diag) {
   return RID_OK;
 }
 
-// R (l x m, stream s) for the sketch, plus Re R + Im R for the 3M kernel. Returns launches.
-rid_status fill_R(rid_ctx* c, uint64_t seed, uint32_t s, int64_t l, int64_t m, double2** R,
-                  double** Rs, int* launches) {
+// The sketch matrix in the form the planned kernel reads: R (l x m) and Re R + Im R for the 3M
+// kernel, or (Strassen plan, k_strassen.cu) R's seven block combinations and their Re + Im planes.
+struct SketchR {
+  double2* R = nullptr;
+  double* Rs = nullptr;
+  bool strassen = false;
+  double2* Rc = nullptr;
+  double* Rsc = nullptr;
+  rid::StrassenWs sw{};
+};
+
+// R (l x m, stream s) for the sketch of an m x n matrix, in the form of the plan (l, m, n) picks.
+// Adds its launches.
+rid_status fill_R(rid_ctx* c, uint64_t seed, uint32_t s, int64_t l, int64_t m, int64_t n,
+                  SketchR* out, int* launches) {
   void *pR, *pRs = nullptr;
   RID_TRY(ws_get(c, "R", sizeof(double2) * l * m, &pR));
   rid::sketch_key() = rid::SketchKey{seed, s};
   RID_CUDA(c, rid::normal_fill(seed, s, l, m, 0, 0, (double2*)pR, l, c->stream));
   *launches += 1;
-  if (rid::sketch_mults() == 3) {
+  *out = SketchR{};
+  out->R = (double2*)pR;
+  if (rid::strassen_plan(l, m, n, c->num_sms)) {
+    out->strassen = true;
+    out->sw = rid::strassen_ws(l, m, 0);
+    void *pc, *ps;
+    RID_TRY(ws_get(c, "Rstr", out->sw.rc_bytes, &pc));
+    RID_TRY(ws_get(c, "Rsstr", out->sw.rs_bytes, &ps));
+    RID_CUDA(c, rid::strassen_rcomb((const double2*)pR, l, m, l, (double2*)pc, out->sw.ldc,
+                                    (double*)ps, out->sw.lds, c->stream));
+    *launches += 1;
+    out->Rc = (double2*)pc;
+    out->Rsc = (double*)ps;
+  } else if (rid::sketch_mults() == 3) {
     RID_TRY(ws_get(c, "Rs", sizeof(double) * rid::rsum_ld(l) * m, &pRs));
     RID_CUDA(c, rid::rsum_fill((const double2*)pR, l, m, l, (double*)pRs, rid::rsum_ld(l),
                                c->stream));
     *launches += 1;
+    out->Rs = (double*)pRs;
   }
-  *R = (double2*)pR;
-  *Rs = (double*)pRs;
+  return RID_OK;
+}
+
+// The aux stream and its fork/join events (created on first use) unless RID_SKETCH_NOAUX
+rid_status sketch_aux(rid_ctx* c, rid::SketchAux* aux, const rid::SketchAux** out) {
+  *out = nullptr;
+  if (rid::select_env("RID_SKETCH_NOAUX")) return RID_OK;
+  if (!c->aux_stream) {
+    RID_CUDA(c, cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
+    RID_CUDA(c, cudaEventCreateWithFlags(&c->aux_fork, cudaEventDisableTiming));
+    RID_CUDA(c, cudaEventCreateWithFlags(&c->aux_join, cudaEventDisableTiming));
+  }
+  *aux = rid::SketchAux{c->aux_stream, c->aux_fork, c->aux_join};
+  *out = aux;
+  return RID_OK;
+}
+
+// Y[:, 0:ncols] = R A for the columns [col0, col0 + ncols) of the m x n matrix, by the plan of sr
+rid_status sketch_block(rid_ctx* c, const SketchR& sr, const double2* A, int64_t lda, double2* Y,
+                        int64_t ldy, int64_t l, int64_t ncols, int64_t m, int64_t col0, int64_t n,
+                        int S, double2* partial, int* launches, const rid::SketchAux* aux) {
+  int dummy = 0;
+  if (!launches) launches = &dummy;
+  if (sr.strassen) {
+    if (col0 % 64 != 0 || ncols % 64 != 0)
+      return fail(c, RID_EINVAL,
+                  "sketch: with the Strassen plan of (l=%lld, m=%lld, n=%lld) a column block must "
+                  "start and end on multiples of 64 (col0=%lld, ncols=%lld); RID_SKETCH_STRASSEN=0 "
+                  "selects the plain 3M sketch", (long long)l, (long long)m, (long long)n,
+                  (long long)col0, (long long)ncols);
+    void* pm;
+    RID_TRY(ws_get(c, "Mstr", rid::strassen_ws(l, m, ncols).m_bytes, &pm));
+    RID_CUDA(c, rid::strassen_sketch(sr.Rc, sr.sw.ldc, sr.Rsc, sr.sw.lds, A, lda, Y, ldy, l, ncols,
+                                     m, (double2*)pm, c->stream, aux, launches));
+    return RID_OK;
+  }
+  RID_CUDA(c, rid::sketch_gemm(sr.R, l, sr.Rs, A, lda, Y, ldy, l, ncols, m, c->stream, S, partial,
+                               col0, n, c->num_sms, launches, aux));
   return RID_OK;
 }
 
@@ -461,7 +523,7 @@ rid_status fill_R(rid_ctx* c, uint64_t seed, uint32_t s, int64_t l, int64_t m, d
 // of ~1 GiB on a copy stream, double-buffered, each chunk's sketch overlapping the copy of the
 // next. The sketch of a column does not depend on the chunking, so Y is bit-identical to the
 // device-resident call. The device never holds more than two chunks of A.
-rid_status sketch_streamed(rid_ctx* c, const double2* R, const double* Rs, const rid_z* hostA,
+rid_status sketch_streamed(rid_ctx* c, const SketchR& sr, const rid_z* hostA,
                            int64_t m, int64_t n, int64_t col0, int64_t n_loc, int64_t lda,
                            int64_t l, double2* Y, int* launches, double* t_h2d, int ksplit,
                            double2* partial) {
@@ -474,7 +536,7 @@ rid_status sketch_streamed(rid_ctx* c, const double2* R, const double* Rs, const
     RID_CUDA(c, cudaEventCreate(&c->ev_copy0));
     RID_CUDA(c, cudaEventCreate(&c->ev_copy1));
   }
-  int64_t chunk = (int64_t)(1 << 30) / (16 * m);
+  int64_t chunk = (int64_t)(1 << 30) / (16 * m) / 64 * 64;  // whole 64-column groups
   if (chunk < 64) chunk = 64;
   if (chunk > n_loc) chunk = n_loc;
   void* buf[2];
@@ -494,8 +556,8 @@ rid_status sketch_streamed(rid_ctx* c, const double2* R, const double* Rs, const
                                   cudaMemcpyHostToDevice, c->copy_stream));
     RID_CUDA(c, cudaEventRecord(c->ev_copied[b], c->copy_stream));
     RID_CUDA(c, cudaStreamWaitEvent(c->stream, c->ev_copied[b], 0));
-    RID_CUDA(c, rid::sketch_gemm(R, l, Rs, (const double2*)buf[b], m, Y + j0 * l, l, l, nc, m,
-                                 c->stream, ksplit, partial, col0 + j0, n, c->num_sms, launches));
+    RID_TRY(sketch_block(c, sr, (const double2*)buf[b], m, Y + j0 * l, l, l, nc, m, col0 + j0, n,
+                         ksplit, partial, launches, nullptr));
     RID_CUDA(c, cudaEventRecord(c->ev_used[b], c->stream));
   }
   RID_CUDA(c, cudaEventRecord(c->ev_copy1, c->copy_stream));
@@ -840,6 +902,11 @@ int rid_sketch_splits(const rid_ctx* c, int64_t m, int64_t l, int64_t n) {
 
 int rid_sketch_mults(void) { return rid::sketch_mults(); }
 
+int rid_sketch_strassen(const rid_ctx* c, int64_t m, int64_t l, int64_t n) {
+  if (!c || m < 1 || l < 1 || n < 1) return 0;
+  return rid::strassen_plan(l, m, n, c->num_sms) ? 1 : 0;
+}
+
 rid_status rid_sketch(rid_ctx* c, uint64_t seed, uint32_t stream, int64_t l, const rid_z* A,
                       int64_t m, int64_t n, int64_t n_loc, int64_t lda, rid_z* Y, int64_t ldy) {
   return rid_sketch_cols(c, seed, stream, l, A, m, n, 0, n_loc, lda, Y, ldy);
@@ -857,16 +924,20 @@ rid_status rid_sketch_cols(rid_ctx* c, uint64_t seed, uint32_t stream, int64_t l
   RID_TRY(stage_in(c, "stage_A", A, m, n_loc, lda, sizeof(rid_z), true, &a));
   RID_TRY(stage_in(c, "stage_Y", Y, l, n_loc, ldy, sizeof(rid_z), false, &y));
   void* pS = nullptr;
-  double2* R;
-  double* Rs;
+  SketchR sr;
   int nl = 0;
-  RID_TRY(fill_R(c, seed, stream, l, m, &R, &Rs, &nl));
+  if (rid::strassen_plan(l, m, n, c->num_sms) && (col0 % 64 != 0 || n_loc % 64 != 0))
+    return fail(c, RID_EINVAL, "rid_sketch: with the Strassen plan of this (l, m, n) a column "
+                               "block must start and end on multiples of 64");
+  RID_TRY(fill_R(c, seed, stream, l, m, n, &sr, &nl));
   const int S = rid::sketch_ksplit(l, m, n / 8, c->num_sms);
-  const int64_t pe = rid::sketch_partial_elems(l, m, n, n_loc, c->num_sms);
+  const int64_t pe = sr.strassen ? 0 : rid::sketch_partial_elems(l, m, n, n_loc, c->num_sms);
   if (pe > 0) RID_TRY(ws_get(c, "splitk", sizeof(double2) * pe, &pS));
-  RID_CUDA(c, rid::sketch_gemm(R, l, Rs, (const double2*)a.dev, lda, (double2*)y.dev, ldy, l,
-                               n_loc, m, c->stream, S, (double2*)pS, col0, n, c->num_sms,
-                               nullptr));
+  rid::SketchAux auxv;
+  const rid::SketchAux* aux = nullptr;
+  if (sr.strassen) RID_TRY(sketch_aux(c, &auxv, &aux));  // the row split of the products
+  RID_TRY(sketch_block(c, sr, (const double2*)a.dev, lda, (double2*)y.dev, ldy, l, n_loc, m, col0,
+                       n, S, (double2*)pS, &nl, aux));
   RID_TRY(stage_out(c, y, Y, l, n_loc, ldy, sizeof(rid_z)));
   if (a.host || y.host) RID_CUDA(c, cudaStreamSynchronize(c->stream));
   return RID_OK;
@@ -907,8 +978,12 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
   double2* Yw = (double2*)pY;
   // K-split of the sketch: a function of (m, l, n) only, so Y is identical for every sharding
   const int S = rid::sketch_ksplit(l, m, n / 8, c->num_sms);
+  const bool strassen = c->sketch_kind != RID_SKETCH_SRFT && rid::strassen_plan(l, m, n, c->num_sms);
+  if (strassen && (col0 % 64 != 0 || n_loc % 64 != 0))
+    return fail(c, RID_EINVAL, "rid_decompose: with the Strassen sketch plan of this (l, m, n) a "
+                               "shard must start and end on multiples of 64 columns");
   void* pS = nullptr;
-  {
+  if (!strassen) {
     const int64_t cols = a_host ? std::min<int64_t>(n_loc, std::max<int64_t>(64, (int64_t)(1 << 30) / (16 * m)))
                                 : n_loc;
     const int64_t pe = rid::sketch_partial_elems(l, m, n, cols, c->num_sms);
@@ -935,24 +1010,18 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
       RID_TRY(srft_into(c, seed, attempt == 1, l, A, a_host ? nullptr : a.dev, m, n, n_loc, lda,
                         Yw + col0 * l, l, &d.launches));
     } else {
-    double2* Rg;
-    double* Rsg;
-    RID_TRY(fill_R(c, seed, sR, l, m, &Rg, &Rsg, &d.launches));
+    SketchR sr;
+    RID_TRY(fill_R(c, seed, sR, l, m, n, &sr, &d.launches));
     RID_CUDA(c, rec(ev[3]));
     if (a_host) {
-      RID_TRY(sketch_streamed(c, Rg, Rsg, A, m, n, col0, n_loc, lda, l, Yw + col0 * l,
-                              &d.launches, nullptr, S, (double2*)pS));
+      RID_TRY(sketch_streamed(c, sr, A, m, n, col0, n_loc, lda, l, Yw + col0 * l, &d.launches,
+                              nullptr, S, (double2*)pS));
     } else {
-      if (!c->aux_stream && !rid::select_env("RID_SKETCH_NOAUX")) {
-        RID_CUDA(c, cudaStreamCreateWithFlags(&c->aux_stream, cudaStreamNonBlocking));
-        RID_CUDA(c, cudaEventCreateWithFlags(&c->aux_fork, cudaEventDisableTiming));
-        RID_CUDA(c, cudaEventCreateWithFlags(&c->aux_join, cudaEventDisableTiming));
-      }
-      const rid::SketchAux aux{c->aux_stream, c->aux_fork, c->aux_join};
-      RID_CUDA(c, rid::sketch_gemm(Rg, l, Rsg, (const double2*)a.dev, lda, Yw + col0 * l, l, l,
-                                   n_loc, m, c->stream, S, (double2*)pS, col0, n, c->num_sms,
-                                   &d.launches, (c->aux_stream && !rid::select_env("RID_SKETCH_NOAUX"))
-                                                    ? &aux : nullptr));
+      rid::SketchAux auxv;
+      const rid::SketchAux* aux = nullptr;
+      RID_TRY(sketch_aux(c, &auxv, &aux));
+      RID_TRY(sketch_block(c, sr, (const double2*)a.dev, lda, Yw + col0 * l, l, l, n_loc, m, col0,
+                           n, S, (double2*)pS, &d.launches, aux));
     }
     }
     RID_CUDA(c, rec(ev[4]));

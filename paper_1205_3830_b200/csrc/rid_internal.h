@@ -90,6 +90,23 @@ cudaError_t sketch_gemm(const double2* R, int64_t ldr, const double* Rs, const d
                         int64_t lda, double2* Y, int64_t ldy, int64_t l, int64_t ncols, int64_t m,
                         cudaStream_t st, int ksplit, double2* partial, int64_t col0, int64_t n,
                         int num_sms, int* launches, const SketchAux* aux = nullptr);
+// The sketch with one level of Strassen over Gauss's 3M (k_strassen.cu, R32): planned
+// from (l, m, n) only; then every column block passed must start and end on multiples of 64.
+bool strassen_enabled();
+bool strassen_plan(int64_t l, int64_t m, int64_t n, int num_sms);
+struct StrassenWs {
+  int64_t ldc, lds;                 // leading dimensions of Rc (complex) and Rs (double)
+  size_t rc_bytes, rs_bytes, m_bytes;
+};
+StrassenWs strassen_ws(int64_t l, int64_t m, int64_t ncols);
+// Rc / Rs: the seven R combinations (7 l/2 rows x m/2) and their Re + Im planes, from R (l x m)
+cudaError_t strassen_rcomb(const double2* R, int64_t l, int64_t m, int64_t ldr, double2* Rc,
+                           int64_t ldc, double* Rs, int64_t lds, cudaStream_t st);
+// Y (l x ncols, ncols % 64 == 0) = R A for a 64-aligned column block; M: m_bytes of workspace
+cudaError_t strassen_sketch(const double2* Rc, int64_t ldc, const double* Rs, int64_t lds,
+                            const double2* A, int64_t lda, double2* Y, int64_t ldy, int64_t l,
+                            int64_t ncols, int64_t m, double2* M, cudaStream_t st,
+                            const SketchAux* aux, int* launches);
 // K slices for a sketch of Mout rows, K = m, chosen from n_ref = n_global / 8 only (G-invariant)
 int zgemm_ksplit(int64_t Mout, int64_t K, int64_t n_ref, int num_sms);
 

@@ -299,6 +299,7 @@ def test_sketch_wave_tail_split(rid, orc, monkeypatch):
     column is bitwise the unsplit kernel's, and the plan is a function of the global column index
     — shards reproduce the whole matrix bit for bit."""
     seed, m, n, k, l, noise = 4, 1024, 13824, 64, 528, 1e-9  # 11 x 216 tiles = 8 over 8 waves
+    monkeypatch.setenv("RID_SKETCH_STRASSEN", "0")  # this shape's default plan is Strassen's
     A = rid.generate(seed, m, n, k, noise)
     Y = np_(rid.sketch(A, seed, l))
     monkeypatch.setenv("RID_SKETCH_NOTAIL", "1")
