@@ -154,20 +154,21 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
   // raster 0: blockIdx = (row tile, column tile, product); raster 1: blockIdx.x = product +
   // nz * row tile, so every product of a column tile runs at once and they share its A tiles in L2
   constexpr int nz = TWO ? 5 : 2;
-  const int zi = raster ? (int)(blockIdx.x % nz) : (int)blockIdx.z;
-  const int rti = raster ? (int)(blockIdx.x / nz) : (int)blockIdx.x;
-  const int z = TWO ? (int)((0x65320u >> (4 * zi)) & 15u)  // M1 M3 M4 M6 M7
-                    : (zi ? 4 : 1);                         // M2 M5
-  const int r0 = rbeg + rti * Cf::BR;  // first product row of the tile
-  const int64_t j0 = (int64_t)blockIdx.y * Cf::BJ;  // first half-column
-  const int grp = (int)(j0 >> 5);                    // its first 64-column group (of two)
-  const int kh1 = c_strassen_a[z][0], h1 = c_strassen_a[z][1];
-  const int kh2 = c_strassen_a[z][2], h2 = c_strassen_a[z][3];
-  const double sg = (double)c_strassen_a[z][4];
+  // the tile (product z, first product row, first half-column), recomputed from blockIdx where
+  // used so no index is live across the K loop (the loop runs at the 128-register limit)
+  auto tile_z = [&]() -> int {
+    const int zi = raster ? (int)(blockIdx.x % nz) : (int)blockIdx.z;
+    return TWO ? (int)((0x65320u >> (4 * zi)) & 15u)  // M1 M3 M4 M6 M7
+               : (zi ? 4 : 1);                         // M2 M5
+  };
+  auto tile_r0 = [&]() -> int {
+    return rbeg + (int)(raster ? blockIdx.x / nz : blockIdx.x) * Cf::BR;
+  };
+  // sign of the second A term as a mask on the high word: v - w = v + (w with its sign flipped),
+  // an integer XOR off the FP64 pipe, then one DADD (the exact sum / difference, one rounding)
+  const unsigned sgmask = c_strassen_a[tile_z()][4] < 0 ? 0x80000000u : 0u;
   constexpr bool two = TWO;
-  const int rrow = z * lh + r0;  // first row of the tile in Rc / Rs
   const int nk = mh / Cf::BKC;
-  M += (int64_t)z * lh * nh;
 
   if (tid == 0) {
     tma_prefetch_map(&mapA);
@@ -182,7 +183,12 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
   }
   __syncthreads();
 
-  auto issue = [&](int kt) {  // thread 0 only
+  auto issue = [&](int kt) {  // thread 0 only (tile coordinates recomputed: short live ranges)
+    const int zz = tile_z();
+    const int grp = (int)(blockIdx.y * (Cf::BJ / 32));  // the tile's first 64-column group
+    const int rrow = zz * lh + tile_r0();                // the tile's first row in Rc / Rs
+    const int kh1 = c_strassen_a[zz][0], h1 = c_strassen_a[zz][1];
+    const int kh2 = c_strassen_a[zz][2], h2 = c_strassen_a[zz][3];
     const int s = kt % STAGES;
     unsigned char* st = sm + (size_t)s * Cf::kStage;
     mbar_expect_tx(&full[s], two ? Cf::kStage : Cf::kStage - Cf::kAterm);
@@ -230,8 +236,10 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
         double2 v = *reinterpret_cast<const double2*>(pa);
         if constexpr (decltype(TWO)::value) {
           const double2 w = *reinterpret_cast<const double2*>(pa + Cf::kAterm);
-          v.x = __fma_rn(sg, w.x, v.x);  // v +- w, exact sign, one rounding
-          v.y = __fma_rn(sg, w.y, v.y);
+          v.x = __dadd_rn(v.x, __hiloint2double(__double2hiint(w.x) ^ (int)sgmask,
+                                                __double2loint(w.x)));
+          v.y = __dadd_rn(v.y, __hiloint2double(__double2hiint(w.y) ^ (int)sgmask,
+                                                __double2loint(w.y)));
         }
         a[f][0] = v.x;
         a[f][1] = v.y;
@@ -273,6 +281,9 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
   }
 
   // epilogue: lane (g, t) holds half-column π(g) and rows t, t + 4 of each 8 x 8 fragment
+  M += (int64_t)tile_z() * lh * nh;
+  const int r0 = tile_r0();
+  const int64_t j0 = (int64_t)blockIdx.y * Cf::BJ;  // first half-column
 #pragma unroll
   for (int fa = 0; fa < FJ; ++fa) {
     const int64_t j = j0 + wj * FJ * 8 + fa * 8 + pg;
@@ -372,16 +383,17 @@ static cudaError_t launch_products(const CUtensorMap& mapA, const double2* Rc, i
 }
 
 // rows = the tile height. The 48-row main part: 8 warps along j (1 x 6 fragments: one A fragment,
-// so one A combination, per warp) with the product-major raster when the remainder is small
-// (C4: 264 = 5 x 48 + 24: 90.95 ms against 92.20 for 2 x 4 warps and the (row, column, product)
-// raster), else 2 x 4 warps, (row, column, product) raster (C5: 136 = 2 x 48 + 40: 201.6 against
-// 204.8 ms). tools/strassen_check.py; RID_STR_TILE / RID_STR_RASTER in an experiments build.
+// so one A combination, per warp) with the product-major raster (measured, tools/strassen_check.py,
+// profiles/r02/s2_strassen_variants.txt: C4 90.7 ms, C5 201.6 ms against 92.1-92.7 / 202.9-203.5
+// for 2 x 4 warps or the (row, column, product) raster; RID_STR_TILE / RID_STR_RASTER in an
+// experiments build).
 static cudaError_t products_rows(int rows, int rem, const CUtensorMap& mapA, const double2* Rc,
                                  int64_t ldc, const double* Rs, int64_t lds, double2* M, int lh,
                                  int64_t nh, int64_t mh, int rbeg, int rend, cudaStream_t st) {
-  int tile = rem == 24 ? 1 : 0;
+  (void)rem;
+  int tile = 1;
   if (const char* v = experiment_env("RID_STR_TILE")) tile = atoi(v);
-  const int raster = rem == 24 ? 1 : 0;
+  const int raster = 1;
 #define RID_LP(...) \
   launch_products<__VA_ARGS__>(mapA, Rc, ldc, Rs, lds, M, lh, nh, mh, rbeg, rend, st, raster)
   if (rows == 48 && tile == 1) return RID_LP(1, 6, 8, 1, 2, 2);
