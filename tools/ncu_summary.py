@@ -71,6 +71,7 @@ def main(tag, cfg):
             f.write("\n".join(ll) + "\n")
     traffic_path = os.path.join(PROF, "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    seen = {}
     for kind in ("sketch", "qrcp", "update"):
         rep = os.path.join(OUT, f"prof_{kind}_{cfg}.ncu-rep")
         if not os.path.exists(rep):
@@ -90,8 +91,15 @@ def main(tag, cfg):
                 scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
                 scale_w = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(
                     d["dram__bytes_write.sum"][1], 1)
-                traffic[f"{cfg}/{kind}"] = {"dram_bytes_per_launch": rd * scale + wr * scale_w,
-                                            "source": f"profiles/{tag}_{cfg}_ncu_summary.txt"}
+                if rd != rd or wr != wr:  # a replay that returned no counters (nan): skip
+                    raise ValueError("nan")
+                # the sketch phase = every launch in its report (the Strassen products: four)
+                key = f"{cfg}/{kind}"
+                prev = traffic.get(key, {}) if seen.get(key) else {}
+                seen[key] = True
+                traffic[key] = {"dram_bytes_per_launch":
+                                prev.get("dram_bytes_per_launch", 0.0) + rd * scale + wr * scale_w,
+                                "source": f"profiles/{tag}_{cfg}_ncu_summary.txt"}
             except (KeyError, ValueError):
                 pass
     with open(os.path.join(PROF, f"{tag}_{cfg}_ncu_summary.txt"), "w") as f:
