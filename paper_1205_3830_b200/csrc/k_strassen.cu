@@ -114,13 +114,13 @@ __device__ __forceinline__ void tma_box4_g2s(void* dst, const CUtensorMap* map, 
       : "memory");
 }
 
-template <int FJ, int FR, int WJ, int WR, int STAGES>
+template <int FJ, int FR, int WJ, int WR, int STAGES, int BK = 16>
 struct SCfg {
   static constexpr int kWarps = WJ * WR;
   static constexpr int kThreads = kWarps * 32;
   static constexpr int BJ = WJ * FJ * 8;     // half-columns per CTA (64: two 32-column boxes)
   static constexpr int BR = WR * FR * 8;     // product rows per CTA
-  static constexpr int BKC = 16;             // complex K per stage
+  static constexpr int BKC = BK;             // complex K per stage (8 or 16)
   static constexpr int kABox = 128 * BJ;     // 8 complex K x BJ half-columns
   static constexpr int kRBox = 128 * BKC;    // 8 complex rows x BKC K
   static constexpr int kRsBox = 64 * BKC;    // 8 rows of Re + Im x BKC K
@@ -129,7 +129,8 @@ struct SCfg {
   static constexpr int kStage = 2 * kAterm + kNR * kRBox + kNR * kRsBox;
   static constexpr size_t kSmem = (size_t)STAGES * kStage + 1024;
   static_assert(BJ == 64, "a tile is two 32-column halves of one column half");
-  static_assert(kABox % 1024 == 0 && kRBox % 1024 == 0, "boxes keep 1 KB alignment");
+  static_assert(kABox % 1024 == 0 && kRBox % 1024 == 0 && kStage % 1024 == 0,
+                "boxes and stages keep 1 KB alignment (128-byte swizzle)");
 };
 
 // One launch computes rows [rbeg, rend) of the products selected by blockIdx.z: TWO = the
@@ -137,12 +138,12 @@ struct SCfg {
 // two with a single block (M2, M5) — separate instantiations, so neither carries the other's
 // registers. mapA: the A block as 4D (2m doubles, 32 columns, 2 halves, n/64 groups); mapR /
 // mapS: Rc / Rs.
-template <int FJ, int FR, int WJ, int WR, int STAGES, int MINB, bool TWO>
+template <int FJ, int FR, int WJ, int WR, int STAGES, int MINB, bool TWO, int BK>
 __global__ void __launch_bounds__(WJ* WR * 32, MINB)
     k_strassen3m(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapR,
                  const __grid_constant__ CUtensorMap mapS, double2* __restrict__ M, int lh,
                  int64_t nh, int mh, int rbeg, int rend, int raster) {
-  using Cf = SCfg<FJ, FR, WJ, WR, STAGES>;
+  using Cf = SCfg<FJ, FR, WJ, WR, STAGES, BK>;
   extern __shared__ __align__(1024) unsigned char smraw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
   unsigned char* sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
@@ -337,13 +338,13 @@ cudaError_t strassen_rcomb(const double2* R, int64_t l, int64_t m, int64_t ldr, 
   return cudaGetLastError();
 }
 
-template <int FJ, int FR, int WJ, int WR, int STAGES, int MINB>
+template <int FJ, int FR, int WJ, int WR, int STAGES, int MINB, int BK = 16>
 static cudaError_t launch_products(const CUtensorMap& mapA, const double2* Rc, int64_t ldc,
                                    const double* Rs, int64_t lds, double2* M, int lh, int64_t nh,
                                    int64_t mh, int rbeg, int rend, cudaStream_t st, int raster) {
-  using Cf = SCfg<FJ, FR, WJ, WR, STAGES>;
-  auto kern2 = k_strassen3m<FJ, FR, WJ, WR, STAGES, MINB, true>;
-  auto kern1 = k_strassen3m<FJ, FR, WJ, WR, STAGES, MINB, false>;
+  using Cf = SCfg<FJ, FR, WJ, WR, STAGES, BK>;
+  auto kern2 = k_strassen3m<FJ, FR, WJ, WR, STAGES, MINB, true, BK>;
+  auto kern1 = k_strassen3m<FJ, FR, WJ, WR, STAGES, MINB, false, BK>;
   cudaError_t e;
   if ((e = ensure_dyn_smem((const void*)kern2, Cf::kSmem)) != cudaSuccess) return e;
   if ((e = ensure_dyn_smem((const void*)kern1, Cf::kSmem)) != cudaSuccess) return e;
