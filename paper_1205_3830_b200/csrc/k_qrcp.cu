@@ -39,6 +39,7 @@
 #include <cstdint>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -424,14 +425,26 @@ __global__ void __launch_bounds__(kQrcpThreads, 2)
 // CTA's local best. The trailing update and the exact norms run from shared memory; the columns
 // go back to Y after the last step.
 // =============================================================================================
-template <int MAXQ>
+//
+// CLUSTER = true (k_qrcp_cluster, sketches of at most a few MB: C1): the grid is ONE thread-block
+// cluster of up to 16 CTAs and the exchange moves from global memory to distributed shared
+// memory: every CTA publishes its candidate triple and its best column into its OWN shared
+// memory (double-buffered by step parity), the grid barrier becomes the cluster barrier
+// (barrier.cluster arrive.release / wait.acquire), and the pivot reduction and the winner's
+// column are read from the peers' shared memory (mapa / ld.shared::cluster). The arithmetic is
+// unchanged: the same bits as the grid-wide kernel (tested).
+template <int MAXQ, bool CLUSTER = false>
 __global__ void __launch_bounds__(kQrcpThreads, 1)
     k_qrcp_smem(double2* __restrict__ Y, int64_t ldy, int l, int64_t n, int k, double tol_rel,
                 QrcpOut out, QrcpWork w, int per) {
+  namespace cg = cooperative_groups;
   extern __shared__ __align__(16) unsigned char qs_raw[];
   double2* sv = reinterpret_cast<double2*>(qs_raw);                   // MAXQ*32: v_j, rows j..
   double* snu = reinterpret_cast<double*>(sv + MAXQ * 32);            // per (even): norms, -1 chosen
   double2* sy = reinterpret_cast<double2*>(snu + ((per + 1) & ~1));   // per x l: the columns
+  // CLUSTER: the exchange, in this CTA's shared memory: 2 x l slot, 2 x 3 candidate (parity)
+  double2* sslot = sy + (size_t)per * l;
+  double* scand = reinterpret_cast<double*>(sslot + (CLUSTER ? 2 * l : 0));
   __shared__ double s_tau[2];
   __shared__ Top2 sred[kQrcpWarps];
   __shared__ long long s_p;
@@ -447,6 +460,26 @@ __global__ void __launch_bounds__(kQrcpThreads, 1)
   double nu0max = 0.0;
   unsigned phase = 0;
 
+  // where CTA q's candidates / slot of a parity live (global, or q's shared memory)
+  auto cand_of = [&](int parity, int q) -> const double* {
+    if constexpr (CLUSTER)
+      return cg::this_cluster().map_shared_rank(scand + 3 * parity, (unsigned)q);
+    else
+      return w.cand + ((size_t)parity * w.max_blocks + q) * 3;
+  };
+  auto slot_of = [&](int parity, int q) -> double2* {
+    if constexpr (CLUSTER)
+      return cg::this_cluster().map_shared_rank(sslot + (size_t)parity * l, (unsigned)q);
+    else
+      return w.xslot + ((size_t)parity * w.max_blocks + q) * l;
+  };
+  auto exchange_barrier = [&]() {
+    if constexpr (CLUSTER)
+      cg::this_cluster().sync();
+    else
+      grid_barrier(w.bar, (unsigned)nb * (++phase));
+  };
+
   // publish the CTA's (best, second, index) and copy its best column's rows r0..l-1 to the slot
   auto publish = [&](Top2 loc, int parity, int r0) {
     top2_warp(loc);
@@ -455,7 +488,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1)
     if (threadIdx.x == 0) {
       Top2 tt = sred[0];
       for (int q = 1; q < kQrcpWarps; ++q) top2_merge(tt, sred[q]);
-      double* c = w.cand + ((size_t)parity * w.max_blocks + b) * 3;
+      double* c = const_cast<double*>(cand_of(parity, b));
       c[0] = tt.b1;
       c[1] = tt.b2;
       c[2] = (double)tt.i1;
@@ -464,7 +497,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1)
     __syncthreads();
     const int bl = s_best;
     if (bl >= 0) {
-      double2* slot = w.xslot + ((size_t)parity * w.max_blocks + b) * l;
+      double2* slot = slot_of(parity, b);
       for (int r = r0 + threadIdx.x; r < l; r += kQrcpThreads) slot[r] = sy[(int64_t)bl * l + r];
     }
   };
@@ -500,7 +533,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1)
       }
     }
     publish(loc, 0, 0);
-    grid_barrier(w.bar, (unsigned)nb * (++phase));
+    exchange_barrier();
   }
 
   for (int j = 0; j < k; ++j) {
@@ -510,12 +543,12 @@ __global__ void __launch_bounds__(kQrcpThreads, 1)
     if (warp == 0) {
       Top2 tt;
       top2_init(tt);
-      const double* cb = w.cand + (size_t)(j & 1) * w.max_blocks * 3;
       for (int q = lane; q < nb; q += 32) {
+        const double* cb = cand_of(j & 1, q);
         Top2 o;
-        o.b1 = cb[q * 3 + 0];
-        o.b2 = cb[q * 3 + 1];
-        o.i1 = (long long)cb[q * 3 + 2];
+        o.b1 = cb[0];
+        o.b2 = cb[1];
+        o.i1 = (long long)cb[2];
         top2_merge(tt, o);
       }
       top2_warp(tt);
@@ -536,6 +569,9 @@ __global__ void __launch_bounds__(kQrcpThreads, 1)
         out.info[0] = 2;
         out.info[1] = j;
       }
+      // (CLUSTER: every CTA stops at the same step; no peer reads this CTA's shared memory after
+      // the barrier it passed, and a CTA only exits after all peers' reads of its memory)
+      if constexpr (CLUSTER) cg::this_cluster().sync();
       return;
     }
     const int64_t p = s_p;
@@ -543,7 +579,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1)
 
     // ---- 2. reflector H_j from the winner's slot (rows j..l-1 of column p) -------------------
     if (warp == 0) {
-      const double2* xs = w.xslot + ((size_t)(j & 1) * w.max_blocks + bp) * l + j;
+      const double2* xs = slot_of(j & 1, bp) + j;
       double2 x[MAXQ];
 #pragma unroll
       for (int q = 0; q < MAXQ; ++q) {
@@ -659,7 +695,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1)
     }
     publish(loc, (j + 1) & 1, j + 1);
     if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 2] = globaltimer();
-    grid_barrier(w.bar, (unsigned)nb * (++phase));
+    exchange_barrier();
     if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 3] = globaltimer();
   }
   // ---- the columns go back: rows 0..k-1 hold R (R12 for the solve), the rest the residual ----
@@ -671,6 +707,7 @@ __global__ void __launch_bounds__(kQrcpThreads, 1)
     out.info[0] = 0;
     out.info[1] = k;
   }
+  // CLUSTER: the last step's candidates are not read; no peer touches this CTA's memory now
 }
 
 // =============================================================================================
@@ -1308,6 +1345,55 @@ static cudaError_t launch_qrcp_smem(double2* Y, int64_t ldy, int l, int64_t n, i
   return cudaErrorNotSupported;
 }
 
+// The shared-memory-resident exact kernel as ONE cluster of cs CTAs (distributed shared memory
+// exchange, cluster barrier; small sketches: C1): cudaErrorNotSupported when the columns do not
+// fit (the caller falls back to the grid-wide kernel).
+template <int MAXQ>
+static cudaError_t launch_qrcp_cluster(double2* Y, int64_t ldy, int l, int64_t n, int k,
+                                       double tol_rel, const QrcpOut& out, const QrcpWork& w,
+                                       cudaStream_t st, int* launches) {
+  auto kern = k_qrcp_smem<MAXQ, true>;
+  cudaError_t e;
+  int optin = 0;
+  size_t fstatic = 0;
+  if ((e = optin_smem(&optin)) != cudaSuccess) return e;
+  if ((e = static_smem((const void*)kern, &fstatic)) != cudaSuccess) return e;
+  if ((e = ensure_func_attr((const void*)kern, cudaFuncAttributeNonPortableClusterSizeAllowed,
+                            1)) != cudaSuccess)
+    return e;
+  for (int cs : {16, 8}) {
+    int per = (int)((n + cs - 1) / cs);
+    if (per < 1) per = 1;
+    const int blocks = (int)((n + per - 1) / per);
+    const size_t smem = (size_t)MAXQ * 32 * sizeof(double2) + (size_t)((per + 1) & ~1) * 8 +
+                        (size_t)per * l * sizeof(double2) + (size_t)2 * l * sizeof(double2) +
+                        6 * sizeof(double);
+    if (smem > (size_t)optin - fstatic - 1024) continue;
+    if ((e = ensure_dyn_smem((const void*)kern, smem)) != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)blocks);
+    cfg.blockDim = dim3(kQrcpThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)blocks;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int clusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&clusters, (const void*)kern, &cfg) != cudaSuccess ||
+        clusters < 1) {
+      cudaGetLastError();
+      continue;
+    }
+    *launches += 1;
+    return cudaLaunchKernelEx(&cfg, kern, Y, ldy, l, n, k, tol_rel, out, w, per);
+  }
+  return cudaErrorNotSupported;
+}
+
 // Panels of nb steps (k_qrcp_ring), each followed by the tensor-core trailing update
 // Y[jend:l, :] -= V[jend:l, 0:nb] · F[0:nb, :] (k_zgemm.cu mode 2) of every rank's block.
 // The grid is G rank groups of cpr CTAs (G = 1: the whole-sketch QR).
@@ -1458,6 +1544,9 @@ cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, doubl
   // Blocked panels pay off once the sketch no longer fits in L2 (C4: 34.2 -> 21.1 ms, C5: 9.2 ->
   // 6.6 ms); small sketches (C2/C3, ~10 MB) are latency-bound and the single persistent kernel
   // is faster there (C2: 0.68 vs 1.04 ms). Measured on B200, tools/trace_qrcp.py.
+  // variant 0 (small sketches): the one-cluster kernel when the sketch fits in 16 (8) CTAs'
+  // shared memory (C1), else the grid-wide shared-memory kernel, else the global-memory one;
+  // 3 forces the cluster kernel, 4 the grid-wide shared-memory kernel (tests)
   if (variant < 0) {
     variant = (16.0 * (double)l * (double)n >= 64.0 * (1 << 20)) ? 1 : 0;
     if (const char* v = select_env("RID_QRCP_VARIANT")) variant = atoi(v);
@@ -1470,7 +1559,12 @@ cudaError_t qrcp(double2* Y, int64_t ldy, int64_t l, int64_t n, int64_t k, doubl
     if (variant == 1)                                                                          \
       return launch_qrcp_blocked<QV>(one_shard(Y, n, out, w), ldy, li, ki, tol_rel, num_sms,   \
                                      st, launches, nbw);                                       \
-    if (variant == 0) {                                                                        \
+    if (variant == 0 || variant == 3) {                                                        \
+      const cudaError_t ec =                                                                   \
+          launch_qrcp_cluster<QV>(Y, ldy, li, n, ki, tol_rel, out, w, st, launches);           \
+      if (ec != cudaErrorNotSupported || variant == 3) return ec;                              \
+    }                                                                                          \
+    if (variant == 0 || variant == 4) {                                                        \
       const cudaError_t es =                                                                   \
           launch_qrcp_smem<QV>(Y, ldy, li, n, ki, tol_rel, out, w, num_sms, st, launches);     \
       if (es != cudaErrorNotSupported) return es;                                              \

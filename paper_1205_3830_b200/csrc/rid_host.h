@@ -43,6 +43,23 @@ inline cudaError_t ensure_dyn_smem(const void* func, size_t bytes) {
   return e;
 }
 
+// Set a function attribute once per (function, device, attribute) — e.g. the non-portable
+// cluster size of the one-cluster QR — thread-safe like ensure_dyn_smem.
+inline cudaError_t ensure_func_attr(const void* func, cudaFuncAttribute attr, int value) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  static std::mutex mu;
+  static std::map<std::pair<std::pair<const void*, int>, int>, int> set;
+  std::lock_guard<std::mutex> g(mu);
+  auto key = std::make_pair(std::make_pair(func, dev), (int)attr);
+  auto it = set.find(key);
+  if (it != set.end() && it->second == value) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, attr, value);
+  if (e == cudaSuccess) set[key] = value;
+  return e;
+}
+
 // Per-device cached queries: the launchers of the small configs run on the critical path of a
 // ~0.2 ms call, where each host API query costs microseconds. Keyed by device (and function /
 // launch shape), thread-safe.

@@ -62,7 +62,7 @@ def oracle_dec(orc):
     return get
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "2"])
+@pytest.mark.parametrize("variant", ["0", "1", "2", "4"])
 @pytest.mark.parametrize("name,seed,m,n,k,l,noise", CASES)
 def test_variant_parity(rid, oracle_dec, monkeypatch, variant, name, seed, m, n, k, l, noise):
     monkeypatch.setenv("RID_QRCP_VARIANT", variant)
@@ -139,3 +139,42 @@ def test_large_l_blocked_only(rid, oracle_dec, name, seed, m, n, k, l, noise):
     assert J.tolist() == d.J.tolist()
     assert np.array_equal(P[:, J], np.eye(k, dtype=complex))
     assert relf(P, d.P) <= 1e-10
+
+
+CLUSTER_CASES = [  # sketches that fit one cluster's shared memory (16 CTAs)
+    ("C1", 1, 1024, 512, 16, 24, 0.0),
+    ("C2s", 1, 2048, 2048, 64, 80, 1e-10),
+    ("C3s", 1, 8192, 1024, 128, 144, 1e-12),
+    ("k=l", 1, 500, 300, 24, 24, 1e-9),
+    ("k=n", 2, 300, 40, 40, 48, 0.0),
+    ("k=1", 4, 256, 100, 1, 9, 1e-6),
+    ("one column", 5, 128, 1, 1, 4, 0.0),
+    ("ragged", 6, 1001, 777, 13, 29, 1e-8),
+]
+
+
+@pytest.mark.parametrize("name,seed,m,n,k,l,noise", CLUSTER_CASES)
+def test_cluster_qr_bitwise_vs_grid_kernel(rid, oracle_dec, monkeypatch, name, seed, m, n, k, l,
+                                           noise):
+    """The one-cluster QR (variant 3: distributed-shared-memory exchange, cluster barrier) gives
+    the same J and P bits as the grid-wide shared-memory kernel (variant 4), and the oracle's J."""
+    A = rid.generate(seed, m, n, k, noise)
+    monkeypatch.setenv("RID_QRCP_VARIANT", "4")
+    r4 = rid.decompose(A, k, l, seed)
+    monkeypatch.setenv("RID_QRCP_VARIANT", "3")
+    r3 = rid.decompose(A, k, l, seed)
+    assert np.array_equal(np_(r3.J), np_(r4.J))
+    assert np.array_equal(np.ascontiguousarray(np_(r3.P)).view(np.uint64),
+                          np.ascontiguousarray(np_(r4.P)).view(np.uint64))
+    A_o, d = oracle_dec(seed, m, n, k, l, noise)
+    if k == 1 or d.tie_margins[:-1].min() >= 1e-10:
+        assert np_(r3.J).tolist() == d.J.tolist()
+    assert relf(np_(r3.P), d.P) <= 1e-10
+
+
+def test_cluster_qr_rank_failure(rid, monkeypatch):
+    monkeypatch.setenv("RID_QRCP_VARIANT", "3")
+    A = rid.generate(1, 400, 200, 3, 0.0)  # exact rank 3
+    with pytest.raises(rid.RidError) as e:
+        rid.decompose(A, 6, 10, 1)
+    assert e.value.status == rid.RID_ERANK
