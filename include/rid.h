@@ -190,11 +190,11 @@ rid_status rid_set_qr_dist(rid_ctx* ctx, int mode);
 int rid_sketch_splits(const rid_ctx* ctx, int64_t m, int64_t l, int64_t n);
 /* 1 when the Gaussian sketch of an m x n matrix with l rows runs one level of Strassen's
  * algorithm over Gauss's three products (R32: 7/8 of the tensor work, 5.25 l m n flop;
- * Y agrees with the oracle to ~1e-14 relative), 0 otherwise. A function of (m, l, n) only: the
- * unsplit plan (rid_sketch_splits == 1), l % 4 == 0, l >= 96, m % 32 == 0, m >= 1024, n % 64 == 0,
- * and RID_SKETCH_STRASSEN != 0 in the environment. When it is 1, every column block passed to
- * rid_sketch_cols / rid_decompose must start and end on a multiple of 64 (RID_EINVAL otherwise):
- * the algorithm pairs the two 32-column halves of each aligned 64-column group. */
+ * Y agrees with the oracle to ~1e-14 relative), 0 otherwise. A function of (m, l, n) only:
+ * l % 4 == 0, l >= 64, m % 32 == 0, m >= 1024, n % 512 == 0 (C2-C5), and RID_SKETCH_STRASSEN != 0
+ * in the environment. When it is 1, every column block passed to rid_sketch_cols / rid_decompose
+ * must start and end on a multiple of 64 (RID_EINVAL otherwise; every G <= 8 dividing n gives such
+ * shards): the algorithm pairs the two 32-column halves of each aligned 64-column group. */
 int rid_sketch_strassen(const rid_ctx* ctx, int64_t m, int64_t l, int64_t n);
 /* Real multiplications per complex multiply-add in the sketch kernel: 3 (Gauss, 6 l m n flops,
  * default) or 4 (real embedding, 8 l m n flops, bit-exact ordered chain; RID_SKETCH_4M=1). */

@@ -77,16 +77,27 @@ __global__ void k_strassen_rcomb(const double2* __restrict__ R, int64_t ldr, int
   }
 }
 
-// Y (l x ncols block, ld ldy) from M (7 products of lh x nh, ld lh, product stride lh nh)
-__global__ void k_strassen_combine(const double2* __restrict__ M, int lh, int64_t nh,
+// Y (l x ncols block, ld ldy) from M (S K slices of 7 products of lh x nh, ld lh, product stride
+// lh nh, slice stride 7 lh nh): each product's slices added in slice order, then combined
+__global__ void k_strassen_combine(const double2* __restrict__ M, int lh, int64_t nh, int S,
                                    double2* __restrict__ Y, int64_t ldy) {
-  const int64_t total = (int64_t)lh * nh, zs = total;
+  const int64_t total = (int64_t)lh * nh, zs = total, ss = 7 * total;
   for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < total;
        q += (int64_t)gridDim.x * blockDim.x) {
     const int64_t c = q / lh;
     const int r = (int)(q - c * lh);
-    const double2 m1 = M[q], m2 = M[zs + q], m3 = M[2 * zs + q], m4 = M[3 * zs + q];
-    const double2 m5 = M[4 * zs + q], m6 = M[5 * zs + q], m7 = M[6 * zs + q];
+    double2 mz[7];
+#pragma unroll
+    for (int z = 0; z < 7; ++z) {
+      double2 a = M[z * zs + q];
+      for (int s = 1; s < S; ++s) {
+        const double2 b = M[s * ss + z * zs + q];
+        a = make_double2(__dadd_rn(a.x, b.x), __dadd_rn(a.y, b.y));
+      }
+      mz[z] = a;
+    }
+    const double2 m1 = mz[0], m2 = mz[1], m3 = mz[2], m4 = mz[3];
+    const double2 m5 = mz[4], m6 = mz[5], m7 = mz[6];
     double2 y11, y12, y21, y22;
     y11.x = __dadd_rn(__dsub_rn(__dadd_rn(m1.x, m4.x), m5.x), m7.x);
     y11.y = __dadd_rn(__dsub_rn(__dadd_rn(m1.y, m4.y), m5.y), m7.y);
@@ -142,7 +153,7 @@ template <int FJ, int FR, int WJ, int WR, int STAGES, int MINB, bool TWO, int BK
 __global__ void __launch_bounds__(WJ* WR * 32, MINB)
     k_strassen3m(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapR,
                  const __grid_constant__ CUtensorMap mapS, double2* __restrict__ M, int lh,
-                 int64_t nh, int mh, int rbeg, int rend, int raster) {
+                 int64_t nh, int mh, int rbeg, int rend, int raster, int kslice) {
   using Cf = SCfg<FJ, FR, WJ, WR, STAGES, BK>;
   extern __shared__ __align__(1024) unsigned char smraw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES];
@@ -169,7 +180,11 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
   // an integer XOR off the FP64 pipe, then one DADD (the exact sum / difference, one rounding)
   const unsigned sgmask = c_strassen_a[tile_z()][4] < 0 ? 0x80000000u : 0u;
   constexpr bool two = TWO;
-  const int nk = mh / Cf::BKC;
+  // K slice blockIdx.z (raster 1; the launcher forces it when there are slices): complex K
+  // [kbeg, kbeg + kslice) of the product's m/2, its partial product to slice z of M
+  const int kbeg = raster ? (int)blockIdx.z * kslice : 0;
+  const int kend = raster ? min(mh, kbeg + kslice) : mh;
+  const int nk = (kend - kbeg) / Cf::BKC;
 
   if (tid == 0) {
     tma_prefetch_map(&mapA);
@@ -193,7 +208,7 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
     const int s = kt % STAGES;
     unsigned char* st = sm + (size_t)s * Cf::kStage;
     mbar_expect_tx(&full[s], two ? Cf::kStage : Cf::kStage - Cf::kAterm);
-    const int kc0 = kt * Cf::BKC;
+    const int kc0 = kbeg + kt * Cf::BKC;
 #pragma unroll
     for (int b = 0; b < Cf::kNA; ++b) {
       tma_box4_g2s(st + b * Cf::kABox, &mapA, 2 * (kh1 * mh + kc0) + 16 * b, 0, h1, grp,
@@ -282,7 +297,7 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
   }
 
   // epilogue: lane (g, t) holds half-column π(g) and rows t, t + 4 of each 8 x 8 fragment
-  M += (int64_t)tile_z() * lh * nh;
+  M += (int64_t)tile_z() * lh * nh + (raster ? (int64_t)blockIdx.z * 7 * lh * nh : 0);
   const int r0 = tile_r0();
   const int64_t j0 = (int64_t)blockIdx.y * Cf::BJ;  // first half-column
 #pragma unroll
@@ -308,13 +323,41 @@ bool strassen_enabled() {
   return !(v && atoi(v) == 0);
 }
 
-// The plan is a function of (l, m, n) only (G-invariance): the unsplit 3M plan (no K slices:
-// C4, C5), l % 4 == 0 (even row halves), m % 32 == 0 (whole stages per K half), n % 64 == 0.
+// The plan is a function of (l, m, n) only (G-invariance): l % 4 == 0 (even row halves), l >= 64,
+// m % 32 == 0 (whole stages per K half), m >= 1024, n % 512 == 0 — C2 to C5; K slices
+// (strassen_ksplit) where the 3M plan would split K too (C2, C3).
+// The tile height of a product's rows: 48 (the remainder on its own height), or the smallest of
+// 24 / 32 / 40 that holds l/2 < 48 rows (C2: 40)
+static int strassen_main_rows(int64_t lh) {
+  if (lh >= 48) return 48;
+  return lh <= 24 ? 24 : lh <= 32 ? 32 : 40;
+}
+
 bool strassen_plan(int64_t l, int64_t m, int64_t n, int num_sms) {
+  (void)num_sms;
   if (!strassen_enabled() || sketch_mults() != 3 || !zgemm3m_tma_enabled(l)) return false;
-  if (l % 4 != 0 || l < 96 || m % 32 != 0 || m < 1024 || n % 64 != 0 || n < 128) return false;
+  // n % 512: every G <= 8 that divides n gives 64-aligned shards (the column pairing's groups)
+  if (l % 4 != 0 || l < 64 || m % 32 != 0 || m < 1024 || n % 512 != 0) return false;
   if (l / 2 > 0x3FFFFFFF / 7) return false;
-  return zgemm3m_ksplit(l, m, n / 8, num_sms) == 1;
+  if (const char* v = experiment_env("RID_STR_UNSPLIT_ONLY"))  // round-2 first plan: C4, C5
+    if (atoi(v) != 0 && zgemm3m_ksplit(l, m, n / 8, num_sms) != 1) return false;
+  return true;
+}
+
+// K slices of the Strassen products: enough CTAs for two per SM at the n/8-column shard of an
+// 8-GPU run (a function of (l, m, n) only, so every column's bits are independent of the
+// sharding), slices of at least 256 complex K, at most 16. C4, C5: 1; C3: 6; C2: 5.
+int strassen_ksplit(int64_t l, int64_t m, int64_t n, int num_sms) {
+  const int64_t lh = l / 2, mh = m / 2;
+  const int64_t h = strassen_main_rows(lh);
+  const int64_t rt = (lh + h - 1) / h;
+  const int64_t ct = (n / 16 + 63) / 64;  // half-column tiles of the n/8 shard
+  const int64_t ctas = 7 * rt * (ct > 0 ? ct : 1);
+  int64_t s = (2 * (int64_t)num_sms + ctas - 1) / ctas;
+  const int64_t smax = mh / 256 > 1 ? mh / 256 : 1;
+  if (s > smax) s = smax;
+  if (s > 16) s = 16;
+  return s < 1 ? 1 : (int)s;
 }
 
 StrassenWs strassen_ws(int64_t l, int64_t m, int64_t ncols) {
@@ -324,7 +367,7 @@ StrassenWs strassen_ws(int64_t l, int64_t m, int64_t ncols) {
   w.lds = rsum_ld(7 * lh);
   w.rc_bytes = sizeof(double2) * (size_t)w.ldc * mh;
   w.rs_bytes = sizeof(double) * (size_t)w.lds * mh;
-  w.m_bytes = sizeof(double2) * (size_t)7 * lh * (ncols / 2);
+  w.m_bytes = sizeof(double2) * (size_t)7 * lh * (ncols / 2);  // per K slice
   return w;
 }
 
@@ -341,7 +384,8 @@ cudaError_t strassen_rcomb(const double2* R, int64_t l, int64_t m, int64_t ldr, 
 template <int FJ, int FR, int WJ, int WR, int STAGES, int MINB, int BK = 16>
 static cudaError_t launch_products(const CUtensorMap& mapA, const double2* Rc, int64_t ldc,
                                    const double* Rs, int64_t lds, double2* M, int lh, int64_t nh,
-                                   int64_t mh, int rbeg, int rend, cudaStream_t st, int raster) {
+                                   int64_t mh, int rbeg, int rend, cudaStream_t st, int raster,
+                                   int S) {
   using Cf = SCfg<FJ, FR, WJ, WR, STAGES, BK>;
   auto kern2 = k_strassen3m<FJ, FR, WJ, WR, STAGES, MINB, true, BK>;
   auto kern1 = k_strassen3m<FJ, FR, WJ, WR, STAGES, MINB, false, BK>;
@@ -373,13 +417,18 @@ static cudaError_t launch_products(const CUtensorMap& mapA, const double2* Rc, i
   const int64_t tr = (rend - rbeg + Cf::BR - 1) / Cf::BR, tj = (nh + Cf::BJ - 1) / Cf::BJ;
   if (tr < 1 || tj > 65535) return cudaErrorInvalidConfiguration;
   if (const char* v = experiment_env("RID_STR_RASTER")) raster = atoi(v);
-  const dim3 g2 = raster ? dim3((unsigned)(tr * 5), (unsigned)tj, 1u) : dim3((unsigned)tr, (unsigned)tj, 5u);
-  const dim3 g1 = raster ? dim3((unsigned)(tr * 2), (unsigned)tj, 1u) : dim3((unsigned)tr, (unsigned)tj, 2u);
+  if (S > 1) raster = 1;  // blockIdx.z is the K slice
+  // complex K per slice: whole stages
+  const int kslice = (int)(((mh + S - 1) / S + Cf::BKC - 1) / Cf::BKC * Cf::BKC);
+  const dim3 g2 = raster ? dim3((unsigned)(tr * 5), (unsigned)tj, (unsigned)S)
+                         : dim3((unsigned)tr, (unsigned)tj, 5u);
+  const dim3 g1 = raster ? dim3((unsigned)(tr * 2), (unsigned)tj, (unsigned)S)
+                         : dim3((unsigned)tr, (unsigned)tj, 2u);
   kern2<<<g2, Cf::kThreads, Cf::kSmem, st>>>(mapA, mapR, mapS, M, lh, nh, (int)mh, rbeg, rend,
-                                             raster);
+                                             raster, kslice);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   kern1<<<g1, Cf::kThreads, Cf::kSmem, st>>>(mapA, mapR, mapS, M, lh, nh, (int)mh, rbeg, rend,
-                                             raster);
+                                             raster, kslice);
   return cudaGetLastError();
 }
 
@@ -390,13 +439,14 @@ static cudaError_t launch_products(const CUtensorMap& mapA, const double2* Rc, i
 // experiments build).
 static cudaError_t products_rows(int rows, int rem, const CUtensorMap& mapA, const double2* Rc,
                                  int64_t ldc, const double* Rs, int64_t lds, double2* M, int lh,
-                                 int64_t nh, int64_t mh, int rbeg, int rend, cudaStream_t st) {
+                                 int64_t nh, int64_t mh, int rbeg, int rend, cudaStream_t st,
+                                 int S) {
   (void)rem;
   int tile = 1;
   if (const char* v = experiment_env("RID_STR_TILE")) tile = atoi(v);
   const int raster = 1;
 #define RID_LP(...) \
-  launch_products<__VA_ARGS__>(mapA, Rc, ldc, Rs, lds, M, lh, nh, mh, rbeg, rend, st, raster)
+  launch_products<__VA_ARGS__>(mapA, Rc, ldc, Rs, lds, M, lh, nh, mh, rbeg, rend, st, raster, S)
   if (rows == 48 && tile == 1) return RID_LP(1, 6, 8, 1, 2, 2);
   switch (rows) {
     case 48: return RID_LP(2, 3, 4, 2, 2, 2);
@@ -410,10 +460,10 @@ static cudaError_t products_rows(int rows, int rem, const CUtensorMap& mapA, con
 
 cudaError_t strassen_sketch(const double2* Rc, int64_t ldc, const double* Rs, int64_t lds,
                             const double2* A, int64_t lda, double2* Y, int64_t ldy, int64_t l,
-                            int64_t ncols, int64_t m, double2* M, cudaStream_t st,
+                            int64_t ncols, int64_t m, double2* M, int S, cudaStream_t st,
                             const SketchAux* aux, int* launches) {
   if (ncols <= 0) return cudaSuccess;
-  if (l % 4 || m % 32 || ncols % 64) return cudaErrorInvalidValue;
+  if (l % 4 || m % 32 || ncols % 64 || S < 1) return cudaErrorInvalidValue;
   const int lh = (int)(l / 2);
   const int64_t mh = m / 2, nh = ncols / 2;
   cudaError_t e;
@@ -435,7 +485,9 @@ cudaError_t strassen_sketch(const double2* Rc, int64_t ldc, const double* Rs, in
       return cudaErrorInvalidValue;
   }
   // rows of every product: 48-row tiles, the remainder r = 24 / 32 / 40 on r-row tiles beside
-  // them on the aux stream (as sketch_gemm's row split); other remainders pad the last 48-row tile
+  // them on the aux stream (as sketch_gemm's row split); other remainders pad the last 48-row tile;
+  // fewer than 48 rows (C2: 40) on one tile of the smallest height that holds them
+  const int h = strassen_main_rows(lh);
   const int rem = lh % 48;
   // (padding the last 48-row tile instead, RID_STR_PAD=1: C4 99.8 vs 91.0 ms, C5 208.2 vs 201.6)
   bool split = aux && aux->stream && lh > 48 && (rem == 24 || rem == 32 || rem == 40);
@@ -445,13 +497,13 @@ cudaError_t strassen_sketch(const double2* Rc, int64_t ldc, const double* Rs, in
     if ((e = cudaEventRecord(aux->fork, st)) != cudaSuccess) return e;
     if ((e = cudaStreamWaitEvent(aux->stream, aux->fork, 0)) != cudaSuccess) return e;
   }
-  if ((e = products_rows(48, rem, mapA, Rc, ldc, Rs, lds, M, lh, nh, mh, 0, main_end, st)) !=
+  if ((e = products_rows(h, rem, mapA, Rc, ldc, Rs, lds, M, lh, nh, mh, 0, main_end, st, S)) !=
       cudaSuccess)
     return e;
   *launches += 2;
   if (split) {
     if ((e = products_rows(rem, rem, mapA, Rc, ldc, Rs, lds, M, lh, nh, mh, main_end, lh,
-                           aux->stream)) != cudaSuccess)
+                           aux->stream, S)) != cudaSuccess)
       return e;
     *launches += 2;
     if ((e = cudaEventRecord(aux->join, aux->stream)) != cudaSuccess) return e;
@@ -460,7 +512,7 @@ cudaError_t strassen_sketch(const double2* Rc, int64_t ldc, const double* Rs, in
   const int64_t total = (int64_t)lh * nh;
   int64_t blocks = (total + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_strassen_combine<<<(unsigned)blocks, 256, 0, st>>>(M, lh, nh, Y, ldy);
+  k_strassen_combine<<<(unsigned)blocks, 256, 0, st>>>(M, lh, nh, S, Y, ldy);
   *launches += 1;
   return cudaGetLastError();
 }

@@ -509,9 +509,10 @@ rid_status sketch_block(rid_ctx* c, const SketchR& sr, const double2* A, int64_t
                   "selects the plain 3M sketch", (long long)l, (long long)m, (long long)n,
                   (long long)col0, (long long)ncols);
     void* pm;
-    RID_TRY(ws_get(c, "Mstr", rid::strassen_ws(l, m, ncols).m_bytes, &pm));
+    const int Sk = rid::strassen_ksplit(l, m, n, c->num_sms);
+    RID_TRY(ws_get(c, "Mstr", (size_t)Sk * rid::strassen_ws(l, m, ncols).m_bytes, &pm));
     RID_CUDA(c, rid::strassen_sketch(sr.Rc, sr.sw.ldc, sr.Rsc, sr.sw.lds, A, lda, Y, ldy, l, ncols,
-                                     m, (double2*)pm, c->stream, aux, launches));
+                                     m, (double2*)pm, Sk, c->stream, aux, launches));
     return RID_OK;
   }
   RID_CUDA(c, rid::sketch_gemm(sr.R, l, sr.Rs, A, lda, Y, ldy, l, ncols, m, c->stream, S, partial,

@@ -94,6 +94,7 @@ cudaError_t sketch_gemm(const double2* R, int64_t ldr, const double* Rs, const d
 // from (l, m, n) only; then every column block passed must start and end on multiples of 64.
 bool strassen_enabled();
 bool strassen_plan(int64_t l, int64_t m, int64_t n, int num_sms);
+int strassen_ksplit(int64_t l, int64_t m, int64_t n, int num_sms);  // K slices, from (l, m, n)
 struct StrassenWs {
   int64_t ldc, lds;                 // leading dimensions of Rc (complex) and Rs (double)
   size_t rc_bytes, rs_bytes, m_bytes;
@@ -102,10 +103,11 @@ StrassenWs strassen_ws(int64_t l, int64_t m, int64_t ncols);
 // Rc / Rs: the seven R combinations (7 l/2 rows x m/2) and their Re + Im planes, from R (l x m)
 cudaError_t strassen_rcomb(const double2* R, int64_t l, int64_t m, int64_t ldr, double2* Rc,
                            int64_t ldc, double* Rs, int64_t lds, cudaStream_t st);
-// Y (l x ncols, ncols % 64 == 0) = R A for a 64-aligned column block; M: m_bytes of workspace
+// Y (l x ncols, ncols % 64 == 0) = R A for a 64-aligned column block; M: S * m_bytes of workspace
+// (S = strassen_ksplit of the whole matrix's (l, m, n))
 cudaError_t strassen_sketch(const double2* Rc, int64_t ldc, const double* Rs, int64_t lds,
                             const double2* A, int64_t lda, double2* Y, int64_t ldy, int64_t l,
-                            int64_t ncols, int64_t m, double2* M, cudaStream_t st,
+                            int64_t ncols, int64_t m, double2* M, int S, cudaStream_t st,
                             const SketchAux* aux, int* launches);
 // K slices for a sketch of Mout rows, K = m, chosen from n_ref = n_global / 8 only (G-invariant)
 int zgemm_ksplit(int64_t Mout, int64_t K, int64_t n_ref, int num_sms);

@@ -49,6 +49,7 @@ SHAPES = [  # (seed, m, n, k, l, noise)
 
 @pytest.mark.parametrize("seed,m,n,k,l,noise", SHAPES)
 def test_tma_sketch_bitwise_vs_cpasync_and_oracle(rid, orc, monkeypatch, seed, m, n, k, l, noise):
+    monkeypatch.setenv("RID_SKETCH_STRASSEN", "0")  # the plain 3M kernels on both sides
     A = rid.generate(seed, m, n, k, noise)
     monkeypatch.setenv("RID_Z3_TMA", "0")
     Y_old = rid.sketch(A, seed, l).cpu().numpy()
@@ -76,7 +77,8 @@ def test_tma_wave_tail_and_shards_bitwise(rid, monkeypatch):
     """Column blocks of a matrix sketched as shards (different tensor maps, base pointers and the
     wave-tail split set) equal the whole-matrix sketch bit for bit, and equal the old kernel."""
     seed, m, n, k, l = 8, 2048, 4096, 64, 96
-    A = rid.generate(seed, m, n, k, 1e-10)
+    monkeypatch.setenv("RID_SKETCH_STRASSEN", "0")  # the plain 3M kernels (this shape's default
+    A = rid.generate(seed, m, n, k, 1e-10)            # plan is Strassen's, tests/test_gpu_strassen)
     Y = rid.sketch(A, seed, l).cpu().numpy()
     for G in (2, 8):
         w = n // G
@@ -145,6 +147,7 @@ def test_row_split_sketch_bitwise(rid, monkeypatch, seed, m, n, l):
     """l = 48 a + r with r in {24, 32, 40} runs as 48-row tiles plus r-row tiles (sketch_gemm's
     row split); every element is the same chain: Y equals the single-height plan bit for bit,
     with and without split-K, and the decomposition is unchanged."""
+    monkeypatch.setenv("RID_SKETCH_STRASSEN", "0")  # the 3M row split (not Strassen's plan)
     A = rid.generate(seed, m, n, 16, 1e-9)
     Y_s = rid.sketch(A, seed, l).cpu().numpy()
     monkeypatch.setenv("RID_SKETCH_NOROWSPLIT", "1")

@@ -37,9 +37,10 @@ def bits(a):
 def test_plan(rid):
     assert rid.sketch_strassen(M, L, N)
     assert rid.sketch_strassen(32768, 528, 32768) and rid.sketch_strassen(131072, 272, 32768)
-    assert not rid.sketch_strassen(8192, 80, 8192)  # C2: K-split plan
-    assert not rid.sketch_strassen(65536, 144, 4096)  # C3: K-split plan
-    assert not rid.sketch_strassen(M, L, N - 32)  # n not a multiple of 64
+    assert rid.sketch_strassen(8192, 80, 8192) and rid.sketch_strassen(65536, 144, 4096)  # C2, C3
+    assert not rid.sketch_strassen(1024, 24, 512)  # C1: l < 64
+    assert not rid.sketch_strassen(M, L, N - 64)  # n not a multiple of 512
+    assert not rid.sketch_strassen(M, 90, N)  # l not a multiple of 4
 
 
 def test_sketch_vs_oracle_and_3m(rid, orc, monkeypatch):
