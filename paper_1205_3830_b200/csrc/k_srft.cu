@@ -16,8 +16,12 @@
 // u = ((s_k i1) mod m) / m. Agreement with the oracle's direct ascending sum is to rounding.
 #include <cstdlib>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "rid_device.cuh"
 #include "rid_internal.h"
+#include "rid_tma.cuh"
 
 namespace rid {
 
@@ -152,6 +156,256 @@ __global__ void __launch_bounds__(128) k_srft_pass1(const double2* __restrict__ 
     }
 }
 
+// =============================================================================================
+// Single-pass SRFT (default for m >= 2048; SURVEY.md §8(f) NEXT-1's "one HBM pass" model).
+// With m = m1 * 256 and i = i1 + m1 * i2:
+//     Y(k, c) = sum_{i1 < m1} W_m^{(s_k i1) mod m} * Z_c(i1, s_k mod 256),
+//     Z_c(i1, r) = sum_{i2 < 256} W_256^{r i2} * d(i1 + m1 i2) * A(i1 + m1 i2, c).
+// One CTA per SM walks column PAIRS; for each pair it streams A in chunks of 8 consecutive i1 x
+// all 256 i2 (one 3D TMA box of 32 KB per column, rows 8 KB apart) plus the matching box of the
+// phases d, computes the 16 = 2 x 8 DFTs of 256 points in shared memory (radix 16 x 16: pass A
+// over i2 = p + 16 q with the W_256^{p r1} twiddle, pass B over p), and accumulates every sampled
+// row Y(k, c) += W_m^{s_k i1} Z_c(i1, s_k mod 256) over the chunk's 8 i1 in registers (W_m^{s_k
+// i1} = W_m^{(8 q s_k) mod m} from the spec'd sincos, times W_m^{s_k} repeatedly). A is read once
+// from HBM; Z never leaves shared memory. Agreement with the oracle's direct ascending sum is to
+// rounding (the FFT's log m rounding steps).
+// =============================================================================================
+constexpr int kSfR = 256;            // first-level DFT length
+constexpr int kSfC = 8;              // i1 per chunk
+constexpr int kSfStages = 2;
+constexpr int kSfBox = kSfR * kSfC * 16;       // bytes: one column's (or d's) chunk, 32 KB
+constexpr int kSfStage = 3 * kSfBox;           // A of two columns + d
+constexpr size_t kSfSmem = (size_t)kSfStages * kSfStage + kSfR * 16 + 1024;
+
+// 16-point DFT in registers (4 x 4; the pass-1 kernel's scheme): x[p] in, x[4 r1 + r2] = X(r1 + 4 r2)
+__device__ __forceinline__ void dft16(double2 (&x)[16]) {
+  const double c1 = 0.92387953251128674, s1 = 0.38268343236508978, h = 0.70710678118654757;
+  const double2 W[10] = {make_double2(1, 0),   make_double2(c1, -s1), make_double2(h, -h),
+                         make_double2(s1, -c1), make_double2(0, -1),  make_double2(-s1, -c1),
+                         make_double2(-h, -h),  make_double2(-c1, -s1), make_double2(-1, 0),
+                         make_double2(-c1, s1)};
+#pragma unroll
+  for (int p = 0; p < 4; ++p) dft4(x[p], x[p + 4], x[p + 8], x[p + 12]);
+#pragma unroll
+  for (int p = 1; p < 4; ++p)
+#pragma unroll
+    for (int r1 = 1; r1 < 4; ++r1) x[p + 4 * r1] = cmul(x[p + 4 * r1], W[p * r1]);
+#pragma unroll
+  for (int r1 = 0; r1 < 4; ++r1) dft4(x[4 * r1], x[4 * r1 + 1], x[4 * r1 + 2], x[4 * r1 + 3]);
+}
+
+__device__ __forceinline__ void tma_box3_g2s(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                             uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(b))
+      : "memory");
+}
+
+// KPT: sampled rows per thread (l <= 256 KPT). Pairs (2c, 2c + 1) of the n_loc columns (an odd
+// last column is paired with itself and written once).
+template <int KPT>
+__global__ void __launch_bounds__(256, 1)
+    k_srft_fused(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapD,
+                 int64_t m, int64_t m1, int64_t n_loc, int64_t l,
+                 const int64_t* __restrict__ samples, double2* __restrict__ Y, int64_t ldy) {
+  extern __shared__ __align__(1024) unsigned char sfraw[];
+  __shared__ __align__(8) uint64_t full[kSfStages];
+  unsigned char* sm = sfraw + ((1024 - (smem_u32(sfraw) & 1023)) & 1023);
+  double2* tw256 = reinterpret_cast<double2*>(sm + (size_t)kSfStages * kSfStage);  // W_256^e
+  const int tid = threadIdx.x;
+  const int64_t npairs = (n_loc + 1) / 2;
+  const int nq = (int)(m1 / kSfC);  // chunks per column pair
+  // this CTA's items: (pair, chunk) for its pairs b, b + G, ...
+  const int64_t mypairs = (npairs > blockIdx.x) ? (npairs - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  const int64_t nitems = mypairs * nq;
+
+  for (int e = tid; e < kSfR; e += blockDim.x) {  // W_256^e = (cos, -sin)(2 pi e / 256)
+    const double2 cs = rid_cossin2pi(__ddiv_rn((double)e, 256.0));
+    tw256[e] = make_double2(cs.x, -cs.y);
+  }
+  if (tid == 0) {
+    tma_prefetch_map(&mapA);
+    tma_prefetch_map(&mapD);
+    for (int s = 0; s < kSfStages; ++s) mbar_init(&full[s], 1);
+    mbar_init_fence();
+  }
+  __syncthreads();
+
+  auto issue = [&](int64_t it) {  // thread 0
+    const int s = (int)(it % kSfStages);
+    const int64_t pr = blockIdx.x + (it / nq) * (int64_t)gridDim.x;
+    const int q = (int)(it % nq);
+    const int64_t c0 = 2 * pr, c1 = (2 * pr + 1 < n_loc) ? 2 * pr + 1 : 2 * pr;
+    unsigned char* st = sm + (size_t)s * kSfStage;
+    mbar_expect_tx(&full[s], kSfStage);
+    tma_box3_g2s(st, &mapA, 2 * kSfC * q, 0, (int)c0, &full[s]);
+    tma_box3_g2s(st + kSfBox, &mapA, 2 * kSfC * q, 0, (int)c1, &full[s]);
+    tma_box3_g2s(st + 2 * kSfBox, &mapD, 2 * kSfC * q, 0, 0, &full[s]);
+  };
+  if (tid == 0)
+    for (int64_t it = 0; it < kSfStages && it < nitems; ++it) issue(it);
+
+  // owned samples k = tid + 256 j: s_k, W_m^{s_k}, and W_m^{s_k rot}: a lane reads the chunk's 8
+  // i1 of Z starting at c = rot = tid & 7 (the 8 lanes of a shared-memory wavefront then hit 8
+  // different bank groups), so its twiddle starts at W_m^{s_k (8 q + rot)}
+  const int rot = tid & 7;
+  int64_t sk[KPT];
+  double2 step[KPT], steprot[KPT];
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) {
+    const int64_t k = tid + 256 * j;
+    sk[j] = k < l ? samples[k] : 0;
+    const double2 cs = rid_cossin2pi(__ddiv_rn((double)sk[j], (double)m));
+    step[j] = make_double2(cs.x, -cs.y);
+    const uint64_t tr = ((uint64_t)sk[j] * (uint64_t)rot) & (uint64_t)(m - 1);
+    const double2 cr = rid_cossin2pi(__ddiv_rn((double)tr, (double)m));
+    steprot[j] = make_double2(cr.x, -cr.y);
+  }
+  double2 acc[2][KPT];
+#pragma unroll
+  for (int j = 0; j < KPT; ++j) acc[0][j] = acc[1][j] = make_double2(0.0, 0.0);
+
+  // pass roles: thread -> (column cc, i1c, p) for pass A and (cc, i1c, r1) for pass B, i1c fastest:
+  // a row of the box holds the 8 i1 of one i2, so the 8 lanes of a wavefront hit 8 bank groups
+  const int cc = tid >> 7, i1c = tid & 7, pp = (tid >> 3) & 15;
+  for (int64_t it = 0; it < nitems; ++it) {
+    const int s = (int)(it % kSfStages);
+    const int q = (int)(it % nq);
+    mbar_wait(&full[s], (unsigned)((it / kSfStages) & 1));
+    double2* Zc = reinterpret_cast<double2*>(sm + (size_t)s * kSfStage + (size_t)cc * kSfBox);
+    const double2* Dd = reinterpret_cast<const double2*>(sm + (size_t)s * kSfStage + 2 * kSfBox);
+    // ---- pass A: x(pp + 16 q2) d(.) over q2, DFT-16, twiddle W_256^{pp r1}, in place ---------
+    {
+      double2 x[16];
+#pragma unroll
+      for (int q2 = 0; q2 < 16; ++q2) {
+        const int i2 = pp + 16 * q2;
+        x[q2] = cmul(Dd[i2 * kSfC + i1c], Zc[i2 * kSfC + i1c]);
+      }
+      dft16(x);  // x[4 a + b] = y(r1 = a + 4 b)
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int r1 = a + 4 * b;
+          Zc[(pp + 16 * r1) * kSfC + i1c] = cmul(x[4 * a + b], tw256[pp * r1]);
+        }
+    }
+    __syncthreads();
+    // ---- pass B: thread (cc, i1c, r1 = pp) reads y(p, r1) for p < 16, DFT-16 over p ----------
+    {
+      double2 x[16];
+#pragma unroll
+      for (int p = 0; p < 16; ++p) x[p] = Zc[(p + 16 * pp) * kSfC + i1c];
+      dft16(x);  // x[4 a + b] = X(r1 + 16 r2), r2 = a + 4 b
+      __syncthreads();  // every read of pass B before any write
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) Zc[(pp + 16 * (a + 4 * b)) * kSfC + i1c] = x[4 * a + b];
+    }
+    __syncthreads();
+    // ---- accumulate the chunk's 8 i1 into every owned sampled row, both columns -------------
+    const double2* Z0 = reinterpret_cast<const double2*>(sm + (size_t)s * kSfStage);
+    const double2* Z1 = reinterpret_cast<const double2*>(sm + (size_t)s * kSfStage + kSfBox);
+#pragma unroll
+    for (int j = 0; j < KPT; ++j) {
+      if (tid + 256 * j >= l) continue;
+      const int r = (int)(sk[j] & (kSfR - 1));
+      const uint64_t t0 = ((uint64_t)sk[j] * (uint64_t)(kSfC * q)) & (uint64_t)(m - 1);
+      const double2 cs = rid_cossin2pi(__ddiv_rn((double)t0, (double)m));
+      const double2 wbase = make_double2(cs.x, -cs.y);  // W_m^{s_k 8 q}
+      double2 w = cmul(wbase, steprot[j]);              // W_m^{s_k (8 q + rot)}
+#pragma unroll
+      for (int i = 0; i < kSfC; ++i) {
+        const int c = (i + rot) & (kSfC - 1);  // i1 = 8 q + c
+        if (c == 0 && i > 0) w = wbase;        // wrapped past c = 7
+        const double2 z0 = Z0[r * kSfC + c], z1 = Z1[r * kSfC + c];
+        acc[0][j].x = __fma_rn(w.x, z0.x, __fma_rn(-w.y, z0.y, acc[0][j].x));
+        acc[0][j].y = __fma_rn(w.x, z0.y, __fma_rn(w.y, z0.x, acc[0][j].y));
+        acc[1][j].x = __fma_rn(w.x, z1.x, __fma_rn(-w.y, z1.y, acc[1][j].x));
+        acc[1][j].y = __fma_rn(w.x, z1.y, __fma_rn(w.y, z1.x, acc[1][j].y));
+        w = cmul(w, step[j]);
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();  // stage s consumed by every thread
+    if (tid == 0 && it + kSfStages < nitems) issue(it + kSfStages);
+    if (q == nq - 1) {  // the pair is complete
+      const int64_t pr = blockIdx.x + (it / nq) * (int64_t)gridDim.x;
+#pragma unroll
+      for (int j = 0; j < KPT; ++j) {
+        const int64_t k = tid + 256 * j;
+        if (k < l) {
+          Y[(2 * pr) * ldy + k] = acc[0][j];
+          if (2 * pr + 1 < n_loc) Y[(2 * pr + 1) * ldy + k] = acc[1][j];
+        }
+        acc[0][j] = acc[1][j] = make_double2(0.0, 0.0);
+      }
+    }
+  }
+}
+
+bool srft_fused_enabled(int64_t m, int64_t l) {
+  const char* v = select_env("RID_SRFT_FUSED");  // 0: the two-pass SRFT (DFT-16 + DMMA products)
+  return !(v && atoi(v) == 0) && m >= (int64_t)kSfR * kSfC && l <= 2048;
+}
+
+static cudaError_t srft_fused(uint64_t seed, bool retry, int64_t l, const double2* A, int64_t m,
+                              int64_t n_loc, int64_t lda, double2* Y, int64_t ldy, void* work,
+                              int num_sms, cudaStream_t st, int* launches) {
+  const int64_t m1 = m / kSfR;
+  char* w = (char*)work;
+  double2* d = (double2*)w;
+  int64_t* samples = (int64_t*)(w + (((size_t)m * sizeof(double2) + 255) & ~(size_t)255));
+  const uint32_t sp = retry ? 22u : 6u, ss = retry ? 23u : 7u;
+  int64_t blocks = ((m > l ? m : l) + 255) / 256;
+  if (blocks > 4096) blocks = 4096;
+  k_srft_plan<<<(unsigned)blocks, 256, 0, st>>>(seed, sp, ss, m, l, d, samples);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  *launches += 1;
+  PFN_cuTensorMapEncodeTiled encode;
+  if ((e = tensor_map_encoder(&encode)) != cudaSuccess) return e;
+  // A as (2 m1 doubles: i1) x 256 (i2, m1 complex apart) x n_loc (columns); d the same, 1 column
+  CUtensorMap mapA, mapD;
+  const cuuint32_t box[3] = {(cuuint32_t)(2 * kSfC), (cuuint32_t)kSfR, 1u};
+  const cuuint32_t estr[3] = {1u, 1u, 1u};
+  {
+    const cuuint64_t gdim[3] = {(cuuint64_t)(2 * m1), (cuuint64_t)kSfR, (cuuint64_t)n_loc};
+    const cuuint64_t gstr[2] = {(cuuint64_t)m1 * sizeof(double2), (cuuint64_t)lda * sizeof(double2)};
+    if (encode(&mapA, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)A, gdim, gstr, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {
+    const cuuint64_t gdim[3] = {(cuuint64_t)(2 * m1), (cuuint64_t)kSfR, 1u};
+    const cuuint64_t gstr[2] = {(cuuint64_t)m1 * sizeof(double2), (cuuint64_t)m * sizeof(double2)};
+    if (encode(&mapD, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, (void*)d, gdim, gstr, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  const int64_t npairs = (n_loc + 1) / 2;
+  const unsigned grid = (unsigned)(npairs < num_sms ? npairs : num_sms);
+#define RID_SF(K)                                                                              \
+  {                                                                                            \
+    auto kern = k_srft_fused<K>;                                                               \
+    if ((e = ensure_dyn_smem((const void*)kern, kSfSmem)) != cudaSuccess) return e;           \
+    kern<<<grid, 256, kSfSmem, st>>>(mapA, mapD, m, m1, n_loc, l, samples, Y, ldy);           \
+    *launches += 1;                                                                            \
+    return cudaGetLastError();                                                                 \
+  }
+  if (l <= 256) RID_SF(1)
+  if (l <= 512) RID_SF(2)
+  if (l <= 1024) RID_SF(4)
+  RID_SF(8)
+#undef RID_SF
+}
+
 __global__ void k_srft_scatter(const double2* __restrict__ Yg, const int* __restrict__ order,
                                int64_t l, int64_t n_loc, double2* __restrict__ Y, int64_t ldy) {
   const int64_t total = l * n_loc;
@@ -183,6 +437,8 @@ cudaError_t srft_sketch(uint64_t seed, bool retry, int64_t l, const double2* A, 
                         double2* splitk, size_t splitk_elems, int num_sms, cudaStream_t st,
                         int* launches) {
   if (m < kSrftR || (m & (m - 1)) != 0) return cudaErrorInvalidValue;
+  if (srft_fused_enabled(m, l))
+    return srft_fused(seed, retry, l, A, m, n_loc, lda, Y, ldy, work, num_sms, st, launches);
   const int64_t m1 = m / kSrftR, ch = srft_chunk_cols(m, n_loc);
   if (ch > 65535) return cudaErrorInvalidConfiguration;
   char* w = (char*)work;
