@@ -172,10 +172,14 @@ __global__ void __launch_bounds__(128) k_srft_pass1(const double2* __restrict__ 
 // =============================================================================================
 constexpr int kSfR = 256;            // first-level DFT length
 constexpr int kSfC = 8;              // i1 per chunk
-constexpr int kSfStages = 2;
 constexpr int kSfBox = kSfR * kSfC * 16;       // bytes: one column's (or d's) chunk, 32 KB
 constexpr int kSfStage = 3 * kSfBox;           // A of two columns + d
-constexpr size_t kSfSmem = (size_t)kSfStages * kSfStage + kSfR * 16 + 1024;
+// NS stages per CTA, NB CTAs per SM: (2, 1) double-buffers one CTA; (1, 2) runs two
+// single-buffered CTAs per SM that hide each other's loads (twice the warps)
+template <int NS>
+constexpr size_t sf_smem() {
+  return (size_t)NS * kSfStage + kSfR * 16 + 1024;
+}
 
 // 16-point DFT in registers (4 x 4; the pass-1 kernel's scheme): x[p] in, x[4 r1 + r2] = X(r1 + 4 r2)
 __device__ __forceinline__ void dft16(double2 (&x)[16]) {
@@ -205,8 +209,8 @@ __device__ __forceinline__ void tma_box3_g2s(void* dst, const CUtensorMap* map, 
 
 // KPT: sampled rows per thread (l <= 256 KPT). Pairs (2c, 2c + 1) of the n_loc columns (an odd
 // last column is paired with itself and written once).
-template <int KPT>
-__global__ void __launch_bounds__(256, 1)
+template <int KPT, int kSfStages, int NB>
+__global__ void __launch_bounds__(256, NB)
     k_srft_fused(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapD,
                  int64_t m, int64_t m1, int64_t n_loc, int64_t l,
                  const int64_t* __restrict__ samples, double2* __restrict__ Y, int64_t ldy) {
@@ -251,6 +255,7 @@ __global__ void __launch_bounds__(256, 1)
   // i1 of Z starting at c = rot = tid & 7 (the 8 lanes of a shared-memory wavefront then hit 8
   // different bank groups), so its twiddle starts at W_m^{s_k (8 q + rot)}
   const int rot = tid & 7;
+  const double inv_m = __drcp_rn((double)m);  // m = 2^p: exact
   int64_t sk[KPT];
   double2 step[KPT], steprot[KPT];
 #pragma unroll
@@ -315,7 +320,7 @@ __global__ void __launch_bounds__(256, 1)
       if (tid + 256 * j >= l) continue;
       const int r = (int)(sk[j] & (kSfR - 1));
       const uint64_t t0 = ((uint64_t)sk[j] * (uint64_t)(kSfC * q)) & (uint64_t)(m - 1);
-      const double2 cs = rid_cossin2pi(__ddiv_rn((double)t0, (double)m));
+      const double2 cs = rid_cossin2pi(__dmul_rn((double)t0, inv_m));  // t0 / m, exact
       const double2 wbase = make_double2(cs.x, -cs.y);  // W_m^{s_k 8 q}
       double2 w = cmul(wbase, steprot[j]);              // W_m^{s_k (8 q + rot)}
 #pragma unroll
@@ -390,12 +395,23 @@ static cudaError_t srft_fused(uint64_t seed, bool retry, int64_t l, const double
       return cudaErrorInvalidValue;
   }
   const int64_t npairs = (n_loc + 1) / 2;
-  const unsigned grid = (unsigned)(npairs < num_sms ? npairs : num_sms);
+  // 1: two single-buffered CTAs per SM (128 registers: l <= 512 fits without spills); 0: one
+  // double-buffered CTA per SM
+  int cfg = l <= 512 ? 1 : 0;
+  if (const char* v = experiment_env("RID_SRFT_CFG")) cfg = atoi(v);
+  const int64_t slots = (int64_t)num_sms * (cfg ? 2 : 1);
+  const unsigned grid = (unsigned)(npairs < slots ? npairs : slots);
 #define RID_SF(K)                                                                              \
   {                                                                                            \
-    auto kern = k_srft_fused<K>;                                                               \
-    if ((e = ensure_dyn_smem((const void*)kern, kSfSmem)) != cudaSuccess) return e;           \
-    kern<<<grid, 256, kSfSmem, st>>>(mapA, mapD, m, m1, n_loc, l, samples, Y, ldy);           \
+    if (cfg) {                                                                                 \
+      auto kern = k_srft_fused<K, 1, 2>;                                                       \
+      if ((e = ensure_dyn_smem((const void*)kern, sf_smem<1>())) != cudaSuccess) return e;     \
+      kern<<<grid, 256, sf_smem<1>(), st>>>(mapA, mapD, m, m1, n_loc, l, samples, Y, ldy);     \
+    } else {                                                                                   \
+      auto kern = k_srft_fused<K, 2, 1>;                                                       \
+      if ((e = ensure_dyn_smem((const void*)kern, sf_smem<2>())) != cudaSuccess) return e;     \
+      kern<<<grid, 256, sf_smem<2>(), st>>>(mapA, mapD, m, m1, n_loc, l, samples, Y, ldy);     \
+    }                                                                                          \
     *launches += 1;                                                                            \
     return cudaGetLastError();                                                                 \
   }
