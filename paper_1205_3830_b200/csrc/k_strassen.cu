@@ -132,14 +132,14 @@ struct SCfg {
   static constexpr int BJ = WJ * FJ * 8;     // half-columns per CTA (64: two 32-column boxes)
   static constexpr int BR = WR * FR * 8;     // product rows per CTA
   static constexpr int BKC = BK;             // complex K per stage (8 or 16)
-  static constexpr int kABox = 128 * BJ;     // 8 complex K x BJ half-columns
+  static constexpr int kABox = 128 * BJ;     // 8 complex K x BJ half-columns (BJ / 64 TMA boxes)
   static constexpr int kRBox = 128 * BKC;    // 8 complex rows x BKC K
   static constexpr int kRsBox = 64 * BKC;    // 8 rows of Re + Im x BKC K
   static constexpr int kNA = BKC / 8, kNR = BR / 8;
   static constexpr int kAterm = kNA * kABox;
   static constexpr int kStage = 2 * kAterm + kNR * kRBox + kNR * kRsBox;
   static constexpr size_t kSmem = (size_t)STAGES * kStage + 1024;
-  static_assert(BJ == 64, "a tile is two 32-column halves of one column half");
+  static_assert(BJ % 64 == 0, "a tile is whole pairs of 32-column groups of one column half");
   static_assert(kABox % 1024 == 0 && kRBox % 1024 == 0 && kStage % 1024 == 0,
                 "boxes and stages keep 1 KB alignment (128-byte swizzle)");
 };
@@ -210,13 +210,15 @@ __global__ void __launch_bounds__(WJ* WR * 32, MINB)
     mbar_expect_tx(&full[s], two ? Cf::kStage : Cf::kStage - Cf::kAterm);
     const int kc0 = kbeg + kt * Cf::BKC;
 #pragma unroll
-    for (int b = 0; b < Cf::kNA; ++b) {
-      tma_box4_g2s(st + b * Cf::kABox, &mapA, 2 * (kh1 * mh + kc0) + 16 * b, 0, h1, grp,
-                   &full[s]);
-      if (two)
-        tma_box4_g2s(st + Cf::kAterm + b * Cf::kABox, &mapA, 2 * (kh2 * mh + kc0) + 16 * b, 0,
-                     h2, grp, &full[s]);
-    }
+    for (int b = 0; b < Cf::kNA; ++b)
+#pragma unroll
+      for (int i = 0; i < Cf::BJ / 64; ++i) {  // one 4D box = 64 half-columns (two groups)
+        tma_box4_g2s(st + b * Cf::kABox + i * 8192, &mapA, 2 * (kh1 * mh + kc0) + 16 * b, 0, h1,
+                     grp + 2 * i, &full[s]);
+        if (two)
+          tma_box4_g2s(st + Cf::kAterm + b * Cf::kABox + i * 8192, &mapA,
+                       2 * (kh2 * mh + kc0) + 16 * b, 0, h2, grp + 2 * i, &full[s]);
+      }
 #pragma unroll
     for (int b = 0; b < Cf::kNR; ++b)
       tma_box_g2s(st + 2 * Cf::kAterm + b * Cf::kRBox, &mapR, 2 * (rrow + 8 * b), kc0, &full[s]);
@@ -448,6 +450,7 @@ static cudaError_t products_rows(int rows, int rem, const CUtensorMap& mapA, con
 #define RID_LP(...) \
   launch_products<__VA_ARGS__>(mapA, Rc, ldc, Rs, lds, M, lh, nh, mh, rbeg, rend, st, raster, S)
   if (rows == 48 && tile == 1) return RID_LP(1, 6, 8, 1, 2, 2);
+  if (rows == 48 && tile == 5) return RID_LP(1, 6, 16, 1, 2, 1);      // 48 x 128, one CTA/SM
   switch (rows) {
     case 48: return RID_LP(2, 3, 4, 2, 2, 2);
     case 40: return RID_LP(1, 5, 8, 1, 2, 2);
