@@ -1,4 +1,4 @@
-for c in C1 C2 C3 C4 C5; do python bench.py --config $c --q 5 > gpurun_out/bench_all_$c.log 2>&1; tail -1 gpurun_out/bench_all_$c.log | python -c "
+for c in C1 C2 C3 C4 C5; do python bench.py --config $c --q 5 > gpurun_out/bench_all_$c.log 2>&1 || echo "bench $c failed"; tail -1 gpurun_out/bench_all_$c.log | python -c "
 import json,sys
 d=json.loads(sys.stdin.read())
 p=d['phases']

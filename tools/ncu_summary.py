@@ -1,11 +1,13 @@
 """Summarise ncu outputs (launch list CSV + --set full reports) into profiles/ text files.
 
     python tools/ncu_summary.py <round-tag> <cfg>
-reads gpurun_out/launches_<cfg>.csv, gpurun_out/prof_sketch_<cfg>.ncu-rep, prof_qrcp_<cfg>.ncu-rep
+reads gpurun_out/launches_<cfg>.csv, gpurun_out/prof_sketch*_<cfg>.ncu-rep (one per sketch
+launch), prof_qrcp_<cfg>.ncu-rep, prof_update_<cfg>.ncu-rep
 writes profiles/<tag>_<cfg>_launches.txt, profiles/<tag>_<cfg>_ncu_summary.txt and updates
 profiles/traffic.json (dram bytes per launch of the sketch, read by bench.py's roofline.traffic).
 """
 import csv
+import glob
 import io
 import json
 import os
@@ -26,7 +28,7 @@ KEYS = [
     "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
     "launch__occupancy_limit_registers", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "smsp__warp_issue_stalled_barrier_per_warp_active.pct",
-    "dram__bytes.sum.per_second",
+    "dram__bytes.sum.per_second", "sm__inst_executed_pipe_tensor_subpipe_dmma.sum",
 ]
 
 
@@ -72,8 +74,9 @@ def main(tag, cfg):
     traffic_path = os.path.join(PROF, "traffic.json")
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     seen = {}
-    for kind in ("sketch", "qrcp", "update"):
-        rep = os.path.join(OUT, f"prof_{kind}_{cfg}.ncu-rep")
+    reps = [("sketch", p) for p in sorted(glob.glob(os.path.join(OUT, f"prof_sketch*_{cfg}.ncu-rep")))]
+    reps += [(kind, os.path.join(OUT, f"prof_{kind}_{cfg}.ncu-rep")) for kind in ("qrcp", "update")]
+    for kind, rep in reps:
         if not os.path.exists(rep):
             continue
         for d in raw(rep):
@@ -82,6 +85,13 @@ def main(tag, cfg):
             for k in KEYS:
                 if k in d:
                     lines.append(f"  {k:80s} {d[k][0]:>16s} {d[k][1]}")
+            if "sm__inst_executed_pipe_tensor_subpipe_dmma.sum" in d:
+                try:  # executed tensor work: one DMMA.8x8x4 = 8 x 8 x 4 FMA = 512 flop
+                    cnt = float(d["sm__inst_executed_pipe_tensor_subpipe_dmma.sum"][0]
+                                .replace(",", ""))
+                    lines.append(f"  DMMA instructions x 512 flop = {cnt * 512:.4e} flop executed")
+                except ValueError:
+                    pass
             lines.append("  top stall reasons (% of samples): " +
                          ", ".join(f"{k} {v:.1f}" for k, v in stalls(d)))
             try:

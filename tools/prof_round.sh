@@ -1,12 +1,15 @@
 #!/bin/bash
-# Round evidence: GPU tests, default bench line, ncu launch list + full set of the sketch GEMM.
-CFG=${CFG:-C4}
+# Round evidence in one call on one B200: GPU tests, smoke, the default bench line (C4), every
+# config's bench line (tools/bench_all.sh), the reference arm, and the C4 ncu evidence
+# (tools/prof_c4.sh: launch list + full sets of the sketch, one QR panel, one panel update).
 mkdir -p gpurun_out
-python -m pytest tests -q -m gpu > gpurun_out/gpu_tests.log 2>&1; tail -3 gpurun_out/gpu_tests.log
-python bench.py --config $CFG > gpurun_out/bench_round_$CFG.log 2>&1; tail -1 gpurun_out/bench_round_$CFG.log | cut -c1-400
-CMD="python bench.py --config $CFG --steps 1 --warmup 1 --q 1 --no-e2e --no-cpu-baseline"
-$CMD > gpurun_out/prof_plain.log 2>&1 && \
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$CFG.csv $CMD > gpurun_out/ncu_launch.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_zgemm_dmma -s 1 -c 1 -o gpurun_out/prof_sketch_$CFG -f $CMD > gpurun_out/ncu_sketch.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:k_qrcp -c 1 -o gpurun_out/prof_qrcp_$CFG -f $CMD > gpurun_out/ncu_qrcp.log 2>&1
-echo "prof exit $?"
+python -m pytest tests -q -m gpu > gpurun_out/gpu_tests.log 2>&1; echo "rc=$?" >> gpurun_out/gpu_tests.log
+tail -3 gpurun_out/gpu_tests.log
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
+tail -2 gpurun_out/smoke.log
+python bench.py > gpurun_out/bench_default.log 2>&1; echo "bench rc=$?"
+tail -1 gpurun_out/bench_default.log | cut -c1-400
+bash tools/bench_all.sh
+python bench.py --impl reference > gpurun_out/bench_reference.log 2>&1; echo "reference rc=$?"
+tail -1 gpurun_out/bench_reference.log | cut -c1-300
+bash tools/prof_c4.sh
