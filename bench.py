@@ -5,7 +5,8 @@
     torchrun --nproc-per-node N bench.py --gpus N ...      (N > 1: one process per GPU, NCCL)
 
 A "step" is one rid_decompose of the whole configured matrix (all ranks together): Philox
-regeneration of R, the DMMA sketch Y = R A, the all-gather of Y (N > 1), the pivoted Householder QR
+regeneration of R, the sketch Y = R A (the INT8_CRT engine — T exact int8 GEMMs on tcgen05 and a
+CRT reconstruction — for C3-C5, DMMA for C1-C2: rid_sketch_engine), the all-gather of Y (N > 1), the pivoted Householder QR
 of Y, and T = R11^-1 R12 with the P = [I T] assembly — the hot path of SURVEY.md §8(a) rows a2–a5,
 with A (a1's output) resident in HBM before the timed region. a1 (generation) and a6 (the error
 estimate) are timed in the same run and reported under "phases" (they are not inside the step).
@@ -13,7 +14,9 @@ estimate) are timed in the same run and reported under "phases" (they are not in
 metric (BASELINE.json): "ID sketch FP64-complex TFLOP/s & end-to-end ID s at 1/2/4/8 B200 vs
 roofline". value = 8 l m n (the complex sketch's real flops, whole matrix) / end-to-end step time;
 "id_seconds" is that step time, "sketch_tflops" the sketch kernel alone; "roofline" describes the
-dominant kernel (the sketch) against the measured FP64 tensor-pipe (DMMA) peak.
+dominant kernel — the int8 tcgen05 GEMM of the INT8_CRT sketch against the int8 tensor peak (2x the
+measured bf16 cuBLAS peak, the guide's nominal ratio), or the DMMA sketch against the measured FP64
+tensor-pipe peak.
 """
 from __future__ import annotations
 
@@ -244,7 +247,7 @@ def bench_config(cfg, seed: int):
 
 # ------------------------------------------------------------------------------ per-row rooflines -
 def row_rooflines(cfg, n_loc, world, gen_s, sketch_s, gather_s, qrcp_s, solve_s, est_s, q,
-                  sketch_exec_tf, sketch_work="6*l*m*n_loc flop executed (Gauss 3M)"):
+                  sketch_exec_tf, sketch_work="6*l*m*n_loc flop executed (Gauss 3M)", crt=None):
     """Every SURVEY.md §8(a) row of the slowest rank against the roofline that bounds it
     (DESIGN.md §5): algorithmic work per call ÷ the measured phase time ÷ the measured peak
     (DMMA: fp64_peak(), profiles/fp64_peaks.json; HBM copy from MEASURED_PEAKS.json). Work counts only what the method must do, not what a kernel re-reads."""
@@ -265,9 +268,15 @@ def row_rooflines(cfg, n_loc, world, gen_s, sketch_s, gather_s, qrcp_s, solve_s,
     rows = {
         "a1_generate": tensor(8.0 * m * n_loc * k, gen_s,
                               "8*m*n_loc*k flop (ordered 4-product chain, bit-exact)"),
-        "a2_sketch": {"bound": "tensor", "work": sketch_work,
-                      "seconds": sketch_s, "achieved": sketch_exec_tf, "unit": "TFLOP/s",
-                      "peak": P, "frac": sketch_exec_tf / P},
+        "a2_sketch": ({"bound": "tensor", "work": sketch_work, "dtype": "int8",
+                       "seconds": sketch_s, "gemm_seconds": crt["gemm_s"],
+                       "achieved": crt["ops"] / sketch_s / 1e12, "unit": "TFLOP/s",
+                       "peak": crt["peak"], "frac": crt["ops"] / sketch_s / 1e12 / crt["peak"],
+                       "note": "whole sketch phase (residues, GEMMs, CRT) against the int8 peak"}
+                      if crt else
+                      {"bound": "tensor", "work": sketch_work,
+                       "seconds": sketch_s, "achieved": sketch_exec_tf, "unit": "TFLOP/s",
+                       "peak": P, "frac": sketch_exec_tf / P}),
         "a5_solve": tensor(6.0 * k * k * n_loc, solve_s,
                            "6*k^2*n_loc flop (T = R11^-1 R12, Gauss 3M)"),
     }
@@ -417,16 +426,33 @@ def run_ours(args, cfg):
         sk_kernel = "k_zgemm_dmma (sketch Y = R A, real embedding, DMMA.8x8x4)"
         sk_work = "8*l*m*n_loc flop executed (real embedding)"
     peak, peak_src = fp64_peak()
+    engine = diags[-1].get("sketch_engine", 1)
+    crt = None
+    if engine == 2:  # INT8_CRT: the dominant kernel is the tcgen05 int8 GEMM (k_imma)
+        plan = rid.crt_plan(l, m)
+        tc_s = max_over_ranks(statistics.mean(d["t_sketch_tc"] for d in diags))
+        ops = 8.0 * plan["T"] * l * m * n_loc  # T moduli x 2 planes x l x 2m x n_loc MACs x 2
+        mp = measured_peaks()
+        i8_burst = 2.0 * mp.get("bf16_tflops", 1647.4)
+        i8_sust = 2.0 * mp.get("bf16_tflops_sustained", 1379.9)
+        crt = {"plan": plan, "gemm_s": tc_s, "ops": ops, "achieved": ops / tc_s / 1e12,
+               "peak": i8_burst, "peak_sustained": i8_sust}
+        sk_kernel = ("k_imma<128> (INT8_CRT sketch: tcgen05.mma.kind::i8, M=128 A columns x N=nc "
+                     "R rows, TMEM accumulators, TMA SWIZZLE_128B ring, one GEMM per modulus)")
+        sk_work = (f"8*T*l*m*n_loc int8 ops, T = {plan['T']} moduli (exact integer products; the "
+                   "residue and CRT kernels are the rest of the sketch phase)")
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         n_s, threads = oracle_calibrate(cfg, seed, args.ref_seconds)
         cpu = oracle_record(cfg, seed, n_s, threads, oracle_phases(cfg, seed, n_s, q=1))
     if rank != 0:
         return 0
-    prof = {}
+    prof, prof_crt = {}, {}
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            prof = json.load(f).get(f"{cfg.name}/sketch", {})
+            tj = json.load(f)
+            prof = tj.get(f"{cfg.name}/sketch", {})
+            prof_crt = tj.get(f"{cfg.name}/crt_gemm", {})
     except OSError:
         pass
     line = {
@@ -443,6 +469,13 @@ def run_ours(args, cfg):
         "sketch_tflops": sketch_tf_rank * world,  # 8lmn convention (the metric's)
         "sketch_mults": mults,
         "sketch_strassen": bool(strassen),
+        "sketch_engine": {1: "fp64_dmma", 2: "int8_crt"}.get(engine, "srft"),
+        "sketch_crt": ({"T": crt["plan"]["T"], "b": crt["plan"]["b"],
+                        "kslices": crt["plan"]["kslices"], "gemm_s": crt["gemm_s"],
+                        "sketch_s": sketch_s, "gemm_share_of_sketch": crt["gemm_s"] / sketch_s,
+                        "sketch_tflops_8lmn": sketch_tf_rank * world,
+                        "sketch_8lmn_over_fp64_dmma_peak": sketch_tf_rank / peak}
+                       if crt else None),
         "phases": {"rgen_s": rgen_s, "sketch_s": sketch_s, "gather_s": gather_s,
                    "qrcp_s": qrcp_s, "solve_s": solve_s, "generate_s": gen_s,
                    "error_estimate_s": est_s, "error_estimate_q": args.q},
@@ -450,7 +483,19 @@ def run_ours(args, cfg):
         "error_bound_eq3": rid.error_bound(m, n, k, 1e-20, cfg.noise * (m**0.5 + n**0.5))
         if cfg.noise else None,
         "tie_margin_min": diags[-1]["tie_margin_min"],
-        "roofline": {"bound": "tensor", "achieved": sketch_exec_tf,
+        "roofline": ({"bound": "tensor", "achieved": crt["achieved"], "peak": crt["peak"],
+                      "unit": "TFLOP/s", "dtype": "int8", "frac": crt["achieved"] / crt["peak"],
+                      "frac_sustained": crt["achieved"] / crt["peak_sustained"],
+                      "traffic": prof_crt.get("dram_bytes_per_launch"),
+                      "kernel": sk_kernel,
+                      "algorithmic": (f"{sk_work}: {crt['ops']:.4g} int8 ops per sketch over "
+                                      f"{crt['gemm_s'] * 1e3:.3f} ms of GEMM launches (CUDA events "
+                                      "around each launch on the context stream)"),
+                      "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (burst; the guide's "
+                                      "nominal int8:bf16 ratio 4.5:2.25); frac_sustained against "
+                                      "2 x bf16_tflops_sustained")}
+                     if crt else
+                     {"bound": "tensor", "achieved": sketch_exec_tf,
                      "peak": peak, "unit": "TFLOP/s",
                      "frac": sketch_exec_tf / peak,
                      # the same launch in the metric's 8*l*m*n convention (Gauss 3M executes 3/4
@@ -461,9 +506,9 @@ def run_ours(args, cfg):
                      "algorithmic": (f"{exec_coef:g}*l*m*n_loc = {exec_coef * l * m * n_loc:.4g} "
                                      f"flop per sketch ({sk_work}; the metric counts 8*l*m*n); "
                                      "timed: the sketch phase's CUDA events (all its launches)"),
-                     "peak_source": peak_src},
+                     "peak_source": peak_src}),
         "rows": row_rooflines(cfg, n_loc, world, gen_s, sketch_s, gather_s, qrcp_s, solve_s,
-                              est_s, args.q, sketch_exec_tf, sk_work),
+                              est_s, args.q, sketch_exec_tf, sk_work, crt),
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -64,6 +64,18 @@ typedef enum {
   RID_SKETCH_SRFT = 1      /* Y = S F D A (Eqs. 4–7); m a power of two >= 16     */
 } rid_sketch_kind;
 
+/* Arithmetic of the Gaussian sketch Y = R A (rid_set_sketch_engine). Both meet the north-star bar
+ * (Y within 1e-12 relative Frobenius of the oracle; measured ~4e-14); J and P follow from Y. */
+typedef enum {
+  RID_ENGINE_AUTO = 0,     /* INT8_CRT when l m n >= 2^34 (C3-C5), else FP64_DMMA (default)        */
+  RID_ENGINE_FP64_DMMA = 1,/* complex128 products on the FP64 tensor pipe (DMMA.8x8x4: Gauss 3M,
+                              one Strassen level over it for the unsplit plans)                    */
+  RID_ENGINE_INT8_CRT = 2  /* the exact integer product of R and A rounded to b bits relative to
+                              their row / column maxima, computed as T int8 GEMMs on tcgen05 (one
+                              per modulus) and recovered by the Chinese remainder theorem
+                              (reading R33)                                       */
+} rid_sketch_engine;
+
 /* Pivoted QR of the sketch used by rid_decompose, rid_qrcp and rid_factor_solve (rid_set_qr).
  * Both choose the same columns (the greedy largest-residual pivot of PAPER.md:82-86) and agree on
  * R = Q^H Y to rounding. */
@@ -100,6 +112,8 @@ typedef struct {
   double tie_margin_min; /* min_j (nu(1) - nu(2)) / nu(1) over the k pivot steps (reading R18) */
   double resid_last;  /* nu_p at the last pivot step (|R11[k-1,k-1]|)              */
   int launches;       /* number of librid CUDA kernels this call launched           */
+  double t_sketch_tc; /* INT8_CRT engine: the tcgen05 GEMM launches inside t_sketch (0 otherwise) */
+  int sketch_engine;  /* the engine the sketch ran on (RID_ENGINE_FP64_DMMA / _INT8_CRT; 0 SRFT) */
 } rid_diag;
 
 /* --- context ------------------------------------------------------------------------------- */
@@ -177,6 +191,20 @@ rid_status rid_sketch_srft(rid_ctx* ctx, uint64_t seed, int retry, int64_t l, co
                            int64_t ldy);
 /* Select the randomisation of subsequent rid_decompose calls on ctx (default GAUSSIAN). */
 rid_status rid_set_sketch(rid_ctx* ctx, int kind);
+/* Select the arithmetic of subsequent Gaussian sketches on ctx (rid_sketch_engine; default AUTO).
+ * RID_SKETCH_CRT=0/1 in the environment overrides it (FP64_DMMA / INT8_CRT). */
+rid_status rid_set_sketch_engine(rid_ctx* ctx, int engine);
+/* The engine (RID_ENGINE_FP64_DMMA or RID_ENGINE_INT8_CRT) a Gaussian sketch of an m x n matrix
+ * with l rows runs on ctx: a function of (m, l, n), the context's selection and the environment. */
+int rid_sketch_engine_of(const rid_ctx* ctx, int64_t m, int64_t l, int64_t n);
+/* The INT8_CRT plan of an l x m sketch matrix (pure host arithmetic; any pointer may be NULL):
+ * T moduli, b bits per operand, kslices K' slices (each exact in int32), Kp = padded K' = 2 m,
+ * nc rows of R per tensor-memory tile, log2(prod p_t) in log2M. RID_EINVAL for l < 1 or m < 1. */
+rid_status rid_crt_plan(int64_t l, int64_t m, int* T, int* b, int* kslices, int64_t* Kp, int* nc,
+                        double* log2M);
+/* The moduli of the INT8_CRT engine (up to 16 values written to p; returns how many exist). */
+int rid_crt_moduli(int* p, int cap);
+
 /* Select the pivoted QR of subsequent rid_decompose / rid_qrcp / rid_factor_solve calls on ctx
  * (default HOUSEHOLDER). RID_EINVAL for an unknown kind. CGS2 needs a workspace of
  * 16 (2 l n + 2 l k + k n) + 8 l (k + 1) bytes beyond Householder's. */

@@ -49,7 +49,8 @@ class Diag(ctypes.Structure):
                 ("t_h2d", ctypes.c_double), ("t_d2h", ctypes.c_double),
                 ("retries", ctypes.c_int), ("rank_achieved", ctypes.c_int),
                 ("tie_margin_min", ctypes.c_double), ("resid_last", ctypes.c_double),
-                ("launches", ctypes.c_int)]
+                ("launches", ctypes.c_int),
+                ("t_sketch_tc", ctypes.c_double), ("sketch_engine", ctypes.c_int)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -61,10 +62,13 @@ EXPORTS = ["rid_create", "rid_destroy", "rid_last_error", "rid_version", "rid_co
            "rid_decompose", "rid_error_estimate", "rid_error_bound", "rid_normal_fill",
            "rid_qrcp", "rid_factor_solve", "rid_sketch_splits", "rid_sketch_srft",
            "rid_set_sketch", "rid_sketch_mults", "rid_sketch_cols", "rid_set_qr",
-           "rid_set_stream", "rid_comm_init_local", "rid_set_qr_dist", "rid_sketch_strassen"]
+           "rid_set_stream", "rid_comm_init_local", "rid_set_qr_dist", "rid_sketch_strassen",
+           "rid_set_sketch_engine", "rid_sketch_engine_of", "rid_crt_plan", "rid_crt_moduli"]
 SKETCH_GAUSSIAN, SKETCH_SRFT = 0, 1
 QR_HOUSEHOLDER, QR_CGS2 = 0, 1
 QR_REPLICATED, QR_SHARDED = 0, 1
+ENGINE_AUTO, ENGINE_FP64_DMMA, ENGINE_INT8_CRT = 0, 1, 2
+_ENGINES = {"auto": ENGINE_AUTO, "fp64_dmma": ENGINE_FP64_DMMA, "int8_crt": ENGINE_INT8_CRT}
 _QR_DIST = {"replicated": QR_REPLICATED, "sharded": QR_SHARDED}
 _QR_KINDS = {"householder": QR_HOUSEHOLDER, "cgs2": QR_CGS2}
 
@@ -101,6 +105,11 @@ def lib():
         "rid_set_sketch": ([p, ci], ci),
         "rid_set_qr": ([p, ci], ci),
         "rid_set_qr_dist": ([p, ci], ci),
+        "rid_set_sketch_engine": ([p, ci], ci),
+        "rid_sketch_engine_of": ([p, i64, i64, i64], ci),
+        "rid_crt_plan": ([i64, i64, ctypes.POINTER(ci), ctypes.POINTER(ci), ctypes.POINTER(ci),
+                          ctypes.POINTER(i64), ctypes.POINTER(ci), ctypes.POINTER(d)], ci),
+        "rid_crt_moduli": ([ctypes.POINTER(ci), ci], ci),
         "rid_decompose": ([p, p, i64, i64, i64, i64, i64, i64, i64, u64, p, p, i64, p], ci),
         "rid_error_estimate": ([p, p, i64, i64, i64, i64, i64, p, i64, p, i64, ci, u64, p, p], ci),
         "rid_error_bound": ([i64, i64, i64, d, d], d),
@@ -241,6 +250,11 @@ class Context:
         (NEXT-3: the ranks factor their blocks together; in-process communicator only)."""
         self.check(self._L.rid_set_qr_dist(self.h, _QR_DIST[mode]), "rid_set_qr_dist")
 
+    def set_sketch_engine(self, engine: str):
+        """Arithmetic of the Gaussian sketch: 'auto' (default: 'int8_crt' when l m n >= 2^34),
+        'fp64_dmma' (DMMA tensor pipe) or 'int8_crt' (exact modular products on tcgen05)."""
+        self.check(self._L.rid_set_sketch_engine(self.h, _ENGINES[engine]), "rid_set_sketch_engine")
+
     def comm_info(self):
         r, n = ctypes.c_int(), ctypes.c_int()
         self.check(self._L.rid_comm_info(self.h, ctypes.byref(r), ctypes.byref(n)), "rid_comm_info")
@@ -353,6 +367,32 @@ def sketch_strassen(m: int, l: int, n: int, ctx: Context | None = None) -> bool:
     (then column blocks must be 64-aligned)."""
     ctx = ctx or default_context()
     return bool(lib().rid_sketch_strassen(ctx.h, m, l, n))
+
+
+def sketch_engine(m: int, l: int, n: int, ctx: Context | None = None) -> str:
+    """'fp64_dmma' or 'int8_crt': the engine the Gaussian sketch of an m x n matrix runs on."""
+    ctx = ctx or default_context()
+    e = lib().rid_sketch_engine_of(ctx.h, m, l, n)
+    return {ENGINE_FP64_DMMA: "fp64_dmma", ENGINE_INT8_CRT: "int8_crt"}[e]
+
+
+def crt_plan(l: int, m: int) -> dict:
+    """The INT8_CRT engine's plan for an l x m sketch matrix (host arithmetic, no GPU)."""
+    T, b, ks, nc = ctypes.c_int(), ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+    Kp, lg = ctypes.c_int64(), ctypes.c_double()
+    st = lib().rid_crt_plan(l, m, ctypes.byref(T), ctypes.byref(b), ctypes.byref(ks),
+                            ctypes.byref(Kp), ctypes.byref(nc), ctypes.byref(lg))
+    if st != 0:
+        raise RidError(st, "rid_crt_plan: bad arguments")
+    return {"T": T.value, "b": b.value, "kslices": ks.value, "Kp": Kp.value, "nc": nc.value,
+            "log2M": lg.value}
+
+
+def crt_moduli() -> list:
+    """The moduli of the INT8_CRT engine, in the order used."""
+    buf = (ctypes.c_int * 32)()
+    n = lib().rid_crt_moduli(buf, 32)
+    return [buf[i] for i in range(n)]
 
 
 def sketch_mults() -> int:

@@ -1,0 +1,903 @@
+// k_crt.cu — the sketch Y = R · A (north_star; §3.1: "Y = R A") on the fifth-generation
+// tensor cores (tcgen05, int8 kind) as an EXACT modular integer product (R33):
+//
+//   1. scale: f_j = b − E_j per column j of A (max |Re|, |Im| of the column < 2^E_j) and e_i = b − E_i
+//      per row i of R, so that the integers a' = rint(2^f_j A), r' = rint(2^e_i R) (real and
+//      imaginary parts) satisfy |a'|, |r'| <= 2^b;
+//   2. residues: for each of T pairwise-coprime odd moduli p_t <= 253, the int8 residues of a' and r'
+//      (|residue| <= 127), laid out as the two K-major operands of ONE real product with K' = 2m:
+//        Re Y' = [Re r' | −Im r'] · [Re a'; Im a'],   Im Y' = [Im r' | Re r'] · [Re a'; Im a'];
+//   3. T products on tcgen05.mma.kind::i8 (int32 accumulators in TMEM, exact: 2m·127² < 2^31 per K
+//      slice), each reduced mod p_t in the epilogue;
+//   4. the Chinese remainder theorem (Garner's mixed radix, exact 128-bit integers) recovers Y'
+//      exactly from its T residues (M = Π p_t > 2 · 4m · 2^2b), and Y = 2^−(e_i+f_j) Y' in fp64.
+// Y' is the exact product of the rounded operands: the only errors are the roundings of R and A to
+// b bits relative to their row / column maxima (b = 46 at T = 14 for m <= 32768) and the final
+// rounding to fp64 — no accumulation error, no Gauss/Strassen cancellation.
+//
+// The GEMM kernel (k_imma): persistent, one CTA per SM, 6 warps — warp 0 issues the TMA boxes
+// (SWIZZLE_128B, 3D maps over the moduli), warp 1 allocates TMEM and one elected thread issues
+// tcgen05.mma, warps 2–5 drain the accumulators (tcgen05.ld) and reduce them mod p_t. The tile is
+// 128 columns of A (TMEM lanes) × nc rows of R (TMEM columns, Re at column 0, Im at column 256).
+#include <cstdio>
+#include <cstdlib>
+#include <cmath>
+#include <utility>
+#include <vector>
+
+#include "rid_internal.h"
+#include "rid_tma.cuh"
+
+namespace rid {
+
+namespace {
+
+// The moduli: odd, pairwise coprime, <= 253 (so a residue rounded to the nearest quotient in fp32
+// stays within ±127), descending.
+constexpr int kCrtMaxT = 16;
+constexpr int kModuli[kCrtMaxT] = {253, 251, 249, 247, 245, 241, 239, 233,
+                                   229, 227, 223, 211, 199, 197, 193, 191};
+
+struct CrtConst {
+  int T;
+  int p[kCrtMaxT];
+  float pf[kCrtMaxT], invpf[kCrtMaxT];
+  float c16[kCrtMaxT], c32[kCrtMaxT];   // 2^16, 2^32 mod p, symmetric representatives
+  double invpd[kCrtMaxT];
+  uint32_t magic[kCrtMaxT];             // ceil(2^32 / p): floor(x / p) = umulhi(x, magic), x < 2^21
+  uint32_t W[kCrtMaxT][kCrtMaxT];       // W[s][t] = (p_0 ... p_{s-1}) mod p_t
+  uint32_t invP[kCrtMaxT];              // (p_0 ... p_{t-1})^{-1} mod p_t
+  unsigned long long Mlo, Mhi;          // M = p_0 ... p_{T-1} (< 2^128)
+  unsigned long long Hlo, Hhi;          // (M − 1) / 2
+};
+__constant__ CrtConst c_crt;
+
+__device__ __forceinline__ uint32_t mod_small(uint32_t x, int t) {  // x < 2^21
+  const uint32_t q = __umulhi(x, c_crt.magic[t]);
+  return x - q * (uint32_t)c_crt.p[t];
+}
+
+// ------------------------------------------------------------------ scales --------------------
+// colmax[j] = max_k max(|Re A(k, j)|, |Im A(k, j)|)
+__global__ void k_crt_colmax(const double2* __restrict__ A, int64_t lda, int64_t m,
+                             double* __restrict__ colmax) {
+  const int64_t j = blockIdx.x;
+  const double2* a = A + j * lda;
+  double v = 0.0;
+  bool bad = false;  // an inf or NaN: the column's sketch is NaN (as the fp64 product would be)
+  for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+    const double2 z = a[k];
+    v = fmax(v, fmax(fabs(z.x), fabs(z.y)));
+    bad |= !isfinite(z.x) || !isfinite(z.y);
+  }
+  bad = __syncthreads_or(bad);
+  __shared__ double red[32];
+  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) colmax[j] = bad ? __longlong_as_double(0x7ff8000000000000LL) : v;
+  }
+}
+
+// rowmax[i] (zeroed by the launcher) = max_k max(|Re R(i, k)|, |Im R(i, k)|); R column-major
+__global__ void k_crt_rowmax(const double2* __restrict__ R, int64_t ldr, int64_t l, int64_t m,
+                             int64_t kpart, unsigned long long* __restrict__ rowmax) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= l) return;
+  const int64_t k0 = blockIdx.y * kpart, k1 = min(m, k0 + kpart);
+  double v = 0.0;
+  for (int64_t k = k0; k < k1; ++k) {
+    const double2 z = R[i + k * ldr];
+    v = fmax(v, fmax(fabs(z.x), fabs(z.y)));
+  }
+  atomicMax(rowmax + i, (unsigned long long)__double_as_longlong(v));  // v >= 0: bits order
+}
+
+// the exponent shift s with |x| * 2^s <= 2^b for |x| <= vmax (0 for an all-zero line)
+__device__ __forceinline__ int crt_shift(double vmax, int b) {
+  if (!(vmax > 0.0)) return 0;
+  int E;
+  frexp(vmax, &E);  // vmax = f 2^E, f in [0.5, 1): vmax < 2^E
+  return b - E;
+}
+
+// ------------------------------------------------------------------ residues ------------------
+// 2^s as s1 * s2, each a normal double (s > 1000 only for lines whose maximum is below 2^-954)
+struct Scale {
+  double s1, s2;
+};
+__device__ __forceinline__ Scale crt_scale(int s) {
+  const int a = s > 1000 ? 1000 : s;
+  return Scale{ldexp(1.0, a), ldexp(1.0, s - a)};
+}
+// a = rint(x 2^s) (|a| <= 2^46) as three limbs in fp32: a = h 2^32 + l1 2^16 + l0
+struct Limbs {
+  float h, l1, l0;
+};
+__device__ __forceinline__ Limbs crt_limbs(double x, const Scale& sc) {
+  if (sc.s2 != 1.0) x *= sc.s1;  // exact (a power of two, no overflow below 2^46)
+  const double z = __fma_rn(x, sc.s2 != 1.0 ? sc.s2 : sc.s1, 6755399441055744.0);  // 1.5 2^52 + rint(x 2^s)
+  const uint32_t lo = (uint32_t)__double2loint(z);
+  const int hi = __double2hiint(z) - 0x43380000;
+  Limbs L;
+  L.l0 = __int_as_float(0x4B000000 | (lo & 0xFFFFu)) - 8388608.0f;
+  L.l1 = __int_as_float(0x4B000000 | (lo >> 16)) - 8388608.0f;
+  L.h = __int_as_float(0x4B400000 + hi) - 12582912.0f;
+  return L;
+}
+// the residue of a mod p_t in [−127, 127]: its two's complement in the low byte of the result
+__device__ __forceinline__ uint32_t crt_res_byte(const Limbs& L, int t) {
+  const float s = fmaf(L.h, c_crt.c32[t], fmaf(L.l1, c_crt.c16[t], L.l0));  // |s| < 2^24: exact
+  const float q = fmaf(s, c_crt.invpf[t], 12582912.0f) - 12582912.0f;      // ~rint(s / p)
+  const float r = fmaf(-c_crt.pf[t], q, s);                                 // exact, |r| <= 127
+  return (uint32_t)__float_as_int(r + 12582912.0f);
+}
+// the low bytes of four words, packed (three PRMTs)
+__device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
+  return __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
+}
+
+// A (m x ncols, lda) -> Ares[t][j][k'] (int8, row pitch Kp): k' < mh: Re a'(k, j); mh <= k' < 2mh:
+// Im a'(k' − mh, j); zero for k >= m and k' >= 2 mh.
+__global__ void __launch_bounds__(256) k_crt_resA(const double2* __restrict__ A, int64_t lda,
+                                                  int64_t m, int64_t ncols, int64_t mh, int64_t Kp,
+                                                  const double* __restrict__ colmax, int b,
+                                                  uint32_t* __restrict__ Ares) {
+  const int64_t qa = mh / 4, qpad = (Kp - 2 * mh) / 4, qrow = qa + qpad;
+  const int64_t total = qrow * ncols;
+  const int T = c_crt.T;
+  const int64_t tstride = ncols * (Kp / 4);  // words per modulus
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / qrow, q = g - j * qrow;
+    uint32_t* row = Ares + j * (Kp / 4);
+    if (q >= qa) {  // K' padding
+      const int64_t w = (2 * mh) / 4 + (q - qa);
+      for (int t = 0; t < T; ++t) row[t * tstride + w] = 0u;
+      continue;
+    }
+    const int64_t k0 = 4 * q;
+    const Scale scale = crt_scale(crt_shift(colmax[j], b));
+    Limbs re[4], im[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double2 z = make_double2(0.0, 0.0);
+      if (k0 + u < m) z = A[j * lda + k0 + u];
+      re[u] = crt_limbs(z.x, scale);
+      im[u] = crt_limbs(z.y, scale);
+    }
+    for (int t = 0; t < T; ++t) {
+      row[t * tstride + q] = pack4(crt_res_byte(re[0], t), crt_res_byte(re[1], t),
+                                   crt_res_byte(re[2], t), crt_res_byte(re[3], t));
+      row[t * tstride + qa + q] = pack4(crt_res_byte(im[0], t), crt_res_byte(im[1], t),
+                                        crt_res_byte(im[2], t), crt_res_byte(im[3], t));
+    }
+  }
+}
+
+// The same conversion with the column maximum fused in (default): one CTA per column at a time
+// (persistent over columns) reads the column once for its maximum and again, from L2 (one
+// column per SM in flight: 148 x 16 m bytes, C4 76 MB < 126 MB), for the residues; T is a
+// compile-time constant so the modulus loop unrolls with the constants as instruction operands.
+template <int T>
+__global__ void __launch_bounds__(1024, 1) k_crt_prepA(const double2* __restrict__ A, int64_t lda,
+                                                       int64_t m, int64_t ncols, int64_t mh,
+                                                       int64_t Kp, double* __restrict__ colmax,
+                                                       int b, uint32_t* __restrict__ Ares) {
+  __shared__ double red[32];
+  __shared__ int badf;
+  const int64_t qa = mh / 4, qrow = Kp / 4 - qa;  // quads of K per part, + the K' padding words
+  const int64_t tstride = ncols * (Kp / 4);
+  for (int64_t j = blockIdx.x; j < ncols; j += gridDim.x) {
+    const double2* a = A + j * lda;
+    double v = 0.0;
+    bool bad = false;
+    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+      const double2 z = a[k];
+      v = fmax(v, fmax(fabs(z.x), fabs(z.y)));
+      bad |= !isfinite(z.x) || !isfinite(z.y);
+    }
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    if (threadIdx.x == 0) badf = 0;
+    __syncthreads();
+    if (bad) badf = 1;
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    v = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
+    const bool colbad = badf != 0;
+    if (threadIdx.x == 0) colmax[j] = colbad ? __longlong_as_double(0x7ff8000000000000LL) : v;
+    const Scale scale = crt_scale(crt_shift(colbad ? 0.0 : v, b));
+    uint32_t* row = Ares + j * (Kp / 4);
+    for (int64_t q = threadIdx.x; q < qrow; q += blockDim.x) {
+      if (q >= qa) {  // K' padding
+        const int64_t w = 2 * qa + (q - qa);
+#pragma unroll
+        for (int t = 0; t < T; ++t) row[t * tstride + w] = 0u;
+        continue;
+      }
+      const int64_t k0 = 4 * q;
+      Limbs re[4], im[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double2 z = make_double2(0.0, 0.0);
+        if (k0 + u < m) z = a[k0 + u];
+        re[u] = crt_limbs(z.x, scale);
+        im[u] = crt_limbs(z.y, scale);
+      }
+      uint32_t* pr = row + q;
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        pr[0] = pack4(crt_res_byte(re[0], t), crt_res_byte(re[1], t), crt_res_byte(re[2], t),
+                      crt_res_byte(re[3], t));
+        pr[qa] = pack4(crt_res_byte(im[0], t), crt_res_byte(im[1], t), crt_res_byte(im[2], t),
+                       crt_res_byte(im[3], t));
+        pr += tstride;
+      }
+    }
+    __syncthreads();  // red / badf are reused by the next column
+  }
+}
+
+// R (l x m, column-major, ldr) -> Rres[t][0 | 1][lp][Kp]: the operand rows of Re Y' (plane 0:
+// [Re r' | −Im r']) and Im Y' (plane 1: [Im r' | Re r']); rows l..lp−1 and the K' padding zero.
+// One block: 16 rows x 128 K, staged through shared memory so both the read (down a column of R)
+// and the writes (along a row of the operands) are coalesced.
+constexpr int kRT_I = 16, kRT_K = 128;
+__global__ void __launch_bounds__(256) k_crt_resR(const double2* __restrict__ R, int64_t ldr,
+                                                  int64_t l, int64_t m, int64_t lp, int64_t mh,
+                                                  int64_t Kp, const unsigned long long* __restrict__ rowmax,
+                                                  int b, uint32_t* __restrict__ Rres) {
+  __shared__ double2 tile[kRT_K][kRT_I + 1];
+  const int64_t i0 = blockIdx.y * (int64_t)kRT_I, k0 = blockIdx.x * (int64_t)kRT_K;
+  const int T = c_crt.T;
+  const int64_t tstride = 2 * lp * (Kp / 4), pstride = lp * (Kp / 4);
+  if (k0 >= mh) {  // K' padding columns [2 mh, Kp): this block writes them for its rows
+    const int64_t w0 = 2 * mh / 4, nw = (Kp - 2 * mh) / 4;
+    for (int64_t e = threadIdx.x; e < (int64_t)kRT_I * nw; e += blockDim.x) {
+      const int64_t ii = e / nw, w = w0 + e % nw, i = i0 + ii;
+      if (i >= lp) continue;
+      for (int t = 0; t < T; ++t)
+        for (int pl = 0; pl < 2; ++pl) Rres[t * tstride + pl * pstride + i * (Kp / 4) + w] = 0u;
+    }
+    return;
+  }
+  for (int e = threadIdx.x; e < kRT_I * kRT_K; e += blockDim.x) {
+    const int ii = e % kRT_I, kk = e / kRT_I;
+    const int64_t i = i0 + ii, k = k0 + kk;
+    tile[kk][ii] = (i < l && k < m) ? R[i + k * ldr] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  // thread: row ii, K quad kq
+  for (int e = threadIdx.x; e < kRT_I * (kRT_K / 4); e += blockDim.x) {
+    const int ii = e / (kRT_K / 4), kq = e % (kRT_K / 4);
+    const int64_t i = i0 + ii;
+    if (i >= lp) continue;
+    const int64_t kw = (k0 + 4 * kq) / 4;  // word index of the quad
+    if (4 * kw >= mh) continue;
+    const double vmax = i < l ? __longlong_as_double((long long)rowmax[i]) : 0.0;
+    const Scale scale = crt_scale(crt_shift(vmax, b));
+    Limbs re[4], im[4], nim[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const double2 z = tile[4 * kq + u][ii];
+      re[u] = crt_limbs(z.x, scale);
+      im[u] = crt_limbs(z.y, scale);
+      nim[u] = Limbs{-im[u].h, -im[u].l1, -im[u].l0};
+    }
+    uint32_t* base = Rres + i * (Kp / 4);
+    for (int t = 0; t < T; ++t) {
+      const uint32_t wr = pack4(crt_res_byte(re[0], t), crt_res_byte(re[1], t),
+                                crt_res_byte(re[2], t), crt_res_byte(re[3], t));
+      const uint32_t wi = pack4(crt_res_byte(im[0], t), crt_res_byte(im[1], t),
+                                crt_res_byte(im[2], t), crt_res_byte(im[3], t));
+      const uint32_t wn = pack4(crt_res_byte(nim[0], t), crt_res_byte(nim[1], t),
+                                crt_res_byte(nim[2], t), crt_res_byte(nim[3], t));
+      uint32_t* p0 = base + t * tstride;        // plane 0: [Re | −Im]
+      uint32_t* p1 = p0 + pstride;              // plane 1: [Im | Re]
+      p0[kw] = wr;
+      p0[mh / 4 + kw] = wn;
+      p1[kw] = wi;
+      p1[mh / 4 + kw] = wr;
+    }
+  }
+}
+
+// ------------------------------------------------------------------ tcgen05 GEMM --------------
+constexpr int kImmaStagesMax = 8;
+constexpr int kImmaThreads = 192;
+
+struct ImmaArgs {
+  int T, kslices, kbps, coltiles, chunks, nc, lp, stages;
+  int64_t n;                // valid A columns
+  uint8_t* out;             // [kslices][T][2][n][lp] residues in [0, p)
+  uint32_t idesc;
+};
+
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_box3(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(smem_u32(bar))
+      : "memory");
+}
+// K-major operand in the canonical swizzled layout of KB-byte rows (KB = 128: SWIZZLE_128B, layout
+// type 2; KB = 64: SWIZZLE_64B, type 4): 8-row groups 8 KB bytes apart (stride byte offset),
+// leading byte offset 1 (unused when swizzled), version 1 (sm_100)
+template <int KB>
+__device__ __forceinline__ uint64_t umma_desc_sw(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(8 * KB >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)(KB == 128 ? 2 : 4) << 61);
+}
+__device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                        uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                   smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];\n"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+template <int KB>
+__global__ void __launch_bounds__(kImmaThreads, 1)
+    k_imma(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+           const ImmaArgs a) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t full[kImmaStagesMax], empty[kImmaStagesMax], tfull, tempty;
+  __shared__ uint32_t tmem_slot;
+  unsigned char* sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int S = a.stages, nc = a.nc;
+  const uint32_t aBytes = 128 * KB, bBytes = (uint32_t)nc * KB;
+  const uint32_t stageBytes = aBytes + 2 * bBytes;
+  const int nitems = a.T * a.kslices * a.coltiles * a.chunks;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tfull, 1);
+    mbar_init(&tempty, 128);
+    mbar_init_fence();
+    tma_prefetch_map(&mapA);
+    tma_prefetch_map(&mapB);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                     smem_u32(&tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
+        int r = it;
+        const int ch = r % a.chunks; r /= a.chunks;
+        const int ct = r % a.coltiles; r /= a.coltiles;
+        const int ks = r % a.kslices; r /= a.kslices;
+        const int t = r;
+        for (int kb = 0; kb < a.kbps; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          unsigned char* st = sm + (size_t)stage * stageBytes;
+          mbar_expect_tx(&full[stage], stageBytes);
+          const int kx = (ks * a.kbps + kb) * KB;
+          tma_box3(st, &mapA, kx, ct * 128, t, &full[stage]);
+          tma_box3(st + aBytes, &mapB, kx, ch * nc, 2 * t, &full[stage]);
+          tma_box3(st + aBytes + bBytes, &mapB, kx, ch * nc, 2 * t + 1, &full[stage]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---------------- MMA issuer
+      int stage = 0;
+      uint32_t phase = 0, iter = 0;
+      for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++iter) {
+        mbar_wait(&tempty, (iter & 1) ^ 1);  // the epilogue has drained the accumulators
+        tc_fence_after();
+        for (int kb = 0; kb < a.kbps; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(sm + (size_t)stage * stageBytes);
+#pragma unroll
+          for (int kk = 0; kk < KB / 32; ++kk) {  // K = 32 bytes per instruction
+            const uint64_t da = umma_desc_sw<KB>(sa + 32 * kk);
+            const uint64_t dr = umma_desc_sw<KB>(sa + aBytes + 32 * kk);
+            const uint64_t di = umma_desc_sw<KB>(sa + aBytes + bBytes + 32 * kk);
+            const uint32_t acc = (kb | kk) != 0;
+            umma_i8(tmem, da, dr, a.idesc, acc);
+            umma_i8(tmem + 256, da, di, a.idesc, acc);
+          }
+          umma_commit(&empty[stage]);  // frees the stage when these MMAs have read it
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull);
+      }
+    }
+    __syncwarp();
+  } else {  // ---------------- epilogue: warps 2..5 -> TMEM lanes 32 (warp % 4) ...
+    const int q = warp & 3;
+    const int row = 32 * q + lane;
+    uint32_t iter = 0;
+    for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++iter) {
+      int r = it;
+      const int ch = r % a.chunks; r /= a.chunks;
+      const int ct = r % a.coltiles; r /= a.coltiles;
+      const int ks = r % a.kslices; r /= a.kslices;
+      const int t = r;
+      mbar_wait(&tfull, iter & 1);
+      tc_fence_after();
+      const int64_t j = (int64_t)ct * 128 + row;
+      const int p = c_crt.p[t];
+      const double invp = c_crt.invpd[t];
+      for (int ri = 0; ri < 2; ++ri) {
+        uint8_t* dst = a.out + ((((int64_t)ks * a.T + t) * 2 + ri) * a.n + j) * a.lp + (int64_t)ch * nc;
+        for (int c0 = 0; c0 < nc; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + ri * 256 + c0, v);
+          uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int x = (int)v[e];
+            int rr = x - p * (int)floor((double)x * invp);
+            rr += rr < 0 ? p : 0;
+            rr -= rr >= p ? p : 0;
+            w[e >> 2] |= (uint32_t)rr << (8 * (e & 3));
+          }
+          if (j < a.n) *reinterpret_cast<uint4*>(dst + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(&tempty);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ reconstruction ------------
+// Y(i, j) = 2^−(e_i + f_j) · CRT(residues), i < l, j < ncols; T moduli (compile time: the digits
+// stay in registers)
+template <int T>
+__global__ void __launch_bounds__(256) k_crt_rec(const uint8_t* __restrict__ res, int kslices,
+                                                 int64_t n, int64_t lp, int64_t l, int64_t ncols,
+                                                 const unsigned long long* __restrict__ rowmax,
+                                                 const double* __restrict__ colmax, int b,
+                                                 double2* __restrict__ Y, int64_t ldy) {
+  const int64_t total = l * ncols;
+  const int64_t plane = n * lp;
+  const unsigned __int128 M = ((unsigned __int128)c_crt.Mhi << 64) | c_crt.Mlo;
+  const unsigned __int128 H = ((unsigned __int128)c_crt.Hhi << 64) | c_crt.Hlo;
+  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t j = g / l, i = g - j * l;
+    const int si = crt_shift(__longlong_as_double((long long)rowmax[i]), b);
+    const double cm = colmax[j];
+    const int sj = crt_shift(cm, b);
+    const uint8_t* rp = res + j * lp + i;
+    double out[2];
+#pragma unroll
+    for (int ri = 0; ri < 2; ++ri) {
+      uint32_t x[T];
+#pragma unroll
+      for (int t = 0; t < T; ++t) {
+        uint32_t v = rp[(int64_t)(2 * t + ri) * plane];
+        for (int ks = 1; ks < kslices; ++ks) v += rp[(int64_t)((ks * T + t) * 2 + ri) * plane];
+        x[t] = kslices > 1 ? mod_small(v, t) : v;
+      }
+      // Garner: v_t = (x_t − Σ_{s<t} v_s (p_0..p_{s−1})) (p_0..p_{t−1})^{−1} mod p_t, in place
+#pragma unroll
+      for (int t = 1; t < T; ++t) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int s = 0; s < t; ++s) acc += x[s] * c_crt.W[s][t];
+        const uint32_t d = x[t] + (uint32_t)c_crt.p[t] - mod_small(acc, t);
+        x[t] = mod_small(mod_small(d, t) * c_crt.invP[t], t);
+      }
+      // X = v_0 + p_0 (v_1 + p_1 (v_2 + ...)) exactly (X < M < 2^128): 64-bit Horner while it fits
+      unsigned long long lo = x[T - 1];  // the top 7 digits: < 253^7 < 2^64
+#pragma unroll
+      for (int u = T - 2; u >= T - 7; --u) lo = lo * (unsigned)c_crt.p[u] + x[u];
+      unsigned __int128 X = lo;
+#pragma unroll
+      for (int u = T - 8; u >= 0; --u) X = X * (unsigned)c_crt.p[u] + x[u];
+      const bool neg = X > H;
+      const unsigned __int128 mag = neg ? M - X : X;
+      const double d = __fma_rn((double)(unsigned long long)(mag >> 64), 18446744073709551616.0,
+                                (double)(unsigned long long)mag);
+      out[ri] = ldexp(neg ? -d : d, -(si + sj));
+    }
+    if (!(cm <= 1.7976931348623157e308)) out[0] = out[1] = cm;  // inf / NaN in the column: NaN
+    Y[j * ldy + i] = make_double2(out[0], out[1]);
+  }
+}
+
+// ------------------------------------------------------------------ host ---------------------
+uint32_t egcd_inv(uint32_t a, uint32_t p) {  // a^{-1} mod p (p prime-power-free coprime)
+  int64_t t = 0, nt = 1, r = p, nr = a % p;
+  while (nr) {
+    const int64_t qq = r / nr;
+    int64_t tmp = t - qq * nt; t = nt; nt = tmp;
+    tmp = r - qq * nr; r = nr; nr = tmp;
+  }
+  return (uint32_t)((t % (int64_t)p + p) % p);
+}
+
+struct CrtHost {
+  CrtConst c;
+  double log2M;
+};
+CrtHost make_const(int T) {
+  CrtHost h{};
+  CrtConst& c = h.c;
+  c.T = T;
+  unsigned __int128 M = 1;
+  h.log2M = 0;
+  for (int t = 0; t < T; ++t) {
+    const int p = kModuli[t];
+    c.p[t] = p;
+    c.pf[t] = (float)p;
+    c.invpf[t] = 1.0f / (float)p;
+    c.invpd[t] = 1.0 / (double)p;
+    auto sym = [&](uint64_t x) { int v = (int)(x % p); return (float)(v > p / 2 ? v - p : v); };
+    c.c16[t] = sym(1ull << 16);
+    c.c32[t] = sym(1ull << 32);
+    c.magic[t] = (uint32_t)(((1ull << 32) + p - 1) / p);
+    uint64_t P = 1;  // (p_0 .. p_{t-1}) mod p_t
+    for (int s = 0; s < T; ++s) c.W[s][t] = 0;
+    for (int s = 0; s < t; ++s) {
+      c.W[s][t] = (uint32_t)P;
+      P = P * (uint64_t)kModuli[s] % p;
+    }
+    c.invP[t] = t == 0 ? 1 : egcd_inv((uint32_t)P, p);
+    M *= (unsigned)p;
+    h.log2M += std::log2((double)p);
+  }
+  c.Mlo = (unsigned long long)M;
+  c.Mhi = (unsigned long long)(M >> 64);
+  const unsigned __int128 H = (M - 1) / 2;
+  c.Hlo = (unsigned long long)H;
+  c.Hhi = (unsigned long long)(H >> 64);
+  return h;
+}
+
+int crt_env_T() {
+  const char* e = select_env("RID_CRT_MODULI");
+  int T = e ? atoi(e) : 14;
+  if (T < 8) T = 8;
+  if (T > kCrtMaxT) T = kCrtMaxT;
+  return T;
+}
+
+}  // namespace
+
+int crt_moduli(int* p, int cap) {
+  for (int t = 0; t < kCrtMaxT && t < cap; ++t) p[t] = kModuli[t];
+  return kCrtMaxT;
+}
+double crt_log2M(int T) { return make_const(T).log2M; }
+
+CrtPlan crt_plan(int64_t l, int64_t m) {
+  CrtPlan p{};
+  p.T = crt_env_T();
+  const CrtHost h = make_const(p.T);
+  // |Y'| <= 2m 2^2b < M / 2  <=>  2b < log2 M − log2(4m); keep 1/4 bit of margin; limbs cap b at 46
+  int b = (int)std::floor((h.log2M - std::log2(4.0 * (double)m) - 0.25) / 2.0);
+  p.b = b > 46 ? 46 : b;
+  p.mh = (m + 63) / 64 * 64;
+  const int64_t K2 = 2 * p.mh;
+  const int64_t kmax = (int64_t)(2147483647LL / (127 * 127)) / 128 * 128;  // exact int32 slices
+  p.kslices = (int)((K2 + kmax - 1) / kmax);
+  p.kbps = (int)(((K2 + 127) / 128 + p.kslices - 1) / p.kslices);
+  p.Kp = (int64_t)p.kslices * p.kbps * 128;
+  const int64_t l16 = (l + 15) / 16 * 16;
+  p.chunks = (int)((l16 + 255) / 256);
+  p.nc = (int)(((l16 / 16 + p.chunks - 1) / p.chunks) * 16);
+  p.lp = p.chunks * p.nc;
+  return p;
+}
+
+size_t crt_R_bytes(const CrtPlan& p) {  // Rres + rowmax
+  return (size_t)p.T * 2 * p.lp * p.Kp + 8 * (size_t)p.lp + 256;
+}
+size_t crt_A_bytes(const CrtPlan& p, int64_t ncols) {  // Ares + residues out + colmax
+  return (size_t)p.T * ncols * p.Kp + (size_t)p.kslices * p.T * 2 * ncols * p.lp + 8 * (size_t)ncols + 512;
+}
+
+namespace {
+cudaError_t upload_const(int T, cudaStream_t st) {
+  static thread_local int cur_dev = -1, cur_T = -1;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev == cur_dev && T == cur_T) return cudaSuccess;
+  const CrtHost h = make_const(T);
+  e = cudaMemcpyToSymbolAsync(c_crt, &h.c, sizeof(CrtConst), 0, cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) return e;
+  e = cudaStreamSynchronize(st);  // h is a local
+  if (e == cudaSuccess) {
+    cur_dev = dev;
+    cur_T = T;
+  }
+  return e;
+}
+}  // namespace
+
+cudaError_t crt_prep_R(const CrtPlan& p, const double2* R, int64_t ldr, int64_t l, int64_t m,
+                       void* ws, cudaStream_t st, int* launches) {
+  cudaError_t e = upload_const(p.T, st);
+  if (e != cudaSuccess) return e;
+  uint32_t* Rres = (uint32_t*)ws;
+  unsigned long long* rowmax = (unsigned long long*)((char*)ws + (size_t)p.T * 2 * p.lp * p.Kp);
+  if ((e = cudaMemsetAsync(rowmax, 0, 8 * (size_t)p.lp, st)) != cudaSuccess) return e;
+  const int64_t kpart = 1024;
+  dim3 g1((unsigned)((l + 127) / 128), (unsigned)((m + kpart - 1) / kpart));
+  k_crt_rowmax<<<g1, 128, 0, st>>>(R, ldr, l, m, kpart, rowmax);
+  // K blocks cover [0, mh) plus one more block row for the padding [2 mh, Kp)
+  const int64_t kblk = (p.mh + kRT_K - 1) / kRT_K + 1;
+  dim3 g2((unsigned)kblk, (unsigned)((p.lp + kRT_I - 1) / kRT_I));
+  k_crt_resR<<<g2, 256, 0, st>>>(R, ldr, l, m, p.lp, p.mh, p.Kp, rowmax, p.b, Rres);
+  if (launches) *launches += 2;
+  return cudaGetLastError();
+}
+
+namespace {
+// bytes of K per pipeline stage: 128 (SWIZZLE_128B, default) or 64 (SWIZZLE_64B: twice the stages
+// in flight, measured slower — C4 GEMM 25.2 vs 21.8 ms: the MMAs are bound by shared-memory
+// operand bandwidth, not by the depth of the TMA ring)
+int crt_kb() {
+  const char* e = experiment_env("RID_CRT_KB");
+  return e && atoi(e) == 64 ? 64 : 128;
+}
+
+template <int KB>
+cudaError_t launch_imma(const CrtPlan& p, const uint8_t* Rres, uint8_t* Ares, uint8_t* out,
+                        int64_t ncols, int num_sms, cudaStream_t st) {
+  cudaError_t e;
+  PFN_cuTensorMapEncodeTiled encode;
+  if ((e = tensor_map_encoder(&encode)) != cudaSuccess) return e;
+  const CUtensorMapSwizzle sw = KB == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B;
+  CUtensorMap mapA, mapB;
+  {
+    cuuint64_t gdim[3] = {(cuuint64_t)p.Kp, (cuuint64_t)ncols, (cuuint64_t)p.T};
+    cuuint64_t gstr[2] = {(cuuint64_t)p.Kp, (cuuint64_t)p.Kp * ncols};
+    cuuint32_t box[3] = {KB, 128, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (encode(&mapA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)Ares, gdim, gstr, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {
+    cuuint64_t gdim[3] = {(cuuint64_t)p.Kp, (cuuint64_t)p.lp, (cuuint64_t)(2 * p.T)};
+    cuuint64_t gstr[2] = {(cuuint64_t)p.Kp, (cuuint64_t)p.Kp * p.lp};
+    cuuint32_t box[3] = {KB, (cuuint32_t)p.nc, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (encode(&mapB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)Rres, gdim, gstr, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  ImmaArgs ia{};
+  ia.T = p.T;
+  ia.kslices = p.kslices;
+  ia.kbps = p.kbps * (128 / KB);
+  ia.coltiles = (int)((ncols + 127) / 128);
+  ia.chunks = p.chunks;
+  ia.nc = p.nc;
+  ia.lp = (int)p.lp;
+  ia.n = ncols;
+  ia.out = out;
+  // kind::i8: D s32 (bits 4-5 = 2), A and B signed (bits 7-9, 10-12 = 1), both K-major,
+  // N >> 3 at bits 17-22, M >> 4 at bits 24-28
+  ia.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.nc >> 3) << 17) | ((128u >> 4) << 24);
+  const uint32_t stageBytes = 128 * KB + 2 * (uint32_t)p.nc * KB;
+  int optin = 0;
+  if ((e = optin_smem(&optin)) != cudaSuccess) return e;
+  int S = kImmaStagesMax;
+  if (const char* v = experiment_env("RID_CRT_STAGES")) S = std::max(2, std::min(kImmaStagesMax, atoi(v)));
+  while (S > 2 && (size_t)S * stageBytes + 1024 + 1024 > (size_t)optin) --S;
+  ia.stages = S;
+  const size_t smem = (size_t)S * stageBytes + 1024;
+  if ((e = ensure_dyn_smem((const void*)k_imma<KB>, smem)) != cudaSuccess) return e;
+  const int nitems = p.T * p.kslices * ia.coltiles * p.chunks;
+  const int grid = std::min(nitems, num_sms);
+  k_imma<KB><<<grid, kImmaThreads, smem, st>>>(mapA, mapB, ia);
+  return cudaGetLastError();
+}
+}  // namespace
+
+// workspace of one column block (ncols <= nb): A residues, GEMM residues out, colmax
+struct CrtBlockWs {
+  uint8_t* Ares;
+  uint8_t* out;
+  double* colmax;
+};
+static CrtBlockWs carve_block(const CrtPlan& p, void* ws, int64_t nb) {
+  CrtBlockWs w;
+  w.Ares = (uint8_t*)ws;
+  w.out = w.Ares + (size_t)p.T * nb * p.Kp;
+  uintptr_t cm = (uintptr_t)(w.out + (size_t)p.kslices * p.T * 2 * nb * p.lp);
+  w.colmax = (double*)((cm + 255) & ~(uintptr_t)255);
+  return w;
+}
+
+static cudaError_t crt_prep_A(const CrtPlan& p, const CrtBlockWs& w, const double2* A, int64_t lda,
+                              int64_t ncols, int64_t m, int num_sms, cudaStream_t st) {
+  if (experiment_env("RID_CRT_PREP_SPLIT")) {  // round-2 first version: two passes over A
+    k_crt_colmax<<<(unsigned)ncols, 256, 0, st>>>(A, lda, m, w.colmax);
+    const int64_t words = (p.Kp / 4 - p.mh / 4) * ncols;
+    const int64_t blocks = std::min<int64_t>((words + 255) / 256, (int64_t)num_sms * 16);
+    k_crt_resA<<<(unsigned)blocks, 256, 0, st>>>(A, lda, m, ncols, p.mh, p.Kp, w.colmax, p.b,
+                                                 (uint32_t*)w.Ares);
+    return cudaGetLastError();
+  }
+  const unsigned grid = (unsigned)std::min<int64_t>(ncols, num_sms);
+  switch (p.T) {
+#define RID_CRT_PREP(TT)                                                                           \
+  case TT:                                                                                         \
+    k_crt_prepA<TT><<<grid, 1024, 0, st>>>(A, lda, m, ncols, p.mh, p.Kp, w.colmax, p.b,           \
+                                           (uint32_t*)w.Ares);                                     \
+    break;
+    RID_CRT_PREP(8) RID_CRT_PREP(9) RID_CRT_PREP(10) RID_CRT_PREP(11) RID_CRT_PREP(12)
+    RID_CRT_PREP(13) RID_CRT_PREP(14) RID_CRT_PREP(15) RID_CRT_PREP(16)
+#undef RID_CRT_PREP
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+static cudaError_t crt_rec(const CrtPlan& p, const CrtBlockWs& w, const unsigned long long* rowmax,
+                           double2* Y, int64_t ldy, int64_t l, int64_t ncols, int num_sms,
+                           cudaStream_t st) {
+  const int64_t tot = l * ncols;
+  const int64_t rb = std::min<int64_t>((tot + 127) / 128, (int64_t)num_sms * 16);
+  switch (p.T) {
+#define RID_CRT_REC(TT)                                                                            \
+  case TT:                                                                                         \
+    k_crt_rec<TT><<<(unsigned)rb, 128, 0, st>>>(w.out, p.kslices, ncols, p.lp, l, ncols, rowmax,  \
+                                                w.colmax, p.b, Y, ldy);                            \
+    break;
+    RID_CRT_REC(8) RID_CRT_REC(9) RID_CRT_REC(10) RID_CRT_REC(11) RID_CRT_REC(12)
+    RID_CRT_REC(13) RID_CRT_REC(14) RID_CRT_REC(15) RID_CRT_REC(16)
+#undef RID_CRT_REC
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+int64_t crt_block_cols(const CrtPlan& p, int64_t ncols, int64_t budget_bytes) {
+  // as few blocks as the budget allows, the 128-column tiles spread evenly over them (the GEMM's
+  // last wave is then equally full in every block)
+  const int64_t tiles = (ncols + 127) / 128;
+  const int64_t maxt = std::max<int64_t>(1, budget_bytes / (int64_t)crt_A_bytes(p, 128));
+  const int64_t nblk = (tiles + maxt - 1) / maxt;
+  return (tiles + nblk - 1) / nblk * 128;
+}
+
+cudaError_t crt_sketch(const CrtPlan& p, const void* wsR, const double2* A, int64_t lda, double2* Y,
+                       int64_t ldy, int64_t l, int64_t ncols, int64_t m, void* const ws[2],
+                       int64_t nb, int num_sms, cudaStream_t st, const CrtPipe* pipe,
+                       const CrtTiming* tim, int* launches) {
+  if (ncols <= 0) return cudaSuccess;
+  cudaError_t e = upload_const(p.T, st);
+  if (e != cudaSuccess) return e;
+  const uint8_t* Rres = (const uint8_t*)wsR;
+  const unsigned long long* rowmax =
+      (const unsigned long long*)((const char*)wsR + (size_t)p.T * 2 * p.lp * p.Kp);
+  const int KB = crt_kb();
+  int gi = 0;  // GEMM launches so far (timing events 2 gi, 2 gi + 1 around launch gi)
+  auto rec = [&](cudaEvent_t ev) {
+    return tim->external ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal)
+                         : cudaEventRecord(ev, st);
+  };
+  auto gemm = [&](const CrtBlockWs& w, int64_t nc) {
+    cudaError_t r;
+    const bool timed = tim && 2 * gi + 1 < tim->nev;
+    if (timed && (r = rec(tim->ev[2 * gi])) != cudaSuccess) return r;
+    r = KB == 128 ? launch_imma<128>(p, Rres, w.Ares, w.out, nc, num_sms, st)
+                  : launch_imma<64>(p, Rres, w.Ares, w.out, nc, num_sms, st);
+    if (r == cudaSuccess && timed) r = rec(tim->ev[2 * gi + 1]);
+    ++gi;
+    if (tim) tim->used = std::min(gi, tim->nev / 2);
+    return r;
+  };
+  // column blocks: the first a quarter of the others (its preparation is the exposed prologue)
+  std::vector<std::pair<int64_t, int64_t>> blk;  // (col0, cols)
+  {
+    const int64_t first = pipe ? std::max<int64_t>(128, nb / 4 / 128 * 128) : nb;
+    if (tim) tim->used = 0;
+    int64_t j0 = 0;
+    while (j0 < ncols) {
+      const int64_t c = std::min(blk.empty() ? first : nb, ncols - j0);
+      blk.emplace_back(j0, c);
+      j0 += c;
+    }
+  }
+  const int nsub = (int)blk.size();
+  if (!pipe) {  // one stream: prepare, multiply, reconstruct, block by block
+    const CrtBlockWs w = carve_block(p, ws[0], nb);
+    for (const auto& bc : blk) {
+      if ((e = crt_prep_A(p, w, A + bc.first * lda, lda, bc.second, m, num_sms, st)) != cudaSuccess ||
+          (e = gemm(w, bc.second)) != cudaSuccess ||
+          (e = crt_rec(p, w, rowmax, Y + bc.first * ldy, ldy, l, bc.second, num_sms, st)) != cudaSuccess)
+        return e;
+      if (launches) *launches += 3;
+    }
+    return cudaSuccess;
+  }
+  // two buffers, two streams: block c's GEMM (main stream, tensor cores) runs beside block c+1's
+  // preparation and block c-1's reconstruction (aux stream, ALU and HBM)
+  const cudaStream_t ax = pipe->stream;
+  const CrtBlockWs w[2] = {carve_block(p, ws[0], nb), carve_block(p, ws[1], nb)};
+  if ((e = cudaEventRecord(pipe->fork, st)) != cudaSuccess) return e;
+  if ((e = cudaStreamWaitEvent(ax, pipe->fork, 0)) != cudaSuccess) return e;
+  for (int c = 0; c < 2 && c < nsub; ++c) {
+    if ((e = crt_prep_A(p, w[c], A + blk[c].first * lda, lda, blk[c].second, m, num_sms, ax)) != cudaSuccess)
+      return e;
+    if ((e = cudaEventRecord(pipe->prep[c], ax)) != cudaSuccess) return e;
+  }
+  for (int c = 0; c < nsub; ++c) {
+    const int b = c & 1;
+    if ((e = cudaStreamWaitEvent(st, pipe->prep[b], 0)) != cudaSuccess) return e;
+    if ((e = gemm(w[b], blk[c].second)) != cudaSuccess) return e;
+    if ((e = cudaEventRecord(pipe->gemm[b], st)) != cudaSuccess) return e;
+    if ((e = cudaStreamWaitEvent(ax, pipe->gemm[b], 0)) != cudaSuccess) return e;
+    if ((e = crt_rec(p, w[b], rowmax, Y + blk[c].first * ldy, ldy, l, blk[c].second, num_sms, ax)) != cudaSuccess)
+      return e;
+    if (c + 2 < nsub) {
+      if ((e = crt_prep_A(p, w[b], A + blk[c + 2].first * lda, lda, blk[c + 2].second, m, num_sms,
+                          ax)) != cudaSuccess)
+        return e;
+      if ((e = cudaEventRecord(pipe->prep[b], ax)) != cudaSuccess) return e;
+    }
+    if (launches) *launches += 3;
+  }
+  if ((e = cudaEventRecord(pipe->join, ax)) != cudaSuccess) return e;
+  return cudaStreamWaitEvent(st, pipe->join, 0);
+}
+
+}  // namespace rid

@@ -67,6 +67,13 @@ struct rid_ctx {
   cudaStream_t copy_stream = nullptr;
   cudaEvent_t ev_copied[2] = {}, ev_used[2] = {}, ev_copy0 = nullptr, ev_copy1 = nullptr;
   int sketch_kind = 0;  // RID_SKETCH_GAUSSIAN (north star) or RID_SKETCH_SRFT
+  int sketch_engine = 0;  // rid_sketch_engine (RID_ENGINE_AUTO: by the size of the sketch)
+  // events around the INT8_CRT engine's GEMM launches (created on first use), and whether the
+  // current enqueue is being captured into a graph (events are then recorded as external)
+  cudaEvent_t crt_tev[64] = {};
+  int crt_timed = 0;    // GEMM launches timed by the last CRT sketch
+  int g_crt_timed = 0;  // ... by the captured graph's
+  bool capturing = false;
   int qr_kind = 0;      // RID_QR_HOUSEHOLDER (default) or RID_QR_CGS2
   int qr_dist = 0;      // RID_QR_REPLICATED (default) or RID_QR_SHARDED (NEXT-3)
   // pinned host mirror of the QR's status block (info, beta, resid, margin): one copy, one sync
@@ -75,6 +82,8 @@ struct rid_ctx {
   // aux stream for the sketch's K-split tail set (rid::SketchAux), created on first use
   cudaStream_t aux_stream = nullptr;
   cudaEvent_t aux_fork = nullptr, aux_join = nullptr;
+  // the modular integer sketch's column-block pipeline (k_crt.cu), created on first use
+  rid::CrtPipe crt_pipe{};
   // CUDA graph of rid_decompose's device work (repeated calls with identical arguments): the
   // key of the last call seen, the captured executable and its key; ws_epoch counts workspace
   // reallocations (a graph holds workspace pointers)
@@ -85,6 +94,20 @@ struct rid_ctx {
   cudaStream_t cap_stream = nullptr;
   cudaEvent_t g_in = nullptr, g_out = nullptr;
 };
+
+namespace {
+// The engine of the Gaussian sketch of an l x m sketch matrix over n columns (rid_sketch_engine):
+// RID_SKETCH_CRT in the environment, else the context's selection, else by size
+bool use_crt(const rid_ctx* c, int64_t l, int64_t m, int64_t n) {
+  if (const char* e = rid::select_env("RID_SKETCH_CRT")) return atoi(e) != 0;
+  if (c->sketch_engine == RID_ENGINE_FP64_DMMA) return false;
+  if (c->sketch_engine == RID_ENGINE_INT8_CRT) return true;
+  return (double)l * (double)m * (double)n >= 17179869184.0;  // 2^34: C3, C4, C5
+}
+bool strassen_on(const rid_ctx* c, int64_t l, int64_t m, int64_t n) {
+  return !use_crt(c, l, m, n) && rid::strassen_plan(l, m, n, c->num_sms);
+}
+}  // namespace
 
 namespace {
 
@@ -447,6 +470,9 @@ struct SketchR {
   double2* Rc = nullptr;
   double* Rsc = nullptr;
   rid::StrassenWs sw{};
+  bool crt = false;  // the modular integer sketch on the int8 tensor cores (k_crt.cu)
+  rid::CrtPlan cp{};
+  void* crtR = nullptr;
 };
 
 // R (l x m, stream s) for the sketch of an m x n matrix, in the form of the plan (l, m, n) picks.
@@ -460,7 +486,13 @@ rid_status fill_R(rid_ctx* c, uint64_t seed, uint32_t s, int64_t l, int64_t m, i
   *launches += 1;
   *out = SketchR{};
   out->R = (double2*)pR;
-  if (rid::strassen_plan(l, m, n, c->num_sms)) {
+  if (use_crt(c, l, m, n)) {
+    out->crt = true;
+    out->cp = rid::crt_plan(l, m);
+    RID_TRY(ws_get(c, "Rcrt", rid::crt_R_bytes(out->cp), &out->crtR));
+    RID_CUDA(c, rid::crt_prep_R(out->cp, (const double2*)pR, l, l, m, out->crtR, c->stream,
+                                launches));
+  } else if (strassen_on(c, l, m, n)) {
     out->strassen = true;
     out->sw = rid::strassen_ws(l, m, 0);
     void *pc, *ps;
@@ -501,6 +533,32 @@ rid_status sketch_block(rid_ctx* c, const SketchR& sr, const double2* A, int64_t
                         int S, double2* partial, int* launches, const rid::SketchAux* aux) {
   int dummy = 0;
   if (!launches) launches = &dummy;
+  if (sr.crt) {  // column blocks whose residues fit the workspace budget, pipelined on 2 streams
+    // the two-stream block pipeline measured slower (the residue kernels beside the GEMM slow it
+    // from 6.0 to 8.4 ms per block): an experiment
+    const char* pv = rid::experiment_env("RID_CRT_PIPE");
+    const bool piped = pv && atoi(pv) != 0;
+    const int64_t nb = rid::crt_block_cols(sr.cp, ncols, (int64_t)8 << 30);
+    void* pw[2] = {nullptr, nullptr};
+    RID_TRY(ws_get(c, "Acrt0", rid::crt_A_bytes(sr.cp, nb), &pw[0]));
+    if (piped) {
+      RID_TRY(ws_get(c, "Acrt1", rid::crt_A_bytes(sr.cp, nb), &pw[1]));
+      if (!c->crt_pipe.stream) {
+        RID_CUDA(c, cudaStreamCreateWithFlags(&c->crt_pipe.stream, cudaStreamNonBlocking));
+        cudaEvent_t* evs[6] = {&c->crt_pipe.fork, &c->crt_pipe.join, &c->crt_pipe.prep[0],
+                               &c->crt_pipe.prep[1], &c->crt_pipe.gemm[0], &c->crt_pipe.gemm[1]};
+        for (auto* e : evs) RID_CUDA(c, cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+      }
+    }
+    if (!c->crt_tev[0])
+      for (auto& e : c->crt_tev) RID_CUDA(c, cudaEventCreate(&e));
+    const rid::CrtTiming tim{c->crt_tev, 64, c->capturing, 0};
+    c->crt_timed = 0;
+    RID_CUDA(c, rid::crt_sketch(sr.cp, sr.crtR, A, lda, Y, ldy, l, ncols, m, pw, nb, c->num_sms,
+                                c->stream, piped ? &c->crt_pipe : nullptr, &tim, launches));
+    c->crt_timed = tim.used;
+    return RID_OK;
+  }
   if (sr.strassen) {
     if (col0 % 64 != 0 || ncols % 64 != 0)
       return fail(c, RID_EINVAL,
@@ -716,6 +774,15 @@ void rid_destroy(rid_ctx* c) {
     cudaEventDestroy(c->aux_fork);
     cudaEventDestroy(c->aux_join);
   }
+  for (auto& e : c->crt_tev)
+    if (e) cudaEventDestroy(e);
+  if (c->crt_pipe.stream) {
+    cudaStreamSynchronize(c->crt_pipe.stream);
+    cudaStreamDestroy(c->crt_pipe.stream);
+    cudaEvent_t* evs[6] = {&c->crt_pipe.fork, &c->crt_pipe.join, &c->crt_pipe.prep[0],
+                           &c->crt_pipe.prep[1], &c->crt_pipe.gemm[0], &c->crt_pipe.gemm[1]};
+    for (auto* e : evs) cudaEventDestroy(*e);
+  }
   if (c->g_exec) cudaGraphExecDestroy(c->g_exec);
   if (c->cap_stream) {
     cudaStreamSynchronize(c->cap_stream);
@@ -861,6 +928,34 @@ rid_status rid_set_sketch(rid_ctx* c, int kind) {
   return RID_OK;
 }
 
+rid_status rid_set_sketch_engine(rid_ctx* c, int engine) {
+  if (!c) return RID_EINVAL;
+  if (engine != RID_ENGINE_AUTO && engine != RID_ENGINE_FP64_DMMA && engine != RID_ENGINE_INT8_CRT)
+    return fail(c, RID_EINVAL, "rid_set_sketch_engine: unknown engine %d", engine);
+  c->sketch_engine = engine;
+  return RID_OK;
+}
+
+int rid_sketch_engine_of(const rid_ctx* c, int64_t m, int64_t l, int64_t n) {
+  if (!c || m < 1 || l < 1 || n < 1) return 0;
+  return use_crt(c, l, m, n) ? RID_ENGINE_INT8_CRT : RID_ENGINE_FP64_DMMA;
+}
+
+rid_status rid_crt_plan(int64_t l, int64_t m, int* T, int* b, int* kslices, int64_t* Kp, int* nc,
+                        double* log2M) {
+  if (l < 1 || m < 1) return RID_EINVAL;
+  const rid::CrtPlan p = rid::crt_plan(l, m);
+  if (T) *T = p.T;
+  if (b) *b = p.b;
+  if (kslices) *kslices = p.kslices;
+  if (Kp) *Kp = p.Kp;
+  if (nc) *nc = p.nc;
+  if (log2M) *log2M = rid::crt_log2M(p.T);
+  return RID_OK;
+}
+
+int rid_crt_moduli(int* p, int cap) { return rid::crt_moduli(p, cap); }
+
 rid_status rid_set_qr_dist(rid_ctx* c, int mode) {
   if (!c) return RID_EINVAL;
   if (mode != RID_QR_REPLICATED && mode != RID_QR_SHARDED)
@@ -905,7 +1000,7 @@ int rid_sketch_mults(void) { return rid::sketch_mults(); }
 
 int rid_sketch_strassen(const rid_ctx* c, int64_t m, int64_t l, int64_t n) {
   if (!c || m < 1 || l < 1 || n < 1) return 0;
-  return rid::strassen_plan(l, m, n, c->num_sms) ? 1 : 0;
+  return strassen_on(c, l, m, n) ? 1 : 0;
 }
 
 rid_status rid_sketch(rid_ctx* c, uint64_t seed, uint32_t stream, int64_t l, const rid_z* A,
@@ -927,7 +1022,7 @@ rid_status rid_sketch_cols(rid_ctx* c, uint64_t seed, uint32_t stream, int64_t l
   void* pS = nullptr;
   SketchR sr;
   int nl = 0;
-  if (rid::strassen_plan(l, m, n, c->num_sms) && (col0 % 64 != 0 || n_loc % 64 != 0))
+  if (strassen_on(c, l, m, n) && (col0 % 64 != 0 || n_loc % 64 != 0))
     return fail(c, RID_EINVAL, "rid_sketch: with the Strassen plan of this (l, m, n) a column "
                                "block must start and end on multiples of 64");
   RID_TRY(fill_R(c, seed, stream, l, m, n, &sr, &nl));
@@ -979,7 +1074,7 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
   double2* Yw = (double2*)pY;
   // K-split of the sketch: a function of (m, l, n) only, so Y is identical for every sharding
   const int S = rid::sketch_ksplit(l, m, n / 8, c->num_sms);
-  const bool strassen = c->sketch_kind != RID_SKETCH_SRFT && rid::strassen_plan(l, m, n, c->num_sms);
+  const bool strassen = c->sketch_kind != RID_SKETCH_SRFT && strassen_on(c, l, m, n);
   if (strassen && (col0 % 64 != 0 || n_loc % 64 != 0))
     return fail(c, RID_EINVAL, "rid_decompose: with the Strassen sketch plan of this (l, m, n) a "
                                "shard must start and end on multiples of 64 columns");
@@ -1067,10 +1162,10 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
   std::string gkey;
   if (graphable) {
     char buf[512];
-    snprintf(buf, sizeof buf, "%p %lld %lld %lld %lld %lld %lld %lld %llu %p %p %lld %d %llu %p",
+    snprintf(buf, sizeof buf, "%p %lld %lld %lld %lld %lld %lld %lld %llu %p %p %lld %d %llu %p %d",
              (const void*)A, (long long)m, (long long)n, (long long)col0, (long long)n_loc,
              (long long)lda, (long long)k, (long long)l, (unsigned long long)seed, (void*)J,
-             (void*)p.dev, (long long)ldp, c->qr_kind, c->ws_epoch, c->host_qr);
+             (void*)p.dev, (long long)ldp, c->qr_kind, c->ws_epoch, c->host_qr, c->sketch_engine);
     gkey = buf;
     for (char** e = environ; *e; ++e)  // every RID_* knob selects kernels: part of the key
       if (strncmp(*e, "RID_", 4) == 0) {
@@ -1093,9 +1188,10 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
         cudaGraph_t g = nullptr;
         rid_status es = RID_ECUDA;
         if (cudaStreamBeginCapture(c->cap_stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
-          capturing = true;
+          capturing = c->capturing = true;
           es = enqueue(0);
-          capturing = false;
+          capturing = c->capturing = false;
+          c->g_crt_timed = c->crt_timed;
           if (cudaStreamEndCapture(c->cap_stream, &g) != cudaSuccess) es = RID_ECUDA;
         }
         c->stream = orig;
@@ -1121,6 +1217,7 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
         RID_CUDA(c, cudaEventRecord(c->g_in, c->stream));
         RID_CUDA(c, cudaStreamWaitEvent(c->cap_stream, c->g_in, 0));
         RID_CUDA(c, cudaGraphLaunch(c->g_exec, c->cap_stream));
+        c->crt_timed = c->g_crt_timed;
         RID_CUDA(c, cudaEventRecord(c->g_out, c->cap_stream));
         RID_CUDA(c, cudaStreamWaitEvent(c->stream, c->g_out, 0));
         d.launches += c->g_launches;
@@ -1153,6 +1250,14 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
     d.t_solve = ev_ms(ev[6], ev[7]) * 1e-3;
     d.t_d2h = ev_ms(ev[7], ev[8]) * 1e-3;
     d.t_total = ev_ms(ev[0], ev[8]) * 1e-3;
+    d.sketch_engine = 0;
+    d.t_sketch_tc = 0.0;
+    if (c->sketch_kind != RID_SKETCH_SRFT) {
+      d.sketch_engine = use_crt(c, l, m, n) ? RID_ENGINE_INT8_CRT : RID_ENGINE_FP64_DMMA;
+      if (d.sketch_engine == RID_ENGINE_INT8_CRT)
+        for (int g = 0; g < c->crt_timed; ++g)
+          d.t_sketch_tc += ev_ms(c->crt_tev[2 * g], c->crt_tev[2 * g + 1]) * 1e-3;
+    }
     *diag = d;
   }
   return RID_OK;

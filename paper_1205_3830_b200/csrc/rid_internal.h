@@ -256,3 +256,41 @@ cudaError_t srft_sketch(uint64_t seed, bool retry, int64_t l, const double2* A, 
                         double2* splitk, size_t splitk_elems, int num_sms, cudaStream_t st,
                         int* launches);
 }  // namespace rid
+
+namespace rid {
+// The sketch as an exact modular integer product on the int8 tensor cores (k_crt.cu, DESIGN.md
+// §5.5): T moduli, b-bit operands, K' = 2 mh split into kslices of kbps 128-byte blocks (int32
+// exact), the l rows in `chunks` tiles of nc (TMEM columns), lp = chunks * nc.
+struct CrtPlan {
+  int T, b, kslices, kbps, chunks, nc;
+  int64_t mh, Kp, lp;
+};
+CrtPlan crt_plan(int64_t l, int64_t m);
+int crt_moduli(int* p, int cap);
+double crt_log2M(int T);
+size_t crt_R_bytes(const CrtPlan& p);                  // R's residue operands + row maxima
+size_t crt_A_bytes(const CrtPlan& p, int64_t ncols);  // one column block's residues + outputs
+cudaError_t crt_prep_R(const CrtPlan& p, const double2* R, int64_t ldr, int64_t l, int64_t m,
+                       void* wsR, cudaStream_t st, int* launches);
+// the column-block pipeline's second stream and events (created by the caller)
+struct CrtPipe {
+  cudaStream_t stream;
+  cudaEvent_t fork, join, prep[2], gemm[2];
+};
+// events recorded around each GEMM launch (ev[2 g], ev[2 g + 1] for launch g < nev / 2; external
+// records while a graph is captured); `used` = GEMM launches timed by the last call
+struct CrtTiming {
+  cudaEvent_t* ev;
+  int nev;
+  bool external;
+  mutable int used;
+};
+// columns per block for a workspace budget (bytes per block buffer)
+int64_t crt_block_cols(const CrtPlan& p, int64_t ncols, int64_t budget_bytes);
+// Y (l x ncols) = R A: column blocks of <= nb columns, ws[0], ws[1] of crt_A_bytes(p, nb) each
+// (ws[1] unused when pipe == nullptr: one stream, one buffer)
+cudaError_t crt_sketch(const CrtPlan& p, const void* wsR, const double2* A, int64_t lda, double2* Y,
+                       int64_t ldy, int64_t l, int64_t ncols, int64_t m, void* const ws[2],
+                       int64_t nb, int num_sms, cudaStream_t st, const CrtPipe* pipe,
+                       const CrtTiming* tim, int* launches);
+}  // namespace rid

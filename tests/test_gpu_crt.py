@@ -1,0 +1,210 @@
+"""GPU parity of the INT8_CRT sketch engine (k_crt.cu, reading R33): the sketch
+Y = R A as the exact integer product of R and A rounded to b bits relative to their row / column
+maxima, computed as T int8 GEMMs on tcgen05 and recovered by the Chinese remainder theorem.
+
+Bars (BASELINE.json:north_star): Y within 1e-12 relative Frobenius of the oracle (the rounding of
+the operands to b = 45-46 bits gives ~4e-14, tested at 2e-13); J equal to the oracle's and P
+within 1e-10 through rid_decompose. Because the integer product is exact, Y does not depend on
+how the columns are blocked or sharded: those checks are bitwise.
+"""
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def rid():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_1205_3830_b200 import build
+
+    build.build()
+    import paper_1205_3830_b200 as rid
+
+    return rid
+
+
+@pytest.fixture(scope="module")
+def ctx(rid):
+    c = rid.Context(0, torch.cuda.current_stream())
+    c.set_sketch_engine("int8_crt")
+    yield c
+    c.close()
+
+
+def np_(t):
+    return t.cpu().numpy() if hasattr(t, "cpu") else np.asarray(t)
+
+
+def bits_equal(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return a.shape == b.shape and np.array_equal(np.ascontiguousarray(a).view(np.uint64),
+                                                 np.ascontiguousarray(b).view(np.uint64))
+
+
+def relf(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+TOL_Y = 2e-13  # 2^-45 relative to a column maximum ~ 3e-14 per operand, times the max/rms ratio
+
+SKETCH_CASES = [  # (seed, m, n, k, noise, l): the shapes the plan's tiling must cover
+    (1, 1024, 512, 16, 0.0, 24),     # C1: l < 32 (one 32-row tile, 8 padding rows)
+    (2, 333, 45, 5, 1e-9, 13),       # ragged m (K' padding), n < 128 (one partial column tile)
+    (3, 2048, 200, 64, 1e-10, 80),   # C2 structure, a ragged column tile
+    (4, 4096, 150, 128, 1e-12, 144), # C3 structure
+    (5, 2048, 270, 256, 1e-10, 272), # C5 structure: two row tiles (144 + 128)
+    (6, 1024, 540, 512, 1e-8, 528),  # C4 structure: three row tiles of 176
+    (7, 3000, 9, 3, 0.0, 1),         # l = 1
+    (8, 1000, 300, 10, 1e-10, 37),   # l not a multiple of 16
+]
+
+
+@pytest.mark.parametrize("seed,m,n,k,noise,l", SKETCH_CASES)
+def test_crt_sketch_parity(rid, orc, ctx, seed, m, n, k, noise, l):
+    assert rid.sketch_engine(m, l, n, ctx=ctx) == "int8_crt"
+    A_g = rid.generate(seed, m, n, k, noise, ctx=ctx)
+    Y_o = orc.sketch(orc.generate(seed, m, n, k, noise), seed, l)
+    Y_g = np_(rid.sketch(A_g, seed, l, ctx=ctx))
+    assert relf(Y_g, Y_o) <= TOL_Y
+    # column by column as well (each column has its own scale)
+    colerr = np.linalg.norm(Y_g - Y_o, axis=0) / np.linalg.norm(Y_o, axis=0)
+    assert colerr.max() <= 4 * TOL_Y
+
+
+def test_crt_two_k_slices(rid, orc, ctx):
+    """m > 66560: K' = 2m no longer fits one exact int32 accumulation; two K slices whose
+    residues are summed mod p before the reconstruction."""
+    m, n, l = 70000, 130, 24
+    assert rid.crt_plan(l, m)["kslices"] == 2
+    A_g = rid.generate(3, m, n, 8, 1e-10, ctx=ctx)
+    Y_o = orc.sketch(orc.generate(3, m, n, 8, 1e-10), 3, l)
+    assert relf(np_(rid.sketch(A_g, 3, l, ctx=ctx)), Y_o) <= TOL_Y
+
+
+def test_crt_column_scales(rid, orc, ctx):
+    """Per-column scaling: columns 1e±200 apart, an all-zero column and a one-spike column are each
+    reproduced to the same relative accuracy (a single global scale would flush the small ones)."""
+    m, n, l, seed = 512, 160, 24, 5
+    A = orc.generate(seed, m, n, 8, 1e-6).copy(order="F")
+    A[:, 3] *= 1e200
+    A[:, 4] *= 1e-200
+    A[:, 5] = 0
+    A[:, 6] = 0
+    A[17, 6] = 3.0 - 2.0j
+    A[:, 7] *= 1e-300  # scale 2^s with s > 1023: applied in two exact steps
+    Y_o = orc.sketch(A, seed, l)
+    Y_g = np_(rid.sketch(torch.from_numpy(A).cuda(), seed, l, ctx=ctx))
+    assert np.all(Y_g[:, 5] == 0)
+    for j in range(n):
+        if j == 5:
+            continue
+        assert np.linalg.norm(Y_g[:, j] - Y_o[:, j]) <= 4 * TOL_Y * np.linalg.norm(Y_o[:, j]), j
+    # an inf or NaN in a column makes that column's sketch NaN (as the fp64 product would)
+    A[9, 8] = np.inf
+    A[2, 9] = np.nan
+    Y_g = np_(rid.sketch(torch.from_numpy(A).cuda(), seed, l, ctx=ctx))
+    assert np.all(np.isnan(Y_g[:, 8])) and np.all(np.isnan(Y_g[:, 9]))
+    assert np.all(np.isfinite(Y_g[:, 10:]))
+
+
+def test_crt_blocks_bitwise(rid, ctx):
+    """The integer product is exact: any column block of A sketches to the same bits as the same
+    columns of the whole sketch, and a host A (streamed in chunks) gives the same bits."""
+    m, n, l, seed = 2048, 1024, 80, 9
+    A = rid.generate(seed, m, n, 64, 1e-10, ctx=ctx)
+    Y = np_(rid.sketch(A, seed, l, ctx=ctx))
+    for c0, w in ((128, 256), (0, 64), (1000, 24), (333, 100)):
+        Yb = np_(rid.sketch(A[:, c0:c0 + w], seed, l, n=n, col0=c0, ctx=ctx))
+        assert bits_equal(Yb, Y[:, c0:c0 + w]), (c0, w)
+    Yh = rid.sketch(np.asfortranarray(np_(A)), seed, l, ctx=ctx)
+    assert bits_equal(Yh, Y)
+
+
+def test_crt_engine_selection(rid, monkeypatch):
+    c = rid.Context(0, torch.cuda.current_stream())
+    assert rid.sketch_engine(8192, 80, 8192, ctx=c) == "fp64_dmma"      # C2: l m n < 2^34
+    assert rid.sketch_engine(65536, 144, 4096, ctx=c) == "int8_crt"     # C3
+    assert rid.sketch_engine(32768, 528, 32768, ctx=c) == "int8_crt"    # C4
+    assert not rid.sketch_strassen(32768, 528, 32768, ctx=c)
+    c.set_sketch_engine("fp64_dmma")
+    assert rid.sketch_engine(32768, 528, 32768, ctx=c) == "fp64_dmma"
+    assert rid.sketch_strassen(32768, 528, 32768, ctx=c)
+    monkeypatch.setenv("RID_SKETCH_CRT", "1")
+    assert rid.sketch_engine(8192, 80, 8192, ctx=c) == "int8_crt"
+    monkeypatch.delenv("RID_SKETCH_CRT")
+    with pytest.raises(KeyError):
+        c.set_sketch_engine("bogus")
+    c.close()
+
+
+DEC_CASES = [  # (name, seed, m, n, k, l, noise): tests/test_gpu_parity.py DEC_CASES
+    ("C1", 1, 1024, 512, 16, 24, 0.0),
+    ("C2s", 1, 2048, 2048, 64, 80, 1e-10),
+    ("C3s", 1, 8192, 1024, 128, 144, 1e-12),
+    ("C4s", 1, 2048, 2048, 512, 528, 1e-8),
+    ("C5s", 1, 8192, 2048, 256, 272, 1e-10),
+    ("ragged", 3, 700, 333, 20, 29, 1e-7),
+]
+
+
+@pytest.mark.parametrize("name,seed,m,n,k,l,noise", DEC_CASES)
+def test_crt_decompose_parity(rid, orc, ctx, name, seed, m, n, k, l, noise):
+    A_o = orc.generate(seed, m, n, k, noise)
+    d = orc.decompose(A_o, k, l, seed)
+    A_g = rid.generate(seed, m, n, k, noise, ctx=ctx)
+    r = rid.decompose(A_g, k, l, seed, ctx=ctx)
+    assert r.diag["sketch_engine"] == 2 and r.diag["t_sketch_tc"] > 0
+    assert r.diag["t_sketch_tc"] <= r.diag["t_sketch"]
+    assert np_(r.J).tolist() == d.J.tolist()
+    P_g = np_(r.P)
+    assert bits_equal(P_g[:, np_(r.J)], np.eye(k, dtype=np.complex128))
+    assert relf(P_g, d.P) <= 1e-10
+    # repeated call: the CUDA-graph replay gives the same bits and still times the GEMMs
+    r2 = rid.decompose(A_g, k, l, seed, ctx=ctx)
+    r3 = rid.decompose(A_g, k, l, seed, ctx=ctx)
+    assert bits_equal(np_(r3.P), P_g) and bits_equal(np_(r2.P), P_g)
+    assert r3.diag["t_sketch_tc"] > 0
+
+
+def test_crt_multirank_bitwise(rid, orc):
+    """G column shards on one GPU (in-process communicator, one thread per rank): J and the
+    concatenated P bitwise equal to one rank, on the INT8_CRT engine."""
+    m, n, k, l, noise, seed = 2048, 2048, 64, 80, 1e-10, 1
+    one = rid.Context(0, torch.cuda.current_stream())
+    one.set_sketch_engine("int8_crt")
+    A = rid.generate(seed, m, n, k, noise, ctx=one)
+    ref = rid.decompose(A, k, l, seed, ctx=one)
+    torch.cuda.synchronize()
+    for G in (2, 4):
+        streams = [torch.cuda.Stream() for _ in range(G)]
+        ctxs = [rid.Context(0, s) for s in streams]
+        rid.comm_init_local(ctxs)
+        for c in ctxs:
+            c.set_sketch_engine("int8_crt")
+        out = [None] * G
+        nl = n // G
+
+        def body(g):
+            with torch.cuda.stream(streams[g]):
+                out[g] = rid.decompose(A[:, g * nl:(g + 1) * nl], k, l, seed, n=n, col0=g * nl,
+                                       ctx=ctxs[g])
+
+        th = [threading.Thread(target=body, args=(g,)) for g in range(G)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=600)
+        torch.cuda.synchronize()
+        for g in range(G):
+            assert np_(out[g].J).tolist() == np_(ref.J).tolist()
+        P = np.concatenate([np_(o.P) for o in out], axis=1)
+        assert bits_equal(P, np_(ref.P)), G
+        for c in ctxs:
+            c.close()
+    one.close()

@@ -71,13 +71,18 @@ def test_fullsize_against_oracle_golden(rid, orc, name):
     # sketch: sampled columns bitwise, Frobenius norm
     Y = rid.sketch(A, seed, c.l)
     S = rid.sketch_splits(c.m, c.l, c.n)
+    # per-column bar: DMMA (3M / Strassen / K slices) to rounding, 1e-13; the INT8_CRT engine
+    # (R33) rounds each operand to b bits of its row / column maximum: ~3.6 2^-b, bar 8 2^-b
+    tol = 1e-13
+    if rid.sketch_engine(c.m, c.l, c.n) == "int8_crt":
+        tol = 8.0 * 2.0 ** -rid.crt_plan(c.l, c.m)["b"]
     for j in cols:
         y_o = unhex(g["Y_cols"][str(j)])
         y_g = Y[:, j].cpu().numpy()
         if S == 1 and rid.sketch_mults() == 4:  # one ascending fused chain: bit-identical
             assert np.array_equal(bits(y_g), bits(y_o)), f"Y[:, {j}]"
         else:  # Gauss's three products (R31) and/or S fixed-order slice sums: to rounding
-            assert np.linalg.norm(y_g - y_o) <= 1e-13 * np.linalg.norm(y_o), f"Y[:, {j}]"
+            assert np.linalg.norm(y_g - y_o) <= tol * np.linalg.norm(y_o), f"Y[:, {j}]"
     yf = float(torch.linalg.norm(Y))
     assert abs(yf - g["Y_fro"]) <= 1e-12 * g["Y_fro"]
     del Y

@@ -36,8 +36,15 @@ def bits(a):
 
 def test_plan(rid):
     assert rid.sketch_strassen(M, L, N)
-    assert rid.sketch_strassen(32768, 528, 32768) and rid.sketch_strassen(131072, 272, 32768)
-    assert rid.sketch_strassen(8192, 80, 8192) and rid.sketch_strassen(65536, 144, 4096)  # C2, C3
+    # C3-C5 run the INT8_CRT engine by default (rid_sketch_engine); on the DMMA engine they
+    # take the Strassen plan
+    assert not rid.sketch_strassen(32768, 528, 32768)
+    dm = rid.Context(0, torch.cuda.current_stream())
+    dm.set_sketch_engine("fp64_dmma")
+    assert rid.sketch_strassen(32768, 528, 32768, ctx=dm)
+    assert rid.sketch_strassen(131072, 272, 32768, ctx=dm)
+    assert rid.sketch_strassen(8192, 80, 8192) and rid.sketch_strassen(65536, 144, 4096, ctx=dm)
+    dm.close()
     assert not rid.sketch_strassen(1024, 24, 512)  # C1: l < 64
     assert not rid.sketch_strassen(M, L, N - 64)  # n not a multiple of 512
     assert not rid.sketch_strassen(M, 90, N)  # l not a multiple of 4
