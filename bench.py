@@ -60,6 +60,23 @@ def fp64_peak():
     return 37.11, "profiles/r01_box_facts_fp64_microbench.txt (round 1, DMMA sustained)"
 
 
+def int8_peak():
+    """(burst, sustained, source) int8 tensor TOPS: profiles/int8_peaks.json (cuBLASLt int8 GEMM
+    measured on this pool's B200 with clock samples, tools/int8_peaks.py), else 2 x the measured
+    bf16 peaks of MEASURED_PEAKS.json (the guide's nominal int8:bf16 ratio)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "int8_peaks.json")) as f:
+            d = json.load(f)
+        return (float(d["int8_tops_burst"]), float(d["int8_tops_sustained"]),
+                f"profiles/int8_peaks.json: cuBLASLt int8 GEMM 8192^3 burst "
+                f"{d['int8_tops_burst']:.0f} TOPS, sustained {d['int8_tops_sustained']:.0f} "
+                f"(SM {d['clocks'].get('sm_mhz')} MHz, {d['clocks'].get('reasons')}), {d['when']}")
+    except (OSError, ValueError, KeyError):
+        mp = measured_peaks()
+        return (2.0 * mp.get("bf16_tflops", 1647.4), 2.0 * mp.get("bf16_tflops_sustained", 1379.9),
+                "2 x MEASURED_PEAKS.json bf16 (burst / sustained; nominal int8:bf16 ratio)")
+
+
 def measured_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -432,9 +449,7 @@ def run_ours(args, cfg):
         plan = rid.crt_plan(l, m)
         tc_s = max_over_ranks(statistics.mean(d["t_sketch_tc"] for d in diags))
         ops = 8.0 * plan["T"] * l * m * n_loc  # T moduli x 2 planes x l x 2m x n_loc MACs x 2
-        mp = measured_peaks()
-        i8_burst = 2.0 * mp.get("bf16_tflops", 1647.4)
-        i8_sust = 2.0 * mp.get("bf16_tflops_sustained", 1379.9)
+        i8_burst, i8_sust, i8_src = int8_peak()
         crt = {"plan": plan, "gemm_s": tc_s, "ops": ops, "achieved": ops / tc_s / 1e12,
                "peak": i8_burst, "peak_sustained": i8_sust}
         sk_kernel = ("k_imma<128> (INT8_CRT sketch: tcgen05.mma.kind::i8, M=128 A columns x N=nc "
@@ -491,9 +506,7 @@ def run_ours(args, cfg):
                       "algorithmic": (f"{sk_work}: {crt['ops']:.4g} int8 ops per sketch over "
                                       f"{crt['gemm_s'] * 1e3:.3f} ms of GEMM launches (CUDA events "
                                       "around each launch on the context stream)"),
-                      "peak_source": ("2 x MEASURED_PEAKS.json bf16_tflops (burst; the guide's "
-                                      "nominal int8:bf16 ratio 4.5:2.25); frac_sustained against "
-                                      "2 x bf16_tflops_sustained")}
+                      "peak_source": i8_src}
                      if crt else
                      {"bound": "tensor", "achieved": sketch_exec_tf,
                      "peak": peak, "unit": "TFLOP/s",

@@ -128,6 +128,17 @@ __device__ __forceinline__ Limbs crt_limbs(double x, const Scale& sc) {
   L.h = __int_as_float(0x4B400000 + hi) - 12582912.0f;
   return L;
 }
+// the same with the whole scale in one factor (|x scale| < 2^46)
+__device__ __forceinline__ Limbs crt_limbs1(double x, double scale) {
+  const double z = __fma_rn(x, scale, 6755399441055744.0);  // 1.5 2^52 + rint(x 2^s)
+  const uint32_t lo = (uint32_t)__double2loint(z);
+  const int hi = __double2hiint(z) - 0x43380000;
+  Limbs L;
+  L.l0 = __int_as_float(0x4B000000 | (lo & 0xFFFFu)) - 8388608.0f;
+  L.l1 = __int_as_float(0x4B000000 | (lo >> 16)) - 8388608.0f;
+  L.h = __int_as_float(0x4B400000 + hi) - 12582912.0f;
+  return L;
+}
 // the residue of a mod p_t in [−127, 127]: its two's complement in the low byte of the result
 __device__ __forceinline__ uint32_t crt_res_byte(const Limbs& L, int t) {
   const float s = fmaf(L.h, c_crt.c32[t], fmaf(L.l1, c_crt.c16[t], L.l0));  // |s| < 2^24: exact
@@ -182,63 +193,96 @@ __global__ void __launch_bounds__(256) k_crt_resA(const double2* __restrict__ A,
 // (persistent over columns) reads the column once for its maximum and again, from L2 (one
 // column per SM in flight: 148 x 16 m bytes, C4 76 MB < 126 MB), for the residues; T is a
 // compile-time constant so the modulus loop unrolls with the constants as instruction operands.
+template <int T, bool TWO_STEP>
+__device__ __forceinline__ void crt_prep_quads(const double2* __restrict__ a, int64_t m,
+                                               int64_t qa, int64_t qrow, int64_t tstride,
+                                               const Scale scale, uint32_t* __restrict__ row) {
+  for (int64_t q = threadIdx.x; q < qrow; q += blockDim.x) {
+    if (q >= qa) {  // K' padding
+      const int64_t w = 2 * qa + (q - qa);
+#pragma unroll
+      for (int t = 0; t < T; ++t) __stcs(row + t * tstride + w, 0u);
+      continue;
+    }
+    const int64_t k0 = 4 * q;
+    Limbs re[4], im[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      double2 z = make_double2(0.0, 0.0);
+      if (k0 + u < m) z = __ldcs(a + k0 + u);  // last use of A here: evict first
+      if (TWO_STEP) {
+        z.x *= scale.s1;
+        z.y *= scale.s1;
+      }
+      re[u] = crt_limbs1(z.x, TWO_STEP ? scale.s2 : scale.s1);
+      im[u] = crt_limbs1(z.y, TWO_STEP ? scale.s2 : scale.s1);
+    }
+    uint32_t* pr = row + q;
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+      __stcs(pr, pack4(crt_res_byte(re[0], t), crt_res_byte(re[1], t), crt_res_byte(re[2], t),
+                       crt_res_byte(re[3], t)));
+      __stcs(pr + qa, pack4(crt_res_byte(im[0], t), crt_res_byte(im[1], t),
+                            crt_res_byte(im[2], t), crt_res_byte(im[3], t)));
+      pr += tstride;
+    }
+  }
+}
+
+// The conversion with the column maximum fused in (default): one CTA per column at a time
+// (persistent over columns) reads the column once for its maximum and again for the residues
+// (the second read mostly from L2: one column per SM in flight, C4 148 x 512 KB = 76 MB, with the
+// residue stores and the second read marked evict-first). Only the maximum's EXPONENT matters
+// (crt_shift), so the first pass takes the integer maximum of the high words of |Re|, |Im| — two
+// integer operations per value, and an exponent field of 0x7FF (inf / NaN) marks the column bad.
+// T is a compile-time constant so the modulus loop unrolls with the constants as operands.
 template <int T>
 __global__ void __launch_bounds__(1024, 1) k_crt_prepA(const double2* __restrict__ A, int64_t lda,
                                                        int64_t m, int64_t ncols, int64_t mh,
                                                        int64_t Kp, double* __restrict__ colmax,
                                                        int b, uint32_t* __restrict__ Ares) {
-  __shared__ double red[32];
-  __shared__ int badf;
+  __shared__ uint32_t red[32];
+  __shared__ double red_d[32];
   const int64_t qa = mh / 4, qrow = Kp / 4 - qa;  // quads of K per part, + the K' padding words
   const int64_t tstride = ncols * (Kp / 4);
   for (int64_t j = blockIdx.x; j < ncols; j += gridDim.x) {
     const double2* a = A + j * lda;
-    double v = 0.0;
-    bool bad = false;
+    uint32_t hmax = 0;
     for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
       const double2 z = a[k];
-      v = fmax(v, fmax(fabs(z.x), fabs(z.y)));
-      bad |= !isfinite(z.x) || !isfinite(z.y);
+      hmax = max(hmax, max((uint32_t)__double2hiint(z.x) & 0x7FFFFFFFu,
+                           (uint32_t)__double2hiint(z.y) & 0x7FFFFFFFu));
     }
-    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (threadIdx.x == 0) badf = 0;
+    hmax = __reduce_max_sync(0xffffffffu, hmax);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = hmax;
     __syncthreads();
-    if (bad) badf = 1;
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    v = red[0];
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red[w]);
-    const bool colbad = badf != 0;
-    if (threadIdx.x == 0) colmax[j] = colbad ? __longlong_as_double(0x7ff8000000000000LL) : v;
-    const Scale scale = crt_scale(crt_shift(colbad ? 0.0 : v, b));
+    hmax = red[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) hmax = max(hmax, red[w]);
+    double vmax = __hiloint2double((int)hmax, 0);  // the maximum's exponent, in a double
+    const bool bad = hmax >= 0x7FF00000u;
+    if (!bad && hmax < 0x00100000u) {  // subnormal or zero column: the exact maximum (rare)
+      double v = 0.0;
+      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+        const double2 z = a[k];
+        v = fmax(v, fmax(fabs(z.x), fabs(z.y)));
+      }
+      for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+      __syncthreads();
+      if ((threadIdx.x & 31) == 0) red_d[threadIdx.x >> 5] = v;
+      __syncthreads();
+      v = red_d[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red_d[w]);
+      vmax = v;
+    }
+    if (threadIdx.x == 0) colmax[j] = bad ? __longlong_as_double(0x7ff8000000000000LL) : vmax;
+    const int sh = crt_shift(bad ? 0.0 : vmax, b);
+    const Scale scale = crt_scale(sh);
     uint32_t* row = Ares + j * (Kp / 4);
-    for (int64_t q = threadIdx.x; q < qrow; q += blockDim.x) {
-      if (q >= qa) {  // K' padding
-        const int64_t w = 2 * qa + (q - qa);
-#pragma unroll
-        for (int t = 0; t < T; ++t) row[t * tstride + w] = 0u;
-        continue;
-      }
-      const int64_t k0 = 4 * q;
-      Limbs re[4], im[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        double2 z = make_double2(0.0, 0.0);
-        if (k0 + u < m) z = a[k0 + u];
-        re[u] = crt_limbs(z.x, scale);
-        im[u] = crt_limbs(z.y, scale);
-      }
-      uint32_t* pr = row + q;
-#pragma unroll
-      for (int t = 0; t < T; ++t) {
-        pr[0] = pack4(crt_res_byte(re[0], t), crt_res_byte(re[1], t), crt_res_byte(re[2], t),
-                      crt_res_byte(re[3], t));
-        pr[qa] = pack4(crt_res_byte(im[0], t), crt_res_byte(im[1], t), crt_res_byte(im[2], t),
-                       crt_res_byte(im[3], t));
-        pr += tstride;
-      }
-    }
-    __syncthreads();  // red / badf are reused by the next column
+    if (sh > 1000)
+      crt_prep_quads<T, true>(a, m, qa, qrow, tstride, scale, row);
+    else
+      crt_prep_quads<T, false>(a, m, qa, qrow, tstride, scale, row);
+    __syncthreads();  // red / red_d are reused by the next column
   }
 }
 
@@ -499,59 +543,90 @@ __global__ void __launch_bounds__(kImmaThreads, 1)
 }
 
 // ------------------------------------------------------------------ reconstruction ------------
-// Y(i, j) = 2^−(e_i + f_j) · CRT(residues), i < l, j < ncols; T moduli (compile time: the digits
-// stay in registers)
+// One output's value from its T residues x[t] in [0, p_t): Garner's mixed radix
+// v_t = (x_t − Σ_{s<t} v_s (p_0..p_{s−1})) (p_0..p_{t−1})^{−1} mod p_t, then
+// X = v_0 + p_0 (v_1 + p_1 (v_2 + ...)) exactly (< M < 2^128), the symmetric representative and
+// its conversion to fp64 (two roundings at most: |error| <= 2 ulp).
+template <int T>
+__device__ __forceinline__ double crt_value(uint32_t (&x)[T]) {
+#pragma unroll
+  for (int t = 1; t < T; ++t) {
+    uint32_t acc = 0;
+#pragma unroll
+    for (int s = 0; s < t; ++s) acc += x[s] * c_crt.W[s][t];
+    const uint32_t d = x[t] + (uint32_t)c_crt.p[t] - mod_small(acc, t);
+    x[t] = mod_small(mod_small(d, t) * c_crt.invP[t], t);
+  }
+  unsigned long long lo = x[T - 1];  // the top 7 digits: < 253^7 < 2^64
+#pragma unroll
+  for (int u = T - 2; u >= T - 7; --u) lo = lo * (unsigned)c_crt.p[u] + x[u];
+  unsigned __int128 X = lo;
+#pragma unroll
+  for (int u = T - 8; u >= 0; --u) X = X * (unsigned)c_crt.p[u] + x[u];
+  const unsigned __int128 M = ((unsigned __int128)c_crt.Mhi << 64) | c_crt.Mlo;
+  const unsigned __int128 H = ((unsigned __int128)c_crt.Hhi << 64) | c_crt.Hlo;
+  const bool neg = X > H;
+  const unsigned __int128 mag = neg ? M - X : X;
+  const double d = __fma_rn((double)(unsigned long long)(mag >> 64), 18446744073709551616.0,
+                            (double)(unsigned long long)mag);
+  return neg ? -d : d;
+}
+
+// Y(i, j) = 2^−(e_i + f_j) · CRT(residues), i < l, j < ncols. A thread takes four consecutive rows
+// of one column: one 32-bit load per (slice, modulus, part) instead of four byte loads.
 template <int T>
 __global__ void __launch_bounds__(256) k_crt_rec(const uint8_t* __restrict__ res, int kslices,
                                                  int64_t n, int64_t lp, int64_t l, int64_t ncols,
                                                  const unsigned long long* __restrict__ rowmax,
                                                  const double* __restrict__ colmax, int b,
                                                  double2* __restrict__ Y, int64_t ldy) {
-  const int64_t total = l * ncols;
-  const int64_t plane = n * lp;
-  const unsigned __int128 M = ((unsigned __int128)c_crt.Mhi << 64) | c_crt.Mlo;
-  const unsigned __int128 H = ((unsigned __int128)c_crt.Hhi << 64) | c_crt.Hlo;
+  const int64_t l4 = (l + 3) / 4;
+  const int64_t total = l4 * ncols;
+  const int64_t plane = n * lp / 4;  // words
+  const uint32_t* rw = reinterpret_cast<const uint32_t*>(res);
   for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
        g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = g / l, i = g - j * l;
-    const int si = crt_shift(__longlong_as_double((long long)rowmax[i]), b);
+    const int64_t j = g / l4, i0 = 4 * (g - j * l4);
     const double cm = colmax[j];
     const int sj = crt_shift(cm, b);
-    const uint8_t* rp = res + j * lp + i;
-    double out[2];
-#pragma unroll
+    const uint32_t* rp = rw + (j * lp + i0) / 4;
+    double out[2][4];
+#pragma unroll 1
     for (int ri = 0; ri < 2; ++ri) {
-      uint32_t x[T];
+      uint32_t w[T];
 #pragma unroll
       for (int t = 0; t < T; ++t) {
-        uint32_t v = rp[(int64_t)(2 * t + ri) * plane];
-        for (int ks = 1; ks < kslices; ++ks) v += rp[(int64_t)((ks * T + t) * 2 + ri) * plane];
-        x[t] = kslices > 1 ? mod_small(v, t) : v;
+        w[t] = __ldcs(rp + (int64_t)(2 * t + ri) * plane);
+        if (kslices > 1) {  // add the other slices' residues bytewise, mod p_t
+          uint32_t sum[4] = {w[t] & 0xFFu, (w[t] >> 8) & 0xFFu, (w[t] >> 16) & 0xFFu, w[t] >> 24};
+          for (int ks = 1; ks < kslices; ++ks) {
+            const uint32_t v = __ldcs(rp + (int64_t)((ks * T + t) * 2 + ri) * plane);
+            sum[0] += v & 0xFFu;
+            sum[1] += (v >> 8) & 0xFFu;
+            sum[2] += (v >> 16) & 0xFFu;
+            sum[3] += v >> 24;
+          }
+          w[t] = mod_small(sum[0], t) | mod_small(sum[1], t) << 8 | mod_small(sum[2], t) << 16 |
+                 mod_small(sum[3], t) << 24;
+        }
       }
-      // Garner: v_t = (x_t − Σ_{s<t} v_s (p_0..p_{s−1})) (p_0..p_{t−1})^{−1} mod p_t, in place
+#pragma unroll 1
+      for (int u = 0; u < 4; ++u) {
+        uint32_t x[T];
 #pragma unroll
-      for (int t = 1; t < T; ++t) {
-        uint32_t acc = 0;
-#pragma unroll
-        for (int s = 0; s < t; ++s) acc += x[s] * c_crt.W[s][t];
-        const uint32_t d = x[t] + (uint32_t)c_crt.p[t] - mod_small(acc, t);
-        x[t] = mod_small(mod_small(d, t) * c_crt.invP[t], t);
+        for (int t = 0; t < T; ++t) x[t] = (w[t] >> (8 * u)) & 0xFFu;
+        out[ri][u] = crt_value<T>(x);
       }
-      // X = v_0 + p_0 (v_1 + p_1 (v_2 + ...)) exactly (X < M < 2^128): 64-bit Horner while it fits
-      unsigned long long lo = x[T - 1];  // the top 7 digits: < 253^7 < 2^64
-#pragma unroll
-      for (int u = T - 2; u >= T - 7; --u) lo = lo * (unsigned)c_crt.p[u] + x[u];
-      unsigned __int128 X = lo;
-#pragma unroll
-      for (int u = T - 8; u >= 0; --u) X = X * (unsigned)c_crt.p[u] + x[u];
-      const bool neg = X > H;
-      const unsigned __int128 mag = neg ? M - X : X;
-      const double d = __fma_rn((double)(unsigned long long)(mag >> 64), 18446744073709551616.0,
-                                (double)(unsigned long long)mag);
-      out[ri] = ldexp(neg ? -d : d, -(si + sj));
     }
-    if (!(cm <= 1.7976931348623157e308)) out[0] = out[1] = cm;  // inf / NaN in the column: NaN
-    Y[j * ldy + i] = make_double2(out[0], out[1]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t i = i0 + u;
+      if (i >= l) break;
+      const int si = crt_shift(__longlong_as_double((long long)rowmax[i]), b);
+      double2 y = make_double2(ldexp(out[0][u], -(si + sj)), ldexp(out[1][u], -(si + sj)));
+      if (!(cm <= 1.7976931348623157e308)) y = make_double2(cm, cm);  // inf / NaN: NaN
+      Y[j * ldy + i] = y;
+    }
   }
 }
 
@@ -776,10 +851,13 @@ static cudaError_t crt_prep_A(const CrtPlan& p, const CrtBlockWs& w, const doubl
     return cudaGetLastError();
   }
   const unsigned grid = (unsigned)std::min<int64_t>(ncols, num_sms);
+  // threads per CTA: 1024 alone; fewer when it is to share the SMs with the GEMM (RID_CRT_PIPE)
+  int thr = 1024;
+  if (const char* v = experiment_env("RID_CRT_PREP_THREADS")) thr = std::max(128, std::min(1024, atoi(v)));
   switch (p.T) {
 #define RID_CRT_PREP(TT)                                                                           \
   case TT:                                                                                         \
-    k_crt_prepA<TT><<<grid, 1024, 0, st>>>(A, lda, m, ncols, p.mh, p.Kp, w.colmax, p.b,           \
+    k_crt_prepA<TT><<<grid, thr, 0, st>>>(A, lda, m, ncols, p.mh, p.Kp, w.colmax, p.b,           \
                                            (uint32_t*)w.Ares);                                     \
     break;
     RID_CRT_PREP(8) RID_CRT_PREP(9) RID_CRT_PREP(10) RID_CRT_PREP(11) RID_CRT_PREP(12)
@@ -793,12 +871,12 @@ static cudaError_t crt_prep_A(const CrtPlan& p, const CrtBlockWs& w, const doubl
 static cudaError_t crt_rec(const CrtPlan& p, const CrtBlockWs& w, const unsigned long long* rowmax,
                            double2* Y, int64_t ldy, int64_t l, int64_t ncols, int num_sms,
                            cudaStream_t st) {
-  const int64_t tot = l * ncols;
-  const int64_t rb = std::min<int64_t>((tot + 127) / 128, (int64_t)num_sms * 16);
+  const int64_t tot = (l + 3) / 4 * ncols;
+  const int64_t rb = std::min<int64_t>((tot + 255) / 256, (int64_t)num_sms * 8);
   switch (p.T) {
 #define RID_CRT_REC(TT)                                                                            \
   case TT:                                                                                         \
-    k_crt_rec<TT><<<(unsigned)rb, 128, 0, st>>>(w.out, p.kslices, ncols, p.lp, l, ncols, rowmax,  \
+    k_crt_rec<TT><<<(unsigned)rb, 256, 0, st>>>(w.out, p.kslices, ncols, p.lp, l, ncols, rowmax,  \
                                                 w.colmax, p.b, Y, ldy);                            \
     break;
     RID_CRT_REC(8) RID_CRT_REC(9) RID_CRT_REC(10) RID_CRT_REC(11) RID_CRT_REC(12)
