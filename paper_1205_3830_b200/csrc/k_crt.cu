@@ -237,7 +237,7 @@ __device__ __forceinline__ void crt_prep_quads(const double2* __restrict__ a, in
 // integer operations per value, and an exponent field of 0x7FF (inf / NaN) marks the column bad.
 // T is a compile-time constant so the modulus loop unrolls with the constants as operands.
 template <int T>
-__global__ void __launch_bounds__(1024, 1) k_crt_prepA(const double2* __restrict__ A, int64_t lda,
+__global__ void __launch_bounds__(1024) k_crt_prepA(const double2* __restrict__ A, int64_t lda,
                                                        int64_t m, int64_t ncols, int64_t mh,
                                                        int64_t Kp, double* __restrict__ colmax,
                                                        int b, uint32_t* __restrict__ Ares) {
@@ -850,7 +850,9 @@ static cudaError_t crt_prep_A(const CrtPlan& p, const CrtBlockWs& w, const doubl
                                                  (uint32_t*)w.Ares);
     return cudaGetLastError();
   }
-  const unsigned grid = (unsigned)std::min<int64_t>(ncols, num_sms);
+  int per_sm = 1;
+  if (const char* v = experiment_env("RID_CRT_PREP_CTAS")) per_sm = std::max(1, std::min(16, atoi(v)));
+  const unsigned grid = (unsigned)std::min<int64_t>(ncols, (int64_t)num_sms * per_sm);
   // threads per CTA: 1024 alone; fewer when it is to share the SMs with the GEMM (RID_CRT_PIPE)
   int thr = 1024;
   if (const char* v = experiment_env("RID_CRT_PREP_THREADS")) thr = std::max(128, std::min(1024, atoi(v)));

@@ -29,6 +29,13 @@ KEYS = [
     "launch__occupancy_limit_registers", "sm__warps_active.avg.pct_of_peak_sustained_active",
     "smsp__warp_issue_stalled_barrier_per_warp_active.pct",
     "dram__bytes.sum.per_second", "sm__inst_executed_pipe_tensor_subpipe_dmma.sum",
+    "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "sm__pipe_tensor_subpipe_imma_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+    "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+    "smsp__inst_executed.sum",
 ]
 
 
@@ -75,7 +82,8 @@ def main(tag, cfg):
     traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
     seen = {}
     reps = [("sketch", p) for p in sorted(glob.glob(os.path.join(OUT, f"prof_sketch*_{cfg}.ncu-rep")))]
-    reps += [(kind, os.path.join(OUT, f"prof_{kind}_{cfg}.ncu-rep")) for kind in ("qrcp", "update")]
+    reps += [(kind, os.path.join(OUT, f"prof_{kind}_{cfg}.ncu-rep"))
+             for kind in ("crt_gemm", "crt_prep", "crt_rec", "qrcp", "update")]
     for kind, rep in reps:
         if not os.path.exists(rep):
             continue
