@@ -322,9 +322,23 @@ constexpr uint32_t kStreamR = 4, kStreamRRetry = 20;
 // k = 48 a + r (r = 24/32/40; C3 128, C4 512) runs its last r rows of T on r-row tiles beside the
 // 48-row launch (bitwise the same T). Adds its kernel launches to *launches.
 rid_status solve_T(rid_ctx* c, const double2* Rinv, int64_t k, const double2* Y, int64_t ldy,
-                   double2* P, int64_t ldp, int64_t n_loc, int* launches = nullptr) {
+                   double2* P, int64_t ldp, int64_t n_loc, int* launches = nullptr,
+                   bool crt = false) {
   int dummy = 0;
   if (!launches) launches = &dummy;
+  if (crt && !(rid::select_env("RID_SOLVE_CRT") && atoi(rid::select_env("RID_SOLVE_CRT")) == 0)) {
+    // the INT8_CRT engine of the sketch (R33) for T = R11^-1 R12 as well: P = Rinv Y[0:k, :]
+    const rid::CrtPlan cp = rid::crt_plan(k, k);
+    void *pr, *pa;
+    RID_TRY(ws_get(c, "Rcrt_solve", rid::crt_R_bytes(cp), &pr));
+    RID_CUDA(c, rid::crt_prep_R(cp, Rinv, k, k, k, pr, c->stream, launches));
+    const int64_t nb = rid::crt_block_cols(cp, n_loc, (int64_t)2 << 30);
+    RID_TRY(ws_get(c, "Acrt_solve", rid::crt_A_bytes(cp, nb), &pa));
+    void* pw[2] = {pa, nullptr};
+    RID_CUDA(c, rid::crt_sketch(cp, pr, Y, ldy, P, ldp, k, n_loc, k, pw, nb, c->num_sms, c->stream,
+                                nullptr, nullptr, launches));
+    return RID_OK;
+  }
   if (rid::sketch_mults() == 3) {
     void* ps;
     RID_TRY(ws_get(c, "Rinvs", sizeof(double) * rid::rsum_ld(k) * k, &ps));
@@ -1139,7 +1153,7 @@ rid_status rid_decompose(rid_ctx* c, const rid_z* A, int64_t m, int64_t n, int64
       RID_TRY(ws_get(c, "Rinv", sizeof(double2) * k * k, &pRinv));
       RID_CUDA(c, rid::tri_inverse((const double2*)pR11, k, (double2*)pRinv, c->stream));
       RID_TRY(solve_T(c, (const double2*)pRinv, k, Yw + col0 * l, l, (double2*)p.dev, ldp, n_loc,
-                      &d.launches));
+                      &d.launches, c->sketch_kind != RID_SKETCH_SRFT && use_crt(c, l, m, n)));
       RID_CUDA(c, rid::assemble_identity(Jdev, k, col0, n_loc, (double2*)p.dev, ldp, c->stream));
       d.launches += 2;  // R11^-1, identity (solve_T counts the sum plane and the T GEMM)
     }
