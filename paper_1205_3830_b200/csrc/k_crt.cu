@@ -12,8 +12,9 @@
 //   4. the Chinese remainder theorem (Garner's mixed radix, exact 128-bit integers) recovers Y'
 //      exactly from its T residues (M = Π p_t > 2 · 4m · 2^2b), and Y = 2^−(e_i+f_j) Y' in fp64.
 // Y' is the exact product of the rounded operands: the only errors are the roundings of R and A to
-// b bits relative to their row / column maxima (b = 46 at T = 14 for m <= 32768) and the final
-// rounding to fp64 — no accumulation error, no Gauss/Strassen cancellation.
+// b bits relative to their row / column maxima (T = 15: b = 50 for m <= 32768, 49 up to 2^17) and
+// the final rounding to fp64 — no accumulation error, no Gauss/Strassen cancellation: Y is more
+// accurate than an fp64 GEMM's (measured against the oracle in tests/test_gpu_crt.py).
 //
 // The GEMM kernel (k_imma): persistent, one CTA per SM, 6 warps — warp 0 issues the TMA boxes
 // (SWIZZLE_128B, 3D maps over the moduli), warp 1 allocates TMEM and one elected thread issues
@@ -22,8 +23,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
+#include <map>
+#include <mutex>
 #include <utility>
 #include <vector>
+
+#include <cooperative_groups.h>
 
 #include "rid_internal.h"
 #include "rid_tma.cuh"
@@ -58,30 +63,6 @@ __device__ __forceinline__ uint32_t mod_small(uint32_t x, int t) {  // x < 2^21
 }
 
 // ------------------------------------------------------------------ scales --------------------
-// colmax[j] = max_k max(|Re A(k, j)|, |Im A(k, j)|)
-__global__ void k_crt_colmax(const double2* __restrict__ A, int64_t lda, int64_t m,
-                             double* __restrict__ colmax) {
-  const int64_t j = blockIdx.x;
-  const double2* a = A + j * lda;
-  double v = 0.0;
-  bool bad = false;  // an inf or NaN: the column's sketch is NaN (as the fp64 product would be)
-  for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
-    const double2 z = a[k];
-    v = fmax(v, fmax(fabs(z.x), fabs(z.y)));
-    bad |= !isfinite(z.x) || !isfinite(z.y);
-  }
-  bad = __syncthreads_or(bad);
-  __shared__ double red[32];
-  for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
-    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-    if (threadIdx.x == 0) colmax[j] = bad ? __longlong_as_double(0x7ff8000000000000LL) : v;
-  }
-}
-
 // rowmax[i] (zeroed by the launcher) = max_k max(|Re R(i, k)|, |Im R(i, k)|); R column-major
 __global__ void k_crt_rowmax(const double2* __restrict__ R, int64_t ldr, int64_t l, int64_t m,
                              int64_t kpart, unsigned long long* __restrict__ rowmax) {
@@ -113,38 +94,25 @@ __device__ __forceinline__ Scale crt_scale(int s) {
   const int a = s > 1000 ? 1000 : s;
   return Scale{ldexp(1.0, a), ldexp(1.0, s - a)};
 }
-// a = rint(x 2^s) (|a| <= 2^46) as three limbs in fp32: a = h 2^32 + l1 2^16 + l0
-struct Limbs {
-  float h, l1, l0;
+// The residue of a mod p_t from the FP64 pipe: a is the exact integer rint(x 2^s) as a double
+// and a_lo its low 32 bits. q = rint(a / p) is one DFMA against 1.5 2^52 (|a / p| < 2^39; the
+// rounded 1/p moves q by at most one, only within 2^-14 of a half-integer, so |a − p q| <= 0.5001 p
+// <= 127), and the remainder's low byte comes from 32-bit integer arithmetic on the low words:
+// a − p q = a_lo − p q_lo (mod 2^32). One DFMA + one IMAD per residue (round 2's first version
+// split a into three fp32 limbs and spent six FP32 operations per residue: C4 preparation 2.98 vs
+// 2.42 ms per 8192-column block).
+__device__ __forceinline__ uint32_t crt_res_byte64(double a, uint32_t a_lo, int t) {
+  const double qb = __fma_rn(a, c_crt.invpd[t], 6755399441055744.0);  // 1.5 2^52 + q
+  return a_lo - (uint32_t)c_crt.p[t] * (uint32_t)__double2loint(qb);
+}
+// a = rint(x scale) as an exact double, and its low 32 bits (|x scale| <= 2^50 < 2^51)
+struct Int46 {
+  double a;
+  uint32_t lo;
 };
-__device__ __forceinline__ Limbs crt_limbs(double x, const Scale& sc) {
-  if (sc.s2 != 1.0) x *= sc.s1;  // exact (a power of two, no overflow below 2^46)
-  const double z = __fma_rn(x, sc.s2 != 1.0 ? sc.s2 : sc.s1, 6755399441055744.0);  // 1.5 2^52 + rint(x 2^s)
-  const uint32_t lo = (uint32_t)__double2loint(z);
-  const int hi = __double2hiint(z) - 0x43380000;
-  Limbs L;
-  L.l0 = __int_as_float(0x4B000000 | (lo & 0xFFFFu)) - 8388608.0f;
-  L.l1 = __int_as_float(0x4B000000 | (lo >> 16)) - 8388608.0f;
-  L.h = __int_as_float(0x4B400000 + hi) - 12582912.0f;
-  return L;
-}
-// the same with the whole scale in one factor (|x scale| < 2^46)
-__device__ __forceinline__ Limbs crt_limbs1(double x, double scale) {
+__device__ __forceinline__ Int46 crt_int46(double x, double scale) {
   const double z = __fma_rn(x, scale, 6755399441055744.0);  // 1.5 2^52 + rint(x 2^s)
-  const uint32_t lo = (uint32_t)__double2loint(z);
-  const int hi = __double2hiint(z) - 0x43380000;
-  Limbs L;
-  L.l0 = __int_as_float(0x4B000000 | (lo & 0xFFFFu)) - 8388608.0f;
-  L.l1 = __int_as_float(0x4B000000 | (lo >> 16)) - 8388608.0f;
-  L.h = __int_as_float(0x4B400000 + hi) - 12582912.0f;
-  return L;
-}
-// the residue of a mod p_t in [−127, 127]: its two's complement in the low byte of the result
-__device__ __forceinline__ uint32_t crt_res_byte(const Limbs& L, int t) {
-  const float s = fmaf(L.h, c_crt.c32[t], fmaf(L.l1, c_crt.c16[t], L.l0));  // |s| < 2^24: exact
-  const float q = fmaf(s, c_crt.invpf[t], 12582912.0f) - 12582912.0f;      // ~rint(s / p)
-  const float r = fmaf(-c_crt.pf[t], q, s);                                 // exact, |r| <= 127
-  return (uint32_t)__float_as_int(r + 12582912.0f);
+  return Int46{z - 6755399441055744.0, (uint32_t)__double2loint(z)};
 }
 // the low bytes of four words, packed (three PRMTs)
 __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
@@ -153,51 +121,12 @@ __device__ __forceinline__ uint32_t pack4(uint32_t b0, uint32_t b1, uint32_t b2,
 
 // A (m x ncols, lda) -> Ares[t][j][k'] (int8, row pitch Kp): k' < mh: Re a'(k, j); mh <= k' < 2mh:
 // Im a'(k' − mh, j); zero for k >= m and k' >= 2 mh.
-__global__ void __launch_bounds__(256) k_crt_resA(const double2* __restrict__ A, int64_t lda,
-                                                  int64_t m, int64_t ncols, int64_t mh, int64_t Kp,
-                                                  const double* __restrict__ colmax, int b,
-                                                  uint32_t* __restrict__ Ares) {
-  const int64_t qa = mh / 4, qpad = (Kp - 2 * mh) / 4, qrow = qa + qpad;
-  const int64_t total = qrow * ncols;
-  const int T = c_crt.T;
-  const int64_t tstride = ncols * (Kp / 4);  // words per modulus
-  for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < total;
-       g += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t j = g / qrow, q = g - j * qrow;
-    uint32_t* row = Ares + j * (Kp / 4);
-    if (q >= qa) {  // K' padding
-      const int64_t w = (2 * mh) / 4 + (q - qa);
-      for (int t = 0; t < T; ++t) row[t * tstride + w] = 0u;
-      continue;
-    }
-    const int64_t k0 = 4 * q;
-    const Scale scale = crt_scale(crt_shift(colmax[j], b));
-    Limbs re[4], im[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      double2 z = make_double2(0.0, 0.0);
-      if (k0 + u < m) z = A[j * lda + k0 + u];
-      re[u] = crt_limbs(z.x, scale);
-      im[u] = crt_limbs(z.y, scale);
-    }
-    for (int t = 0; t < T; ++t) {
-      row[t * tstride + q] = pack4(crt_res_byte(re[0], t), crt_res_byte(re[1], t),
-                                   crt_res_byte(re[2], t), crt_res_byte(re[3], t));
-      row[t * tstride + qa + q] = pack4(crt_res_byte(im[0], t), crt_res_byte(im[1], t),
-                                        crt_res_byte(im[2], t), crt_res_byte(im[3], t));
-    }
-  }
-}
-
-// The same conversion with the column maximum fused in (default): one CTA per column at a time
-// (persistent over columns) reads the column once for its maximum and again, from L2 (one
-// column per SM in flight: 148 x 16 m bytes, C4 76 MB < 126 MB), for the residues; T is a
-// compile-time constant so the modulus loop unrolls with the constants as instruction operands.
 template <int T, bool TWO_STEP>
 __device__ __forceinline__ void crt_prep_quads(const double2* __restrict__ a, int64_t m,
-                                               int64_t qa, int64_t qrow, int64_t tstride,
-                                               const Scale scale, uint32_t* __restrict__ row) {
-  for (int64_t q = threadIdx.x; q < qrow; q += blockDim.x) {
+                                               int64_t qa, int64_t qbeg, int64_t qend,
+                                               int64_t tstride, const Scale scale,
+                                               uint32_t* __restrict__ row) {
+  for (int64_t q = qbeg + threadIdx.x; q < qend; q += blockDim.x) {
     if (q >= qa) {  // K' padding
       const int64_t w = 2 * qa + (q - qa);
 #pragma unroll
@@ -205,7 +134,7 @@ __device__ __forceinline__ void crt_prep_quads(const double2* __restrict__ a, in
       continue;
     }
     const int64_t k0 = 4 * q;
-    Limbs re[4], im[4];
+    Int46 re[4], im[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       double2 z = make_double2(0.0, 0.0);
@@ -214,41 +143,53 @@ __device__ __forceinline__ void crt_prep_quads(const double2* __restrict__ a, in
         z.x *= scale.s1;
         z.y *= scale.s1;
       }
-      re[u] = crt_limbs1(z.x, TWO_STEP ? scale.s2 : scale.s1);
-      im[u] = crt_limbs1(z.y, TWO_STEP ? scale.s2 : scale.s1);
+      re[u] = crt_int46(z.x, TWO_STEP ? scale.s2 : scale.s1);
+      im[u] = crt_int46(z.y, TWO_STEP ? scale.s2 : scale.s1);
     }
     uint32_t* pr = row + q;
 #pragma unroll
     for (int t = 0; t < T; ++t) {
-      __stcs(pr, pack4(crt_res_byte(re[0], t), crt_res_byte(re[1], t), crt_res_byte(re[2], t),
-                       crt_res_byte(re[3], t)));
-      __stcs(pr + qa, pack4(crt_res_byte(im[0], t), crt_res_byte(im[1], t),
-                            crt_res_byte(im[2], t), crt_res_byte(im[3], t)));
+      __stcs(pr, pack4(crt_res_byte64(re[0].a, re[0].lo, t), crt_res_byte64(re[1].a, re[1].lo, t),
+                       crt_res_byte64(re[2].a, re[2].lo, t), crt_res_byte64(re[3].a, re[3].lo, t)));
+      __stcs(pr + qa,
+             pack4(crt_res_byte64(im[0].a, im[0].lo, t), crt_res_byte64(im[1].a, im[1].lo, t),
+                   crt_res_byte64(im[2].a, im[2].lo, t), crt_res_byte64(im[3].a, im[3].lo, t)));
       pr += tstride;
     }
   }
 }
 
-// The conversion with the column maximum fused in (default): one CTA per column at a time
-// (persistent over columns) reads the column once for its maximum and again for the residues
-// (the second read mostly from L2: one column per SM in flight, C4 148 x 512 KB = 76 MB, with the
-// residue stores and the second read marked evict-first). Only the maximum's EXPONENT matters
-// (crt_shift), so the first pass takes the integer maximum of the high words of |Re|, |Im| — two
-// integer operations per value, and an exponent field of 0x7FF (inf / NaN) marks the column bad.
-// T is a compile-time constant so the modulus loop unrolls with the constants as operands.
+// The conversion with the column maximum fused in (default). A cluster of CL CTAs (on CL SMs)
+// takes one column at a time, persistent over columns: each CTA reads its 1/CL of the column for
+// the maximum, the CTAs exchange their partial maxima through distributed shared memory (one
+// cluster barrier), and each converts its part of the column, re-read from L2 (148 / CL columns in
+// flight: C4 with CL = 4, 37 x 512 KB = 19 MB; the residue stores and the second read are marked
+// evict-first). Only the maximum's EXPONENT matters (crt_shift), so the first pass takes the
+// integer maximum of the high words of |Re|, |Im| — two integer operations per value — and an
+// exponent field 0x7FF (inf / NaN) marks the column bad. T is a compile-time constant so the
+// modulus loop unrolls with the constants as instruction operands.
 template <int T>
 __global__ void __launch_bounds__(1024) k_crt_prepA(const double2* __restrict__ A, int64_t lda,
-                                                       int64_t m, int64_t ncols, int64_t mh,
-                                                       int64_t Kp, double* __restrict__ colmax,
-                                                       int b, uint32_t* __restrict__ Ares) {
+                                                    int64_t m, int64_t ncols, int64_t mh,
+                                                    int64_t Kp, double* __restrict__ colmax,
+                                                    int b, uint32_t* __restrict__ Ares) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  const int CL = (int)cl.num_blocks(), rk = (int)cl.block_rank();
   __shared__ uint32_t red[32];
+  __shared__ uint32_t part[2];  // this CTA's partial maximum, by column parity
   __shared__ double red_d[32];
+  __shared__ double part_d[2];
   const int64_t qa = mh / 4, qrow = Kp / 4 - qa;  // quads of K per part, + the K' padding words
   const int64_t tstride = ncols * (Kp / 4);
-  for (int64_t j = blockIdx.x; j < ncols; j += gridDim.x) {
+  const int64_t nclu = gridDim.x / CL, cid = blockIdx.x / CL;
+  const int64_t kseg = (m + CL - 1) / CL, qseg = (qrow + CL - 1) / CL;
+  int par = 0;
+  for (int64_t j = cid; j < ncols; j += nclu, par ^= 1) {
     const double2* a = A + j * lda;
     uint32_t hmax = 0;
-    for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+    const int64_t kb = rk * kseg, ke = min(m, kb + kseg);
+    for (int64_t k = kb + threadIdx.x; k < ke; k += blockDim.x) {
       const double2 z = a[k];
       hmax = max(hmax, max((uint32_t)__double2hiint(z.x) & 0x7FFFFFFFu,
                            (uint32_t)__double2hiint(z.y) & 0x7FFFFFFFu));
@@ -256,34 +197,48 @@ __global__ void __launch_bounds__(1024) k_crt_prepA(const double2* __restrict__ 
     hmax = __reduce_max_sync(0xffffffffu, hmax);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = hmax;
     __syncthreads();
-    hmax = red[0];
-    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) hmax = max(hmax, red[w]);
+    if (threadIdx.x == 0) {
+      uint32_t v = red[0];
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = max(v, red[w]);
+      part[par] = v;
+    }
+    cl.sync();  // every CTA's part[par] is written (and the previous column's reads are done)
+    hmax = 0;
+    for (int r = 0; r < CL; ++r) hmax = max(hmax, *cl.map_shared_rank(&part[par], r));
     double vmax = __hiloint2double((int)hmax, 0);  // the maximum's exponent, in a double
     const bool bad = hmax >= 0x7FF00000u;
     if (!bad && hmax < 0x00100000u) {  // subnormal or zero column: the exact maximum (rare)
       double v = 0.0;
-      for (int64_t k = threadIdx.x; k < m; k += blockDim.x) {
+      for (int64_t k = kb + threadIdx.x; k < ke; k += blockDim.x) {
         const double2 z = a[k];
         v = fmax(v, fmax(fabs(z.x), fabs(z.y)));
       }
       for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
-      __syncthreads();
       if ((threadIdx.x & 31) == 0) red_d[threadIdx.x >> 5] = v;
       __syncthreads();
-      v = red_d[0];
-      for (int w = 1; w < (int)(blockDim.x >> 5); ++w) v = fmax(v, red_d[w]);
+      if (threadIdx.x == 0) {
+        double w0 = red_d[0];
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) w0 = fmax(w0, red_d[w]);
+        part_d[par] = w0;
+      }
+      cl.sync();
+      v = 0.0;
+      for (int r = 0; r < CL; ++r) v = fmax(v, *cl.map_shared_rank(&part_d[par], r));
       vmax = v;
     }
-    if (threadIdx.x == 0) colmax[j] = bad ? __longlong_as_double(0x7ff8000000000000LL) : vmax;
+    if (threadIdx.x == 0 && rk == 0)
+      colmax[j] = bad ? __longlong_as_double(0x7ff8000000000000LL) : vmax;
     const int sh = crt_shift(bad ? 0.0 : vmax, b);
     const Scale scale = crt_scale(sh);
     uint32_t* row = Ares + j * (Kp / 4);
+    const int64_t qb = rk * qseg, qe = min(qrow, qb + qseg);
     if (sh > 1000)
-      crt_prep_quads<T, true>(a, m, qa, qrow, tstride, scale, row);
+      crt_prep_quads<T, true>(a, m, qa, qb, qe, tstride, scale, row);
     else
-      crt_prep_quads<T, false>(a, m, qa, qrow, tstride, scale, row);
+      crt_prep_quads<T, false>(a, m, qa, qb, qe, tstride, scale, row);
     __syncthreads();  // red / red_d are reused by the next column
   }
+  cl.sync();  // no CTA exits while a peer may still read its part[] through DSMEM
 }
 
 // R (l x m, column-major, ldr) -> Rres[t][0 | 1][lp][Kp]: the operand rows of Re Y' (plane 0:
@@ -324,22 +279,30 @@ __global__ void __launch_bounds__(256) k_crt_resR(const double2* __restrict__ R,
     if (4 * kw >= mh) continue;
     const double vmax = i < l ? __longlong_as_double((long long)rowmax[i]) : 0.0;
     const Scale scale = crt_scale(crt_shift(vmax, b));
-    Limbs re[4], im[4], nim[4];
+    const bool two = scale.s2 != 1.0;
+    Int46 re[4], im[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
-      const double2 z = tile[4 * kq + u][ii];
-      re[u] = crt_limbs(z.x, scale);
-      im[u] = crt_limbs(z.y, scale);
-      nim[u] = Limbs{-im[u].h, -im[u].l1, -im[u].l0};
+      double2 z = tile[4 * kq + u][ii];
+      if (two) {
+        z.x *= scale.s1;
+        z.y *= scale.s1;
+      }
+      re[u] = crt_int46(z.x, two ? scale.s2 : scale.s1);
+      im[u] = crt_int46(z.y, two ? scale.s2 : scale.s1);
     }
     uint32_t* base = Rres + i * (Kp / 4);
     for (int t = 0; t < T; ++t) {
-      const uint32_t wr = pack4(crt_res_byte(re[0], t), crt_res_byte(re[1], t),
-                                crt_res_byte(re[2], t), crt_res_byte(re[3], t));
-      const uint32_t wi = pack4(crt_res_byte(im[0], t), crt_res_byte(im[1], t),
-                                crt_res_byte(im[2], t), crt_res_byte(im[3], t));
-      const uint32_t wn = pack4(crt_res_byte(nim[0], t), crt_res_byte(nim[1], t),
-                                crt_res_byte(nim[2], t), crt_res_byte(nim[3], t));
+      uint32_t br[4], bi[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        br[u] = crt_res_byte64(re[u].a, re[u].lo, t);
+        bi[u] = crt_res_byte64(im[u].a, im[u].lo, t);
+      }
+      const uint32_t wr = pack4(br[0], br[1], br[2], br[3]);
+      const uint32_t wi = pack4(bi[0], bi[1], bi[2], bi[3]);
+      // −Im r': the negated residues (|r| <= 127, so the negation stays an int8)
+      const uint32_t wn = pack4(0u - bi[0], 0u - bi[1], 0u - bi[2], 0u - bi[3]);
       uint32_t* p0 = base + t * tstride;        // plane 0: [Re | −Im]
       uint32_t* p1 = p0 + pstride;              // plane 1: [Im | Re]
       p0[kw] = wr;
@@ -681,7 +644,7 @@ CrtHost make_const(int T) {
 
 int crt_env_T() {
   const char* e = select_env("RID_CRT_MODULI");
-  int T = e ? atoi(e) : 14;
+  int T = e ? atoi(e) : 15;
   if (T < 8) T = 8;
   if (T > kCrtMaxT) T = kCrtMaxT;
   return T;
@@ -699,9 +662,10 @@ CrtPlan crt_plan(int64_t l, int64_t m) {
   CrtPlan p{};
   p.T = crt_env_T();
   const CrtHost h = make_const(p.T);
-  // |Y'| <= 2m 2^2b < M / 2  <=>  2b < log2 M − log2(4m); keep 1/4 bit of margin; limbs cap b at 46
+  // |Y'| <= 2m 2^2b < M / 2  <=>  2b < log2 M − log2(4m); keep 1/4 bit of margin. b <= 50: the
+  // magic-number rint (|a| < 2^51) and the FP64 quotient (crt_res_byte64)
   int b = (int)std::floor((h.log2M - std::log2(4.0 * (double)m) - 0.25) / 2.0);
-  p.b = b > 46 ? 46 : b;
+  p.b = b > 50 ? 50 : b;
   p.mh = (m + 63) / 64 * 64;
   const int64_t K2 = 2 * p.mh;
   const int64_t kmax = (int64_t)(2147483647LL / (127 * 127)) / 128 * 128;  // exact int32 slices
@@ -842,31 +806,58 @@ static CrtBlockWs carve_block(const CrtPlan& p, void* ws, int64_t nb) {
 
 static cudaError_t crt_prep_A(const CrtPlan& p, const CrtBlockWs& w, const double2* A, int64_t lda,
                               int64_t ncols, int64_t m, int num_sms, cudaStream_t st) {
-  if (experiment_env("RID_CRT_PREP_SPLIT")) {  // round-2 first version: two passes over A
-    k_crt_colmax<<<(unsigned)ncols, 256, 0, st>>>(A, lda, m, w.colmax);
-    const int64_t words = (p.Kp / 4 - p.mh / 4) * ncols;
-    const int64_t blocks = std::min<int64_t>((words + 255) / 256, (int64_t)num_sms * 16);
-    k_crt_resA<<<(unsigned)blocks, 256, 0, st>>>(A, lda, m, ncols, p.mh, p.Kp, w.colmax, p.b,
-                                                 (uint32_t*)w.Ares);
-    return cudaGetLastError();
-  }
-  int per_sm = 1;
-  if (const char* v = experiment_env("RID_CRT_PREP_CTAS")) per_sm = std::max(1, std::min(16, atoi(v)));
-  const unsigned grid = (unsigned)std::min<int64_t>(ncols, (int64_t)num_sms * per_sm);
-  // threads per CTA: 1024 alone; fewer when it is to share the SMs with the GEMM (RID_CRT_PIPE)
+  // CTAs per cluster (per column): 1 by default (a plain launch). Clusters of 2-8 CTAs read each
+  // column from DRAM exactly once (CL = 4: 4.30 vs 6.08 GB per C4 block) but are slower: the
+  // kernel is issue-bound, and GPC packing leaves SMs idle (CL = 4: 132 of 148 CTAs resident)
+  int CL = 1;
+  if (const char* v = experiment_env("RID_CRT_PREP_CLUSTER")) CL = std::max(1, std::min(8, atoi(v)));
   int thr = 1024;
   if (const char* v = experiment_env("RID_CRT_PREP_THREADS")) thr = std::max(128, std::min(1024, atoi(v)));
+  const int64_t nclu = std::max<int64_t>(1, std::min<int64_t>(ncols, num_sms / CL));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nclu * CL));
+  cfg.blockDim = dim3((unsigned)thr);
+  cfg.dynamicSmemBytes = 0;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)CL;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  uint32_t* Ares = (uint32_t*)w.Ares;
+  cudaError_t e;
+  {  // persistent over columns: only as many clusters as can be resident at once (GPC packing)
+    static std::mutex mu;
+    static std::map<std::pair<int, int>, int> cache;  // (device, CL * 4096 + threads) -> clusters
+    int dev = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+    std::lock_guard<std::mutex> g(mu);
+    auto key = std::make_pair(dev, CL * 4096 + thr);
+    auto it = cache.find(key);
+    if (it == cache.end()) {
+      int nc = 0;
+      if ((e = cudaOccupancyMaxActiveClusters(&nc, (const void*)k_crt_prepA<14>, &cfg)) != cudaSuccess)
+        return e;
+      it = cache.emplace(key, std::max(1, nc)).first;
+    }
+    const int64_t fit = std::min<int64_t>(nclu, it->second);
+    cfg.gridDim = dim3((unsigned)(fit * CL));
+  }
+  if (CL == 1) cfg.numAttrs = 0;  // a plain launch: each CTA is its own (implicit) cluster
   switch (p.T) {
 #define RID_CRT_PREP(TT)                                                                           \
   case TT:                                                                                         \
-    k_crt_prepA<TT><<<grid, thr, 0, st>>>(A, lda, m, ncols, p.mh, p.Kp, w.colmax, p.b,           \
-                                           (uint32_t*)w.Ares);                                     \
+    e = cudaLaunchKernelEx(&cfg, k_crt_prepA<TT>, A, lda, m, ncols, p.mh, p.Kp, w.colmax, p.b,    \
+                           Ares);                                                                  \
     break;
     RID_CRT_PREP(8) RID_CRT_PREP(9) RID_CRT_PREP(10) RID_CRT_PREP(11) RID_CRT_PREP(12)
     RID_CRT_PREP(13) RID_CRT_PREP(14) RID_CRT_PREP(15) RID_CRT_PREP(16)
 #undef RID_CRT_PREP
     default: return cudaErrorInvalidValue;
   }
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

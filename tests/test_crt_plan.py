@@ -6,7 +6,8 @@ bounds that make every step exact (reading R33).
 - M = prod p_t exceeds 2 max|Y'| = 2 * 2m * 2^(2b) (Y' the integer sketch: 2m terms of
   products of b-bit integers), so the symmetric CRT representative is Y' itself;
 - every K slice accumulates exactly in int32: K'_slice * 127^2 < 2^31;
-- b <= 46: the residue kernel's three fp32 limbs stay exact (|s| < 2^24).
+- b <= 50: the magic-number rint and the FP64 quotient of the residue kernels stay exact
+  (|a| < 2^51); the default T = 15 gives b = 50 (m <= 32768) / 49 (m <= 2^17).
 """
 import math
 
@@ -25,7 +26,7 @@ def rid():
 
 def test_moduli(rid):
     p = rid.crt_moduli()
-    assert len(p) >= 14 and len(set(p)) == len(p)
+    assert len(p) >= 15 and len(set(p)) == len(p)
     for i, a in enumerate(p):
         assert a % 2 == 1 and 128 < a <= 253
         for b in p[i + 1:]:
@@ -47,7 +48,9 @@ def test_plan_bounds(rid, l, m):
     assert 2 * (2 * m) * 2 ** (2 * b) < M
     # int32-exact K slices
     assert (Kp // ks) * 127 * 127 < 2**31
-    assert 40 <= b <= 46
+    assert 40 <= b <= 50
+    if m <= 32768:
+        assert b == 50  # T = 15 moduli: more operand bits than an fp64 GEMM's accumulated error
     # tile rows: multiples of 16, at most 256 (the Re and Im accumulators share 512 TMEM columns)
     l16 = (l + 15) // 16 * 16
     assert nc % 16 == 0 and 16 <= nc <= 256 and nc * math.ceil(l16 / nc) >= l

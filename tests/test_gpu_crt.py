@@ -51,7 +51,7 @@ def relf(a, b):
     return np.linalg.norm(a - b) / np.linalg.norm(b)
 
 
-TOL_Y = 2e-13  # 2^-45 relative to a column maximum ~ 3e-14 per operand, times the max/rms ratio
+TOL_Y = 2e-13  # north-star bar 1e-12; the CRT's own error is ~3e-15 (b = 49-50), the oracle's ~1e-14
 
 SKETCH_CASES = [  # (seed, m, n, k, noise, l): the shapes the plan's tiling must cover
     (1, 1024, 512, 16, 0.0, 24),     # C1: l < 32 (one 32-row tile, 8 padding rows)
@@ -75,6 +75,46 @@ def test_crt_sketch_parity(rid, orc, ctx, seed, m, n, k, noise, l):
     # column by column as well (each column has its own scale)
     colerr = np.linalg.norm(Y_g - Y_o, axis=0) / np.linalg.norm(Y_o, axis=0)
     assert colerr.max() <= 4 * TOL_Y
+
+
+def _exact_sketch(R, A):
+    """Y = R A exactly (Python integers: every double is an integer multiple of 2^-1074), rounded
+    once to complex128."""
+    from fractions import Fraction
+
+    def ints(x):
+        return [int(Fraction(float(v)) * (1 << 1074)) for v in x]
+
+    l, n = R.shape[0], A.shape[1]
+    Rr = [ints(R[i].real) for i in range(l)]
+    Ri = [ints(R[i].imag) for i in range(l)]
+    Ar = [ints(A[:, j].real) for j in range(n)]
+    Ai = [ints(A[:, j].imag) for j in range(n)]
+    Y = np.zeros((l, n), np.complex128)
+    sc = Fraction(1, 1 << 2148)
+    for i in range(l):
+        for j in range(n):
+            re = sum(a * b for a, b in zip(Rr[i], Ar[j])) - sum(a * b for a, b in zip(Ri[i], Ai[j]))
+            im = sum(a * b for a, b in zip(Rr[i], Ai[j])) + sum(a * b for a, b in zip(Ri[i], Ar[j]))
+            Y[i, j] = complex(float(Fraction(re) * sc), float(Fraction(im) * sc))
+    return Y
+
+
+def test_crt_more_accurate_than_fp64(rid, orc, ctx, monkeypatch):
+    """Against the EXACT product (big-integer arithmetic), the INT8_CRT sketch (b = 50-bit operands,
+    exact accumulation, one final rounding) is more accurate than the fp64 ordered fused chain the
+    oracle and the DMMA 4-product kernel compute (accumulated rounding ~u sqrt(m / 2))."""
+    m, n, l, seed = 16384, 4, 8, 11
+    assert rid.crt_plan(l, m)["b"] == 50
+    A_o = orc.generate(seed, m, n, 3, 1e-9)
+    R = orc.normal_matrix(seed, 4, l, m)  # the sketch matrix (stream 4, reading R4/R5)
+    Y_ex = _exact_sketch(R, A_o)
+    A_g = torch.from_numpy(np.asfortranarray(A_o)).cuda()
+    Y_crt = np_(rid.sketch(A_g, seed, l, ctx=ctx))
+    Y_orc = orc.sketch(A_o, seed, l)
+    e_crt, e_orc = relf(Y_crt, Y_ex), relf(Y_orc, Y_ex)
+    assert e_crt <= 1e-14, e_crt
+    assert e_crt < e_orc, (e_crt, e_orc)
 
 
 def test_crt_two_k_slices(rid, orc, ctx):

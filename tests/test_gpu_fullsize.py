@@ -72,10 +72,11 @@ def test_fullsize_against_oracle_golden(rid, orc, name):
     Y = rid.sketch(A, seed, c.l)
     S = rid.sketch_splits(c.m, c.l, c.n)
     # per-column bar: DMMA (3M / Strassen / K slices) to rounding, 1e-13; the INT8_CRT engine
-    # (R33) rounds each operand to b bits of its row / column maximum: ~3.6 2^-b, bar 8 2^-b
+    # (R33) rounds each operand to b bits of its row / column maximum (~3.6 2^-b, 3e-15 at b = 50):
+    # there the oracle's own fp64 accumulation error (~1e-14) dominates, so the same 1e-13
     tol = 1e-13
     if rid.sketch_engine(c.m, c.l, c.n) == "int8_crt":
-        tol = 8.0 * 2.0 ** -rid.crt_plan(c.l, c.m)["b"]
+        tol = max(tol, 8.0 * 2.0 ** -rid.crt_plan(c.l, c.m)["b"])
     for j in cols:
         y_o = unhex(g["Y_cols"][str(j)])
         y_g = Y[:, j].cpu().numpy()
