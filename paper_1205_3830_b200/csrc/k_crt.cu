@@ -354,6 +354,19 @@ __device__ __forceinline__ void umma_i8(uint32_t d_tmem, uint64_t adesc, uint64_
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// the same with A from tensor memory (kind::i8 .. [d], [a], b_desc): A staged by tcgen05.cp
+__device__ __forceinline__ void umma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 128 rows x 32 bytes of a K-major shared-memory operand into tensor memory (8 columns)
+__device__ __forceinline__ void tmem_cp_128x256b(uint32_t taddr, uint64_t sdesc) {
+  asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;\n" ::"r"(taddr), "l"(sdesc) : "memory");
+}
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                    smem_u32(bar))
@@ -370,7 +383,11 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
-template <int KB>
+// TS: the A tile of each K step is copied once into tensor memory (tcgen05.cp) and both products
+// (Re, Im) read it from there instead of from shared memory: the shared-memory operand traffic per
+// K step drops from 2 A + 2 B tiles to 1 A + 2 B (nc <= 192: Re accumulator at TMEM column 0, Im
+// at 192, A slots at 384 + 8 (stage 4 / KB·32 + k step))
+template <int KB, bool TS>
 __global__ void __launch_bounds__(kImmaThreads, 1)
     k_imma(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
            const ImmaArgs a) {
@@ -449,8 +466,15 @@ __global__ void __launch_bounds__(kImmaThreads, 1)
             const uint64_t dr = umma_desc_sw<KB>(sa + aBytes + 32 * kk);
             const uint64_t di = umma_desc_sw<KB>(sa + aBytes + bBytes + 32 * kk);
             const uint32_t acc = (kb | kk) != 0;
-            umma_i8(tmem, da, dr, a.idesc, acc);
-            umma_i8(tmem + 256, da, di, a.idesc, acc);
+            if (TS) {
+              const uint32_t ta = tmem + 384 + 8 * (stage * (KB / 32) + kk);
+              tmem_cp_128x256b(ta, da);
+              umma_i8_ts(tmem, ta, dr, a.idesc, acc);
+              umma_i8_ts(tmem + 192, ta, di, a.idesc, acc);
+            } else {
+              umma_i8(tmem, da, dr, a.idesc, acc);
+              umma_i8(tmem + 256, da, di, a.idesc, acc);
+            }
           }
           umma_commit(&empty[stage]);  // frees the stage when these MMAs have read it
           if (++stage == S) {
@@ -481,7 +505,7 @@ __global__ void __launch_bounds__(kImmaThreads, 1)
         uint8_t* dst = a.out + ((((int64_t)ks * a.T + t) * 2 + ri) * a.n + j) * a.lp + (int64_t)ch * nc;
         for (int c0 = 0; c0 < nc; c0 += 16) {
           uint32_t v[16];
-          tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + ri * 256 + c0, v);
+          tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + ri * (TS ? 192 : 256) + c0, v);
           uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
@@ -732,7 +756,17 @@ int crt_kb() {
   return e && atoi(e) == 64 ? 64 : 128;
 }
 
-template <int KB>
+// A from tensor memory (k_imma<128, true>) when the row tile allows it (nc <= 192); RID_CRT_TS=0
+// keeps both operands in shared memory
+// (measured slower: C4 sketch 36.7 vs 34.4 ms, C5 117.8 vs 110.1 — the tensor-memory copy costs
+// more than the shared-memory reads it saves; RID_CRT_TS=1 selects it, bitwise the same Y)
+bool crt_ts(const CrtPlan& p) {
+  if (p.nc > 192) return false;
+  const char* e = select_env("RID_CRT_TS");
+  return e && atoi(e) != 0;
+}
+
+template <int KB, bool TS>
 cudaError_t launch_imma(const CrtPlan& p, const uint8_t* Rres, uint8_t* Ares, uint8_t* out,
                         int64_t ncols, int num_sms, cudaStream_t st) {
   cudaError_t e;
@@ -779,12 +813,13 @@ cudaError_t launch_imma(const CrtPlan& p, const uint8_t* Rres, uint8_t* Ares, ui
   int S = kImmaStagesMax;
   if (const char* v = experiment_env("RID_CRT_STAGES")) S = std::max(2, std::min(kImmaStagesMax, atoi(v)));
   while (S > 2 && (size_t)S * stageBytes + 1024 + 1024 > (size_t)optin) --S;
+  if (TS) S = std::min(S, 512 / KB);  // the A slots: 128 TMEM columns
   ia.stages = S;
   const size_t smem = (size_t)S * stageBytes + 1024;
-  if ((e = ensure_dyn_smem((const void*)k_imma<KB>, smem)) != cudaSuccess) return e;
+  if ((e = ensure_dyn_smem((const void*)k_imma<KB, TS>, smem)) != cudaSuccess) return e;
   const int nitems = p.T * p.kslices * ia.coltiles * p.chunks;
   const int grid = std::min(nitems, num_sms);
-  k_imma<KB><<<grid, kImmaThreads, smem, st>>>(mapA, mapB, ia);
+  k_imma<KB, TS><<<grid, kImmaThreads, smem, st>>>(mapA, mapB, ia);
   return cudaGetLastError();
 }
 }  // namespace
@@ -880,11 +915,19 @@ static cudaError_t crt_rec(const CrtPlan& p, const CrtBlockWs& w, const unsigned
   return cudaGetLastError();
 }
 
-int64_t crt_block_cols(const CrtPlan& p, int64_t ncols, int64_t budget_bytes) {
-  // as few blocks as the budget allows, the 128-column tiles spread evenly over them (the GEMM's
-  // last wave is then equally full in every block)
+int64_t crt_block_cols(const CrtPlan& p, int64_t ncols, int64_t budget_bytes, int num_sms) {
   const int64_t tiles = (ncols + 127) / 128;
   const int64_t maxt = std::max<int64_t>(1, budget_bytes / (int64_t)crt_A_bytes(p, 128));
+  if (tiles <= maxt) return tiles * 128;
+  // blocks whose GEMM work items (ipc per column tile) fill whole waves of num_sms CTAs, when
+  // such a block fits the budget (C4: 148 tiles = 45 waves; C5: 37 tiles = 15 waves), the rest of
+  // the columns in a last block
+  const int64_t ipc = (int64_t)p.T * p.kslices * p.chunks;
+  int64_t g = ipc, h = num_sms > 0 ? num_sms : 1;
+  while (h) { const int64_t r = g % h; g = h; h = r; }
+  const int64_t unit = (num_sms > 0 ? num_sms : 1) / g;
+  if (unit <= maxt) return maxt / unit * unit * 128;
+  // otherwise as few blocks as the budget allows, the tiles spread evenly over them
   const int64_t nblk = (tiles + maxt - 1) / maxt;
   return (tiles + nblk - 1) / nblk * 128;
 }
@@ -909,8 +952,10 @@ cudaError_t crt_sketch(const CrtPlan& p, const void* wsR, const double2* A, int6
     cudaError_t r;
     const bool timed = tim && 2 * gi + 1 < tim->nev;
     if (timed && (r = rec(tim->ev[2 * gi])) != cudaSuccess) return r;
-    r = KB == 128 ? launch_imma<128>(p, Rres, w.Ares, w.out, nc, num_sms, st)
-                  : launch_imma<64>(p, Rres, w.Ares, w.out, nc, num_sms, st);
+    const bool ts = crt_ts(p);
+    r = KB == 128 ? (ts ? launch_imma<128, true>(p, Rres, w.Ares, w.out, nc, num_sms, st)
+                        : launch_imma<128, false>(p, Rres, w.Ares, w.out, nc, num_sms, st))
+                  : launch_imma<64, false>(p, Rres, w.Ares, w.out, nc, num_sms, st);
     if (r == cudaSuccess && timed) r = rec(tim->ev[2 * gi + 1]);
     ++gi;
     if (tim) tim->used = std::min(gi, tim->nev / 2);

@@ -334,7 +334,7 @@ rid_status solve_T(rid_ctx* c, const double2* Rinv, int64_t k, const double2* Y,
     void *pr, *pa;
     RID_TRY(ws_get(c, "Rcrt_solve", rid::crt_R_bytes(cp), &pr));
     RID_CUDA(c, rid::crt_prep_R(cp, Rinv, k, k, k, pr, c->stream, launches));
-    const int64_t nb = rid::crt_block_cols(cp, n_loc, (int64_t)2 << 30);
+    const int64_t nb = rid::crt_block_cols(cp, n_loc, (int64_t)2 << 30, c->num_sms);
     RID_TRY(ws_get(c, "Acrt_solve", rid::crt_A_bytes(cp, nb), &pa));
     void* pw[2] = {pa, nullptr};
     RID_CUDA(c, rid::crt_sketch(cp, pr, Y, ldy, P, ldp, k, n_loc, k, pw, nb, c->num_sms, c->stream,
@@ -554,7 +554,8 @@ rid_status sketch_block(rid_ctx* c, const SketchR& sr, const double2* A, int64_t
     // from 6.0 to 8.4 ms per block): an experiment
     const char* pv = rid::experiment_env("RID_CRT_PIPE");
     const bool piped = pv && atoi(pv) != 0;
-    const int64_t nb = rid::crt_block_cols(sr.cp, ncols, (int64_t)8 << 30);
+    // column blocks of at most 20 GiB of residues (C4: 148 + 108 column tiles; C5: 37-tile blocks)
+    const int64_t nb = rid::crt_block_cols(sr.cp, ncols, (int64_t)20 << 30, c->num_sms);
     void* pw[2] = {nullptr, nullptr};
     RID_TRY(ws_get(c, "Acrt0", rid::crt_A_bytes(sr.cp, nb), &pw[0]));
     if (piped) {

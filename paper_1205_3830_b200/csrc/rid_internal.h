@@ -286,7 +286,7 @@ struct CrtTiming {
   mutable int used;
 };
 // columns per block for a workspace budget (bytes per block buffer)
-int64_t crt_block_cols(const CrtPlan& p, int64_t ncols, int64_t budget_bytes);
+int64_t crt_block_cols(const CrtPlan& p, int64_t ncols, int64_t budget_bytes, int num_sms);
 // Y (l x ncols) = R A: column blocks of <= nb columns, ws[0], ws[1] of crt_A_bytes(p, nb) each
 // (ws[1] unused when pipe == nullptr: one stream, one buffer)
 cudaError_t crt_sketch(const CrtPlan& p, const void* wsR, const double2* A, int64_t lda, double2* Y,
