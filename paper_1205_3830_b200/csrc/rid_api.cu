@@ -554,8 +554,18 @@ rid_status sketch_block(rid_ctx* c, const SketchR& sr, const double2* A, int64_t
     // from 6.0 to 8.4 ms per block): an experiment
     const char* pv = rid::experiment_env("RID_CRT_PIPE");
     const bool piped = pv && atoi(pv) != 0;
-    // column blocks of at most 20 GiB of residues (C4: 148 + 108 column tiles; C5: 37-tile blocks)
-    const int64_t nb = rid::crt_block_cols(sr.cp, ncols, (int64_t)20 << 30, c->num_sms);
+    // column blocks of at most 20 GiB of residues (C4: 148 + 108 column tiles; C5: 37-tile
+    // blocks), and at most half of the memory free beside the workspace already held
+    int64_t budget = (int64_t)20 << 30;
+    {
+      size_t fr = 0, tot = 0;
+      if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
+        const auto it = c->ws.find("Acrt0");
+        const int64_t held = it != c->ws.end() ? (int64_t)it->second.bytes : 0;
+        budget = std::min(budget, std::max<int64_t>((int64_t)1 << 30, ((int64_t)fr + held) / 2));
+      }
+    }
+    const int64_t nb = rid::crt_block_cols(sr.cp, ncols, budget, c->num_sms);
     void* pw[2] = {nullptr, nullptr};
     RID_TRY(ws_get(c, "Acrt0", rid::crt_A_bytes(sr.cp, nb), &pw[0]));
     if (piped) {

@@ -10,7 +10,7 @@ mkdir -p gpurun_out
 $CMD > gpurun_out/prof_plain.log 2>&1 || { echo "plain run failed"; exit 1; }
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_$CFG.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 if [ "${ENGINE:-crt}" = "crt" ]; then
-  NB=${NB:-4}  # GEMM launches (column blocks) per sketch: skip the warm-up step's
+  NB=${NB:-2}  # GEMM launches (column blocks) per sketch at C4 (148 + 108 tiles): skip the warm-up step's
   ncu --set full --clock-control none --import-source on -k regex:k_imma -s $NB -c 1 -o gpurun_out/prof_crt_gemm_$CFG -f $CMD > gpurun_out/ncu_gemm.log 2>&1
   ncu --set full --clock-control none --import-source on -k regex:k_crt_prepA -s $NB -c 1 -o gpurun_out/prof_crt_prep_$CFG -f $CMD > gpurun_out/ncu_prep.log 2>&1
   ncu --set full --clock-control none --import-source on -k regex:k_crt_rec -s $NB -c 1 -o gpurun_out/prof_crt_rec_$CFG -f $CMD > gpurun_out/ncu_rec.log 2>&1
