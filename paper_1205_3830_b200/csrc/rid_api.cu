@@ -72,6 +72,7 @@ struct rid_ctx {
   // current enqueue is being captured into a graph (events are then recorded as external)
   cudaEvent_t crt_tev[64] = {};
   int crt_timed = 0;    // GEMM launches timed by the last CRT sketch
+  int64_t crt_budget = (int64_t)20 << 30;  // workspace budget of the CRT column blocks
   int g_crt_timed = 0;  // ... by the captured graph's
   bool capturing = false;
   int qr_kind = 0;      // RID_QR_HOUSEHOLDER (default) or RID_QR_CGS2
@@ -556,14 +557,17 @@ rid_status sketch_block(rid_ctx* c, const SketchR& sr, const double2* A, int64_t
     const bool piped = pv && atoi(pv) != 0;
     // column blocks of at most 20 GiB of residues (C4: 148 + 108 column tiles; C5: 37-tile
     // blocks), and at most half of the memory free beside the workspace already held
-    int64_t budget = (int64_t)20 << 30;
-    {
+    // (queried outside graph capture only; a capture reuses the last eager call's budget)
+    int64_t budget = c->crt_budget;
+    if (!c->capturing) {
+      budget = (int64_t)20 << 30;
       size_t fr = 0, tot = 0;
       if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) {
         const auto it = c->ws.find("Acrt0");
         const int64_t held = it != c->ws.end() ? (int64_t)it->second.bytes : 0;
         budget = std::min(budget, std::max<int64_t>((int64_t)1 << 30, ((int64_t)fr + held) / 2));
       }
+      c->crt_budget = budget;
     }
     const int64_t nb = rid::crt_block_cols(sr.cp, ncols, budget, c->num_sms);
     void* pw[2] = {nullptr, nullptr};
