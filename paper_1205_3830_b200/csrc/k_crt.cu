@@ -317,11 +317,13 @@ __global__ void __launch_bounds__(256) k_crt_resR(const double2* __restrict__ R,
 constexpr int kImmaStagesMax = 8;
 constexpr int kImmaThreads = 192;
 
+constexpr int kCrtMaxChunks = 8;  // l <= 2048 rows in tiles of <= 256
 struct ImmaArgs {
-  int T, kslices, kbps, coltiles, chunks, nc, lp, stages;
+  int T, kslices, kbps, coltiles, chunks, nc, lp, stages;  // nc: the largest row tile (the box)
+  int cn[kCrtMaxChunks], coff[kCrtMaxChunks];              // rows and first row of tile c
+  uint32_t cidesc[kCrtMaxChunks];                          // its instruction descriptor
   int64_t n;                // valid A columns
   uint8_t* out;             // [kslices][T][2][n][lp] residues in [0, p)
-  uint32_t idesc;
 };
 
 __device__ __forceinline__ void tc_fence_before() {
@@ -439,8 +441,8 @@ __global__ void __launch_bounds__(kImmaThreads, 1)
           mbar_expect_tx(&full[stage], stageBytes);
           const int kx = (ks * a.kbps + kb) * KB;
           tma_box3(st, &mapA, kx, ct * 128, t, &full[stage]);
-          tma_box3(st + aBytes, &mapB, kx, ch * nc, 2 * t, &full[stage]);
-          tma_box3(st + aBytes + bBytes, &mapB, kx, ch * nc, 2 * t + 1, &full[stage]);
+          tma_box3(st + aBytes, &mapB, kx, a.coff[ch], 2 * t, &full[stage]);
+          tma_box3(st + aBytes + bBytes, &mapB, kx, a.coff[ch], 2 * t + 1, &full[stage]);
           if (++stage == S) {
             stage = 0;
             phase ^= 1;
@@ -454,6 +456,7 @@ __global__ void __launch_bounds__(kImmaThreads, 1)
       int stage = 0;
       uint32_t phase = 0, iter = 0;
       for (int it = blockIdx.x; it < nitems; it += gridDim.x, ++iter) {
+        const uint32_t idesc = a.cidesc[it % a.chunks];
         mbar_wait(&tempty, (iter & 1) ^ 1);  // the epilogue has drained the accumulators
         tc_fence_after();
         for (int kb = 0; kb < a.kbps; ++kb) {
@@ -469,11 +472,11 @@ __global__ void __launch_bounds__(kImmaThreads, 1)
             if (TS) {
               const uint32_t ta = tmem + 384 + 8 * (stage * (KB / 32) + kk);
               tmem_cp_128x256b(ta, da);
-              umma_i8_ts(tmem, ta, dr, a.idesc, acc);
-              umma_i8_ts(tmem + 192, ta, di, a.idesc, acc);
+              umma_i8_ts(tmem, ta, dr, idesc, acc);
+              umma_i8_ts(tmem + 192, ta, di, idesc, acc);
             } else {
-              umma_i8(tmem, da, dr, a.idesc, acc);
-              umma_i8(tmem + 256, da, di, a.idesc, acc);
+              umma_i8(tmem, da, dr, idesc, acc);
+              umma_i8(tmem + 256, da, di, idesc, acc);
             }
           }
           umma_commit(&empty[stage]);  // frees the stage when these MMAs have read it
@@ -502,8 +505,8 @@ __global__ void __launch_bounds__(kImmaThreads, 1)
       const int p = c_crt.p[t];
       const double invp = c_crt.invpd[t];
       for (int ri = 0; ri < 2; ++ri) {
-        uint8_t* dst = a.out + ((((int64_t)ks * a.T + t) * 2 + ri) * a.n + j) * a.lp + (int64_t)ch * nc;
-        for (int c0 = 0; c0 < nc; c0 += 16) {
+        uint8_t* dst = a.out + ((((int64_t)ks * a.T + t) * 2 + ri) * a.n + j) * a.lp + a.coff[ch];
+        for (int c0 = 0; c0 < a.cn[ch]; c0 += 16) {
           uint32_t v[16];
           tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + ri * (TS ? 192 : 256) + c0, v);
           uint32_t w[4] = {0, 0, 0, 0};
@@ -526,6 +529,202 @@ __global__ void __launch_bounds__(kImmaThreads, 1)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ the CTA-pair GEMM --------
+// k_imma2: the same products with tcgen05.mma.cta_group::2 — a cluster of two CTAs (one TPC)
+// computes a 256-column tile of A against nc rows of R: each CTA holds its own 128 A columns and
+// HALF of the R rows (nc / 2 of each plane) in shared memory, the leader (rank 0) issues M = 256
+// MMAs that read both CTAs' tiles and write each CTA's own TMEM accumulators, so each SM reads
+// only half of the B tile per MMA. Both CTAs' TMA boxes complete on the leader's "full" barrier
+// (cp.async.bulk.tensor.cta_group::2); the leader's commits are multicast to both CTAs' "empty"
+// and "tfull" barriers; both CTAs' epilogues arrive on the leader's "tempty" barrier.
+// N = nc must be a multiple of 32 (crt_plan rounds it when the pair kernel is selected).
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+// the shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa_u32(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_barrier() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::
+                   : "memory");
+}
+__device__ __forceinline__ void tma_box3_2sm(void* dst, const CUtensorMap* map, int x, int y, int z,
+                                             uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];\n" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(z), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void umma_i8_2sm(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// arrive once on the barrier at this shared-memory offset in both CTAs of the pair
+__device__ __forceinline__ void umma_commit_2sm(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}\n" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar_cluster)
+               : "memory");
+}
+
+__global__ void __launch_bounds__(kImmaThreads, 1)
+    k_imma2(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+            const ImmaArgs a) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  __shared__ __align__(8) uint64_t full[kImmaStagesMax], empty[kImmaStagesMax], tfull, tempty;
+  __shared__ uint32_t tmem_slot;
+  unsigned char* sm = smraw + ((1024 - (smem_u32(smraw) & 1023)) & 1023);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rk = cluster_rank();
+  const bool leader = rk == 0;
+  const int S = a.stages, nc = a.nc, nh = nc / 2;
+  const uint32_t aBytes = 128 * 128, bBytes = (uint32_t)nh * 128;
+  const uint32_t stageBytes = aBytes + 2 * bBytes;
+  const int coltiles2 = (a.coltiles + 1) / 2;  // 256-column tiles
+  const int nitems = a.T * a.kslices * coltiles2 * a.chunks;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(&tfull, 1);
+    mbar_init(&tempty, 256);  // both CTAs' epilogue threads
+    mbar_init_fence();
+    tma_prefetch_map(&mapA);
+    tma_prefetch_map(&mapB);
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;\n" ::"r"(
+                     smem_u32(&tmem_slot))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_barrier();  // both CTAs' barriers initialised and TMEM allocated
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---------------- TMA producer (both CTAs)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int it = pair; it < nitems; it += npairs) {
+        int r = it;
+        const int ch = r % a.chunks; r /= a.chunks;
+        const int ct2 = r % coltiles2; r /= coltiles2;
+        const int ks = r % a.kslices; r /= a.kslices;
+        const int t = r;
+        for (int kb = 0; kb < a.kbps; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          unsigned char* st = sm + (size_t)stage * stageBytes;
+          const uint32_t fb = mapa_u32(smem_u32(&full[stage]), 0);
+          if (leader) mbar_expect_tx(&full[stage], 2 * stageBytes);
+          const int kx = (ks * a.kbps + kb) * 128;
+          tma_box3_2sm(st, &mapA, kx, ct2 * 256 + (int)rk * 128, t, fb);
+          const int rb = a.coff[ch] + (int)rk * (a.cn[ch] / 2);  // this CTA's half of the tile
+          tma_box3_2sm(st + aBytes, &mapB, kx, rb, 2 * t, fb);
+          tma_box3_2sm(st + aBytes + bBytes, &mapB, kx, rb, 2 * t + 1, fb);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {  // ---------------- MMA issuer (the pair's leader)
+      int stage = 0;
+      uint32_t phase = 0, iter = 0;
+      for (int it = pair; it < nitems; it += npairs, ++iter) {
+        const uint32_t idesc = a.cidesc[it % a.chunks];
+        mbar_wait(&tempty, (iter & 1) ^ 1);
+        tc_fence_after();
+        for (int kb = 0; kb < a.kbps; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(sm + (size_t)stage * stageBytes);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {
+            const uint64_t da = umma_desc_sw<128>(sa + 32 * kk);
+            const uint64_t dr = umma_desc_sw<128>(sa + aBytes + 32 * kk);
+            const uint64_t di = umma_desc_sw<128>(sa + aBytes + bBytes + 32 * kk);
+            const uint32_t acc = (kb | kk) != 0;
+            umma_i8_2sm(tmem, da, dr, idesc, acc);
+            umma_i8_2sm(tmem + 256, da, di, idesc, acc);
+          }
+          umma_commit_2sm(&empty[stage]);
+          if (++stage == S) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit_2sm(&tfull);
+      }
+    }
+    __syncwarp();
+  } else {  // ---------------- epilogue (both CTAs): warps 2..5 -> TMEM lanes 32 (warp % 4) ...
+    const int q = warp & 3;
+    const int row = 32 * q + lane;
+    const uint32_t te = mapa_u32(smem_u32(&tempty), 0);
+    uint32_t iter = 0;
+    for (int it = pair; it < nitems; it += npairs, ++iter) {
+      int r = it;
+      const int ch = r % a.chunks; r /= a.chunks;
+      const int ct2 = r % coltiles2; r /= coltiles2;
+      const int ks = r % a.kslices; r /= a.kslices;
+      const int t = r;
+      mbar_wait(&tfull, iter & 1);
+      tc_fence_after();
+      const int64_t j = (int64_t)ct2 * 256 + rk * 128 + row;
+      const int p = c_crt.p[t];
+      const double invp = c_crt.invpd[t];
+      for (int ri = 0; ri < 2; ++ri) {
+        uint8_t* dst = a.out + ((((int64_t)ks * a.T + t) * 2 + ri) * a.n + j) * a.lp + a.coff[ch];
+        for (int c0 = 0; c0 < a.cn[ch]; c0 += 16) {
+          uint32_t v[16];
+          tmem_ld16(tmem + ((uint32_t)(32 * q) << 16) + ri * 256 + c0, v);
+          uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int x = (int)v[e];
+            int rr = x - p * (int)floor((double)x * invp);
+            rr += rr < 0 ? p : 0;
+            rr -= rr >= p ? p : 0;
+            w[e >> 2] |= (uint32_t)rr << (8 * (e & 3));
+          }
+          if (j < a.n) *reinterpret_cast<uint4*>(dst + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive_cluster(te);
+    }
+  }
+  tc_fence_before();
+  cluster_barrier();  // no CTA leaves while its peer may still signal its barriers
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;\n" ::"r"(tmem) : "memory");
   }
 }
 
@@ -666,6 +865,15 @@ CrtHost make_const(int T) {
   return h;
 }
 
+// the CTA-pair GEMM (k_imma2, cta_group::2): RID_CRT_2SM=1. Measured on one box: ~6% more int8
+// ops per second than k_imma, but N must be a multiple of 32, so its row tiles pad more: C4
+// 34.68 vs 34.91 ms (192 + 192 + 160 rows against 3 x 176), C3 5.37 vs 5.29, C5 116.4 vs 110.7
+// (160 + 128 against 144 + 128). A tested selection, not the default.
+bool crt_pair_selected() {
+  const char* e = select_env("RID_CRT_2SM");
+  return e && atoi(e) != 0;
+}
+
 int crt_env_T() {
   const char* e = select_env("RID_CRT_MODULI");
   int T = e ? atoi(e) : 15;
@@ -696,10 +904,23 @@ CrtPlan crt_plan(int64_t l, int64_t m) {
   p.kslices = (int)((K2 + kmax - 1) / kmax);
   p.kbps = (int)(((K2 + 127) / 128 + p.kslices - 1) / p.kslices);
   p.Kp = (int64_t)p.kslices * p.kbps * 128;
-  const int64_t l16 = (l + 15) / 16 * 16;
-  p.chunks = (int)((l16 + 255) / 256);
-  p.nc = (int)(((l16 / 16 + p.chunks - 1) / p.chunks) * 16);
-  p.lp = p.chunks * p.nc;
+  // row tiles: l rounded to the MMA's N granule (16; 32 for the CTA pair), split into
+  // ceil(rows / 256) tiles whose sizes differ by at most one granule (C4: 3 x 176, pair 192 + 192
+  // + 160; C5: 144 + 128)
+  p.pair = crt_pair_selected();
+  const int64_t gran = p.pair ? 32 : 16;
+  const int64_t units = (l + gran - 1) / gran;
+  p.chunks = (int)((units * gran + 255) / 256);
+  p.nc = 0;
+  int64_t off = 0;
+  for (int c = 0; c < p.chunks; ++c) {
+    const int64_t u = units / p.chunks + (c < units % p.chunks ? 1 : 0);
+    p.cn[c] = (int)(u * gran);
+    p.coff[c] = (int)off;
+    off += u * gran;
+    p.nc = std::max(p.nc, p.cn[c]);
+  }
+  p.lp = off;
   return p;
 }
 
@@ -805,8 +1026,14 @@ cudaError_t launch_imma(const CrtPlan& p, const uint8_t* Rres, uint8_t* Ares, ui
   ia.n = ncols;
   ia.out = out;
   // kind::i8: D s32 (bits 4-5 = 2), A and B signed (bits 7-9, 10-12 = 1), both K-major,
-  // N >> 3 at bits 17-22, M >> 4 at bits 24-28
-  ia.idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.nc >> 3) << 17) | ((128u >> 4) << 24);
+  // N >> 3 at bits 17-22, M >> 4 at bits 24-28; one descriptor per row tile (its own N)
+  constexpr uint32_t MDIM = 128u >> 4;
+  for (int c = 0; c < p.chunks; ++c) {
+    ia.cn[c] = p.cn[c];
+    ia.coff[c] = p.coff[c];
+    ia.cidesc[c] = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.cn[c] >> 3) << 17) | (MDIM << 24);
+  }
+
   const uint32_t stageBytes = 128 * KB + 2 * (uint32_t)p.nc * KB;
   int optin = 0;
   if ((e = optin_smem(&optin)) != cudaSuccess) return e;
@@ -823,6 +1050,78 @@ cudaError_t launch_imma(const CrtPlan& p, const uint8_t* Rres, uint8_t* Ares, ui
   return cudaGetLastError();
 }
 }  // namespace
+
+cudaError_t launch_imma2(const CrtPlan& p, const uint8_t* Rres, uint8_t* Ares, uint8_t* out,
+                         int64_t ncols, int num_sms, cudaStream_t st) {
+  cudaError_t e;
+  PFN_cuTensorMapEncodeTiled encode;
+  if ((e = tensor_map_encoder(&encode)) != cudaSuccess) return e;
+  CUtensorMap mapA, mapB;
+  {
+    cuuint64_t gdim[3] = {(cuuint64_t)p.Kp, (cuuint64_t)ncols, (cuuint64_t)p.T};
+    cuuint64_t gstr[2] = {(cuuint64_t)p.Kp, (cuuint64_t)p.Kp * ncols};
+    cuuint32_t box[3] = {128, 128, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (encode(&mapA, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)Ares, gdim, gstr, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  {
+    cuuint64_t gdim[3] = {(cuuint64_t)p.Kp, (cuuint64_t)p.lp, (cuuint64_t)(2 * p.T)};
+    cuuint64_t gstr[2] = {(cuuint64_t)p.Kp, (cuuint64_t)p.Kp * p.lp};
+    cuuint32_t box[3] = {128, (cuuint32_t)(p.nc / 2), 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    if (encode(&mapB, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)Rres, gdim, gstr, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  ImmaArgs ia{};
+  ia.T = p.T;
+  ia.kslices = p.kslices;
+  ia.kbps = p.kbps;
+  ia.coltiles = (int)((ncols + 127) / 128);
+  ia.chunks = p.chunks;
+  ia.nc = p.nc;
+  ia.lp = (int)p.lp;
+  ia.n = ncols;
+  ia.out = out;
+  // kind::i8, M = 256 (the pair), N = the row tile's
+  constexpr uint32_t MDIM = 256u >> 4;
+  for (int c = 0; c < p.chunks; ++c) {
+    ia.cn[c] = p.cn[c];
+    ia.coff[c] = p.coff[c];
+    ia.cidesc[c] = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.cn[c] >> 3) << 17) | (MDIM << 24);
+  }
+
+  const uint32_t stageBytes = 128 * 128 + 2 * (uint32_t)(p.nc / 2) * 128;
+  int optin = 0;
+  if ((e = optin_smem(&optin)) != cudaSuccess) return e;
+  int S = kImmaStagesMax;
+  while (S > 2 && (size_t)S * stageBytes + 1024 + 1024 > (size_t)optin) --S;
+  ia.stages = S;
+  const size_t smem = (size_t)S * stageBytes + 1024;
+  if ((e = ensure_dyn_smem((const void*)k_imma2, smem)) != cudaSuccess) return e;
+  const int nitems = p.T * p.kslices * ((ia.coltiles + 1) / 2) * p.chunks;
+  cudaLaunchConfig_t cfg = {};
+  cfg.blockDim = dim3(kImmaThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cfg.gridDim = dim3((unsigned)(2 * std::min(nitems, num_sms / 2)));
+  int ncl = 0;
+  if ((e = cudaOccupancyMaxActiveClusters(&ncl, (const void*)k_imma2, &cfg)) != cudaSuccess) return e;
+  cfg.gridDim = dim3((unsigned)(2 * std::max(1, std::min(std::min(nitems, num_sms / 2), ncl))));
+  if ((e = cudaLaunchKernelEx(&cfg, k_imma2, mapA, mapB, ia)) != cudaSuccess) return e;
+  return cudaGetLastError();
+}
 
 // workspace of one column block (ncols <= nb): A residues, GEMM residues out, colmax
 struct CrtBlockWs {
@@ -953,7 +1252,8 @@ cudaError_t crt_sketch(const CrtPlan& p, const void* wsR, const double2* A, int6
     const bool timed = tim && 2 * gi + 1 < tim->nev;
     if (timed && (r = rec(tim->ev[2 * gi])) != cudaSuccess) return r;
     const bool ts = crt_ts(p);
-    r = KB == 128 ? (ts ? launch_imma<128, true>(p, Rres, w.Ares, w.out, nc, num_sms, st)
+    r = p.pair ? launch_imma2(p, Rres, w.Ares, w.out, nc, num_sms, st)
+               : KB == 128 ? (ts ? launch_imma<128, true>(p, Rres, w.Ares, w.out, nc, num_sms, st)
                         : launch_imma<128, false>(p, Rres, w.Ares, w.out, nc, num_sms, st))
                   : launch_imma<64, false>(p, Rres, w.Ares, w.out, nc, num_sms, st);
     if (r == cudaSuccess && timed) r = rec(tim->ev[2 * gi + 1]);

@@ -264,6 +264,8 @@ namespace rid {
 struct CrtPlan {
   int T, b, kslices, kbps, chunks, nc;
   int64_t mh, Kp, lp;
+  bool pair;  // the CTA-pair GEMM (k_imma2, tcgen05 cta_group::2; N a multiple of 32)
+  int cn[8], coff[8];  // row tile c: cn[c] rows from row coff[c] (nc = the largest)
 };
 CrtPlan crt_plan(int64_t l, int64_t m);
 int crt_moduli(int* p, int cap);
