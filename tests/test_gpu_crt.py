@@ -230,6 +230,19 @@ def test_crt_decompose_parity(rid, orc, ctx, name, seed, m, n, k, l, noise):
     assert r3.diag["t_sketch_tc"] > 0
 
 
+@pytest.mark.parametrize("name,seed,m,n,k,l,noise", [DEC_CASES[1], DEC_CASES[3], DEC_CASES[5]])
+def test_crt_solve_selection(rid, orc, ctx, monkeypatch, name, seed, m, n, k, l, noise):
+    """RID_SOLVE_CRT=1: T = R11^-1 R12 on the INT8_CRT engine as well (a tested selection)."""
+    monkeypatch.setenv("RID_SOLVE_CRT", "1")
+    A_o = orc.generate(seed, m, n, k, noise)
+    d = orc.decompose(A_o, k, l, seed)
+    r = rid.decompose(rid.generate(seed, m, n, k, noise, ctx=ctx), k, l, seed, ctx=ctx)
+    assert np_(r.J).tolist() == d.J.tolist()
+    P_g = np_(r.P)
+    assert bits_equal(P_g[:, np_(r.J)], np.eye(k, dtype=np.complex128))
+    assert relf(P_g, d.P) <= 1e-10
+
+
 def test_crt_multirank_bitwise(rid, orc):
     """G column shards on one GPU (in-process communicator, one thread per rank): J and the
     concatenated P bitwise equal to one rank, on the INT8_CRT engine."""
