@@ -135,6 +135,17 @@ def test_crt_pair_kernel(rid, orc, monkeypatch, m, n, l):
     c.close()
 
 
+@pytest.mark.parametrize("m,n,l", [(1, 1, 1), (3, 5, 2), (17, 2, 17), (300, 7, 300),
+                                   (2048, 130, 2048), (4100, 33, 1000)])
+def test_crt_edge_shapes(rid, orc, ctx, m, n, l):
+    """Tiny operands (TMA boxes larger than the tensors: zero-filled), l = m, the maximum l = 2048
+    (8 row tiles of 256), uneven row tiles (300 = 160 + 144, 1000 = 4 x 256 - 24)."""
+    A_o = orc.generate(7, m, n, min(m, n, 3), 1e-9)
+    Y_o = orc.sketch(A_o, 7, l)
+    Y_g = np_(rid.sketch(torch.from_numpy(np.asfortranarray(A_o)).cuda(), 7, l, ctx=ctx))
+    assert relf(Y_g, Y_o) <= TOL_Y
+
+
 def test_crt_two_k_slices(rid, orc, ctx):
     """m > 66560: K' = 2m no longer fits one exact int32 accumulation; two K slices whose
     residues are summed mod p before the reconstruction."""
