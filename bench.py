@@ -246,10 +246,7 @@ def run_reference(args, cfg):
     rec["value"] = tf
     line = {"impl": "reference", "metric": METRIC, "value": tf, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": id_s * 1e3,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        # the path's arithmetic: fp64 throughout, except the INT8_CRT sketch's exact int8 x int8
-        # -> int32 tensor-core products (its inputs and outputs are fp64; R33)
-        "dtype": "f64+int8crt" if engine == 2 else "f64",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": bench_config(cfg, args.seed),
             "cpu_baseline": rec,
             "e2e": {"value": tf, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
