@@ -139,3 +139,19 @@ def test_buffer_layouts_rejected_on_host(rid):
     assert ok.ld == 64
     sub = np.zeros((80, 8), np.complex128, order="F")[:64]  # ld 80 > rows: fine
     assert rid._Buf(sub, 64, 8, "A").ld == 80
+
+
+def test_bench_reference_arm_runs_on_cpu():
+    """bench.py --impl reference (the oracle arm the driver runs) prints one valid JSON line."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference",
+                          "--config", "C1", "--steps", "1", "--warmup", "0", "--ref-seconds", "0.5"],
+                         capture_output=True, text=True, timeout=600, cwd=root)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["value"] > 0 and line["dtype"] == "f64"
+    assert line["config"]["workload"] == "C1" and line["e2e"]["h2d_bytes_per_step"] == 0
