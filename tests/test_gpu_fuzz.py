@@ -53,6 +53,26 @@ def test_random_shape_parity(rid, orc, seed, m, n, k, l, noise):
     assert np.linalg.norm(P - d.P) <= 1e-10 * np.linalg.norm(d.P)
 
 
+@pytest.mark.parametrize("seed,m,n,k,l,noise", _shapes(12, 2027))
+def test_random_shape_parity_int8_crt(rid, orc, seed, m, n, k, l, noise):
+    """The same sweep on the INT8_CRT sketch engine (tcgen05 int8 GEMMs + CRT, reading R33)."""
+    ctx = rid.Context(0, torch.cuda.current_stream())
+    ctx.set_sketch_engine("int8_crt")
+    A = rid.generate(seed, m, n, k, noise, ctx=ctx)
+    A_o = orc.generate(seed, m, n, k, noise)
+    Y = rid.sketch(A, seed, l, ctx=ctx).cpu().numpy()
+    Y_o = orc.sketch(A_o, seed, l)
+    assert np.linalg.norm(Y - Y_o) <= 1e-12 * np.linalg.norm(Y_o)
+    d = orc.decompose(A_o, k, l, seed)
+    margin = d.tie_margins[:-1].min() if k > 1 else np.inf
+    if margin > 1e-10:  # J is only defined on well-separated spectra (reading R18)
+        r = rid.decompose(A, k, l, seed, ctx=ctx)
+        assert r.J.cpu().numpy().tolist() == list(d.J)
+        P = r.P.cpu().numpy()
+        assert np.linalg.norm(P - d.P) <= 1e-10 * np.linalg.norm(d.P)
+    ctx.close()
+
+
 def _srft_shapes(count, seed):
     rng = np.random.default_rng(seed)
     out = []
