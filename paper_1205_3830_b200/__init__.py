@@ -373,6 +373,8 @@ def sketch_engine(m: int, l: int, n: int, ctx: Context | None = None) -> str:
     """'fp64_dmma' or 'int8_crt': the engine the Gaussian sketch of an m x n matrix runs on."""
     ctx = ctx or default_context()
     e = lib().rid_sketch_engine_of(ctx.h, m, l, n)
+    if e not in (ENGINE_FP64_DMMA, ENGINE_INT8_CRT):
+        raise RidError(1, f"rid_sketch_engine_of: bad shape (m={m}, l={l}, n={n})")
     return {ENGINE_FP64_DMMA: "fp64_dmma", ENGINE_INT8_CRT: "int8_crt"}[e]
 
 
