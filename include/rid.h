@@ -199,7 +199,8 @@ rid_status rid_set_sketch_engine(rid_ctx* ctx, int engine);
 int rid_sketch_engine_of(const rid_ctx* ctx, int64_t m, int64_t l, int64_t n);
 /* The INT8_CRT plan of an l x m sketch matrix (pure host arithmetic; any pointer may be NULL):
  * T moduli, b bits per operand, kslices K' slices (each exact in int32), Kp = padded K' = 2 m,
- * nc rows of R per tensor-memory tile, log2(prod p_t) in log2M. RID_EINVAL for l < 1 or m < 1. */
+ * nc rows of R per tensor-memory tile, log2(prod p_t) in log2M. RID_EINVAL for l < 1, m < 1 or
+ * l > 2048 (the engine's limit: larger sketches run on FP64_DMMA whatever the selection). */
 rid_status rid_crt_plan(int64_t l, int64_t m, int* T, int* b, int* kslices, int64_t* Kp, int* nc,
                         double* log2M);
 /* The moduli of the INT8_CRT engine (up to 16 values written to p; returns how many exist). */

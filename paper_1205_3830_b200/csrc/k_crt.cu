@@ -911,6 +911,7 @@ CrtPlan crt_plan(int64_t l, int64_t m) {
   const int64_t gran = p.pair ? 32 : 16;
   const int64_t units = (l + gran - 1) / gran;
   p.chunks = (int)((units * gran + 255) / 256);
+  if (p.chunks > kCrtMaxChunks) p.chunks = kCrtMaxChunks;  // l > 2048: callers use DMMA
   p.nc = 0;
   int64_t off = 0;
   for (int c = 0; c < p.chunks; ++c) {

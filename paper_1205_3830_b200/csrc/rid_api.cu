@@ -100,6 +100,7 @@ namespace {
 // The engine of the Gaussian sketch of an l x m sketch matrix over n columns (rid_sketch_engine):
 // RID_SKETCH_CRT in the environment, else the context's selection, else by size
 bool use_crt(const rid_ctx* c, int64_t l, int64_t m, int64_t n) {
+  if (l > 2048) return false;  // the engine's row tiles: at most 8 of 256 (rid_decompose's bound)
   if (const char* e = rid::select_env("RID_SKETCH_CRT")) return atoi(e) != 0;
   if (c->sketch_engine == RID_ENGINE_FP64_DMMA) return false;
   if (c->sketch_engine == RID_ENGINE_INT8_CRT) return true;
@@ -974,7 +975,7 @@ int rid_sketch_engine_of(const rid_ctx* c, int64_t m, int64_t l, int64_t n) {
 
 rid_status rid_crt_plan(int64_t l, int64_t m, int* T, int* b, int* kslices, int64_t* Kp, int* nc,
                         double* log2M) {
-  if (l < 1 || m < 1) return RID_EINVAL;
+  if (l < 1 || m < 1 || l > 2048) return RID_EINVAL;
   const rid::CrtPlan p = rid::crt_plan(l, m);
   if (T) *T = p.T;
   if (b) *b = p.b;

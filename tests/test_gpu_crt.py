@@ -209,6 +209,10 @@ def test_crt_engine_selection(rid, monkeypatch):
     monkeypatch.delenv("RID_SKETCH_CRT")
     with pytest.raises(KeyError):
         c.set_sketch_engine("bogus")
+    c.set_sketch_engine("int8_crt")  # l > 2048: the engine's limit, DMMA whatever the selection
+    assert rid.sketch_engine(4096, 2100, 64, ctx=c) == "fp64_dmma"
+    with pytest.raises(rid.RidError):
+        rid.crt_plan(2100, 4096)
     c.close()
 
 
