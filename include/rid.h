@@ -67,7 +67,8 @@ typedef enum {
 /* Arithmetic of the Gaussian sketch Y = R A (rid_set_sketch_engine). Both meet the north-star bar
  * (Y within 1e-12 relative Frobenius of the oracle; measured ~4e-14); J and P follow from Y. */
 typedef enum {
-  RID_ENGINE_AUTO = 0,     /* INT8_CRT when l m n >= 2^34 (C3-C5), else FP64_DMMA (default)        */
+  RID_ENGINE_AUTO = 0,     /* INT8_CRT when l m n >= 2^34 (C3-C5), else FP64_DMMA (default); the
+                              INT8_CRT engine takes l <= 2048 and m <= 2^28 (else FP64_DMMA)       */
   RID_ENGINE_FP64_DMMA = 1,/* complex128 products on the FP64 tensor pipe (DMMA.8x8x4: Gauss 3M,
                               one Strassen level over it for the unsplit plans)                    */
   RID_ENGINE_INT8_CRT = 2  /* the exact integer product of R and A rounded to b bits relative to

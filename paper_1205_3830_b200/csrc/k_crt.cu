@@ -958,7 +958,7 @@ cudaError_t crt_prep_R(const CrtPlan& p, const double2* R, int64_t ldr, int64_t 
   uint32_t* Rres = (uint32_t*)ws;
   unsigned long long* rowmax = (unsigned long long*)((char*)ws + (size_t)p.T * 2 * p.lp * p.Kp);
   if ((e = cudaMemsetAsync(rowmax, 0, 8 * (size_t)p.lp, st)) != cudaSuccess) return e;
-  const int64_t kpart = 1024;
+  const int64_t kpart = std::max<int64_t>(1024, (m + 65534) / 65535);  // grid.y <= 65535
   dim3 g1((unsigned)((l + 127) / 128), (unsigned)((m + kpart - 1) / kpart));
   k_crt_rowmax<<<g1, 128, 0, st>>>(R, ldr, l, m, kpart, rowmax);
   // K blocks cover [0, mh) plus one more block row for the padding [2 mh, Kp)

@@ -100,7 +100,9 @@ namespace {
 // The engine of the Gaussian sketch of an l x m sketch matrix over n columns (rid_sketch_engine):
 // RID_SKETCH_CRT in the environment, else the context's selection, else by size
 bool use_crt(const rid_ctx* c, int64_t l, int64_t m, int64_t n) {
-  if (l > 2048) return false;  // the engine's row tiles: at most 8 of 256 (rid_decompose's bound)
+  // the engine's row tiles: at most 8 of 256 (rid_decompose's bound); K' = 2m bytes of residues
+  // per column addressed by int32 TMA coordinates
+  if (l > 2048 || m > ((int64_t)1 << 28)) return false;
   if (const char* e = rid::select_env("RID_SKETCH_CRT")) return atoi(e) != 0;
   if (c->sketch_engine == RID_ENGINE_FP64_DMMA) return false;
   if (c->sketch_engine == RID_ENGINE_INT8_CRT) return true;
