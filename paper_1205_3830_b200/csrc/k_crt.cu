@@ -37,8 +37,8 @@ namespace rid {
 
 namespace {
 
-// The moduli: odd, pairwise coprime, <= 253 (so a residue rounded to the nearest quotient in fp32
-// stays within ±127), descending.
+// The moduli: odd, pairwise coprime, <= 253 (so a residue from a quotient that may be off by one
+// near a half-integer stays within ±127: crt_res_byte64), descending.
 constexpr int kCrtMaxT = 16;
 constexpr int kModuli[kCrtMaxT] = {253, 251, 249, 247, 245, 241, 239, 233,
                                    229, 227, 223, 211, 199, 197, 193, 191};
@@ -95,9 +95,10 @@ __device__ __forceinline__ Scale crt_scale(int s) {
   return Scale{ldexp(1.0, a), ldexp(1.0, s - a)};
 }
 // The residue of a mod p_t from the FP64 pipe: a is the exact integer rint(x 2^s) as a double
-// and a_lo its low 32 bits. q = rint(a / p) is one DFMA against 1.5 2^52 (|a / p| < 2^39; the
-// rounded 1/p moves q by at most one, only within 2^-14 of a half-integer, so |a − p q| <= 0.5001 p
-// <= 127), and the remainder's low byte comes from 32-bit integer arithmetic on the low words:
+// and a_lo its low 32 bits. q = rint(a / p) is one DFMA against 1.5 2^52 (|a| <= 2^50, |a / p| <
+// 2^43; the rounded 1/p moves the product by at most 2^50 2^-53 / p < 2^-10, so q is off by one
+// only within 2^-10 of a half-integer and |a − p q| <= 0.501 p <= 127), and the remainder's low
+// byte comes from 32-bit integer arithmetic on the low words:
 // a − p q = a_lo − p q_lo (mod 2^32). One DFMA + one IMAD per residue (round 2's first version
 // split a into three fp32 limbs and spent six FP32 operations per residue: C4 preparation 2.98 vs
 // 2.42 ms per 8192-column block).
@@ -159,12 +160,12 @@ __device__ __forceinline__ void crt_prep_quads(const double2* __restrict__ a, in
   }
 }
 
-// The conversion with the column maximum fused in (default). A cluster of CL CTAs (on CL SMs)
-// takes one column at a time, persistent over columns: each CTA reads its 1/CL of the column for
-// the maximum, the CTAs exchange their partial maxima through distributed shared memory (one
-// cluster barrier), and each converts its part of the column, re-read from L2 (148 / CL columns in
-// flight: C4 with CL = 4, 37 x 512 KB = 19 MB; the residue stores and the second read are marked
-// evict-first). Only the maximum's EXPONENT matters (crt_shift), so the first pass takes the
+// The conversion with the column maximum fused in. Default: one CTA per column at a time,
+// persistent over columns — it reads the column once for its maximum and again for the residues
+// (mostly from L2 at C4: 148 columns of 512 KB in flight; the residue stores and the second read
+// are marked evict-first). Experiment (RID_CRT_PREP_CLUSTER): a cluster of CL CTAs per column, each
+// reading 1/CL of it, the partial maxima exchanged through distributed shared memory (one cluster
+// barrier) — A read from DRAM exactly once, but measured slower (§5.5). Only the maximum's EXPONENT matters (crt_shift), so the first pass takes the
 // integer maximum of the high words of |Re|, |Im| — two integer operations per value — and an
 // exponent field 0x7FF (inf / NaN) marks the column bad. T is a compile-time constant so the
 // modulus loop unrolls with the constants as instruction operands.
