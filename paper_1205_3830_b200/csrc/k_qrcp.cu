@@ -1242,9 +1242,587 @@ __global__ void __launch_bounds__(kRingThreads, 1)
   if (bl == 0 && threadIdx.x == 0) out.info[1] = jend;
 }
 
+// =============================================================================================
+// Lazy-refresh blocked variant (default for l <= 544: C4, C5).
+//
+// The ring kernel above streams rows j..l−1 of EVERY unchosen column at every step (C4: 73 GB
+// over 512 steps) because the greedy rule (R8) needs the exact maximum residual norm. But a
+// residual norm never grows (ν_c(j+1)² = ν_c(j)² − |R(j, c)|²): a norm computed at an earlier
+// step of the panel is an UPPER BOUND on the current one, and a column whose bound is below the
+// current maximum cannot be the pivot. This kernel keeps, per column, the number u of panel steps
+// already applied to it (f_0..f_{u−1}(c) in F, R(j0..j0+u−1, c) in Y, ν_c exact as of step j0+u)
+// and at step j refreshes ONLY the columns whose bound is >= a threshold τ_j:
+//   phase A (FP64 tensor pipe, 8 columns x 16 reflectors per DMMA tile): d_s = v_sᴴ y^(j0)_c for
+//     s = u..t, V of the panel in shared memory, y^(j0)_c[j0+u:l] read once from global memory;
+//   phase B (one lane per column): for s = u..t in order
+//       f_s = conj(τ_s)·(d_s − Σ_{s'<s} (v_sᴴ v_s') f_s'),
+//       R(j0+s, c) = y^(j0)_c[j0+s] − Σ_{s'<=s} V[j0+s, s'] f_s',
+//       ν² ← ν² − |R(j0+s, c)|²  (exact recompute below kRecompTol·ν_ref², as the ring kernel).
+// A column's arithmetic is fixed (fixed lanes, fixed reduction orders, the same per-s formulas),
+// so WHEN it is refreshed changes no bit: J, R, P and the norms equal those of refreshing every
+// column at every step (mode 2, RID_QRCP_LAZY=2; tested bitwise).
+// Exact pivots: the exchange after a pass carries the grid-wide top three of the refreshed
+// columns' exact norms (b1, b2, b3) and m, the largest bound of the columns NOT refreshed at this
+// step; their exact norms are <= m. If b2 > m the top two are exact (the argmax, ties to the
+// lowest index, and the tie margin); otherwise the pass is repeated down to b2 (or to m with fewer
+// than two exact norms), which terminates. The threshold on ν², τ_j = b3(j)·(1 − κ/(l − j)):
+// the third-best norm less κ mean one-step decays of a residual in l − j dimensions (κ = 8), so
+// the next top two are usually among the refreshed columns. The last step of a
+// launch refreshes every column (τ = −1): the trailing update Y −= V·F needs all of f_0..f_{nb−1}
+// and rows j0..jend−1 of every column must hold R.
+// =============================================================================================
+constexpr int kLazyThreads = 256;
+constexpr int kLazyWarps = kLazyThreads / 32;
+constexpr int kLazyChunk = 128;  // columns per phase A / phase B round (s_d rows)
+constexpr int kLazySD = kNB + 1;  // s_d row stride in double2 (conflict-free 16-byte rows)
+constexpr int kLazyScratch = 2 * 4 * 2 * 4 * 32 * 2;  // phase A partials [slot][pp][mt][prod]
+
+// Top three exact norms (ties of the first to the lowest index) and the largest bound among the
+// columns NOT refreshed at this step (m): the exchange record of the lazy kernel.
+struct Top3 {
+  double b1, b2, b3, m;
+  long long i1;
+};
+__device__ __forceinline__ void top3_init(Top3& a) {
+  a.b1 = a.b2 = a.b3 = a.m = -1.0;
+  a.i1 = 0x7FFFFFFFFFFFFFFFLL;
+}
+__device__ __forceinline__ void top3_push(Top3& a, double v, long long i) {
+  if (beats(v, i, a.b1, a.i1)) {
+    a.b3 = a.b2;
+    a.b2 = a.b1;
+    a.b1 = v;
+    a.i1 = i;
+  } else if (v > a.b2) {
+    a.b3 = a.b2;
+    a.b2 = v;
+  } else if (v > a.b3) {
+    a.b3 = v;
+  }
+}
+// top three of the union (as multisets of values; the first by (value, -index)): order-free
+__device__ __forceinline__ void top3_merge(Top3& a, const Top3& c) {
+  const bool cw = beats(c.b1, c.i1, a.b1, a.i1);
+  const Top3& w = cw ? c : a;  // holds the winner
+  const Top3& o = cw ? a : c;
+  Top3 r;
+  r.b1 = w.b1;
+  r.i1 = w.i1;
+  if (o.b1 >= w.b2) {
+    r.b2 = o.b1;
+    r.b3 = fmax(w.b2, o.b2);
+  } else {
+    r.b2 = w.b2;
+    r.b3 = fmax(w.b3, o.b1);
+  }
+  r.m = fmax(a.m, c.m);
+  a = r;
+}
+__device__ __forceinline__ void top3_warp(Top3& a) {
+#pragma unroll
+  for (int msk = 16; msk >= 1; msk >>= 1) {
+    Top3 o;
+    o.b1 = __shfl_xor_sync(0xffffffffu, a.b1, msk);
+    o.b2 = __shfl_xor_sync(0xffffffffu, a.b2, msk);
+    o.b3 = __shfl_xor_sync(0xffffffffu, a.b3, msk);
+    o.m = __shfl_xor_sync(0xffffffffu, a.m, msk);
+    o.i1 = __shfl_xor_sync(0xffffffffu, a.i1, msk);
+    top3_merge(a, o);
+  }
+}
+
+template <int MAXQ>
+__global__ void __launch_bounds__(kLazyThreads, 1)
+    k_qrcp_lazy(const __grid_constant__ QrShards sh, int64_t ldy, int l, int k, int j0, int jend,
+                double tol_rel, int per, int cpr, double kappa, int mode) {
+  constexpr int RP = 32 * MAXQ + 4;  // sV row stride: rows j0..j0+32·MAXQ−1, +64 B so that the
+                                      // DMMA A fragments (8 s x 4 rows) hit 32 distinct banks
+  constexpr int XQ = (32 * MAXQ + kLazyThreads - 1) / kLazyThreads;
+  constexpr int KQ = 2 * MAXQ;  // k-steps (4 rows) per partial: 4 partials x KQ x 4 >= 32 MAXQ
+  extern __shared__ __align__(16) unsigned char lz_smem[];
+  double2* sV = reinterpret_cast<double2*>(lz_smem);           // [kNB][RP]: v_s, zero above j0+s
+  double2* s_d = sV + kNB * RP;                                 // [kLazyChunk][kLazySD]: d_s
+  double* s_sc = reinterpret_cast<double*>(s_d + kLazyChunk * kLazySD);  // [2][4][8][64]
+  double* nu_s = s_sc + kLazyScratch;                           // [per] ν² bound (exact at j0+u)
+  double* ref_s = nu_s + per;                                   // [per] ν² at the last recompute
+  int* upd_s = reinterpret_cast<int*>(ref_s + per);             // [per] u: panel steps applied
+  int* list = upd_s + per;                                      // [per] the pass's columns
+  __shared__ double2 s_G[kNB][kNB];  // s_G[t][s] = v_tᴴ v_s, s < t
+  __shared__ double2 s_M[kNB][kNB];  // f = M d: M = (I + D_conj(τ) G)^-1 D_conj(τ), lower
+  __shared__ double2 s_fp[kNB];      // f_s(p) of the step's pivot
+  __shared__ double s_red[kLazyWarps];
+  __shared__ double s_par[2];
+  __shared__ Top3 sred[kLazyWarps];
+  __shared__ Top3 s_top;
+  __shared__ int s_cnt;
+
+  const int nbk = gridDim.x, b = blockIdx.x;
+  const int g = b / cpr, bl = b - g * cpr;
+  double2* __restrict__ Y = sh.Y[g];
+  const QrcpOut& out = sh.out[g];
+  const QrcpWork& w = sh.w[g];
+  double* const cand = sh.w[0].cand;  // 2 buffers x max_blocks x 5 doubles
+  unsigned* const bar = sh.w[0].bar;
+  const int max_blocks = sh.w[0].max_blocks;
+  const int64_t n = sh.n_loc;
+  const int64_t gbase = (int64_t)g * sh.n_loc;
+  const int64_t nglob = (int64_t)sh.G * sh.n_loc;
+  if (out.info[0] == 2) return;  // an earlier panel stopped on rank failure (uniform)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t c_lo = (int64_t)bl * per;
+  const int ncol = (int)(n - c_lo < per ? (n - c_lo > 0 ? n - c_lo : 0) : per);
+  const int64_t ldv = l;
+  const int Lp = l - j0;          // rows of the panel
+  const int qn = (Lp + 31) / 32;  // q < qn hold them
+  const int nks = (Lp + 3) >> 2;  // 4-row k-steps of the panel
+  unsigned phase = 0;
+  int xc = (j0 > 0) ? (int)__ldcg(sh.w[0].scal + 1) : 0;  // cand buffer of the last exchange
+  double nu0max = (j0 > 0) ? __ldcg(w.scal) : 0.0;
+
+  for (int i = threadIdx.x; i < kNB * RP; i += kLazyThreads) sV[i] = make_double2(0.0, 0.0);
+  for (int i = threadIdx.x; i < ncol; i += kLazyThreads) {
+    upd_s[i] = 0;
+    if (j0 > 0) {
+      nu_s[i] = __ldcg(w.nu + c_lo + i);
+      ref_s[i] = __ldcg(w.nuref + c_lo + i);
+    }
+  }
+  __syncthreads();
+
+  // grid-wide record of the last exchange -> s_top
+  auto read_top = [&]() {
+    if (warp == 0) {
+      Top3 tt;
+      top3_init(tt);
+      const double* cb = cand + (size_t)xc * max_blocks * 5;
+      for (int q0 = 0; q0 < nbk; q0 += 32 * 5) {  // five records per lane, all loads first
+        double rv[5][5];
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+          const int q = q0 + lane + 32 * a;
+#pragma unroll
+          for (int f = 0; f < 5; ++f) rv[a][f] = q < nbk ? __ldcg(cb + q * 5 + f) : -1.0;
+        }
+#pragma unroll
+        for (int a = 0; a < 5; ++a) {
+          if (q0 + lane + 32 * a < nbk) {
+            Top3 o;
+            o.b1 = rv[a][0];
+            o.b2 = rv[a][1];
+            o.b3 = rv[a][2];
+            o.m = rv[a][3];
+            o.i1 = (long long)rv[a][4];
+            top3_merge(tt, o);
+          }
+        }
+      }
+      top3_warp(tt);
+      if (lane == 0) s_top = tt;
+    }
+    __syncthreads();
+  };
+  // the CTA's record over its columns (exact: refreshed as of panel step tf), published; grid
+  // barrier; the grid-wide record
+  auto exchange = [&](int tf) {
+    Top3 loc;
+    top3_init(loc);
+    for (int i = threadIdx.x; i < ncol; i += kLazyThreads) {
+      const double v = nu_s[i];
+      if (v >= 0.0) {
+        if (upd_s[i] == tf)
+          top3_push(loc, v, gbase + c_lo + i);
+        else
+          loc.m = fmax(loc.m, v);
+      }
+    }
+    top3_warp(loc);
+    if (lane == 0) sred[warp] = loc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Top3 tt = sred[0];
+      for (int q = 1; q < kLazyWarps; ++q) top3_merge(tt, sred[q]);
+      double* cc = cand + ((size_t)(xc ^ 1) * max_blocks + b) * 5;
+      cc[0] = tt.b1;
+      cc[1] = tt.b2;
+      cc[2] = tt.b3;
+      cc[3] = tt.m;
+      cc[4] = (double)tt.i1;
+    }
+    xc ^= 1;
+    grid_barrier(bar, (unsigned)nbk * (++phase));
+    read_top();
+  };
+
+  if (j0 == 0) {  // ---- initial exact column norms² (one warp per column) ----------------------
+    for (int i = warp; i < ncol; i += kLazyWarps) {
+      const double2* yc = Y + (c_lo + i) * ldy;
+      double s = 0.0;
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        const int r = lane + 32 * q;
+        if (r < l) {
+          const double2 y = __ldcg(yc + r);
+          s = __fma_rn(y.x, y.x, s);
+          s = __fma_rn(y.y, y.y, s);
+        }
+      }
+      s = group_sum(s, 32);
+      if (lane == 0) {
+        nu_s[i] = s;
+        ref_s[i] = s;
+      }
+    }
+    __syncthreads();
+    exchange(0);
+  } else {
+    read_top();
+  }
+
+  for (int j = j0; j < jend; ++j) {
+    const int t = j - j0;
+    const int L = l - j;
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 0] = globaltimer();
+    // ---- 1. the pivot (every CTA identically, from s_top; values are ν²) ---------------------
+    const Top3 tt = s_top;
+    const double nu1 = __dsqrt_rn(tt.b1 > 0.0 ? tt.b1 : 0.0);
+    if (j == 0) nu0max = nu1;  // max_c ||Y[:, c]||
+    const bool stop = !(nu1 >= tol_rel * nu0max) || tt.b1 <= 0.0 || tt.i1 < 0 || tt.i1 >= nglob;
+    const int64_t p = tt.i1;  // global id
+    if (bl == 0 && threadIdx.x == 0) {  // every rank's replicated outputs
+      if (j == 0) w.scal[0] = nu0max;
+      out.resid[j] = nu1;
+      out.margin[j] = (tt.b2 < 0.0) ? DBL_MAX : (nu1 - __dsqrt_rn(tt.b2)) / nu1;
+      if (!stop) out.J[j] = p;
+    }
+    if (stop) {
+      if (bl == 0 && threadIdx.x == 0) {
+        out.info[0] = 2;
+        out.info[1] = j;
+      }
+      return;
+    }
+    // this step's refresh threshold on ν²: the third-best exact value less kappa mean one-step
+    // decays of a residual in l − j dimensions (-1: every column)
+    double tau = -1.0;
+    if (mode != 2 && j + 1 < jend) {
+      const double base = tt.b3 > 0.0 ? tt.b3 : tt.b2;
+      const double dec = 1.0 - kappa / (double)(L > 1 ? L : 1);
+      tau = (base > 0.0 && dec > 0.0) ? base * dec : -1.0;
+    }
+    const int go = (int)(p / sh.n_loc);
+    const int64_t pl = p - (int64_t)go * sh.n_loc;
+    const double2* __restrict__ Yp = sh.Y[go] + pl * ldy;
+    if (threadIdx.x == 0 && p >= gbase + c_lo && p < gbase + c_lo + ncol)
+      nu_s[p - gbase - c_lo] = -1.0;  // the owner: chosen
+    if (threadIdx.x < t) s_fp[threadIdx.x] = __ldcg(sh.w[go].F + pl * kNB + threadIdx.x);
+    __syncthreads();
+    // ---- 2. reflector H_j from x = y^(j0)_p[j:l] − Σ_{s<t} V[j:l, s] f_s(p) ----------------
+    double2 x[XQ];
+    double s2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < XQ; ++q) {
+      const int rr = threadIdx.x + kLazyThreads * q;
+      double2 z = make_double2(0.0, 0.0);
+      if (rr < L) {
+        z = __ldcg(Yp + j + rr);
+        for (int s = 0; s < t; ++s) cmac_sub(z, sV[s * RP + t + rr], s_fp[s]);
+        if (rr > 0) {
+          s2 = __fma_rn(z.x, z.x, s2);
+          s2 = __fma_rn(z.y, z.y, s2);
+        }
+      }
+      x[q] = z;
+    }
+    s2 = group_sum(s2, 32);
+    if (lane == 0) s_red[warp] = s2;
+    if (threadIdx.x == 0) {
+      s_par[0] = x[0].x;
+      s_par[1] = x[0].y;
+    }
+    if (bl == 0)  // R11 column j: rows 0..j-1 of the pivot are final
+      for (int r = threadIdx.x; r < j; r += kLazyThreads) out.R11[(int64_t)j * k + r] = __ldcg(Yp + r);
+    __syncthreads();
+    {
+      double xnorm2 = 0.0;
+      for (int q = 0; q < kLazyWarps; ++q) xnorm2 = __dadd_rn(xnorm2, s_red[q]);  // fixed order
+      const double ar = s_par[0], ai = s_par[1];
+      double tr, ti, beta, sc_re, sc_im;
+      if (xnorm2 == 0.0 && ai == 0.0) {
+        tr = 0.0;
+        ti = 0.0;
+        beta = ar;
+        sc_re = 0.0;
+        sc_im = 0.0;
+      } else {
+        const double nrm = __dsqrt_rn(__fma_rn(ar, ar, __fma_rn(ai, ai, xnorm2)));
+        beta = (ar >= 0.0) ? -nrm : nrm;
+        tr = __ddiv_rn(__dsub_rn(beta, ar), beta);
+        ti = __ddiv_rn(-ai, beta);
+        const double dr = __dsub_rn(ar, beta), di = ai;  // scal = 1 / (alpha - beta)
+        const double den = __fma_rn(dr, dr, __dmul_rn(di, di));
+        sc_re = __ddiv_rn(dr, den);
+        sc_im = __ddiv_rn(-di, den);
+      }
+#pragma unroll
+      for (int q = 0; q < XQ; ++q) {
+        const int rr = threadIdx.x + kLazyThreads * q;
+        if (rr < L) {
+          double2 v;
+          if (rr == 0) {
+            v = make_double2(1.0, 0.0);
+          } else {
+            v.x = __fma_rn(x[q].x, sc_re, -__dmul_rn(x[q].y, sc_im));
+            v.y = __fma_rn(x[q].x, sc_im, __dmul_rn(x[q].y, sc_re));
+          }
+          sV[t * RP + t + rr] = v;
+          if (bl == 0) w.V[(int64_t)t * ldv + j + rr] = v;  // each rank's copy (trailing update)
+        }
+      }
+      if (threadIdx.x == 0) {
+        s_M[t][t] = make_double2(tr, -ti);  // conj(τ_t)
+        if (bl == 0) {
+          out.beta[j] = beta;
+          out.R11[(int64_t)j * k + j] = make_double2(beta, 0.0);
+        }
+      }
+    }
+    __syncthreads();
+    // s_G[t][s] = v_tᴴ v_s for s < t (one warp per s, rows on fixed lanes)
+    for (int s = warp; s < t; s += kLazyWarps) {
+      double gr = 0.0, gi = 0.0;
+#pragma unroll
+      for (int q = 0; q < MAXQ; ++q) {
+        if (q < qn) {
+          const double2 a = sV[t * RP + lane + 32 * q], v = sV[s * RP + lane + 32 * q];
+          gr = __fma_rn(a.x, v.x, __fma_rn(a.y, v.y, gr));  // conj(a) v
+          gi = __fma_rn(a.x, v.y, __fma_rn(-a.y, v.x, gi));
+        }
+      }
+      gr = group_sum(gr, 32);
+      gi = group_sum(gi, 32);
+      if (lane == 0) s_G[t][s] = make_double2(gr, gi);
+    }
+    __syncthreads();
+    // row t of M: f_t = conj(τ_t)(d_t − Σ_{s<t} G[t][s] f_s) with f_s = Σ_{s'<=s} M[s][s'] d_s',
+    // so M[t][s'] = −conj(τ_t) Σ_{s'<=s<t} G[t][s] M[s][s'] (one thread per s', fixed order)
+    if (threadIdx.x < t) {
+      const int sp = threadIdx.x;
+      double ar = 0.0, ai = 0.0;
+      for (int s = sp; s < t; ++s) cmac_add(ar, ai, s_G[t][s], s_M[s][sp]);
+      const double2 ct = s_M[t][t];
+      s_M[t][sp] = make_double2(-__fma_rn(ct.x, ar, -__dmul_rn(ct.y, ai)),
+                                -__fma_rn(ct.x, ai, __dmul_rn(ct.y, ar)));
+    }
+    __syncthreads();
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 1] = globaltimer();
+
+    // ---- 3. the pass: refresh every live column whose bound is >= thr ------------------------
+    auto pass = [&](double thr) {
+      if (threadIdx.x == 0) s_cnt = 0;
+      __syncthreads();
+      for (int i = threadIdx.x; i < ncol; i += kLazyThreads) {
+        const double v = nu_s[i];
+        if (v >= 0.0 && upd_s[i] <= t && v >= thr) list[atomicAdd(&s_cnt, 1)] = i;
+      }
+      __syncthreads();
+      const int cnt = s_cnt;
+      if (w.trace && threadIdx.x == 0 && cnt > 0)
+        atomicAdd(&w.trace[8 * j + 6], (unsigned long long)cnt);
+      for (int e0 = 0; e0 < cnt; e0 += kLazyChunk) {
+        const int nch = min(kLazyChunk, cnt - e0);
+        // phase A on the FP64 tensor pipe: d_s(c) = v_sᴴ y^(j0)_c for 8 columns x 16 s per tile
+        // (DMMA m8n8k4: A = V from shared memory, B = Y straight from global memory), K = the
+        // panel rows in 4-row steps; step κ goes to partial κ mod 4 (four warps per tile), and
+        // each of the four real products Vx·Yx, Vy·Yy, Vx·Yy, Vy·Yx is its own ascending DMMA
+        // chain (eight independent chains per warp: the DMMA latency is ≈ 8 issues deep);
+        // per product (P0 + P1) + (P2 + P3), then Re d = XX + YY, Im d = XY − YX. Per (s, c) the
+        // bits depend only on v_s and y_c: not on the tile, the pass or the other columns. A
+        // warp's loads for its next tile are issued before the combine (all KQ in flight).
+        const int ntile = (nch + 7) / 8;
+        const int slot = warp >> 2, pp = warp & 3, gq = lane >> 2, tq = lane & 3;
+        double2 yv[KQ];
+        int uc = kNB;
+        auto load_tile = [&](int tl) {
+          const int ecol = tl * 8 + gq;  // this lane's B column (chunk entry)
+          const bool cv = tl < ntile && ecol < nch;
+          const int ic = cv ? list[e0 + ecol] : 0;
+          uc = cv ? upd_s[ic] : kNB;
+          const double2* yc = Y + (c_lo + ic) * ldy + j0;
+#pragma unroll
+          for (int i = 0; i < KQ; ++i) {
+            const int r = 4 * (pp + 4 * i) + tq;
+            // rows >= u of y^(j0) are not written during this launch (only rows j0..j0+u−1
+            // receive R), so the read-only path is coherent for every row read here
+            yv[i] = (cv && r < Lp && r >= uc) ? __ldg(yc + r) : make_double2(0.0, 0.0);
+          }
+        };
+        // the bulk-copy engine pulls a tile's columns into L2 two rounds ahead (the B-fragment
+        // loads below are load-store-unit bound from HBM: lg_throttle in ncu)
+        auto prefetch_tile = [&](int tl) {
+          const int ecol = tl * 8 + lane;
+          if (pp == 0 && lane < 8 && tl < ntile && ecol < nch) {
+            const int ic = list[e0 + ecol];
+            const int u = upd_s[ic];
+            if (u < Lp)
+              bulk_prefetch_l2(Y + (c_lo + ic) * ldy + j0 + u, (unsigned)(Lp - u) * 16u);
+          }
+        };
+        prefetch_tile(slot + 2);
+        load_tile(slot);
+        for (int tb = 0; tb < ntile; tb += 2) {  // two tiles per round, four warps each
+          const int tl = tb + slot;
+          prefetch_tile(tb + 4 + slot);
+          if (tl < ntile) {
+            const int slo = __reduce_min_sync(0xffffffffu, uc);
+            const bool mt0 = slo <= 7, mt1 = t >= 8;
+            // eight independent DMMA chains per warp: [M tile][Vx·Yx, Vy·Yy, Vx·Yy, Vy·Yx]
+            double acc[16];
+#pragma unroll
+            for (int a = 0; a < 16; ++a) acc[a] = 0.0;
+#pragma unroll
+            for (int i = 0; i < KQ; ++i) {
+              const int ks = pp + 4 * i;
+              if (ks < nks) {
+                const int r = 4 * ks + tq;
+                if (mt0) {
+                  const double2 a = sV[gq * RP + r];
+                  dmma8x8x4_nv(acc[0], acc[1], a.x, yv[i].x);
+                  dmma8x8x4_nv(acc[2], acc[3], a.y, yv[i].y);
+                  dmma8x8x4_nv(acc[4], acc[5], a.x, yv[i].y);
+                  dmma8x8x4_nv(acc[6], acc[7], a.y, yv[i].x);
+                }
+                if (mt1) {
+                  const double2 a = sV[(8 + gq) * RP + r];
+                  dmma8x8x4_nv(acc[8], acc[9], a.x, yv[i].x);
+                  dmma8x8x4_nv(acc[10], acc[11], a.y, yv[i].y);
+                  dmma8x8x4_nv(acc[12], acc[13], a.x, yv[i].y);
+                  dmma8x8x4_nv(acc[14], acc[15], a.y, yv[i].x);
+                }
+              }
+            }
+            // scratch [slot][pp][mt * 4 + product][lane][2]
+            double* sc = s_sc + (size_t)((slot * 4 + pp) * 8) * 64;
+#pragma unroll
+            for (int a = 0; a < 8; ++a) {
+              sc[a * 64 + lane * 2 + 0] = acc[2 * a];
+              sc[a * 64 + lane * 2 + 1] = acc[2 * a + 1];
+            }
+          }
+          if (tb + 2 < ntile) load_tile(tb + 2 + slot);  // in flight during the combine
+          __syncthreads();
+          // each product (P0 + P1) + (P2 + P3); Re d = XX + YY, Im d = XY − YX -> s_d[entry][s]
+          for (int idx = threadIdx.x; idx < 2 * 2 * 2 * 64; idx += kLazyThreads) {
+            const int sl = idx >> 8, mt = (idx >> 7) & 1, ri = (idx >> 6) & 1, o = idx & 63;
+            const int tt2 = tb + sl;
+            const int ln = o >> 1, bb = o & 1;
+            const int s = 8 * mt + (ln >> 2), ecol = tt2 * 8 + 2 * (ln & 3) + bb;
+            if (tt2 < ntile && ecol < nch && s <= t) {
+              const double* sc = s_sc + (size_t)(sl * 32 + mt * 4 + 2 * ri) * 64 + o;  // pp stride 512
+              const double p0 = __dadd_rn(__dadd_rn(sc[0], sc[512]), __dadd_rn(sc[1024], sc[1536]));
+              const double p1 =
+                  __dadd_rn(__dadd_rn(sc[64], sc[576]), __dadd_rn(sc[1088], sc[1600]));
+              reinterpret_cast<double*>(s_d + ecol * kLazySD + s)[ri] =
+                  ri == 0 ? __dadd_rn(p0, p1) : __dsub_rn(p0, p1);
+            }
+          }
+          __syncthreads();
+        }
+        // phase B: thread e finishes column e of the chunk: f = M d (d_s of earlier refreshes of
+        // this panel from Dd), R(j0+s, c), the downdates of ν² in s order
+        if (threadIdx.x < nch) {
+          const int e = threadIdx.x;
+          const int i = list[e0 + e];
+          const int64_t c = c_lo + i;
+          const int u = upd_s[i];
+          double2* yc = Y + c * ldy;
+          double2* Fc = w.F + c * kNB;
+          double2* Dc = w.Dd + c * kNB;
+          double nu2 = nu_s[i], ref2 = ref_s[i];
+          double2 dd[kNB], ff[kNB], ys[kNB];
+#pragma unroll
+          for (int s = 0; s < kNB; ++s) {
+            dd[s] = ff[s] = ys[s] = make_double2(0.0, 0.0);
+            if (s <= t) {
+              if (s < u) {
+                dd[s] = __ldcg(Dc + s);
+                ff[s] = __ldcg(Fc + s);
+              } else {
+                dd[s] = s_d[e * kLazySD + s];
+                ys[s] = __ldcg(yc + j0 + s);
+              }
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < kNB; ++s) {
+            if (s <= t && s >= u) {
+              double fr = 0.0, fi = 0.0;
+#pragma unroll
+              for (int s1 = 0; s1 <= s; ++s1) cmac_add(fr, fi, s_M[s][s1], dd[s1]);
+              ff[s] = make_double2(fr, fi);
+              Fc[s] = ff[s];
+              Dc[s] = dd[s];
+            }
+          }
+#pragma unroll
+          for (int s = 0; s < kNB; ++s) {
+            if (s <= t && s >= u) {
+              double rsr = 0.0, rsi = 0.0;
+#pragma unroll
+              for (int s1 = 0; s1 <= s; ++s1) cmac_add(rsr, rsi, sV[s1 * RP + s], ff[s1]);
+              const double2 Rj = make_double2(__dsub_rn(ys[s].x, rsr), __dsub_rn(ys[s].y, rsi));
+              yc[j0 + s] = Rj;
+              // downdate ν² ← ν² − |R(j0+s, c)|²; exact recompute when it has cancelled below
+              // kRecompTol of its last exact value (LAPACK zlaqps's safeguard)
+              const double d2 = __fma_rn(-Rj.x, Rj.x, __fma_rn(-Rj.y, Rj.y, nu2));
+              const bool need = !(nu2 > 0.0) || !(d2 > kRecompTol * ref2);
+              nu2 = d2 > 0.0 ? d2 : 0.0;
+              if (need) {  // rare, this thread alone: rows j0+s+1..l-1 of y^(j0+s+1)
+                double nn = 0.0;
+                for (int rr = s + 1; rr < Lp; ++rr) {
+                  double2 z = __ldcg(yc + j0 + rr);
+#pragma unroll
+                  for (int s1 = 0; s1 <= s; ++s1) cmac_sub(z, sV[s1 * RP + rr], ff[s1]);
+                  nn = __fma_rn(z.x, z.x, nn);
+                  nn = __fma_rn(z.y, z.y, nn);
+                }
+                nu2 = nn;
+                ref2 = nn;
+              }
+            }
+          }
+          nu_s[i] = nu2;
+          ref_s[i] = ref2;
+          upd_s[i] = t + 1;
+        }
+        __syncthreads();
+      }
+    };
+
+    pass(tau);
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 2] = globaltimer();
+    exchange(t + 1);
+    // the top two are exact once every column not refreshed at this step has a bound below b2;
+    // otherwise refresh down to b2 (or, with fewer than two exact values, the top stale bound)
+    while (s_top.m >= 0.0 && !(s_top.b2 > s_top.m)) {
+      const double thr = s_top.b2 >= 0.0 ? s_top.b2 : s_top.m;
+      if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 7] += 1;
+      pass(thr);
+      exchange(t + 1);
+    }
+    if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 3] = globaltimer();
+  }
+  // the norms² go back for the next panel (every column is exact as of step jend)
+  for (int i = threadIdx.x; i < ncol; i += kLazyThreads) {
+    w.nu[c_lo + i] = nu_s[i];
+    w.nuref[c_lo + i] = ref_s[i];
+  }
+  if (b == 0 && threadIdx.x == 0) sh.w[0].scal[1] = (double)xc;
+  if (bl == 0 && threadIdx.x == 0) out.info[1] = jend;
+}
+
 size_t qrcp_work_bytes(int64_t n, int64_t l, int max_blocks) {
-  return (size_t)2 * n * sizeof(double) + (size_t)2 * 3 * max_blocks * sizeof(double) +
-         (size_t)l * kNB * sizeof(double2) + (size_t)kNB * n * sizeof(double2) +
+  return (size_t)2 * n * sizeof(double) + (size_t)2 * 6 * max_blocks * sizeof(double) +
+         (size_t)l * kNB * sizeof(double2) + (size_t)2 * kNB * n * sizeof(double2) +
          (size_t)2 * max_blocks * l * sizeof(double2) + 512;
 }
 
@@ -1256,6 +1834,8 @@ QrcpWork qrcp_work_carve(void* buf, int64_t n, int64_t l, int max_blocks) {
   p += (size_t)l * kNB * sizeof(double2);
   w.F = (double2*)p;
   p += (size_t)kNB * n * sizeof(double2);
+  w.Dd = (double2*)p;  // the lazy kernel's d_s(c) of the panel
+  p += (size_t)kNB * n * sizeof(double2);
   w.xslot = (double2*)p;
   p += (size_t)2 * max_blocks * l * sizeof(double2);
   w.nu = (double*)p;
@@ -1263,7 +1843,7 @@ QrcpWork qrcp_work_carve(void* buf, int64_t n, int64_t l, int max_blocks) {
   w.nuref = (double*)p;
   p += (size_t)n * sizeof(double);
   w.cand = (double*)p;
-  p += (size_t)2 * 3 * max_blocks * sizeof(double);
+  p += (size_t)2 * 6 * max_blocks * sizeof(double);  // 3 (ring) or 5 (lazy) per CTA
   w.scal = (double*)p;
   p += 64;
   w.bar = (unsigned*)p;
@@ -1397,12 +1977,90 @@ static cudaError_t launch_qrcp_cluster(double2* Y, int64_t ldy, int l, int64_t n
 // Panels of nb steps (k_qrcp_ring), each followed by the tensor-core trailing update
 // Y[jend:l, :] -= V[jend:l, 0:nb] · F[0:nb, :] (k_zgemm.cu mode 2) of every rank's block.
 // The grid is G rank groups of cpr CTAs (G = 1: the whole-sketch QR).
+
+// RID_QRCP_LAZY: 1 the lazy-refresh kernel where it fits (l <= 544), 2 the same kernel
+// refreshing every column at every step (bitwise the same results, tested), 0 the ring kernel.
+// Default: lazy for l > 384 (C4: 18.5 -> 17.3 ms), the ring kernel below (C5, l = 272: its
+// streaming pass over 272 rows is cheaper than the lazy kernel's per-step latency, 7.2 vs 8.1 ms).
+static int qrcp_lazy_mode(int l) {
+  if (const char* v = select_env("RID_QRCP_LAZY")) {
+    const int m = atoi(v);
+    return (m == 0 || m == 2) ? m : 1;
+  }
+  return l > 384 ? 1 : 0;
+}
+
+template <int MAXQ>
+static cudaError_t launch_qrcp_lazy(const QrShards& sh, int64_t ldy, int l, int k, double tol_rel,
+                                    int num_sms, cudaStream_t st, int* launches, int nbw,
+                                    int mode) {
+  auto kern = k_qrcp_lazy<MAXQ>;
+  cudaError_t e;
+  const int G = sh.G;
+  const int64_t n = sh.n_loc;
+  if (G < 1 || G > kQrMaxRanks || n < 1 || l > 32 * MAXQ) return cudaErrorInvalidValue;
+  int optin = 0;
+  size_t fstatic = 0;
+  if ((e = optin_smem(&optin)) != cudaSuccess) return e;
+  if ((e = static_smem((const void*)kern, &fstatic)) != cudaSuccess) return e;
+  // CTAs per rank: the SMs split evenly over the ranks (one CTA per SM, cooperative); a
+  // column's arithmetic does not depend on its CTA, so any split gives the same bits
+  int cpr = num_sms / G;
+  if ((int64_t)cpr * 8 > n) cpr = (int)((n + 7) / 8);
+  if (cpr * G > sh.w[0].max_blocks) cpr = sh.w[0].max_blocks / G;
+  if (cpr < 1) cpr = 1;
+  const int per = (int)((n + cpr - 1) / cpr);
+  cpr = (int)((n + per - 1) / per);
+  const int blocks = cpr * G;
+  const size_t smem = (size_t)kNB * (32 * MAXQ + 4) * sizeof(double2) +
+                      (size_t)kLazyChunk * kLazySD * sizeof(double2) + kLazyScratch * sizeof(double) +
+                      (size_t)per * (2 * sizeof(double) + 2 * sizeof(int));
+  if (smem + fstatic + 1024 > (size_t)optin) return cudaErrorNotSupported;  // the ring kernel
+  if ((e = ensure_dyn_smem((const void*)kern, smem)) != cudaSuccess) return e;
+  double kappa = 8.0;  // the refresh threshold's slack (changes no bit of the result, only work;
+                       // C4: 3 / 6 / 10 / 20 -> 18.0 / 17.3 / 17.5 / 18.6 ms)
+  if (const char* v = select_env("RID_QRCP_KAPPA")) kappa = atof(v);
+  for (int g = 0; g < G; ++g) {
+    if ((e = cudaMemsetAsync(sh.out[g].info, 0, 2 * sizeof(int), st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(sh.w[g].F, 0, (size_t)kNB * n * sizeof(double2), st)) != cudaSuccess)
+      return e;
+  }
+  for (int j0 = 0; j0 < k; j0 += nbw) {
+    const int jend = (j0 + nbw < k) ? j0 + nbw : k;
+    if ((e = cudaMemsetAsync(sh.w[0].bar, 0, sizeof(unsigned), st)) != cudaSuccess) return e;
+    QrShards shv = sh;
+    int64_t ldyv = ldy;
+    int lv = l, kv = k, j0v = j0, jendv = jend, perv = per, cprv = cpr, modev = mode;
+    double tolv = tol_rel, kappav = kappa;
+    void* args[] = {&shv, &ldyv, &lv, &kv, &j0v, &jendv, &tolv, &perv, &cprv, &kappav, &modev};
+    e = cudaLaunchCooperativeKernel((void*)kern, dim3(blocks), dim3(kLazyThreads), args, smem, st);
+    if (e != cudaSuccess) return e;
+    *launches += 1;
+    if (jend < k) {  // trailing rows jend..l-1 of every column of every rank (as the ring kernel)
+      for (int g = 0; g < G; ++g) {
+        e = zgemm_ordered(sh.w[g].V + jend, l, sh.w[g].F, kNB, sh.Y[g] + jend, ldy, l - jend, n,
+                          jend - j0, 2, 0.0, 0, 0, st);
+        if (e != cudaSuccess) return e;
+        *launches += 1;
+      }
+    }
+  }
+  return cudaSuccess;
+}
+
 template <int MAXQ>
 static cudaError_t launch_qrcp_blocked(const QrShards& sh, int64_t ldy, int l, int k,
                                        double tol_rel, int num_sms, cudaStream_t st,
                                        int* launches, int nbw) {
   auto kern = k_qrcp_ring<MAXQ>;
   cudaError_t e;
+  if constexpr (MAXQ <= 17) {
+    const int mode = qrcp_lazy_mode(l);
+    if (mode != 0) {
+      e = launch_qrcp_lazy<MAXQ>(sh, ldy, l, k, tol_rel, num_sms, st, launches, nbw, mode);
+      if (e != cudaErrorNotSupported) return e;
+    }
+  }
   const int G = sh.G;
   const int64_t n = sh.n_loc;
   if (G < 1 || G > kQrMaxRanks || n < 1) return cudaErrorInvalidValue;

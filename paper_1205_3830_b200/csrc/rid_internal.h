@@ -138,7 +138,8 @@ struct QrcpOut {
 };
 struct QrcpWork {
   double* nu;        // n: current residual norms (-1 = chosen)
-  double* cand;      // 2 * 3 * max_blocks doubles (best, second, index-as-double) x 2 parities
+  double* cand;      // 2 * 6 * max_blocks doubles: per CTA (best, second, index-as-double) or the
+                     // lazy kernel's (b1, b2, b3, m, index), x 2 parities
   unsigned* bar;     // 1
   int max_blocks;
   unsigned long long* trace = nullptr;  // optional: 4 %globaltimer stamps per step (CTA 0)
@@ -147,6 +148,7 @@ struct QrcpWork {
   double* scal = nullptr;   // 1: max_c ||Y[:, c]||
   double2* V = nullptr;     // l x kNB: the panel's reflectors (column-major, ld = l)
   double2* F = nullptr;     // kNB x n: f_s(c) (column-major, ld = kNB)
+  double2* Dd = nullptr;    // kNB x n: d_s(c) = v_sᴴ y(c) of the panel (lazy kernel)
   // shared-memory-resident exact kernel (k_qrcp_smem)
   double2* xslot = nullptr; // 2 x max_blocks x l: each CTA's best column, by step parity
 };

@@ -45,6 +45,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+// L2 prefetch of `bytes` (a multiple of 16) contiguous bytes by the bulk-copy engine: no shared
+// memory, no load-store-unit slots
+__device__ __forceinline__ void bulk_prefetch_l2(const void* gmem, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(gmem), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void tma_prefetch_map(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];\n" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }

@@ -46,3 +46,11 @@ for a, b in zip(edges[:-1], edges[1:]):
     print(f" steps {a:4d}-{b:4d}: pivot+hh {d_piv[a:b].mean():7.2f} us  pass {d_upd[a:b].mean():8.2f} us"
           f"  barrier {d_bar[a:b].mean():6.2f} us  gap {gap[a:b-1].mean() if b - 1 > a else 0:7.2f} us"
           f"  (rows {c.l-a}..{c.l-b+1})")
+if t.shape[1] > 8 and t[:, 7].any():  # lazy kernel: columns refreshed per step (all CTAs), retries
+    print(f" lazy: columns refreshed {t[:, 7].sum():.0f} (full refresh would be "
+          f"{sum(c.n - j for j in range(c.k))}), retried steps {int((t[:, 8] > 0).sum())}")
+    for a, b in zip(edges[:-1], edges[1:]):
+        if a >= c.k:
+            break
+        b = min(b, c.k)
+        print(f"  steps {a:4d}-{b:4d}: refreshed/step {t[a:b, 7].mean():9.1f}  retries {int(t[a:b, 8].sum())}")
