@@ -306,6 +306,11 @@ def row_rooflines(cfg, n_loc, world, gen_s, sketch_s, gather_s, qrcp_s, solve_s,
                               "sum_j 16*(l-j)*n B (one read of the trailing block per step)" if big
                               else "32*l*n B (Y in and out once; k grid-synchronised steps)",
                               "hbm" if big else "latency")
+    if big and l > 384:  # k_qrcp_lazy: the same greedy pivots, fewer reads
+        rows["a4_qrcp"]["note"] = ("lazy-refresh kernel: only columns whose norm bound reaches "
+                                   "the step's threshold are re-read (C4: ~10% of the streaming "
+                                   "reads, profiles/r02/s13); achieved = the streaming rule's "
+                                   "equivalent rate")
     if est_s:
         rows["a6_estimate"] = hbm_row(2 * q * 16.0 * m * n_loc, est_s,
                                       f"2q*16*m*n_loc B (two passes over A per iteration, q = {q})")
