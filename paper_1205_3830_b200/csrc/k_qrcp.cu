@@ -1638,6 +1638,7 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
         // per product (P0 + P1) + (P2 + P3), then Re d = XX + YY, Im d = XY − YX. Per (s, c) the
         // bits depend only on v_s and y_c: not on the tile, the pass or the other columns. A
         // warp's loads for its next tile are issued before the combine (all KQ in flight).
+        const unsigned long long tA0 = (w.trace && b == 0) ? globaltimer() : 0ull;
         const int ntile = (nch + 7) / 8;
         const int slot = warp >> 2, pp = warp & 3, gq = lane >> 2, tq = lane & 3;
         double2 yv[KQ];
@@ -1727,74 +1728,114 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
           }
           __syncthreads();
         }
-        // phase B: thread e finishes column e of the chunk: f = M d (d_s of earlier refreshes of
-        // this panel from Dd), R(j0+s, c), the downdates of ν² in s order
-        if (threadIdx.x < nch) {
-          const int e = threadIdx.x;
-          const int i = list[e0 + e];
+        if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 4] += globaltimer() - tA0;
+        const unsigned long long tB0 = (w.trace && b == 0) ? globaltimer() : 0ull;
+        // phase B: a half-warp per column, lane s <-> panel step s (compact code: a fully
+        // unrolled thread-per-column form ran out of the instruction cache): f = M d (d_s of
+        // earlier refreshes of this panel from Dd), R(j0+s, c), then the downdates of ν² in s
+        // order, identical on the 16 lanes of the column
+        for (int e1 = 2 * warp; e1 < nch; e1 += 2 * kLazyWarps) {
+          const int hf = lane >> 4, s = lane & 15;
+          const unsigned hmask = hf ? 0xffff0000u : 0x0000ffffu;
+          const int e = e1 + hf;
+          const bool ok = e < nch;  // uniform over the half-warp
+          const int i = ok ? list[e0 + e] : list[e0 + e1];
           const int64_t c = c_lo + i;
-          const int u = upd_s[i];
+          const int u = ok ? upd_s[i] : kNB;
           double2* yc = Y + c * ldy;
           double2* Fc = w.F + c * kNB;
           double2* Dc = w.Dd + c * kNB;
-          double nu2 = nu_s[i], ref2 = ref_s[i];
-          double2 dd[kNB], ff[kNB], ys[kNB];
-#pragma unroll
-          for (int s = 0; s < kNB; ++s) {
-            dd[s] = ff[s] = ys[s] = make_double2(0.0, 0.0);
-            if (s <= t) {
-              if (s < u) {
-                dd[s] = __ldcg(Dc + s);
-                ff[s] = __ldcg(Fc + s);
-              } else {
-                dd[s] = s_d[e * kLazySD + s];
-                ys[s] = __ldcg(yc + j0 + s);
-              }
+          const bool mine = ok && s >= u && s <= t;  // this refresh computes step s
+          double2 dl = make_double2(0.0, 0.0), fl = dl, yl = dl;
+          if (ok && s <= t) {  // F, Dd and these rows of Y are written only by this CTA
+            if (s < u) {
+              dl = Dc[s];
+              fl = Fc[s];
+            } else {
+              dl = s_d[e * kLazySD + s];
+              yl = yc[j0 + s];
             }
           }
+          double fr = 0.0, fi = 0.0;
 #pragma unroll
-          for (int s = 0; s < kNB; ++s) {
-            if (s <= t && s >= u) {
-              double fr = 0.0, fi = 0.0;
-#pragma unroll
-              for (int s1 = 0; s1 <= s; ++s1) cmac_add(fr, fi, s_M[s][s1], dd[s1]);
-              ff[s] = make_double2(fr, fi);
-              Fc[s] = ff[s];
-              Dc[s] = dd[s];
-            }
+          for (int s1 = 0; s1 < kNB; ++s1) {  // f_s = Σ_{s1<=s} M[s][s1] d_s1, ascending
+            const double dx = __shfl_sync(0xffffffffu, dl.x, s1, 16);
+            const double dy = __shfl_sync(0xffffffffu, dl.y, s1, 16);
+            if (mine && s1 <= s) cmac_add(fr, fi, s_M[s][s1], make_double2(dx, dy));
           }
+          if (mine) {
+            fl = make_double2(fr, fi);
+            Fc[s] = fl;
+            Dc[s] = dl;
+          }
+          double rr0 = 0.0, ri0 = 0.0;
 #pragma unroll
-          for (int s = 0; s < kNB; ++s) {
-            if (s <= t && s >= u) {
-              double rsr = 0.0, rsi = 0.0;
+          for (int s1 = 0; s1 < kNB; ++s1) {  // R = y_s − Σ_{s1<=s} V[j0+s, s1] f_s1, ascending
+            const double fx = __shfl_sync(0xffffffffu, fl.x, s1, 16);
+            const double fy = __shfl_sync(0xffffffffu, fl.y, s1, 16);
+            if (mine && s1 <= s) cmac_add(rr0, ri0, sV[s1 * RP + s], make_double2(fx, fy));
+          }
+          const double2 Rj = make_double2(__dsub_rn(yl.x, rr0), __dsub_rn(yl.y, ri0));
+          const double nu2_0 = ok ? nu_s[i] : 0.0, ref2_0 = ok ? ref_s[i] : 0.0;
+          double nu2 = nu2_0, ref2 = ref2_0;
+          // fast path: the downdates in s order without a recompute (unrolled; the shuffles do
+          // not depend on ν²); if any step of either column would need the exact recompute, both
+          // redo their chain in the general loop below (the same arithmetic)
+          bool slow = false;
 #pragma unroll
-              for (int s1 = 0; s1 <= s; ++s1) cmac_add(rsr, rsi, sV[s1 * RP + s], ff[s1]);
-              const double2 Rj = make_double2(__dsub_rn(ys[s].x, rsr), __dsub_rn(ys[s].y, rsi));
-              yc[j0 + s] = Rj;
-              // downdate ν² ← ν² − |R(j0+s, c)|²; exact recompute when it has cancelled below
-              // kRecompTol of its last exact value (LAPACK zlaqps's safeguard)
-              const double d2 = __fma_rn(-Rj.x, Rj.x, __fma_rn(-Rj.y, Rj.y, nu2));
-              const bool need = !(nu2 > 0.0) || !(d2 > kRecompTol * ref2);
+          for (int s1 = 0; s1 < kNB; ++s1) {
+            const double rx = __shfl_sync(0xffffffffu, Rj.x, s1, 16);
+            const double ry = __shfl_sync(0xffffffffu, Rj.y, s1, 16);
+            if (ok && s1 >= u && s1 <= t) {
+              const double d2 = __fma_rn(-rx, rx, __fma_rn(-ry, ry, nu2));
+              slow |= !(nu2 > 0.0) || !(d2 > kRecompTol * ref2);
               nu2 = d2 > 0.0 ? d2 : 0.0;
-              if (need) {  // rare, this thread alone: rows j0+s+1..l-1 of y^(j0+s+1)
-                double nn = 0.0;
-                for (int rr = s + 1; rr < Lp; ++rr) {
-                  double2 z = __ldcg(yc + j0 + rr);
-#pragma unroll
-                  for (int s1 = 0; s1 <= s; ++s1) cmac_sub(z, sV[s1 * RP + rr], ff[s1]);
-                  nn = __fma_rn(z.x, z.x, nn);
-                  nn = __fma_rn(z.y, z.y, nn);
-                }
-                nu2 = nn;
-                ref2 = nn;
-              }
             }
           }
-          nu_s[i] = nu2;
-          ref_s[i] = ref2;
-          upd_s[i] = t + 1;
+          slow = __any_sync(0xffffffffu, slow);
+          if (slow) {
+            nu2 = nu2_0;
+            ref2 = ref2_0;
+          }
+          const int ulo = slow ? min(u, __shfl_xor_sync(0xffffffffu, u, 16)) : t + 1;
+          for (int s1 = ulo; s1 <= t; ++s1) {  // ν² ← ν² − |R(j0+s1, c)|²
+            const double rx = __shfl_sync(0xffffffffu, Rj.x, s1, 16);
+            const double ry = __shfl_sync(0xffffffffu, Rj.y, s1, 16);
+            const bool act = ok && s1 >= u;
+            const double d2 = __fma_rn(-rx, rx, __fma_rn(-ry, ry, nu2));
+            const bool need = act && (!(nu2 > 0.0) || !(d2 > kRecompTol * ref2));
+            if (act) nu2 = d2 > 0.0 ? d2 : 0.0;
+            if (__any_sync(0xffffffffu, need)) {
+              // rare: exact ν² of rows j0+s1+1..l-1 of y^(j0+s1+1) (Y not yet written), the
+              // column's 16 lanes over rows s + 16 q
+              double nn = 0.0;
+              for (int q = 0; q < 2 * qn; ++q) {
+                const int r = s + 16 * q;
+                const bool in = need && r > s1 && r < Lp;
+                double2 z = in ? yc[j0 + r] : make_double2(0.0, 0.0);
+                for (int s2 = 0; s2 <= s1; ++s2) {
+                  const double fx = __shfl_sync(0xffffffffu, fl.x, s2, 16);
+                  const double fy = __shfl_sync(0xffffffffu, fl.y, s2, 16);
+                  if (in) cmac_sub(z, sV[s2 * RP + r], make_double2(fx, fy));
+                }
+                nn = __fma_rn(z.x, z.x, nn);
+                nn = __fma_rn(z.y, z.y, nn);
+              }
+#pragma unroll
+              for (int m = 8; m >= 1; m >>= 1) nn = __dadd_rn(nn, __shfl_xor_sync(0xffffffffu, nn, m));
+              if (need) nu2 = ref2 = nn;
+            }
+          }
+          (void)hmask;
+          if (mine) yc[j0 + s] = Rj;
+          if (ok && s == 0) {
+            nu_s[i] = nu2;
+            ref_s[i] = ref2;
+            upd_s[i] = t + 1;
+          }
         }
         __syncthreads();
+        if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 5] += globaltimer() - tB0;
       }
     };
 

@@ -31,7 +31,8 @@ tot = (t[-1, 4] - t[0, 1]) / 1e6
 print(f"{c.name} variant {variant}: qrcp traced span {tot:.2f} ms (diag t_qrcp {r.diag['t_qrcp']*1e3:.2f} ms)"
       f"; sum pivot+hh {d_piv.sum()/1e3:.2f} ms, pass {d_upd.sum()/1e3:.2f} ms, barrier {d_bar.sum()/1e3:.2f} ms,"
       f" gaps {gap.sum()/1e3:.2f} ms")
-if t.shape[1] > 5 and t[:, 5].any():  # ring kernel: pivot | x-build | zlarfg + sv | G
+lazy = t.shape[1] > 8 and t[:, 7].any()
+if t.shape[1] > 5 and t[:, 5].any() and not lazy:  # ring kernel: pivot | x-build | zlarfg + sv | G
     d_a = (t[:, 5] - t[:, 1]) / 1e3
     d_b = (t[:, 6] - t[:, 5]) / 1e3
     d_c = (t[:, 7] - t[:, 6]) / 1e3
@@ -46,7 +47,10 @@ for a, b in zip(edges[:-1], edges[1:]):
     print(f" steps {a:4d}-{b:4d}: pivot+hh {d_piv[a:b].mean():7.2f} us  pass {d_upd[a:b].mean():8.2f} us"
           f"  barrier {d_bar[a:b].mean():6.2f} us  gap {gap[a:b-1].mean() if b - 1 > a else 0:7.2f} us"
           f"  (rows {c.l-a}..{c.l-b+1})")
-if t.shape[1] > 8 and t[:, 7].any():  # lazy kernel: columns refreshed per step (all CTAs), retries
+if lazy:  # lazy kernel: columns refreshed per step (all CTAs), retries; CTA 0's phase A / B ns
+    full = np.arange(c.k) % 16 == 15
+    print(f" lazy: CTA 0 phase A {t[:, 5].sum()/1e6:.2f} ms (full passes {t[full, 5].sum()/1e6:.2f}),"
+          f" phase B {t[:, 6].sum()/1e6:.2f} ms (full passes {t[full, 6].sum()/1e6:.2f})")
     print(f" lazy: columns refreshed {t[:, 7].sum():.0f} (full refresh would be "
           f"{sum(c.n - j for j in range(c.k))}), retried steps {int((t[:, 8] > 0).sum())}")
     for a, b in zip(edges[:-1], edges[1:]):
