@@ -926,6 +926,33 @@ CrtPlan crt_plan(int64_t l, int64_t m) {
   return p;
 }
 
+// More K slices than exactness needs when a small sketch's GEMM work items (T x slices x column
+// tiles x row tiles) would leave the last wave of num_sms CTAs mostly idle (C3: 15 x 32 items =
+// 3.2 waves -> 2 slices, 6.5 waves). The slices' residues are summed mod p, so Y is bitwise the
+// same for any slicing; large sketches (>= 8 waves) keep the minimum.
+void crt_balance(CrtPlan& p, int64_t ncols, int num_sms) {
+  if (num_sms < 1) return;
+  const int64_t tiles = (ncols + 127) / 128;
+  const int64_t base = (int64_t)p.T * p.chunks * tiles;
+  if (base * p.kslices >= 8 * (int64_t)num_sms) return;
+  const int64_t kb = (2 * p.mh + 127) / 128;  // 128-byte K blocks of K' = 2 mh
+  int best = p.kslices;
+  double beff = 0.0;
+  for (int ks = p.kslices; ks <= 4; ++ks) {
+    if (kb / ks < 16) break;  // keep >= 2048 K per item
+    const int64_t items = base * ks;
+    const double eff = (double)items / (double)(((items + num_sms - 1) / num_sms) * num_sms);
+    if (eff > beff + 0.02) {
+      beff = eff;
+      best = ks;
+    }
+  }
+  if (best == p.kslices) return;
+  p.kslices = best;
+  p.kbps = (int)((kb + p.kslices - 1) / p.kslices);
+  p.Kp = (int64_t)p.kslices * p.kbps * 128;
+}
+
 size_t crt_R_bytes(const CrtPlan& p) {  // Rres + rowmax
   return (size_t)p.T * 2 * p.lp * p.Kp + 8 * (size_t)p.lp + 256;
 }

@@ -1348,7 +1348,8 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
   int* upd_s = reinterpret_cast<int*>(ref_s + per);             // [per] u: panel steps applied
   int* list = upd_s + per;                                      // [per] the pass's columns
   __shared__ double2 s_G[kNB][kNB];  // s_G[t][s] = v_tᴴ v_s, s < t
-  __shared__ double2 s_M[kNB][kNB];  // f = M d: M = (I + D_conj(τ) G)^-1 D_conj(τ), lower
+  __shared__ double2 s_M[kNB][kNB + 1];  // f = M d: M = (I + D_conj(τ) G)^-1 D_conj(τ), lower
+                                         // (padded: phase B's lanes read a column of it)
   __shared__ double2 s_fp[kNB];      // f_s(p) of the step's pivot
   __shared__ double s_red[kLazyWarps];
   __shared__ double s_par[2];

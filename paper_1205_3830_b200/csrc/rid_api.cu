@@ -509,6 +509,7 @@ rid_status fill_R(rid_ctx* c, uint64_t seed, uint32_t s, int64_t l, int64_t m, i
   if (use_crt(c, l, m, n)) {
     out->crt = true;
     out->cp = rid::crt_plan(l, m);
+    if (!rid::select_env("RID_CRT_NOBALANCE")) rid::crt_balance(out->cp, n, c->num_sms);
     RID_TRY(ws_get(c, "Rcrt", rid::crt_R_bytes(out->cp), &out->crtR));
     RID_CUDA(c, rid::crt_prep_R(out->cp, (const double2*)pR, l, l, m, out->crtR, c->stream,
                                 launches));

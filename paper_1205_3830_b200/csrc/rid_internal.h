@@ -270,6 +270,7 @@ struct CrtPlan {
   int cn[8], coff[8];  // row tile c: cn[c] rows from row coff[c] (nc = the largest)
 };
 CrtPlan crt_plan(int64_t l, int64_t m);
+void crt_balance(CrtPlan& p, int64_t ncols, int num_sms);  // extra K slices for wave balance
 int crt_moduli(int* p, int cap);
 double crt_log2M(int T);
 size_t crt_R_bytes(const CrtPlan& p);                  // R's residue operands + row maxima

@@ -294,3 +294,16 @@ def test_crt_multirank_bitwise(rid, orc):
         for c in ctxs:
             c.close()
     one.close()
+
+
+@pytest.mark.parametrize("m,n,l", [(8192, 2048, 144), (65536, 512, 144), (4096, 1000, 80)])
+def test_crt_kslice_balance_bitwise(rid, ctx, monkeypatch, m, n, l):
+    """Small sketches get extra K slices so that the GEMM's work items fill the waves (C3: 2
+    slices); the slices' residues are summed mod p, so Y has the same bits with and without
+    (RID_CRT_NOBALANCE=1)."""
+    seed = 12
+    A = rid.generate(seed, m, n, 32, 1e-10, ctx=ctx)
+    Y1 = np_(rid.sketch(A, seed, l, ctx=ctx))
+    monkeypatch.setenv("RID_CRT_NOBALANCE", "1")
+    Y0 = np_(rid.sketch(A, seed, l, ctx=ctx))
+    assert bits_equal(Y1, Y0)

@@ -2,7 +2,7 @@
 # ncu evidence for a bench config: launch list of one bench step + full sets of the sketch's
 # kernels and of the QR. INT8_CRT engine (C3-C5 default): one k_imma launch (the tcgen05 int8 GEMM,
 # one of the sketch's column blocks), one k_crt_prepA and one k_crt_rec; DMMA engine (ENGINE=dmma
-# or C1/C2): the sketch launches (SK, NSK). Then one blocked-QRCP panel (k_qrcp_ring) and one QRCP
+# or C1/C2): the sketch launches (SK, NSK). Then one blocked-QRCP panel (QRK: k_qrcp_lazy at C4, k_qrcp_ring at C5) and one QRCP
 # trailing update (k_zgemm_dmma mode 2). Each ncu pass runs only after the plain command exits 0.
 CFG=${CFG:-C4}
 CMD="python bench.py --config $CFG --steps 1 --warmup 1 --q 1 --no-e2e --no-cpu-baseline"
@@ -21,6 +21,6 @@ else
     ncu --set full --metrics sm__inst_executed_pipe_tensor_subpipe_dmma.sum --clock-control none --import-source on -k regex:$SK -s $((NSK + i)) -c 1 -o gpurun_out/prof_sketch${i}_$CFG -f $CMD > gpurun_out/ncu_sketch$i.log 2>&1
   done
 fi
-ncu --set full --clock-control none --import-source on -k regex:k_qrcp_ring -s 8 -c 1 -o gpurun_out/prof_qrcp_$CFG -f $CMD > gpurun_out/ncu_qrcp.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:${QRK:-k_qrcp_lazy} -s ${QRS:-1} -c 1 -o gpurun_out/prof_qrcp_$CFG -f $CMD > gpurun_out/ncu_qrcp.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_zgemm_dmma -s 12 -c 1 -o gpurun_out/prof_update_$CFG -f $CMD > gpurun_out/ncu_update.log 2>&1
 echo "exit $?"
