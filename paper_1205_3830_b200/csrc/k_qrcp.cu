@@ -1275,7 +1275,7 @@ constexpr int kLazyThreads = 256;
 constexpr int kLazyWarps = kLazyThreads / 32;
 constexpr int kLazyChunk = 128;  // columns per phase A / phase B round (s_d rows)
 constexpr int kLazySD = kNB + 1;  // s_d row stride in double2 (conflict-free 16-byte rows)
-constexpr int kLazyScratch = 2 * 4 * 2 * 4 * 32 * 2;  // phase A partials [slot][pp][mt][prod]
+constexpr int kLazyScratch = 8 * 2 * 4 * 32 * 2;  // phase A partials [pp][mt][prod][lane][2]
 
 // Top three exact norms (ties of the first to the lowest index) and the largest bound among the
 // columns NOT refreshed at this step (m): the exchange record of the lazy kernel.
@@ -1338,11 +1338,11 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
   constexpr int RP = 32 * MAXQ + 4;  // sV row stride: rows j0..j0+32·MAXQ−1, +64 B so that the
                                       // DMMA A fragments (8 s x 4 rows) hit 32 distinct banks
   constexpr int XQ = (32 * MAXQ + kLazyThreads - 1) / kLazyThreads;
-  constexpr int KQ = 2 * MAXQ;  // k-steps (4 rows) per partial: 4 partials x KQ x 4 >= 32 MAXQ
+  constexpr int KQ = MAXQ;  // k-steps (4 rows) per partial: 8 partials x KQ x 4 >= 32 MAXQ
   extern __shared__ __align__(16) unsigned char lz_smem[];
   double2* sV = reinterpret_cast<double2*>(lz_smem);           // [kNB][RP]: v_s, zero above j0+s
   double2* s_d = sV + kNB * RP;                                 // [kLazyChunk][kLazySD]: d_s
-  double* s_sc = reinterpret_cast<double*>(s_d + kLazyChunk * kLazySD);  // [2][4][8][64]
+  double* s_sc = reinterpret_cast<double*>(s_d + kLazyChunk * kLazySD);  // [8][8][64]
   double* nu_s = s_sc + kLazyScratch;                           // [per] ν² bound (exact at j0+u)
   double* ref_s = nu_s + per;                                   // [per] ν² at the last recompute
   int* upd_s = reinterpret_cast<int*>(ref_s + per);             // [per] u: panel steps applied
@@ -1633,15 +1633,16 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
         const int nch = min(kLazyChunk, cnt - e0);
         // phase A on the FP64 tensor pipe: d_s(c) = v_sᴴ y^(j0)_c for 8 columns x 16 s per tile
         // (DMMA m8n8k4: A = V from shared memory, B = Y straight from global memory), K = the
-        // panel rows in 4-row steps; step κ goes to partial κ mod 4 (four warps per tile), and
-        // each of the four real products Vx·Yx, Vy·Yy, Vx·Yy, Vy·Yx is its own ascending DMMA
-        // chain (eight independent chains per warp: the DMMA latency is ≈ 8 issues deep);
-        // per product (P0 + P1) + (P2 + P3), then Re d = XX + YY, Im d = XY − YX. Per (s, c) the
-        // bits depend only on v_s and y_c: not on the tile, the pass or the other columns. A
-        // warp's loads for its next tile are issued before the combine (all KQ in flight).
+        // panel rows in 4-row steps; step κ goes to partial κ mod 8 (the eight warps of a tile:
+        // short chains for the few-column lazy passes), and each of the four real products
+        // Vx·Yx, Vy·Yy, Vx·Yy, Vy·Yx is its own ascending DMMA chain (eight independent chains per
+        // warp: the DMMA latency is ≈ 8 issues deep); per product the eight partials summed
+        // pairwise in a fixed tree, then Re d = XX + YY, Im d = XY − YX. Per (s, c) the bits
+        // depend only on v_s and y_c: not on the tile, the pass or the other columns. The next
+        // tile's loads are issued before the combine.
         const unsigned long long tA0 = (w.trace && b == 0) ? globaltimer() : 0ull;
         const int ntile = (nch + 7) / 8;
-        const int slot = warp >> 2, pp = warp & 3, gq = lane >> 2, tq = lane & 3;
+        const int pp = warp, gq = lane >> 2, tq = lane & 3;  // warp = partial
         double2 yv[KQ];
         int uc = kNB;
         auto load_tile = [&](int tl) {
@@ -1652,77 +1653,64 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
           const double2* yc = Y + (c_lo + ic) * ldy + j0;
 #pragma unroll
           for (int i = 0; i < KQ; ++i) {
-            const int r = 4 * (pp + 4 * i) + tq;
+            const int r = 4 * (pp + 8 * i) + tq;
             // rows >= u of y^(j0) are not written during this launch (only rows j0..j0+u−1
             // receive R), so the read-only path is coherent for every row read here
             yv[i] = (cv && r < Lp && r >= uc) ? __ldg(yc + r) : make_double2(0.0, 0.0);
           }
         };
-        // the bulk-copy engine pulls a tile's columns into L2 two rounds ahead (the B-fragment
-        // loads below are load-store-unit bound from HBM: lg_throttle in ncu)
-        auto prefetch_tile = [&](int tl) {
-          const int ecol = tl * 8 + lane;
-          if (pp == 0 && lane < 8 && tl < ntile && ecol < nch) {
-            const int ic = list[e0 + ecol];
-            const int u = upd_s[ic];
-            if (u < Lp)
-              bulk_prefetch_l2(Y + (c_lo + ic) * ldy + j0 + u, (unsigned)(Lp - u) * 16u);
-          }
-        };
-        prefetch_tile(slot + 2);
-        load_tile(slot);
-        for (int tb = 0; tb < ntile; tb += 2) {  // two tiles per round, four warps each
-          const int tl = tb + slot;
-          prefetch_tile(tb + 4 + slot);
-          if (tl < ntile) {
-            const int slo = __reduce_min_sync(0xffffffffu, uc);
-            const bool mt0 = slo <= 7, mt1 = t >= 8;
-            // eight independent DMMA chains per warp: [M tile][Vx·Yx, Vy·Yy, Vx·Yy, Vy·Yx]
-            double acc[16];
+        load_tile(0);
+        for (int tl = 0; tl < ntile; ++tl) {  // one tile per round, eight warps (partials)
+          const int slo = __reduce_min_sync(0xffffffffu, uc);
+          const bool mt0 = slo <= 7, mt1 = t >= 8;
+          // eight independent DMMA chains per warp: [M tile][Vx·Yx, Vy·Yy, Vx·Yy, Vy·Yx]
+          double acc[16];
 #pragma unroll
-            for (int a = 0; a < 16; ++a) acc[a] = 0.0;
+          for (int a = 0; a < 16; ++a) acc[a] = 0.0;
 #pragma unroll
-            for (int i = 0; i < KQ; ++i) {
-              const int ks = pp + 4 * i;
-              if (ks < nks) {
-                const int r = 4 * ks + tq;
-                if (mt0) {
-                  const double2 a = sV[gq * RP + r];
-                  dmma8x8x4_nv(acc[0], acc[1], a.x, yv[i].x);
-                  dmma8x8x4_nv(acc[2], acc[3], a.y, yv[i].y);
-                  dmma8x8x4_nv(acc[4], acc[5], a.x, yv[i].y);
-                  dmma8x8x4_nv(acc[6], acc[7], a.y, yv[i].x);
-                }
-                if (mt1) {
-                  const double2 a = sV[(8 + gq) * RP + r];
-                  dmma8x8x4_nv(acc[8], acc[9], a.x, yv[i].x);
-                  dmma8x8x4_nv(acc[10], acc[11], a.y, yv[i].y);
-                  dmma8x8x4_nv(acc[12], acc[13], a.x, yv[i].y);
-                  dmma8x8x4_nv(acc[14], acc[15], a.y, yv[i].x);
-                }
+          for (int i = 0; i < KQ; ++i) {
+            const int ks = pp + 8 * i;
+            if (ks < nks) {
+              const int r = 4 * ks + tq;
+              if (mt0) {
+                const double2 a = sV[gq * RP + r];
+                dmma8x8x4_nv(acc[0], acc[1], a.x, yv[i].x);
+                dmma8x8x4_nv(acc[2], acc[3], a.y, yv[i].y);
+                dmma8x8x4_nv(acc[4], acc[5], a.x, yv[i].y);
+                dmma8x8x4_nv(acc[6], acc[7], a.y, yv[i].x);
+              }
+              if (mt1) {
+                const double2 a = sV[(8 + gq) * RP + r];
+                dmma8x8x4_nv(acc[8], acc[9], a.x, yv[i].x);
+                dmma8x8x4_nv(acc[10], acc[11], a.y, yv[i].y);
+                dmma8x8x4_nv(acc[12], acc[13], a.x, yv[i].y);
+                dmma8x8x4_nv(acc[14], acc[15], a.y, yv[i].x);
               }
             }
-            // scratch [slot][pp][mt * 4 + product][lane][2]
-            double* sc = s_sc + (size_t)((slot * 4 + pp) * 8) * 64;
-#pragma unroll
-            for (int a = 0; a < 8; ++a) {
-              sc[a * 64 + lane * 2 + 0] = acc[2 * a];
-              sc[a * 64 + lane * 2 + 1] = acc[2 * a + 1];
-            }
           }
-          if (tb + 2 < ntile) load_tile(tb + 2 + slot);  // in flight during the combine
+          // scratch [pp][mt * 4 + product][lane][2]
+          double* sc = s_sc + (size_t)(pp * 8) * 64;
+#pragma unroll
+          for (int a = 0; a < 8; ++a) {
+            sc[a * 64 + lane * 2 + 0] = acc[2 * a];
+            sc[a * 64 + lane * 2 + 1] = acc[2 * a + 1];
+          }
+          if (tl + 1 < ntile) load_tile(tl + 1);  // in flight during the combine
           __syncthreads();
-          // each product (P0 + P1) + (P2 + P3); Re d = XX + YY, Im d = XY − YX -> s_d[entry][s]
-          for (int idx = threadIdx.x; idx < 2 * 2 * 2 * 64; idx += kLazyThreads) {
-            const int sl = idx >> 8, mt = (idx >> 7) & 1, ri = (idx >> 6) & 1, o = idx & 63;
-            const int tt2 = tb + sl;
+          // each product ((P0 + P1) + (P2 + P3)) + ((P4 + P5) + (P6 + P7)); Re d = XX + YY,
+          // Im d = XY − YX -> s_d[entry][s]
+          {
+            const int idx = threadIdx.x;  // 2 x 2 x 64 = 256 outputs
+            const int mt = idx >> 7, ri = (idx >> 6) & 1, o = idx & 63;
             const int ln = o >> 1, bb = o & 1;
-            const int s = 8 * mt + (ln >> 2), ecol = tt2 * 8 + 2 * (ln & 3) + bb;
-            if (tt2 < ntile && ecol < nch && s <= t) {
-              const double* sc = s_sc + (size_t)(sl * 32 + mt * 4 + 2 * ri) * 64 + o;  // pp stride 512
-              const double p0 = __dadd_rn(__dadd_rn(sc[0], sc[512]), __dadd_rn(sc[1024], sc[1536]));
-              const double p1 =
-                  __dadd_rn(__dadd_rn(sc[64], sc[576]), __dadd_rn(sc[1088], sc[1600]));
+            const int s = 8 * mt + (ln >> 2), ecol = tl * 8 + 2 * (ln & 3) + bb;
+            if (ecol < nch && s <= t) {
+              const double* sc0 = s_sc + (size_t)(mt * 4 + 2 * ri) * 64 + o;  // pp stride 512
+              auto psum = [&](const double* q) {
+                return __dadd_rn(__dadd_rn(__dadd_rn(q[0], q[512]), __dadd_rn(q[1024], q[1536])),
+                                 __dadd_rn(__dadd_rn(q[2048], q[2560]), __dadd_rn(q[3072], q[3584])));
+              };
+              const double p0 = psum(sc0), p1 = psum(sc0 + 64);
               reinterpret_cast<double*>(s_d + ecol * kLazySD + s)[ri] =
                   ri == 0 ? __dadd_rn(p0, p1) : __dsub_rn(p0, p1);
             }
@@ -1737,7 +1725,6 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
         // order, identical on the 16 lanes of the column
         for (int e1 = 2 * warp; e1 < nch; e1 += 2 * kLazyWarps) {
           const int hf = lane >> 4, s = lane & 15;
-          const unsigned hmask = hf ? 0xffff0000u : 0x0000ffffu;
           const int e = e1 + hf;
           const bool ok = e < nch;  // uniform over the half-warp
           const int i = ok ? list[e0 + e] : list[e0 + e1];
@@ -1827,7 +1814,6 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
               if (need) nu2 = ref2 = nn;
             }
           }
-          (void)hmask;
           if (mine) yc[j0 + s] = Rj;
           if (ok && s == 0) {
             nu_s[i] = nu2;
