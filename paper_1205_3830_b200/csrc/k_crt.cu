@@ -1172,8 +1172,11 @@ static cudaError_t crt_prep_A(const CrtPlan& p, const CrtBlockWs& w, const doubl
   // CTAs per cluster (per column): 1 by default (a plain launch). Clusters of 2-8 CTAs read each
   // column from DRAM exactly once (CL = 4: 4.30 vs 6.08 GB per C4 block) but are slower: the
   // kernel is issue-bound, and GPC packing leaves SMs idle (CL = 4: 132 of 148 CTAs resident)
-  int CL = 1;
-  if (const char* v = experiment_env("RID_CRT_PREP_CLUSTER")) CL = std::max(1, std::min(8, atoi(v)));
+  // a CTA pair per column for the tall matrices (m > 65536: C5's 2 MB columns miss L2 on the
+  // second read; measured C5 sketch 104.9 -> 102.8 ms at CL = 2, 105.0 / 106.6 at CL = 4 / 8;
+  // C4 unchanged at CL = 2, slower beyond): RID_CRT_PREP_CLUSTER selects
+  int CL = m > 65536 ? 2 : 1;
+  if (const char* v = select_env("RID_CRT_PREP_CLUSTER")) CL = std::max(1, std::min(8, atoi(v)));
   int thr = 1024;
   if (const char* v = experiment_env("RID_CRT_PREP_THREADS")) thr = std::max(128, std::min(1024, atoi(v)));
   const int64_t nclu = std::max<int64_t>(1, std::min<int64_t>(ncols, num_sms / CL));

@@ -307,3 +307,14 @@ def test_crt_kslice_balance_bitwise(rid, ctx, monkeypatch, m, n, l):
     monkeypatch.setenv("RID_CRT_NOBALANCE", "1")
     Y0 = np_(rid.sketch(A, seed, l, ctx=ctx))
     assert bits_equal(Y1, Y0)
+
+
+def test_crt_prep_cluster_bitwise(rid, ctx, monkeypatch):
+    """Tall matrices (m > 65536) prepare each column with a CTA pair (partial maxima over
+    distributed shared memory); any cluster size gives the same residues, so the same Y."""
+    m, n, l, seed = 70000, 300, 80, 13
+    A = rid.generate(seed, m, n, 16, 1e-10, ctx=ctx)
+    Y2 = np_(rid.sketch(A, seed, l, ctx=ctx))
+    for cl in ("1", "4"):
+        monkeypatch.setenv("RID_CRT_PREP_CLUSTER", cl)
+        assert bits_equal(np_(rid.sketch(A, seed, l, ctx=ctx)), Y2), cl
