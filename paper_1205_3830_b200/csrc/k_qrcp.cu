@@ -1243,7 +1243,7 @@ __global__ void __launch_bounds__(kRingThreads, 1)
 }
 
 // =============================================================================================
-// Lazy-refresh blocked variant (default for l <= 544: C4, C5).
+// Lazy-refresh blocked variant (default for blocked sketches with 384 < l <= 544: C4).
 //
 // The ring kernel above streams rows j..l−1 of EVERY unchosen column at every step (C4: 73 GB
 // over 512 steps) because the greedy rule (R8) needs the exact maximum residual norm. But a
@@ -1254,8 +1254,8 @@ __global__ void __launch_bounds__(kRingThreads, 1)
 // and at step j refreshes ONLY the columns whose bound is >= a threshold τ_j:
 //   phase A (FP64 tensor pipe, 8 columns x 16 reflectors per DMMA tile): d_s = v_sᴴ y^(j0)_c for
 //     s = u..t, V of the panel in shared memory, y^(j0)_c[j0+u:l] read once from global memory;
-//   phase B (one lane per column): for s = u..t in order
-//       f_s = conj(τ_s)·(d_s − Σ_{s'<s} (v_sᴴ v_s') f_s'),
+//   phase B (a half-warp per column): for s = u..t in order
+//       f_s = conj(τ_s)·(d_s − Σ_{s'<s} (v_sᴴ v_s') f_s')   (as f = M d, M built once per step),
 //       R(j0+s, c) = y^(j0)_c[j0+s] − Σ_{s'<=s} V[j0+s, s'] f_s',
 //       ν² ← ν² − |R(j0+s, c)|²  (exact recompute below kRecompTol·ν_ref², as the ring kernel).
 // A column's arithmetic is fixed (fixed lanes, fixed reduction orders, the same per-s formulas),
