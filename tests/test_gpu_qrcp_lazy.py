@@ -89,6 +89,10 @@ CASES = [  # (name, builder, k)
     ("twins", lambda: twins_Y(4, 144, 2000), 128),
     ("geometric", lambda: geometric_Y(5, 200, 3000), 180),
     ("n < CTAs", lambda: lowrank_Y(6, 64, 100, 48, 1e-9), 48),
+    # > 64 columns per CTA: the thread-per-column phase B of the full passes, and its handover
+    # of the columns whose downdate needs the exact recompute (the twins) to the half-warp form
+    ("twins wide", lambda: twins_Y(9, 144, 12000), 128),
+    ("wide l=528", lambda: lowrank_Y(10, 528, 12000, 512, 1e-8), 512),
 ]
 
 
