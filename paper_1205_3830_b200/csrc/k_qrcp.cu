@@ -1362,7 +1362,7 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
   double2* __restrict__ Y = sh.Y[g];
   const QrcpOut& out = sh.out[g];
   const QrcpWork& w = sh.w[g];
-  double* const cand = sh.w[0].cand;  // 2 buffers x max_blocks x 5 doubles
+  double* const cand = sh.w[0].cand;  // 2 buffers x max_blocks x 8 doubles
   unsigned* const bar = sh.w[0].bar;
   const int max_blocks = sh.w[0].max_blocks;
   const int64_t n = sh.n_loc;
@@ -1390,35 +1390,31 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
   }
   __syncthreads();
 
-  // grid-wide record of the last exchange -> s_top
+  int jx = -1;  // (trace) the step whose exchange is timed
+  // grid-wide record of the last exchange -> s_top: every warp merges a slice of the records
+  // (one per lane, two 16-byte loads), then thread 0 the eight warp results (order-free merges)
   auto read_top = [&]() {
-    if (warp == 0) {
-      Top3 tt;
-      top3_init(tt);
-      const double* cb = cand + (size_t)xc * max_blocks * 5;
-      for (int q0 = 0; q0 < nbk; q0 += 32 * 5) {  // five records per lane, all loads first
-        double rv[5][5];
-#pragma unroll
-        for (int a = 0; a < 5; ++a) {
-          const int q = q0 + lane + 32 * a;
-#pragma unroll
-          for (int f = 0; f < 5; ++f) rv[a][f] = q < nbk ? __ldcg(cb + q * 5 + f) : -1.0;
-        }
-#pragma unroll
-        for (int a = 0; a < 5; ++a) {
-          if (q0 + lane + 32 * a < nbk) {
-            Top3 o;
-            o.b1 = rv[a][0];
-            o.b2 = rv[a][1];
-            o.b3 = rv[a][2];
-            o.m = rv[a][3];
-            o.i1 = (long long)rv[a][4];
-            top3_merge(tt, o);
-          }
-        }
-      }
-      top3_warp(tt);
-      if (lane == 0) s_top = tt;
+    Top3 tt;
+    top3_init(tt);
+    const double* cb = cand + (size_t)xc * max_blocks * 8;
+    for (int q = threadIdx.x; q < nbk; q += kLazyThreads) {
+      const double2 v0 = __ldcg(reinterpret_cast<const double2*>(cb + q * 8));
+      const double2 v1 = __ldcg(reinterpret_cast<const double2*>(cb + q * 8 + 2));
+      Top3 o;
+      o.b1 = v0.x;
+      o.b2 = v0.y;
+      o.b3 = v1.x;
+      o.m = v1.y;
+      o.i1 = (long long)__ldcg(cb + q * 8 + 4);
+      top3_merge(tt, o);
+    }
+    top3_warp(tt);
+    if (lane == 0) sred[warp] = tt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      Top3 a = sred[0];
+      for (int q = 1; q < kLazyWarps; ++q) top3_merge(a, sred[q]);
+      s_top = a;
     }
     __syncthreads();
   };
@@ -1442,16 +1438,20 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
     if (threadIdx.x == 0) {
       Top3 tt = sred[0];
       for (int q = 1; q < kLazyWarps; ++q) top3_merge(tt, sred[q]);
-      double* cc = cand + ((size_t)(xc ^ 1) * max_blocks + b) * 5;
-      cc[0] = tt.b1;
-      cc[1] = tt.b2;
-      cc[2] = tt.b3;
-      cc[3] = tt.m;
+      double* cc = cand + ((size_t)(xc ^ 1) * max_blocks + b) * 8;  // 64-byte records
+      reinterpret_cast<double2*>(cc)[0] = make_double2(tt.b1, tt.b2);
+      reinterpret_cast<double2*>(cc)[1] = make_double2(tt.b3, tt.m);
       cc[4] = (double)tt.i1;
     }
     xc ^= 1;
+    const unsigned long long tX0 = (w.trace && b == 0) ? globaltimer() : 0ull;
     grid_barrier(bar, (unsigned)nbk * (++phase));
+    const unsigned long long tX1 = (w.trace && b == 0) ? globaltimer() : 0ull;
     read_top();
+    if (w.trace && b == 0 && threadIdx.x == 0 && jx >= 0) {
+      w.trace[8 * jx + 4] += tX1 - tX0;
+      w.trace[8 * jx + 5] += globaltimer() - tX1;
+    }
   };
 
   if (j0 == 0) {  // ---- initial exact column norms² (one warp per column) ----------------------
@@ -1482,6 +1482,7 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
   for (int j = j0; j < jend; ++j) {
     const int t = j - j0;
     const int L = l - j;
+    jx = j;
     if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 0] = globaltimer();
     // ---- 1. the pivot (every CTA identically, from s_top; values are ν²) ---------------------
     const Top3 tt = s_top;
@@ -1640,7 +1641,6 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
         // pairwise in a fixed tree, then Re d = XX + YY, Im d = XY − YX. Per (s, c) the bits
         // depend only on v_s and y_c: not on the tile, the pass or the other columns. The next
         // tile's loads are issued before the combine.
-        const unsigned long long tA0 = (w.trace && b == 0) ? globaltimer() : 0ull;
         const int ntile = (nch + 7) / 8;
         const int pp = warp, gq = lane >> 2, tq = lane & 3;  // warp = partial
         double2 yv[KQ];
@@ -1717,8 +1717,6 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
           }
           __syncthreads();
         }
-        if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 4] += globaltimer() - tA0;
-        const unsigned long long tB0 = (w.trace && b == 0) ? globaltimer() : 0ull;
         // phase B: a half-warp per column, lane s <-> panel step s (compact code: a fully
         // unrolled thread-per-column form ran out of the instruction cache): f = M d (d_s of
         // earlier refreshes of this panel from Dd), R(j0+s, c), then the downdates of ν² in s
@@ -1822,7 +1820,6 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
           }
         }
         __syncthreads();
-        if (w.trace && b == 0 && threadIdx.x == 0) w.trace[8 * j + 5] += globaltimer() - tB0;
       }
     };
 
@@ -1849,7 +1846,7 @@ __global__ void __launch_bounds__(kLazyThreads, 1)
 }
 
 size_t qrcp_work_bytes(int64_t n, int64_t l, int max_blocks) {
-  return (size_t)2 * n * sizeof(double) + (size_t)2 * 6 * max_blocks * sizeof(double) +
+  return (size_t)2 * n * sizeof(double) + (size_t)2 * 8 * max_blocks * sizeof(double) +
          (size_t)l * kNB * sizeof(double2) + (size_t)2 * kNB * n * sizeof(double2) +
          (size_t)2 * max_blocks * l * sizeof(double2) + 512;
 }
@@ -1871,7 +1868,7 @@ QrcpWork qrcp_work_carve(void* buf, int64_t n, int64_t l, int max_blocks) {
   w.nuref = (double*)p;
   p += (size_t)n * sizeof(double);
   w.cand = (double*)p;
-  p += (size_t)2 * 6 * max_blocks * sizeof(double);  // 3 (ring) or 5 (lazy) per CTA
+  p += (size_t)2 * 8 * max_blocks * sizeof(double);  // 3 (ring) or 8 (lazy: 64-byte records) per CTA
   w.scal = (double*)p;
   p += 64;
   w.bar = (unsigned*)p;

@@ -138,8 +138,8 @@ struct QrcpOut {
 };
 struct QrcpWork {
   double* nu;        // n: current residual norms (-1 = chosen)
-  double* cand;      // 2 * 6 * max_blocks doubles: per CTA (best, second, index-as-double) or the
-                     // lazy kernel's (b1, b2, b3, m, index), x 2 parities
+  double* cand;      // 2 * 8 * max_blocks doubles: per CTA (best, second, index-as-double) or the
+                     // lazy kernel's 64-byte (b1, b2, b3, m, index) records, x 2 parities
   unsigned* bar;     // 1
   int max_blocks;
   unsigned long long* trace = nullptr;  // optional: 4 %globaltimer stamps per step (CTA 0)

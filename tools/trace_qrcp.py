@@ -48,9 +48,8 @@ for a, b in zip(edges[:-1], edges[1:]):
           f"  barrier {d_bar[a:b].mean():6.2f} us  gap {gap[a:b-1].mean() if b - 1 > a else 0:7.2f} us"
           f"  (rows {c.l-a}..{c.l-b+1})")
 if lazy:  # lazy kernel: columns refreshed per step (all CTAs), retries; CTA 0's phase A / B ns
-    full = np.arange(c.k) % 16 == 15
-    print(f" lazy: CTA 0 phase A {t[:, 5].sum()/1e6:.2f} ms (full passes {t[full, 5].sum()/1e6:.2f}),"
-          f" phase B {t[:, 6].sum()/1e6:.2f} ms (full passes {t[full, 6].sum()/1e6:.2f})")
+    print(f" lazy: CTA 0 grid-barrier wait {t[:, 5].sum()/1e6:.2f} ms, reading the candidates"
+          f" {t[:, 6].sum()/1e6:.2f} ms (of the exchange, all passes of a step)")
     print(f" lazy: columns refreshed {t[:, 7].sum():.0f} (full refresh would be "
           f"{sum(c.n - j for j in range(c.k))}), retried steps {int((t[:, 8] > 0).sum())}")
     for a, b in zip(edges[:-1], edges[1:]):
