@@ -190,3 +190,16 @@ def test_lazy_fuzz(rid, monkeypatch, i, kind, l, n, k, seed):
     J0, R0, _, mar0, _ = run(rid, monkeypatch, Y, k, "0")
     if float(mar0[:-1].min()) > 1e-9 if k > 1 else True:  # the ring downdates differently
         assert torch.equal(J0, J1)
+
+
+def test_lazy_falls_back_to_ring_when_state_exceeds_shared_memory(rid, monkeypatch):
+    """Per-column state (24 B per column of a CTA) beside the 140 KB reflector panel: beyond
+    ≈ 700 columns per CTA the lazy kernel does not fit and the ring kernel runs instead — the
+    same bits as forcing the ring kernel."""
+    g = torch.Generator().manual_seed(11)
+    l, n, k = 400, 120000, 40
+    Y = torch.complex(torch.randn(l, n, generator=g, dtype=torch.float64),
+                      torch.randn(l, n, generator=g, dtype=torch.float64)).T.contiguous().T.cuda()
+    J1, R1, _, _, _ = run(rid, monkeypatch, Y, k, "1")
+    J0, R0, _, _, _ = run(rid, monkeypatch, Y, k, "0")
+    assert torch.equal(J1, J0) and np.array_equal(bits(R1), bits(R0))
