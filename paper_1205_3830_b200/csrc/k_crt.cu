@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(kImmaThreads, 1)
 // only half of the B tile per MMA. Both CTAs' TMA boxes complete on the leader's "full" barrier
 // (cp.async.bulk.tensor.cta_group::2); the leader's commits are multicast to both CTAs' "empty"
 // and "tfull" barriers; both CTAs' epilogues arrive on the leader's "tempty" barrier.
-// N = nc must be a multiple of 32 (crt_plan rounds it when the pair kernel is selected).
+// N = nc is a multiple of 16: each CTA's half (nc / 2 rows per plane) is whole 8-row SW128 atoms.
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
@@ -867,9 +867,11 @@ CrtHost make_const(int T) {
 }
 
 // the CTA-pair GEMM (k_imma2, cta_group::2): RID_CRT_2SM=1. Measured on one box: ~6% more int8
-// ops per second than k_imma, but N must be a multiple of 32, so its row tiles pad more: C4
-// 34.68 vs 34.91 ms (192 + 192 + 160 rows against 3 x 176), C3 5.37 vs 5.29, C5 116.4 vs 110.7
-// (160 + 128 against 144 + 128). A tested selection, not the default.
+// ops per second than k_imma at fixed clocks; with 32-row granules its row tiles padded more (C4
+// 34.68 vs 34.91 ms, C3 5.37 vs 5.29, C5 116.4 vs 110.7). With 16-row granules (the same tiles as
+// k_imma) it draws more power and the step runs under a lower power-capped clock: C4 sketch 36.2-
+// 37.1 vs 34.7-34.8 ms (SM 1511-1545 vs 1785-1793 MHz), C5 117.7-119.8 vs 106.1-107.4, C3 equal
+// (profiles/r02s16_crt_pair.txt). A tested selection, not the default.
 bool crt_pair_selected() {
   const char* e = select_env("RID_CRT_2SM");
   return e && atoi(e) != 0;
@@ -905,11 +907,11 @@ CrtPlan crt_plan(int64_t l, int64_t m) {
   p.kslices = (int)((K2 + kmax - 1) / kmax);
   p.kbps = (int)(((K2 + 127) / 128 + p.kslices - 1) / p.kslices);
   p.Kp = (int64_t)p.kslices * p.kbps * 128;
-  // row tiles: l rounded to the MMA's N granule (16; 32 for the CTA pair), split into
-  // ceil(rows / 256) tiles whose sizes differ by at most one granule (C4: 3 x 176, pair 192 + 192
-  // + 160; C5: 144 + 128)
+  // row tiles: l rounded to the MMA's N granule (16, also for the CTA pair: M = 256 takes any
+  // N % 16 == 0 and each CTA's half, N / 2 rows, is whole 8-row swizzle atoms), split into
+  // ceil(rows / 256) tiles whose sizes differ by at most one granule (C4: 3 x 176; C5: 144 + 128)
   p.pair = crt_pair_selected();
-  const int64_t gran = p.pair ? 32 : 16;
+  const int64_t gran = 16;
   const int64_t units = (l + gran - 1) / gran;
   p.chunks = (int)((units * gran + 255) / 256);
   if (p.chunks > kCrtMaxChunks) p.chunks = kCrtMaxChunks;  // l > 2048: callers use DMMA
