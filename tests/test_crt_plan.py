@@ -54,3 +54,17 @@ def test_plan_bounds(rid, l, m):
     # tile rows: multiples of 16, at most 256 (the Re and Im accumulators share 512 TMEM columns)
     l16 = (l + 15) // 16 * 16
     assert nc % 16 == 0 and 16 <= nc <= 256 and nc * math.ceil(l16 / nc) >= l
+
+
+@pytest.mark.parametrize("l,m", [(528, 32768), (272, 131072), (144, 65536), (16, 1024), (400, 2048)])
+def test_pair_plan_same_tiles(rid, monkeypatch, l, m):
+    """The CTA-pair GEMM (RID_CRT_2SM=1) uses the single-CTA kernel's 16-row granules: the same row
+    tiles (C4 l = 528: 3 x 176, 88 rows per CTA of the pair; C5 l = 272: 144 + 128), and each
+    CTA's half is whole 8-row 128-byte swizzle atoms."""
+    base = rid.crt_plan(l, m)
+    monkeypatch.setenv("RID_CRT_2SM", "1")
+    pair = rid.crt_plan(l, m)
+    assert pair == base
+    assert pair["nc"] % 16 == 0 and (pair["nc"] // 2) % 8 == 0
+    if (l, m) == (528, 32768):
+        assert pair["nc"] == 176
