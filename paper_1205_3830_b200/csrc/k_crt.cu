@@ -872,6 +872,14 @@ CrtHost make_const(int T) {
 // k_imma) it draws more power and the step runs under a lower power-capped clock: C4 sketch 36.2-
 // 37.1 vs 34.7-34.8 ms (SM 1511-1545 vs 1785-1793 MHz), C5 117.7-119.8 vs 106.1-107.4, C3 equal
 // (profiles/r02s16_crt_pair.txt). A tested selection, not the default.
+// the pipelined sketch's SM split (experiment RID_CRT_PIPE_SPLIT = SMs for the preparation; 0 =
+// the two kernels share the SMs)
+int crt_pipe_split(int num_sms) {
+  const char* v = experiment_env("RID_CRT_PIPE_SPLIT");
+  const int s = v ? atoi(v) : 0;
+  return s > 0 && s < num_sms / 2 ? s : 0;
+}
+
 bool crt_pair_selected() {
   const char* e = select_env("RID_CRT_2SM");
   return e && atoi(e) != 0;
@@ -1169,8 +1177,12 @@ static CrtBlockWs carve_block(const CrtPlan& p, void* ws, int64_t nb) {
   return w;
 }
 
+// excl > 0: the preparation runs on excl SMs of its own beside a GEMM on the other SMs (the
+// pipelined sketch, crt_pipe_split): excl CTAs, each with shared memory the GEMM's CTA cannot sit
+// beside, so neither kernel shares an SM with the other
+static constexpr size_t kPrepExclSmem = 120 * 1024;
 static cudaError_t crt_prep_A(const CrtPlan& p, const CrtBlockWs& w, const double2* A, int64_t lda,
-                              int64_t ncols, int64_t m, int num_sms, cudaStream_t st) {
+                              int64_t ncols, int64_t m, int num_sms, cudaStream_t st, int excl = 0) {
   // CTAs per cluster (per column): 1 by default (a plain launch). Clusters of 2-8 CTAs read each
   // column from DRAM exactly once (CL = 4: 4.30 vs 6.08 GB per C4 block) but are slower: the
   // kernel is issue-bound, and GPC packing leaves SMs idle (CL = 4: 132 of 148 CTAs resident)
@@ -1213,10 +1225,16 @@ static cudaError_t crt_prep_A(const CrtPlan& p, const CrtBlockWs& w, const doubl
     const int64_t fit = std::min<int64_t>(nclu, it->second);
     cfg.gridDim = dim3((unsigned)(fit * CL));
   }
+  if (excl > 0) {
+    cfg.gridDim = dim3((unsigned)(std::max(1, excl / CL) * CL));
+    cfg.dynamicSmemBytes = kPrepExclSmem;
+  }
   if (CL == 1) cfg.numAttrs = 0;  // a plain launch: each CTA is its own (implicit) cluster
   switch (p.T) {
 #define RID_CRT_PREP(TT)                                                                           \
   case TT:                                                                                         \
+    if (excl > 0 && (e = ensure_dyn_smem((const void*)k_crt_prepA<TT>, kPrepExclSmem)) != cudaSuccess) \
+      return e;                                                                                    \
     e = cudaLaunchKernelEx(&cfg, k_crt_prepA<TT>, A, lda, m, ncols, p.mh, p.Kp, w.colmax, p.b,    \
                            Ares);                                                                  \
     break;
@@ -1281,15 +1299,18 @@ cudaError_t crt_sketch(const CrtPlan& p, const void* wsR, const double2* A, int6
     return tim->external ? cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal)
                          : cudaEventRecord(ev, st);
   };
+  // the split pipeline: the preparation on `split` SMs of its own, the GEMM on the others
+  const int split = pipe ? crt_pipe_split(num_sms) : 0;
   auto gemm = [&](const CrtBlockWs& w, int64_t nc) {
     cudaError_t r;
+    const int num_sms_g = num_sms - split;
     const bool timed = tim && 2 * gi + 1 < tim->nev;
     if (timed && (r = rec(tim->ev[2 * gi])) != cudaSuccess) return r;
     const bool ts = crt_ts(p);
-    r = p.pair ? launch_imma2(p, Rres, w.Ares, w.out, nc, num_sms, st)
-               : KB == 128 ? (ts ? launch_imma<128, true>(p, Rres, w.Ares, w.out, nc, num_sms, st)
-                        : launch_imma<128, false>(p, Rres, w.Ares, w.out, nc, num_sms, st))
-                  : launch_imma<64, false>(p, Rres, w.Ares, w.out, nc, num_sms, st);
+    r = p.pair ? launch_imma2(p, Rres, w.Ares, w.out, nc, num_sms_g, st)
+               : KB == 128 ? (ts ? launch_imma<128, true>(p, Rres, w.Ares, w.out, nc, num_sms_g, st)
+                        : launch_imma<128, false>(p, Rres, w.Ares, w.out, nc, num_sms_g, st))
+                  : launch_imma<64, false>(p, Rres, w.Ares, w.out, nc, num_sms_g, st);
     if (r == cudaSuccess && timed) r = rec(tim->ev[2 * gi + 1]);
     ++gi;
     if (tim) tim->used = std::min(gi, tim->nev / 2);
@@ -1298,7 +1319,7 @@ cudaError_t crt_sketch(const CrtPlan& p, const void* wsR, const double2* A, int6
   // column blocks: the first a quarter of the others (its preparation is the exposed prologue)
   std::vector<std::pair<int64_t, int64_t>> blk;  // (col0, cols)
   {
-    const int64_t first = pipe ? std::max<int64_t>(128, nb / 4 / 128 * 128) : nb;
+    const int64_t first = pipe && !split ? std::max<int64_t>(128, nb / 4 / 128 * 128) : nb;
     if (tim) tim->used = 0;
     int64_t j0 = 0;
     while (j0 < ncols) {
@@ -1327,7 +1348,7 @@ cudaError_t crt_sketch(const CrtPlan& p, const void* wsR, const double2* A, int6
   if ((e = cudaStreamWaitEvent(ax, pipe->fork, 0)) != cudaSuccess) return e;
   for (int c = 0; c < 2 && c < nsub; ++c) {
     if ((e = crt_prep_A(p, w[c], A + blk[c].first * lda, lda, blk[c].second, m, num_sms, ax)) != cudaSuccess)
-      return e;
+      return e;  // the prologue: the whole machine
     if ((e = cudaEventRecord(pipe->prep[c], ax)) != cudaSuccess) return e;
   }
   for (int c = 0; c < nsub; ++c) {
@@ -1340,7 +1361,7 @@ cudaError_t crt_sketch(const CrtPlan& p, const void* wsR, const double2* A, int6
       return e;
     if (c + 2 < nsub) {
       if ((e = crt_prep_A(p, w[b], A + blk[c + 2].first * lda, lda, blk[c + 2].second, m, num_sms,
-                          ax)) != cudaSuccess)
+                          ax, split)) != cudaSuccess)
         return e;
       if ((e = cudaEventRecord(pipe->prep[b], ax)) != cudaSuccess) return e;
     }

@@ -573,7 +573,9 @@ rid_status sketch_block(rid_ctx* c, const SketchR& sr, const double2* A, int64_t
       }
       c->crt_budget = budget;
     }
-    const int64_t nb = rid::crt_block_cols(sr.cp, ncols, budget, c->num_sms);
+    int64_t nb = rid::crt_block_cols(sr.cp, ncols, budget, c->num_sms);
+    if (const char* v = rid::experiment_env("RID_CRT_PIPE_NB"))  // pipelined blocks (columns)
+      if (piped && atoll(v) >= 128) nb = std::min<int64_t>(nb, atoll(v) / 128 * 128);
     void* pw[2] = {nullptr, nullptr};
     RID_TRY(ws_get(c, "Acrt0", rid::crt_A_bytes(sr.cp, nb), &pw[0]));
     if (piped) {
