@@ -91,7 +91,7 @@ class ClockSampler:
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+         "clocks_event_reasons.sw_power_cap,power.limit")
 
     def __init__(self, index: int):
         self.index = index
@@ -127,7 +127,7 @@ class ClockSampler:
         except subprocess.TimeoutExpired:
             self.proc.kill()
         self.t.join(timeout=2)
-        sm, mx, reasons = [], None, set()
+        sm, mx, reasons, pw, plim = [], None, set(), [], None
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines[first:]:
             f = [x.strip() for x in ln.split(",")]
@@ -138,11 +138,17 @@ class ClockSampler:
                 mx = float(f[1])
             except ValueError:
                 continue
+            try:  # board power (W) and its enforced limit: the sketch runs at the power cap
+                pw.append(float(f[2]))
+                plim = float(f[7]) if len(f) > 7 else plim
+            except ValueError:
+                pass
             for nm, v in zip(names, f[3:7]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w": statistics.median(pw) if pw else None, "power_limit_w": plim}
 
 
 # ------------------------------------------------------------------------------ oracle arm -------
