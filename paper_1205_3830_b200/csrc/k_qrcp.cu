@@ -2031,6 +2031,8 @@ static cudaError_t launch_qrcp_lazy(const QrShards& sh, int64_t ldy, int l, int 
   // CTAs per rank: the SMs split evenly over the ranks (one CTA per SM, cooperative); a
   // column's arithmetic does not depend on its CTA, so any split gives the same bits
   int cpr = num_sms / G;
+  if (const char* v = experiment_env("RID_QRCP_LAZY_CTAS"))  // CTAs per rank (fewer: cheaper
+    if (atoi(v) > 0 && atoi(v) < cpr) cpr = atoi(v);          // exchange, longer passes)
   if ((int64_t)cpr * 8 > n) cpr = (int)((n + 7) / 8);
   if (cpr * G > sh.w[0].max_blocks) cpr = sh.w[0].max_blocks / G;
   if (cpr < 1) cpr = 1;
